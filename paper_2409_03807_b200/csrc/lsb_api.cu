@@ -1,0 +1,710 @@
+// extern "C" entry points of include/lipsub_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../include/lipsub_b200.h"
+#include "lsb_batched.hpp"
+#include "lsb_context.hpp"
+
+using namespace lsb;
+
+namespace lsb {
+
+Context::~Context() {
+    if (stream) cudaStreamSynchronize(stream);
+    impl.reset();
+    batched.reset();
+    for (void* p : allocations) cudaFree(p);
+    if (h_state) cudaFreeHost(h_state);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void* Context::dmalloc(size_t bytes) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(p, 0, std::max<size_t>(bytes, 16), stream), "cudaMemset");
+    allocations.push_back(p);
+    return p;
+}
+
+void Context::upload_real(void* dst, const double* src, size_t count) {
+    if (wsize == 8) {
+        cuda_check(cudaMemcpy(dst, src, count * 8, cudaMemcpyHostToDevice), "upload");
+    } else {
+        std::vector<float> tmp(count);
+        for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(src[i]);
+        cuda_check(cudaMemcpy(dst, tmp.data(), count * 4, cudaMemcpyHostToDevice), "upload");
+    }
+}
+
+void Context::alloc_partials(int g_out, int g_elem, int g_vjp, int n_groups) {
+    d_e_part_out = static_cast<double*>(dmalloc(sizeof(double) * g_out));
+    d_e_part_elem = static_cast<double*>(dmalloc(sizeof(double) * g_elem));
+    d_ybar_part = static_cast<double*>(dmalloc(sizeof(double) * (size_t)g_vjp * hp));
+    d_ybar_grp = static_cast<double*>(dmalloc(sizeof(double) * (size_t)n_groups * hp));
+    d_grp_cnt = static_cast<unsigned int*>(dmalloc(sizeof(unsigned int) * n_groups));
+}
+
+void Context::ensure_step_buffers(int steps) {
+    if (steps <= step_capacity) return;
+    const int cap = std::max(steps, 2 * step_capacity);
+    d_reports = static_cast<lsb_exit_report*>(dmalloc(sizeof(lsb_exit_report) * cap));
+    d_z_traj = static_cast<double*>(dmalloc(sizeof(double) * (size_t)cap * r));
+    step_capacity = cap;
+    void* rp = d_reports;
+    double* zp = d_z_traj;
+    cuda_check(cudaMemcpyAsync(&d_state->reports, &rp, sizeof(void*), cudaMemcpyHostToDevice, stream), "reports ptr");
+    cuda_check(cudaMemcpyAsync(&d_state->z_traj, &zp, sizeof(double*), cudaMemcpyHostToDevice, stream), "ztraj ptr");
+    cuda_check(cudaStreamSynchronize(stream), "sync");
+}
+
+}  // namespace lsb
+
+namespace {
+
+lsb_status run(const std::function<void()>& f) {
+    try {
+        f();
+        return LSB_OK;
+    } catch (const LsbError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return LSB_EINVAL;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = "out of host memory";
+        return LSB_ECUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LSB_EMESH;
+    }
+}
+
+void require(bool ok, const std::string& msg, lsb_status code = LSB_EINVAL) {
+    if (!ok) throw LsbError(code, msg);
+}
+
+void check_ctx(const lsb_context* ctx) { require(ctx != nullptr, "null context"); }
+
+void sync(Context& c) { cuda_check(cudaStreamSynchronize(c.stream), "stream sync"); }
+
+// Write a field of the device state from the host (async on the context stream).
+template <typename F>
+void put_state(Context& c, F DevState::*field, const F& value) {
+    static thread_local F tmp;
+    tmp = value;
+    cuda_check(cudaMemcpyAsync(&(c.d_state->*field), &tmp, sizeof(F), cudaMemcpyHostToDevice, c.stream), "state put");
+    sync(c);
+}
+
+void put_config(Context& c, const lsb_solver_config* cfg) {
+    require(cfg != nullptr, "solver: null config");
+    // reference SolverConfig::validate (reduced_solver.cpp:14-20)
+    require(cfg->epsilon > 0.0, "solver: epsilon must be > 0");
+    require(cfg->max_iters >= 1 && cfg->max_linesearch >= 1, "solver: iteration caps must be >= 1");
+    require(cfg->dt > 0.0, "solver: dt must be > 0");
+    require(cfg->lbfgs_history >= 1, "solver: lbfgs history must be >= 1");
+    require(cfg->lbfgs_history <= kMaxHistory, "solver: lbfgs history exceeds device maximum 16");
+    DevState* h = c.h_state;
+    cuda_check(cudaMemcpyAsync(h, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, c.stream), "state get");
+    sync(c);
+    h->eps = cfg->epsilon;
+    h->max_iters = cfg->max_iters;
+    h->max_ls = cfg->max_linesearch;
+    h->hist_cap = cfg->lbfgs_history;
+    h->dt = cfg->dt;
+    cuda_check(cudaMemcpyAsync(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice, c.stream), "state put");
+    sync(c);
+}
+
+void get_state(Context& c) {
+    cuda_check(cudaMemcpyAsync(c.h_state, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, c.stream), "state get");
+    sync(c);
+}
+
+void fill_report(const DevState* s, lsb_exit_report* rep) {
+    if (!rep) return;
+    rep->code = s->code;
+    rep->iterations = s->iter;
+    rep->final_grad_inf_norm = s->gnorm;
+    rep->wall_time_ms = (double)(s->t_end - s->t_start) * 1e-6;
+    rep->value_evals = s->value_evals;
+    rep->grad_evals = s->grad_evals;
+}
+
+void upload_pins(Context& c) {
+    // pinned rows of U get pin - X; free rows are overwritten by every decode
+    const HostMesh& m = c.mesh;
+    std::vector<double> disp(3 * (size_t)m.V, 0.0);
+    for (int v : m.pinned)
+        for (int k = 0; k < 3; ++k) disp[3 * (size_t)v + k] = c.pin_positions[3 * (size_t)v + k] - m.X[3 * (size_t)v + k];
+    cuda_check(cudaMemcpy(c.d_pin_disp, disp.data(), disp.size() * 8, cudaMemcpyHostToDevice), "pins");
+    std::vector<double> U4(4 * (size_t)m.V, 0.0);
+    for (int v : m.pinned)
+        for (int k = 0; k < 3; ++k) U4[4 * (size_t)v + k] = disp[3 * (size_t)v + k];
+    // free rows: keep whatever the last decode wrote (re-uploading zeros is harmless
+    // because every evaluation rewrites them before the element pass).
+    c.upload_real(c.d_U, U4.data(), U4.size());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lsb_last_error(void) { return g_last_error.c_str(); }
+const char* lsb_version(void) { return "lipsub_b200 0.1 (sm_100a)"; }
+
+lsb_status lsb_bar_mesh_size(int nx, int ny, int nz, int pin_left, int* V, int* E, int* num_pinned) {
+    return run([&] {
+        require(nx >= 1 && ny >= 1 && nz >= 1, "bar: grid sizes must be >= 1");
+        if (V) *V = (nx + 1) * (ny + 1) * (nz + 1);
+        if (E) *E = 6 * nx * ny * nz;
+        if (num_pinned) *num_pinned = pin_left ? (ny + 1) * (nz + 1) : 0;
+    });
+}
+
+lsb_status lsb_make_bar_mesh(int nx, int ny, int nz, double width, double height, double depth, double jitter_frac,
+                             uint64_t seed, int pin_left, double* rest_positions, int32_t* tets, int32_t* pinned) {
+    return run([&] {
+        const HostMesh m = make_bar_mesh(nx, ny, nz, width, height, depth, jitter_frac, seed, pin_left != 0);
+        if (rest_positions) std::memcpy(rest_positions, m.X.data(), m.X.size() * 8);
+        if (tets) std::memcpy(tets, m.T.data(), m.T.size() * 4);
+        if (pinned) std::memcpy(pinned, m.pinned.data(), m.pinned.size() * 4);
+    });
+}
+
+lsb_status lsb_make_bar_decoder(int V, const double* rest_positions, int num_pinned, const int32_t* pinned,
+                                int latent_dim, int hidden_layers, int width, int act, uint64_t seed, double out_scale,
+                                double* weights_packed, double* norm_shift, double* norm_scale) {
+    return run([&] {
+        require(V > 0 && rest_positions != nullptr, "decoder: mesh required");
+        HostMesh m;
+        m.V = V;
+        m.X.assign(rest_positions, rest_positions + 3 * (size_t)V);
+        m.pinned.assign(pinned, pinned + num_pinned);
+        // free numbering only (no elements needed)
+        std::vector<char> pin(V, 0);
+        for (int v : m.pinned) {
+            require(v >= 0 && v < V, "decoder: pinned vertex out of range");
+            pin[v] = 1;
+        }
+        m.free_index.assign(V, -1);
+        for (int v = 0; v < V; ++v)
+            if (!pin[v]) {
+                m.free_index[v] = (int)m.free_vertex.size();
+                m.free_vertex.push_back(v);
+            }
+        m.n_free = (int)m.free_vertex.size();
+        const HostDecoder d = make_bar_decoder(m, latent_dim, hidden_layers, width, act, seed, out_scale);
+        size_t off = 0;
+        for (const HostLayer& L : d.layers) {
+            if (weights_packed) std::memcpy(weights_packed + off, L.W.data(), L.W.size() * 8);
+            off += L.W.size();
+        }
+        if (norm_shift) std::memcpy(norm_shift, d.shift.data(), d.shift.size() * 8);
+        if (norm_scale) std::memcpy(norm_scale, d.scale.data(), d.scale.size() * 8);
+    });
+}
+
+lsb_status lsb_lame_from_young(int num_tets, double E_lo, double E_hi, double nu, uint64_t seed, double* mu,
+                               double* lambda) {
+    return run([&] {
+        require(num_tets >= 0 && mu && lambda, "material: bad arguments");
+        require(E_lo > 0.0 && E_hi >= E_lo, "material: Young's modulus range must be positive");
+        require(nu > -1.0 && nu < 0.5, "material: Poisson ratio must be in (-1, 0.5)");
+        Rng rng = substream(seed, 2);
+        for (int e = 0; e < num_tets; ++e) {
+            const double E = E_hi > E_lo ? E_lo + (E_hi - E_lo) * randu(rng) : E_lo;
+            mu[e] = E / (2.0 * (1.0 + nu));
+            lambda[e] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+        }
+    });
+}
+
+lsb_status lsb_gaussian_stream(uint64_t seed, uint64_t tag, int count, double std_dev, double* out) {
+    return run([&] {
+        require(count >= 0 && (count == 0 || out), "gaussian_stream: bad arguments");
+        Rng rng = substream(seed, tag);
+        for (int i = 0; i < count; ++i) out[i] = std_dev * randn(rng);
+    });
+}
+
+lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, int precision, int device,
+                      lsb_context** out) {
+    return run([&] {
+        require(mesh && dec && out, "create: null argument");
+        require(precision == LSB_FP64 || precision == LSB_FP32, "create: precision must be LSB_FP64 or LSB_FP32");
+        *out = nullptr;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw LsbError(LSB_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+        require(device >= 0 && device < ndev, "create: device index out of range");
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "device props");
+        if (prop.major < 10)
+            throw LsbError(LSB_ECUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a only)");
+
+        auto holder = std::make_unique<lsb_context>();
+        Context& c = holder->c;
+        c.precision = precision;
+        c.device = device;
+        c.num_sms = prop.multiProcessorCount;
+        c.wsize = precision == LSB_FP64 ? 8 : 4;
+        cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
+
+        // ---- mesh (build_mesh semantics) ----
+        require(mesh->num_vertices > 0 && mesh->num_tets > 0, "mesh: empty mesh");
+        require(mesh->rest_positions && mesh->tets, "mesh: null arrays");
+        require(mesh->num_pinned >= 0 && (mesh->num_pinned == 0 || mesh->pinned), "mesh: bad pin list");
+        HostMesh& m = c.mesh;
+        m.V = mesh->num_vertices;
+        m.E = mesh->num_tets;
+        m.X.assign(mesh->rest_positions, mesh->rest_positions + 3 * (size_t)m.V);
+        m.T.assign(mesh->tets, mesh->tets + 4 * (size_t)m.E);
+        m.pinned.assign(mesh->pinned, mesh->pinned + mesh->num_pinned);
+        try {
+            precompute(m);
+        } catch (const std::invalid_argument& e) {
+            throw LsbError(LSB_EINVAL, e.what());
+        } catch (const std::runtime_error& e) {
+            throw LsbError(LSB_EMESH, e.what());
+        }
+        require(m.n_free > 0, "mesh: every vertex is pinned");
+        require(mesh->mu && mesh->lambda, "material: null mu/lambda");
+        c.mu.assign(mesh->mu, mesh->mu + m.E);
+        c.lambda.assign(mesh->lambda, mesh->lambda + m.E);
+        for (int e = 0; e < m.E; ++e) {  // MaterialParams::validate (mesh.cpp:12-18)
+            require(c.mu[e] > 0.0, "material: mu must be > 0");
+            require(c.lambda[e] >= 0.0, "material: lambda must be >= 0");
+        }
+        c.density = mesh->density;
+        c.mass = lump_mass(m, mesh->density, &c.total_mass);
+        c.n = 3 * m.n_free;
+        c.pin_positions = m.X;
+
+        // ---- decoder (SubspaceModel::validate, net.cpp:66-88) ----
+        require(dec->latent_dim >= 1 && dec->latent_dim <= kMaxLatent, "model: latent dim must be in [1, 64]");
+        require(dec->num_layers >= 1 && dec->num_layers - 1 <= kMaxLayers, "model: bad layer count");
+        require(dec->rows && dec->cols && dec->activations && dec->weights && dec->biases, "model: null arrays");
+        require(dec->norm_shift && dec->norm_scale, "model: normalization vectors required");
+        c.r = dec->latent_dim;
+        const int L = dec->num_layers;
+        int width = c.r;
+        for (int l = 0; l < L; ++l) {
+            require(dec->cols[l] == width, "model: decoder layer shapes do not chain");
+            require(dec->rows[l] >= 1, "model: empty layer");
+            require(dec->activations[l] >= 0 && dec->activations[l] <= 3, "activation: unknown tag");
+            require(dec->weights[l] && dec->biases[l], "model: null layer arrays");
+            HostLayer hl;
+            hl.rows = dec->rows[l];
+            hl.cols = dec->cols[l];
+            hl.act = dec->activations[l];
+            hl.W.assign(dec->weights[l], dec->weights[l] + (size_t)hl.rows * hl.cols);
+            hl.b.assign(dec->biases[l], dec->biases[l] + hl.rows);
+            c.layers.push_back(std::move(hl));
+            width = dec->rows[l];
+        }
+        require(width == c.n, "model: decoder output width != n (3 x free vertices)");
+        c.shift.assign(dec->norm_shift, dec->norm_shift + c.n);
+        c.scale.assign(dec->norm_scale, dec->norm_scale + c.n);
+        for (double s : c.scale) require(s > 0.0, "model: norm_scale entries must be positive");
+        c.nhid = L - 1;
+        c.h = c.layers[L - 1].cols;
+        require(c.h <= kMaxHidden, "model: hidden width exceeds device maximum 512");
+        for (int l = 0; l < c.nhid; ++l) require(c.layers[l].rows <= kMaxHidden, "model: hidden width exceeds 512");
+        c.out_act = c.layers[L - 1].act;
+        c.hp = 32;
+        while (c.hp < c.h) c.hp *= 2;
+        if (precision == LSB_FP64) c.hp = std::max(c.hp, 64);  // >= 32 lanes x double2
+        else c.hp = std::max(c.hp, 128);                          // >= 32 lanes x float4
+
+        const size_t w = c.wsize;
+        const int n = c.n;
+        // ---- HBM layout ----
+        // output layer, rows padded to hp
+        {
+            std::vector<double> Wp((size_t)n * c.hp, 0.0);
+            const HostLayer& o = c.layers[L - 1];
+            for (int i = 0; i < n; ++i)
+                std::copy(&o.W[(size_t)i * c.h], &o.W[(size_t)i * c.h] + c.h, &Wp[(size_t)i * c.hp]);
+            c.d_Wout = c.dmalloc(Wp.size() * w);
+            c.upload_real(c.d_Wout, Wp.data(), Wp.size());
+            c.d_bout = c.dmalloc(n * w);
+            c.upload_real(c.d_bout, o.b.data(), n);
+        }
+        c.d_sout = c.dmalloc(n * w);
+        c.upload_real(c.d_sout, c.scale.data(), n);
+        {
+            std::vector<double> cs(n);
+            for (int f = 0; f < m.n_free; ++f)
+                for (int k = 0; k < 3; ++k)
+                    cs[3 * f + k] = c.shift[3 * f + k] - m.X[3 * (size_t)m.free_vertex[f] + k];
+            c.d_cout = c.dmalloc(n * w);
+            c.upload_real(c.d_cout, cs.data(), n);
+        }
+        c.d_dsout = c.dmalloc(n * w);
+        c.d_mass = c.dmalloc(n * w);
+        c.upload_real(c.d_mass, c.mass.data(), n);
+        c.d_ut = c.dmalloc(n * w);
+        c.d_rin = c.dmalloc(n * w);
+        c.d_vfree = static_cast<int*>(c.dmalloc(sizeof(int) * m.n_free));
+        cuda_check(cudaMemcpy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice), "vfree");
+        c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * (size_t)m.E));
+        cuda_check(cudaMemcpy(c.d_tets, m.T.data(), sizeof(int) * 4 * (size_t)m.E, cudaMemcpyHostToDevice), "tets");
+        {
+            std::vector<double> rec(12 * (size_t)m.E);
+            for (int e = 0; e < m.E; ++e) {
+                double* o = &rec[12 * (size_t)e];
+                std::copy(&m.Dminv[9 * (size_t)e], &m.Dminv[9 * (size_t)e] + 9, o);
+                o[9] = m.vol[e];
+                o[10] = c.mu[e];
+                o[11] = c.lambda[e];
+            }
+            c.d_rec = c.dmalloc(rec.size() * w);
+            c.upload_real(c.d_rec, rec.data(), rec.size());
+        }
+        c.d_U = c.dmalloc(4 * (size_t)m.V * w);
+        c.d_forces = c.dmalloc(12 * (size_t)m.E * w);
+        c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
+        cuda_check(cudaMemcpy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice), "csr");
+        c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
+        cuda_check(cudaMemcpy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice), "csr");
+        {  // hidden layers, fp64, row-major and transposed
+            std::vector<double> Wh, WhT, bh;
+            for (int l = 0; l < c.nhid; ++l) {
+                const HostLayer& hl = c.layers[l];
+                c.hoff[l] = (int)Wh.size();
+                c.boff[l] = (int)bh.size();
+                c.hrows[l] = hl.rows;
+                c.hcols[l] = hl.cols;
+                c.hact[l] = hl.act;
+                Wh.insert(Wh.end(), hl.W.begin(), hl.W.end());
+                for (int j = 0; j < hl.cols; ++j)
+                    for (int i = 0; i < hl.rows; ++i) WhT.push_back(hl.W[(size_t)i * hl.cols + j]);
+                bh.insert(bh.end(), hl.b.begin(), hl.b.end());
+            }
+            c.d_Wh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, Wh.size())));
+            c.d_WhT = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, WhT.size())));
+            c.d_bh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, bh.size())));
+            if (!Wh.empty()) {
+                cuda_check(cudaMemcpy(c.d_Wh, Wh.data(), 8 * Wh.size(), cudaMemcpyHostToDevice), "Wh");
+                cuda_check(cudaMemcpy(c.d_WhT, WhT.data(), 8 * WhT.size(), cudaMemcpyHostToDevice), "WhT");
+                cuda_check(cudaMemcpy(c.d_bh, bh.data(), 8 * bh.size(), cudaMemcpyHostToDevice), "bh");
+            }
+        }
+        c.d_a_hid = static_cast<double*>(c.dmalloc(sizeof(double) * kMaxHidden * std::max(1, c.nhid)));
+        c.d_y_last = c.dmalloc(c.hp * w);
+        c.d_state = static_cast<DevState*>(c.dmalloc(sizeof(DevState)));
+        cuda_check(cudaMallocHost(&c.h_state, sizeof(DevState)), "pinned state");
+        std::memset(c.h_state, 0, sizeof(DevState));
+        // dynamics
+        c.d_u_state = static_cast<double*>(c.dmalloc(sizeof(double) * 3 * (size_t)m.V));
+        c.d_v_state = static_cast<double*>(c.dmalloc(sizeof(double) * 3 * (size_t)m.V));
+        c.d_z_state = static_cast<double*>(c.dmalloc(sizeof(double) * c.r));
+        c.d_a_ext = static_cast<double*>(c.dmalloc(sizeof(double) * n));
+        c.d_pin_disp = static_cast<double*>(c.dmalloc(sizeof(double) * 3 * (size_t)m.V));
+        {
+            std::vector<char> vp(m.V, 0);
+            for (int v : m.pinned) vp[v] = 1;
+            c.d_vpinned = static_cast<char*>(c.dmalloc(m.V));
+            cuda_check(cudaMemcpy(c.d_vpinned, vp.data(), m.V, cudaMemcpyHostToDevice), "vpinned");
+        }
+        c.d_launch_acc = static_cast<long long*>(c.dmalloc(sizeof(long long)));
+        cuda_check(cudaStreamSynchronize(c.stream), "sync");
+        upload_pins(c);
+        c.impl = make_impl(precision);
+        c.impl->setup(c);
+        // defaults: dt 0.05 (SolverConfig), history 8, no inertia
+        DevState* h = c.h_state;
+        std::memset(h, 0, sizeof(DevState));
+        h->dt = 0.05;
+        h->inv_dt2 = 1.0 / (0.05 * 0.05);
+        h->has_inertia = 0;
+        h->eps = 1e-5;
+        h->max_iters = 1024;
+        h->max_ls = 128;
+        h->hist_cap = 8;
+        h->phase = kPhaseDone;
+        cuda_check(cudaMemcpy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice), "state init");
+        c.ensure_step_buffers(16);
+        cuda_check(cudaDeviceSynchronize(), "create sync");
+        *out = holder.release();
+    });
+}
+
+void lsb_destroy(lsb_context* ctx) { delete ctx; }
+
+lsb_status lsb_get_info(const lsb_context* ctx, int* n, int* r, int* V, int* E, int* h, int* precision) {
+    return run([&] {
+        check_ctx(ctx);
+        const Context& c = ctx->c;
+        if (n) *n = c.n;
+        if (r) *r = c.r;
+        if (V) *V = c.mesh.V;
+        if (E) *E = c.mesh.E;
+        if (h) *h = c.h;
+        if (precision) *precision = c.precision;
+    });
+}
+
+lsb_status lsb_get_mass(const lsb_context* ctx, double* mass_diag, double* total_mass) {
+    return run([&] {
+        check_ctx(ctx);
+        if (mass_diag) std::memcpy(mass_diag, ctx->c.mass.data(), ctx->c.mass.size() * 8);
+        if (total_mass) *total_mass = ctx->c.total_mass;
+    });
+}
+
+lsb_status lsb_set_pin_positions(lsb_context* ctx, const double* pin_positions) {
+    return run([&] {
+        check_ctx(ctx);
+        require(pin_positions != nullptr, "pins: null array");
+        Context& c = ctx->c;
+        sync(c);
+        c.pin_positions.assign(pin_positions, pin_positions + 3 * (size_t)c.mesh.V);
+        upload_pins(c);
+    });
+}
+
+lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
+    return run([&] {
+        check_ctx(ctx);
+        Context& c = ctx->c;
+        require(dt > 0.0, "solver: dt must be > 0");
+        sync(c);
+        get_state(c);
+        DevState* h = c.h_state;
+        h->dt = dt;
+        h->inv_dt2 = 1.0 / (dt * dt);
+        h->has_inertia = qbar ? 1 : 0;
+        h->quasi_static = qbar ? 0 : 1;
+        if (qbar) {
+            std::vector<double> ut(c.n);
+            for (int f = 0; f < c.mesh.n_free; ++f)
+                for (int k = 0; k < 3; ++k)
+                    ut[3 * f + k] = qbar[3 * f + k] - c.mesh.X[3 * (size_t)c.mesh.free_vertex[f] + k];
+            c.upload_real(c.d_ut, ut.data(), ut.size());
+        }
+        c.has_qbar = qbar != nullptr;
+        c.dt = dt;
+        cuda_check(cudaMemcpy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice), "state put");
+    });
+}
+
+static void put_zt(Context& c, const double* z) {
+    cuda_check(cudaMemcpyAsync(c.d_state->zt, z, sizeof(double) * c.r, cudaMemcpyHostToDevice, c.stream), "z upload");
+}
+
+lsb_status lsb_eval(lsb_context* ctx, const double* z, double* value, double* grad) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z && value, "eval: null argument");
+        Context& c = ctx->c;
+        put_zt(c, z);
+        c.impl->eval(c, grad != nullptr);
+        get_state(c);
+        const DevState* s = c.h_state;
+        if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+        *value = s->f_eval;
+        if (grad) std::memcpy(grad, s->gz, sizeof(double) * c.r);
+    });
+}
+
+lsb_status lsb_decode(lsb_context* ctx, const double* z, double* q) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z && q, "decode: null argument");
+        Context& c = ctx->c;
+        put_zt(c, z);
+        c.impl->eval(c, false);
+        sync(c);
+        const HostMesh& m = c.mesh;
+        std::vector<double> U(4 * (size_t)m.V);
+        if (c.wsize == 8) {
+            cuda_check(cudaMemcpy(U.data(), c.d_U, U.size() * 8, cudaMemcpyDeviceToHost), "U");
+        } else {
+            std::vector<float> Uf(U.size());
+            cuda_check(cudaMemcpy(Uf.data(), c.d_U, U.size() * 4, cudaMemcpyDeviceToHost), "U");
+            for (size_t i = 0; i < U.size(); ++i) U[i] = Uf[i];
+        }
+        for (int f = 0; f < m.n_free; ++f)
+            for (int k = 0; k < 3; ++k)
+                q[3 * f + k] = m.X[3 * (size_t)m.free_vertex[f] + k] + U[4 * (size_t)m.free_vertex[f] + k];
+    });
+}
+
+lsb_status lsb_lbfgs(lsb_context* ctx, double* z, const lsb_solver_config* cfg, lsb_exit_report* report) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z != nullptr, "lbfgs: null z");
+        Context& c = ctx->c;
+        put_config(c, cfg);
+        put_zt(c, z);
+        c.impl->minimize(c);
+        get_state(c);
+        const DevState* s = c.h_state;
+        c.launches += 3LL * s->loop_iters;
+        if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+        std::memcpy(z, s->x, sizeof(double) * c.r);
+        fill_report(s, report);
+    });
+}
+
+lsb_status lsb_set_state(lsb_context* ctx, const double* positions, const double* velocities, const double* z) {
+    return run([&] {
+        check_ctx(ctx);
+        require(positions && velocities && z, "state: null argument");
+        Context& c = ctx->c;
+        sync(c);
+        const HostMesh& m = c.mesh;
+        std::vector<double> u(3 * (size_t)m.V);
+        for (size_t i = 0; i < u.size(); ++i) u[i] = positions[i] - m.X[i];
+        cuda_check(cudaMemcpy(c.d_u_state, u.data(), u.size() * 8, cudaMemcpyHostToDevice), "state u");
+        cuda_check(cudaMemcpy(c.d_v_state, velocities, u.size() * 8, cudaMemcpyHostToDevice), "state v");
+        cuda_check(cudaMemcpy(c.d_z_state, z, c.r * 8, cudaMemcpyHostToDevice), "state z");
+        put_state(c, &DevState::t, 0.0);
+        c.state_set = true;
+    });
+}
+
+lsb_status lsb_get_state(lsb_context* ctx, double* positions, double* velocities, double* z, double* t) {
+    return run([&] {
+        check_ctx(ctx);
+        Context& c = ctx->c;
+        require(c.state_set, "state: lsb_set_state has not been called", LSB_ESTATE);
+        sync(c);
+        const HostMesh& m = c.mesh;
+        if (positions) {
+            cuda_check(cudaMemcpy(positions, c.d_u_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost), "state u");
+            for (size_t i = 0; i < 3 * (size_t)m.V; ++i) positions[i] += m.X[i];
+        }
+        if (velocities) cuda_check(cudaMemcpy(velocities, c.d_v_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost), "state v");
+        if (z) cuda_check(cudaMemcpy(z, c.d_z_state, 8 * (size_t)c.r, cudaMemcpyDeviceToHost), "state z");
+        if (t) {
+            get_state(c);
+            *t = c.h_state->t;
+        }
+    });
+}
+
+lsb_status lsb_set_external_force(lsb_context* ctx, const double* force) {
+    return run([&] {
+        check_ctx(ctx);
+        require(force != nullptr, "force: null array");
+        Context& c = ctx->c;
+        sync(c);
+        std::vector<double> a(c.n);
+        for (int i = 0; i < c.n; ++i) a[i] = force[i] / c.mass[i];  // f / m (reduced_solver.cpp:253)
+        cuda_check(cudaMemcpy(c.d_a_ext, a.data(), a.size() * 8, cudaMemcpyHostToDevice), "force");
+    });
+}
+
+static void prepare_steps(Context& c, int steps, const lsb_solver_config* cfg, int quasi_static) {
+    require(c.state_set, "step: lsb_set_state has not been called", LSB_ESTATE);
+    require(steps >= 0, "simulate: negative step count");
+    put_config(c, cfg);
+    get_state(c);
+    c.h_state->quasi_static = quasi_static ? 1 : 0;
+    c.h_state->step_idx = 0;
+    cuda_check(cudaMemcpy(c.d_state, c.h_state, sizeof(DevState), cudaMemcpyHostToDevice), "state put");
+    c.ensure_step_buffers(std::max(1, steps));
+}
+
+lsb_status lsb_step(lsb_context* ctx, const lsb_solver_config* cfg, int quasi_static, lsb_exit_report* report) {
+    return run([&] {
+        check_ctx(ctx);
+        Context& c = ctx->c;
+        prepare_steps(c, 1, cfg, quasi_static);
+        c.impl->step(c);
+        get_state(c);
+        if (c.h_state->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+        if (report) cuda_check(cudaMemcpy(report, c.d_reports, sizeof(lsb_exit_report), cudaMemcpyDeviceToHost), "report");
+    });
+}
+
+lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cfg, int quasi_static,
+                        lsb_exit_report* reports, double* z_traj) {
+    return run([&] {
+        check_ctx(ctx);
+        Context& c = ctx->c;
+        prepare_steps(c, steps, cfg, quasi_static);
+        for (int s = 0; s < steps; ++s) c.impl->step(c);
+        sync(c);
+        get_state(c);
+        if (reports) cuda_check(cudaMemcpy(reports, c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost), "reports");
+        if (z_traj) cuda_check(cudaMemcpy(z_traj, c.d_z_traj, sizeof(double) * (size_t)steps * c.r, cudaMemcpyDeviceToHost), "z traj");
+        std::vector<lsb_exit_report> tmp(steps);
+        cuda_check(cudaMemcpy(tmp.data(), c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost), "reports");
+        for (int s = 0; s < steps; ++s)
+            if (tmp[s].code == -kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+    });
+}
+
+lsb_status lsb_get_launch_count(const lsb_context* ctx, long long* launches) {
+    return run([&] {
+        check_ctx(ctx);
+        const Context& c = ctx->c;
+        long long dev = 0;
+        cuda_check(cudaMemcpy(&dev, c.d_launch_acc, sizeof(long long), cudaMemcpyDeviceToHost), "launch acc");
+        *launches = c.launches + dev + c.batched_launches;
+    });
+}
+
+lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double* ms_out_fwd, double* ms_elem,
+                            double* ms_vjp, double* ms_total) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z && reps > 0, "profile: bad arguments");
+        Context& c = ctx->c;
+        put_zt(c, z);
+        float ms[4];
+        c.impl->profile(c, reps, ms);
+        if (ms_out_fwd) *ms_out_fwd = ms[0];
+        if (ms_elem) *ms_elem = ms[1];
+        if (ms_vjp) *ms_vjp = ms[2];
+        if (ms_total) *ms_total = ms[3];
+    });
+}
+
+lsb_status lsb_eval_batched(lsb_context* ctx, int B, const double* Z, double* E, double* G) {
+    return run([&] {
+        check_ctx(ctx);
+        require(B >= 0 && (B == 0 || (Z && E)), "eval_batched: bad arguments");
+        if (B == 0) return;
+        batched_eval(ctx->c, B, Z, E, G);
+    });
+}
+
+lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double* H) {
+    return run([&] {
+        check_ctx(ctx);
+        require(B >= 0 && (B == 0 || (Z && H)), "hessian_batched: bad arguments");
+        if (B == 0) return;
+        batched_hessian(ctx->c, B, Z, H);
+    });
+}
+
+lsb_status lsb_lipschitz_loss(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss) {
+    return run([&] {
+        check_ctx(ctx);
+        require(P > 0, "lipschitz loss: no pairs");  // losses.cpp:199
+        require(Z1 && Z2 && loss, "lipschitz loss: null argument");
+        const int r = ctx->c.r;
+        for (int p = 0; p < P; ++p) {  // losses.cpp:202-204
+            double dz2 = 0.0;
+            for (int k = 0; k < r; ++k) dz2 += (Z1[p * r + k] - Z2[p * r + k]) * (Z1[p * r + k] - Z2[p * r + k]);
+            require(dz2 > 0.0, "lipschitz loss: coincident pair");
+        }
+        *loss = lipschitz_loss(ctx->c, P, Z1, Z2);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+// Shared device-side helpers for the B200-native reduced-objective path.
+// Precision model: `T` is the storage/arithmetic type of the bandwidth-bound
+// data (decoder output layer, displacements, element records, forces):
+// double in fp64 mode, float in fp32 mode.  The latent-space work (hidden MLP,
+// L-BFGS state, final reductions) is always fp64: it is tiny and latency-bound.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lsb {
+
+constexpr int kMaxLatent = 64;    // d (latent dim) upper bound
+constexpr int kMaxHistory = 16;   // L-BFGS memory upper bound
+constexpr int kMaxHidden = 512;   // hidden width upper bound
+constexpr int kMaxLayers = 16;    // hidden layers upper bound
+
+enum Act : int { kIdentity = 0, kSilu = 1, kTanh = 2, kElu = 3 };
+
+template <typename T> struct Vec4;
+template <> struct alignas(16) Vec4<float> { float x, y, z, w; };
+template <> struct alignas(32) Vec4<double> { double x, y, z, w; };
+
+// ---- activation derivatives of order 0..3 (reference net.cpp:34-64; ELU is
+// the BASELINE.json extension, the x <= 0 branch owns x == 0). ----------------
+__device__ __forceinline__ double act_eval(int a, double x, int order) {
+    switch (a) {
+        case kIdentity: return order == 0 ? x : (order == 1 ? 1.0 : 0.0);
+        case kSilu: {
+            const double s = 1.0 / (1.0 + exp(-x));
+            const double s1 = s * (1.0 - s);
+            const double s2 = s1 * (1.0 - 2.0 * s);
+            const double s3 = s2 * (1.0 - 2.0 * s) - 2.0 * s1 * s1;
+            if (order == 0) return x * s;
+            if (order == 1) return s + x * s1;
+            if (order == 2) return 2.0 * s1 + x * s2;
+            return 3.0 * s2 + x * s3;
+        }
+        case kTanh: {
+            const double t = tanh(x);
+            const double t1 = 1.0 - t * t;
+            if (order == 0) return t;
+            if (order == 1) return t1;
+            if (order == 2) return -2.0 * t * t1;
+            return -2.0 * t1 * t1 + 4.0 * t * t * t1;
+        }
+        default: {  // kElu
+            if (x > 0.0) return order == 0 ? x : (order == 1 ? 1.0 : 0.0);
+            return order == 0 ? expm1(x) : exp(x);
+        }
+    }
+}
+
+// ---- warp / block reductions ---------------------------------------------------------
+template <typename V>
+__device__ __forceinline__ V warp_sum(V v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block sum (fixed tree); result valid in every thread.
+// `scratch` needs blockDim.x/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (warp == 0) {
+        t = lane < nw ? scratch[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) scratch[0] = t;
+    }
+    __syncthreads();
+    const double r = scratch[0];
+    __syncthreads();
+    return r;
+}
+
+// ---- streaming loads (read-once data: skip L1, evict first from L2) -----------------------
+// sm_100 supports 256-bit per-thread global loads; the L2::evict_first hint
+// requires them.  One 32-byte vector = 8 floats or 4 doubles.
+struct alignas(32) F8 { float v[8]; };
+struct alignas(32) D4 { double v[4]; };
+
+__device__ __forceinline__ F8 ld_stream(const F8* p) {
+    F8 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+                   "=f"(r.v[6]), "=f"(r.v[7])
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ D4 ld_stream(const D4* p) {
+    D4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+                 : "l"(p));
+    return r;
+}
+
+template <typename T> struct VecT;
+template <> struct VecT<float> { using type = F8; static constexpr int N = 8; };
+template <> struct VecT<double> { using type = D4; static constexpr int N = 4; };
+
+template <typename V, typename T>
+__device__ __forceinline__ void vec_fma(T& acc, const V& w, const T* y) {
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(V) / sizeof(T)); ++q) acc = fma(w.v[q], y[q], acc);
+}
+template <typename V, typename T>
+__device__ __forceinline__ void vec_axpy(T* acc, const V& w, T t) {
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(V) / sizeof(T)); ++q) acc[q] = fma(w.v[q], t, acc[q]);
+}
+
+// ---- stable neo-Hookean, cancellation-free (reference energy.cpp:178-221) ---------------
+// log1p(x) - x, accurate for small |x| in either precision.
+__device__ __forceinline__ double log1p_minus_x(double x) {
+    if (fabs(x) < 1e-2) {
+        const double x2 = x * x;
+        return x2 * (-0.5 + x * (1.0 / 3.0 + x * (-0.25 + x * (0.2 + x * (-1.0 / 6.0 + x * (1.0 / 7.0))))));
+    }
+    return log1p(x) - x;
+}
+__device__ __forceinline__ float log1p_minus_x(float x) {
+    if (fabsf(x) < 5e-2f) {
+        const float x2 = x * x;
+        return x2 * (-0.5f + x * (1.0f / 3.0f + x * (-0.25f + x * (0.2f + x * (-1.0f / 6.0f + x * (1.0f / 7.0f))))));
+    }
+    return log1pf(x) - x;
+}
+
+// Given the strain increment A = (Ds - Ds_rest) Dm^-1 (row-major 3x3), Lame mu,
+// lambda, returns psi and the first Piola-Kirchhoff stress P (row-major),
+// algebraically identical to the reference density
+//   psi = mu/2 i - mu/2 log1p(i/4) + lambda/2 (J-1)^2 - 3/4 mu (J-1)
+// with i = |F|^2 - 3 and P = 2 psi_I F + psi_J cof(F), but regrouped so that no
+// O(1) or O(|A|) terms cancel:
+//   psi = 3/8 mu |A|^2 - 3/4 mu (m2 + det A) - mu/2 L(i/4) + lambda/2 (J-1)^2,
+//   P   = 3/4 mu (A + A^T - tr(A) I - cof A) + mu i / (4 (4 + i)) F + lambda (J-1) cof F,
+// with L(x) = log1p(x) - x, cof(F) = I + tr(A) I - A^T + cof(A).
+template <typename T>
+__device__ __forceinline__ T snh_psi_P(const T* A, T mu, T lambda, T* P) {
+    const T trA = A[0] + A[4] + A[8];
+    T q = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) q += A[k] * A[k];
+    const T m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+    // cofactor matrix of A: columns a1 x a2, a2 x a0, a0 x a1 (a_b = column b)
+    T cA[9];
+    cA[0 * 3 + 0] = A[1 * 3 + 1] * A[2 * 3 + 2] - A[2 * 3 + 1] * A[1 * 3 + 2];
+    cA[1 * 3 + 0] = A[2 * 3 + 1] * A[0 * 3 + 2] - A[0 * 3 + 1] * A[2 * 3 + 2];
+    cA[2 * 3 + 0] = A[0 * 3 + 1] * A[1 * 3 + 2] - A[1 * 3 + 1] * A[0 * 3 + 2];
+    cA[0 * 3 + 1] = A[1 * 3 + 2] * A[2 * 3 + 0] - A[2 * 3 + 2] * A[1 * 3 + 0];
+    cA[1 * 3 + 1] = A[2 * 3 + 2] * A[0 * 3 + 0] - A[0 * 3 + 2] * A[2 * 3 + 0];
+    cA[2 * 3 + 1] = A[0 * 3 + 2] * A[1 * 3 + 0] - A[1 * 3 + 2] * A[0 * 3 + 0];
+    cA[0 * 3 + 2] = A[1 * 3 + 0] * A[2 * 3 + 1] - A[2 * 3 + 0] * A[1 * 3 + 1];
+    cA[1 * 3 + 2] = A[2 * 3 + 0] * A[0 * 3 + 1] - A[0 * 3 + 0] * A[2 * 3 + 1];
+    cA[2 * 3 + 2] = A[0 * 3 + 0] * A[1 * 3 + 1] - A[1 * 3 + 0] * A[0 * 3 + 1];
+    const T detA = A[0] * cA[0] + A[3] * cA[3] + A[6] * cA[6];  // column-0 expansion
+    const T jm1 = trA + m2 + detA;
+    const T i_minus = T(2) * trA + q;
+    const T x = i_minus * T(0.25);
+    const T psi = T(0.375) * mu * q - T(0.75) * mu * (m2 + detA) - T(0.5) * mu * log1p_minus_x(x) +
+                  T(0.5) * lambda * jm1 * jm1;
+    const T c1 = T(0.75) * mu;
+    const T c2 = mu * i_minus / (T(4) * (T(4) + i_minus));
+    const T c3 = lambda * jm1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const T Aab = A[a * 3 + b], Aba = A[b * 3 + a];
+            const T id = (a == b) ? T(1) : T(0);
+            const T cofF = id + trA * id - Aba + cA[a * 3 + b];
+            const T F = id + Aab;
+            P[a * 3 + b] = c1 * (Aab + Aba - trA * id - cA[a * 3 + b]) + c2 * F + c3 * cofF;
+        }
+    return psi;
+}
+
+}  // namespace lsb

@@ -1,0 +1,110 @@
+// Context object behind the opaque lsb_context handle: host mesh/decoder
+// copies, the HBM layout of every device buffer and the precision-specific
+// kernel implementation.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lipsub_b200.h"
+#include "lsb_kernels.cuh"
+#include "lsb_setup.hpp"
+
+namespace lsb {
+
+extern thread_local std::string g_last_error;
+
+struct LsbError : std::runtime_error {
+    lsb_status code;
+    LsbError(lsb_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void cuda_check(cudaError_t e, const char* what);
+
+struct Context;
+
+struct ImplBase {
+    virtual ~ImplBase() = default;
+    virtual void setup(Context& c) = 0;
+    virtual void eval(Context& c, bool want_grad) = 0;
+    virtual void minimize(Context& c) = 0;
+    virtual void step(Context& c) = 0;
+    virtual void profile(Context& c, int reps, float* ms) = 0;
+    virtual void invalidate_graphs() = 0;
+};
+std::unique_ptr<ImplBase> make_impl(int precision);
+
+// Batched / second-order engines (lsb_batched.cu, lsb_hessian.cu).
+struct BatchedBase {
+    virtual ~BatchedBase() = default;
+};
+
+struct Context {
+    int precision = LSB_FP64, device = 0, num_sms = 148;
+    size_t wsize = 8;
+    cudaStream_t stream = nullptr;
+    HostMesh mesh;
+    std::vector<double> mass;        // n
+    double total_mass = 0.0;
+    std::vector<double> mu, lambda;  // E
+    double density = 0.0;
+    // decoder (host copy, fp64)
+    int r = 0, n = 0, nhid = 0, h = 0, hp = 0, out_act = 0;
+    std::vector<HostLayer> layers;   // all layers incl. output
+    std::vector<double> shift, scale;
+    int hoff[kMaxLayers] = {}, boff[kMaxLayers] = {}, hrows[kMaxLayers] = {}, hcols[kMaxLayers] = {},
+        hact[kMaxLayers] = {};
+    // objective host mirror
+    std::vector<double> pin_positions;  // V*3
+    bool has_qbar = false;
+    double dt = 0.05;
+
+    // ---- device buffers (T = double or float per precision) ----
+    void* d_Wout = nullptr;  // n x hp
+    void *d_bout = nullptr, *d_sout = nullptr, *d_cout = nullptr, *d_dsout = nullptr;
+    void *d_mass = nullptr, *d_ut = nullptr, *d_rin = nullptr;
+    int* d_vfree = nullptr;
+    int* d_tets = nullptr;
+    void* d_rec = nullptr;
+    void* d_U = nullptr;
+    void* d_forces = nullptr;
+    int *d_csr_ptr = nullptr, *d_csr_ent = nullptr;
+    double *d_Wh = nullptr, *d_WhT = nullptr, *d_bh = nullptr;
+    double* d_a_hid = nullptr;
+    void* d_y_last = nullptr;
+    double *d_e_part_out = nullptr, *d_e_part_elem = nullptr, *d_ybar_part = nullptr, *d_ybar_grp = nullptr;
+    unsigned int* d_grp_cnt = nullptr;
+    DevState* d_state = nullptr;
+    DevState* h_state = nullptr;  // pinned mirror
+    // dynamics
+    double *d_u_state = nullptr, *d_v_state = nullptr, *d_z_state = nullptr, *d_a_ext = nullptr;
+    double* d_pin_disp = nullptr;
+    char* d_vpinned = nullptr;
+    lsb_exit_report* d_reports = nullptr;
+    double* d_z_traj = nullptr;
+    int step_capacity = 0;
+    bool state_set = false;
+    long long* d_launch_acc = nullptr;
+    long long launches = 0;
+    int grid_out = 0, grid_elem = 0, grid_vjp = 0;
+
+    std::unique_ptr<ImplBase> impl;
+    std::unique_ptr<BatchedBase> batched;
+    long long batched_launches = 0;
+    std::vector<void*> allocations;
+
+    ~Context();
+    void* dmalloc(size_t bytes);
+    void alloc_partials(int g_out, int g_elem, int g_vjp, int n_groups);
+    void ensure_step_buffers(int steps);
+    void upload_real(void* dst, const double* src, size_t count);  // converts to wsize
+};
+
+}  // namespace lsb
+
+struct lsb_context {
+    lsb::Context c;
+};

@@ -1,0 +1,125 @@
+"""GPU parity of E(z) and grad E(z) (ReducedObjective::eval, reference
+reduced_solver.cpp:184-202) against the CPU oracle on identical seeded inputs.
+
+Tolerances (north star): rel 1e-10 in fp64 mode, 1e-4 in fp32 mode (norm-wise
+rel_err of reference tests/helpers.hpp:16-18)."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp64": 1e-10, "fp32": 1e-4}
+
+
+def _pair(name, precision, oracle, product):
+    from paper_2409_03807_b200 import configs
+    pr = configs.build(name)
+    sysm = pr.system(precision)
+    ob = oracle.problem(name)
+    return pr, sysm, ob
+
+
+@pytest.mark.parametrize("name,precision", [("c1", "fp64"), ("c1", "fp32"), ("c2", "fp64"), ("c2", "fp32")])
+def test_eval_matches_oracle(name, precision, oracle, product):
+    from paper_2409_03807_b200 import configs
+    pr, sysm, ob = _pair(name, precision, oracle, product)
+    assert np.allclose(sysm.mass, ob.mass, rtol=1e-15, atol=0)
+    qbar = configs.timestep0_qbar(pr, ob.mass)
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    rng = np.random.default_rng(7)
+    worst_e = worst_g = 0.0
+    for trial in range(4):
+        z = 0.5 * rng.standard_normal(pr.model.r) if trial else np.zeros(pr.model.r)
+        g = np.zeros(pr.model.r)
+        E = obj.eval(z, g)
+        Eo, go = ob.eval(z, qbar=qbar, dt=configs.DT)
+        worst_e = max(worst_e, rel_err(E, Eo))
+        worst_g = max(worst_g, rel_err(g, go))
+        assert obj.eval(z) == E  # value-only path gives the same energy
+    assert worst_e < TOL[precision], worst_e
+    assert worst_g < TOL[precision], worst_g
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_quasi_static_potential_and_decode(precision, oracle, product):
+    pr, sysm, ob = _pair("c1", precision, oracle, product)
+    obj = product.ReducedObjective(sysm, None)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        z = 0.7 * rng.standard_normal(pr.model.r)
+        g = np.zeros(pr.model.r)
+        E = obj.eval(z, g)
+        Eo, go = ob.eval(z, qbar=None)
+        assert rel_err(E, Eo) < TOL[precision]
+        assert rel_err(g, go) < TOL[precision]
+        q = sysm.decode(z)
+        assert rel_err(q - ob.decode(np.zeros(pr.model.r)), ob.decode(z) - ob.decode(np.zeros(pr.model.r))) < TOL[precision]
+
+
+def _tiny_problem(oracle, product, act, pinned=True, hidden=2, width=6, r=3, seed=5):
+    """Small explicit mesh + random decoder with non-zero biases and scale != 1."""
+    P = product
+    mesh = P.make_bar_mesh(3, 2, 2, 1.0, 0.4, 0.5, jitter_frac=0.05, seed=seed, pin_left=pinned)
+    rng = np.random.default_rng(seed)
+    n = mesh.num_dofs()
+    dims = [r] + [width] * hidden + [n]
+    layers = []
+    for i in range(len(dims) - 1):
+        W = rng.standard_normal((dims[i + 1], dims[i])) * (0.5 if i < len(dims) - 2 else 0.05)
+        b = rng.standard_normal(dims[i + 1]) * 0.1
+        layers.append(P.Layer(W, b, act if i < len(dims) - 2 else P.Activation.Identity))
+    shift = P.dof_pack(mesh, mesh.vertices) + 0.01 * rng.standard_normal(n)
+    scale = 0.4 + 0.1 * rng.random(n)
+    model = P.SubspaceModel(r, n, layers, shift, scale)
+    mu = 2.0 + rng.random(mesh.num_elements())
+    lam = 1.5 + rng.random(mesh.num_elements())
+    o = oracle.Oracle.from_mesh(mesh.vertices, mesh.elements, mesh.pinned)
+    o.set_material(mu, lam, 5.0)
+    o.set_decoder([(l.W, l.b, int(l.act)) for l in layers], shift, scale, r)
+    return mesh, model, mu, lam, o
+
+
+@pytest.mark.parametrize("act", [1, 2, 3])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_eval_general_decoder(act, precision, oracle, product):
+    P = product
+    mesh, model, mu, lam, o = _tiny_problem(oracle, product, P.Activation(act))
+    sysm = P.ReducedSystem(mesh, mu, lam, 5.0, model, precision)
+    rng = np.random.default_rng(11)
+    qbar = P.dof_pack(mesh, mesh.vertices) + 0.02 * rng.standard_normal(mesh.num_dofs())
+    obj = P.ReducedObjective(sysm, qbar, 0.05)
+    for _ in range(4):
+        z = 0.3 * rng.standard_normal(model.r)
+        g = np.zeros(model.r)
+        E = obj.eval(z, g)
+        Eo, go = o.eval(z, qbar=qbar, dt=0.05)
+        assert rel_err(E, Eo) < TOL[precision]
+        assert rel_err(g, go) < TOL[precision]
+
+
+def test_pinned_positions_enter_energy(oracle, product):
+    P = product
+    mesh, model, mu, lam, o = _tiny_problem(oracle, product, P.Activation.Silu)
+    sysm = P.ReducedSystem(mesh, mu, lam, 5.0, model, "fp64")
+    pins = mesh.vertices.copy()
+    pins[mesh.pinned] += np.array([0.01, -0.02, 0.005])
+    sysm.set_pin_positions(pins)
+    o.set_pins(pins)
+    z = np.array([0.1, -0.2, 0.3])
+    obj = P.ReducedObjective(sysm, None)
+    g = np.zeros(3)
+    E = obj.eval(z, g)
+    Eo, go = o.eval(z, qbar=None)
+    assert rel_err(E, Eo) < 1e-10 and rel_err(g, go) < 1e-10
+
+
+def test_nonfinite_energy_raises(product):
+    P = product
+    mesh = P.make_bar_mesh(2, 2, 2, 1.0, 1.0, 1.0)
+    model = P.make_bar_decoder(mesh, 2, 1, 8, P.Activation.Elu, seed=0, out_scale=1.0)
+    model.decoder[-1].W[:] = 1e200
+    sysm = P.ReducedSystem(mesh, 1.0, 1.0, 1.0, model, "fp64")
+    with pytest.raises(P.LsbError, match="non-finite"):
+        sysm.eval(np.ones(2))
