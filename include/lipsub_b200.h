@@ -172,6 +172,17 @@ lsb_status lsb_get_launch_count(const lsb_context* ctx, long long* launches);
 lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double* ms_out_fwd,
                             double* ms_elem, double* ms_vjp, double* ms_total);
 
+/* K evaluations of the current objective at Z (K*r), each preceded by an L2 flush
+ * (write of flush_bytes) outside the timed interval; per evaluation: device time of
+ * the whole evaluation and of the output-layer kernel (CUDA events on the context
+ * stream), and the energy. */
+lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, double* eval_ms,
+                           double* out_fwd_ms, double* E);
+/* K reduced steps from the current state (lsb_set_state), each preceded by an L2
+ * flush; per step: device time (CUDA events) and exit report. */
+lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg, int quasi_static,
+                           size_t flush_bytes, double* step_ms, lsb_exit_report* reports);
+
 #ifdef __cplusplus
 }
 #endif

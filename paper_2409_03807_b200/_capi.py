@@ -97,6 +97,9 @@ SIGNATURES = [
     ("lsb_eval_batched", C.c_int, [_CTX, C.c_int, _D, _D, _D]),
     ("lsb_hessian_batched", C.c_int, [_CTX, C.c_int, _D, _D]),
     ("lsb_lipschitz_loss", C.c_int, [_CTX, C.c_int, _D, _D, _D]),
+    ("lsb_bench_evals", C.c_int, [_CTX, C.c_int, _D, C.c_size_t, _D, _D, _D]),
+    ("lsb_bench_steps", C.c_int, [_CTX, C.c_int, C.POINTER(lsb_solver_config), C.c_int, C.c_size_t, _D,
+                                  C.POINTER(lsb_exit_report)]),
     ("lsb_get_launch_count", C.c_int, [_CTX, C.POINTER(C.c_longlong)]),
     ("lsb_profile_eval", C.c_int, [_CTX, _D, C.c_int, _D, _D, _D, _D]),
 ]

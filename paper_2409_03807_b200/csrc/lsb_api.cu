@@ -12,6 +12,11 @@
 #include "lsb_batched.hpp"
 #include "lsb_context.hpp"
 
+namespace lsb {
+void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms, double* E);
+void bench_steps(Context& c, int K, size_t flush_bytes, double* step_ms, lsb_exit_report* reps);
+}  // namespace lsb
+
 using namespace lsb;
 
 namespace lsb {
@@ -151,7 +156,7 @@ void upload_pins(Context& c) {
         for (int k = 0; k < 3; ++k) U4[4 * (size_t)v + k] = disp[3 * (size_t)v + k];
     // free rows: keep whatever the last decode wrote (re-uploading zeros is harmless
     // because every evaluation rewrites them before the element pass).
-    c.upload_real(c.d_U, U4.data(), U4.size());
+    cuda_check(cudaMemcpy(c.d_U, U4.data(), U4.size() * 8, cudaMemcpyHostToDevice), "U pins");
 }
 
 }  // namespace
@@ -257,6 +262,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.precision = precision;
         c.device = device;
         c.num_sms = prop.multiProcessorCount;
+        c.l2_bytes = (size_t)prop.l2CacheSize;
         c.wsize = precision == LSB_FP64 ? 8 : 4;
         cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
 
@@ -337,24 +343,24 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
                 std::copy(&o.W[(size_t)i * c.h], &o.W[(size_t)i * c.h] + c.h, &Wp[(size_t)i * c.hp]);
             c.d_Wout = c.dmalloc(Wp.size() * w);
             c.upload_real(c.d_Wout, Wp.data(), Wp.size());
-            c.d_bout = c.dmalloc(n * w);
-            c.upload_real(c.d_bout, o.b.data(), n);
+            c.d_bout = static_cast<double*>(c.dmalloc(n * 8));
+            cuda_check(cudaMemcpy(c.d_bout, o.b.data(), n * 8, cudaMemcpyHostToDevice), "bout");
         }
-        c.d_sout = c.dmalloc(n * w);
-        c.upload_real(c.d_sout, c.scale.data(), n);
+        c.d_sout = static_cast<double*>(c.dmalloc(n * 8));
+        cuda_check(cudaMemcpy(c.d_sout, c.scale.data(), n * 8, cudaMemcpyHostToDevice), "sout");
         {
             std::vector<double> cs(n);
             for (int f = 0; f < m.n_free; ++f)
                 for (int k = 0; k < 3; ++k)
                     cs[3 * f + k] = c.shift[3 * f + k] - m.X[3 * (size_t)m.free_vertex[f] + k];
-            c.d_cout = c.dmalloc(n * w);
-            c.upload_real(c.d_cout, cs.data(), n);
+            c.d_cout = static_cast<double*>(c.dmalloc(n * 8));
+            cuda_check(cudaMemcpy(c.d_cout, cs.data(), n * 8, cudaMemcpyHostToDevice), "cout");
         }
-        c.d_dsout = c.dmalloc(n * w);
-        c.d_mass = c.dmalloc(n * w);
-        c.upload_real(c.d_mass, c.mass.data(), n);
-        c.d_ut = c.dmalloc(n * w);
-        c.d_rin = c.dmalloc(n * w);
+        c.d_dsout = static_cast<double*>(c.dmalloc(n * 8));
+        c.d_mass = static_cast<double*>(c.dmalloc(n * 8));
+        cuda_check(cudaMemcpy(c.d_mass, c.mass.data(), n * 8, cudaMemcpyHostToDevice), "mass");
+        c.d_ut = static_cast<double*>(c.dmalloc(n * 8));
+        c.d_rin = static_cast<double*>(c.dmalloc(n * 8));
         c.d_vfree = static_cast<int*>(c.dmalloc(sizeof(int) * m.n_free));
         cuda_check(cudaMemcpy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice), "vfree");
         c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * (size_t)m.E));
@@ -371,14 +377,14 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             c.d_rec = c.dmalloc(rec.size() * w);
             c.upload_real(c.d_rec, rec.data(), rec.size());
         }
-        c.d_U = c.dmalloc(4 * (size_t)m.V * w);
-        c.d_forces = c.dmalloc(12 * (size_t)m.E * w);
+        c.d_U = static_cast<double*>(c.dmalloc(4 * (size_t)m.V * 8));
+        c.d_forces = static_cast<double*>(c.dmalloc(12 * (size_t)m.E * 8));
         c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
         cuda_check(cudaMemcpy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice), "csr");
         c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
         cuda_check(cudaMemcpy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice), "csr");
         {  // hidden layers, fp64, row-major and transposed
-            std::vector<double> Wh, WhT, bh;
+            std::vector<double> Wh, bh;
             for (int l = 0; l < c.nhid; ++l) {
                 const HostLayer& hl = c.layers[l];
                 c.hoff[l] = (int)Wh.size();
@@ -387,21 +393,17 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
                 c.hcols[l] = hl.cols;
                 c.hact[l] = hl.act;
                 Wh.insert(Wh.end(), hl.W.begin(), hl.W.end());
-                for (int j = 0; j < hl.cols; ++j)
-                    for (int i = 0; i < hl.rows; ++i) WhT.push_back(hl.W[(size_t)i * hl.cols + j]);
                 bh.insert(bh.end(), hl.b.begin(), hl.b.end());
             }
             c.d_Wh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, Wh.size())));
-            c.d_WhT = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, WhT.size())));
             c.d_bh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, bh.size())));
             if (!Wh.empty()) {
                 cuda_check(cudaMemcpy(c.d_Wh, Wh.data(), 8 * Wh.size(), cudaMemcpyHostToDevice), "Wh");
-                cuda_check(cudaMemcpy(c.d_WhT, WhT.data(), 8 * WhT.size(), cudaMemcpyHostToDevice), "WhT");
                 cuda_check(cudaMemcpy(c.d_bh, bh.data(), 8 * bh.size(), cudaMemcpyHostToDevice), "bh");
             }
         }
         c.d_a_hid = static_cast<double*>(c.dmalloc(sizeof(double) * kMaxHidden * std::max(1, c.nhid)));
-        c.d_y_last = c.dmalloc(c.hp * w);
+        c.d_y_last = static_cast<double*>(c.dmalloc(c.hp * 8));
         c.d_state = static_cast<DevState*>(c.dmalloc(sizeof(DevState)));
         cuda_check(cudaMallocHost(&c.h_state, sizeof(DevState)), "pinned state");
         std::memset(c.h_state, 0, sizeof(DevState));
@@ -491,7 +493,7 @@ lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
             for (int f = 0; f < c.mesh.n_free; ++f)
                 for (int k = 0; k < 3; ++k)
                     ut[3 * f + k] = qbar[3 * f + k] - c.mesh.X[3 * (size_t)c.mesh.free_vertex[f] + k];
-            c.upload_real(c.d_ut, ut.data(), ut.size());
+            cuda_check(cudaMemcpy(c.d_ut, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice), "ut");
         }
         c.has_qbar = qbar != nullptr;
         c.dt = dt;
@@ -528,13 +530,7 @@ lsb_status lsb_decode(lsb_context* ctx, const double* z, double* q) {
         sync(c);
         const HostMesh& m = c.mesh;
         std::vector<double> U(4 * (size_t)m.V);
-        if (c.wsize == 8) {
-            cuda_check(cudaMemcpy(U.data(), c.d_U, U.size() * 8, cudaMemcpyDeviceToHost), "U");
-        } else {
-            std::vector<float> Uf(U.size());
-            cuda_check(cudaMemcpy(Uf.data(), c.d_U, U.size() * 4, cudaMemcpyDeviceToHost), "U");
-            for (size_t i = 0; i < U.size(); ++i) U[i] = Uf[i];
-        }
+        cuda_check(cudaMemcpy(U.data(), c.d_U, U.size() * 8, cudaMemcpyDeviceToHost), "U");
         for (int f = 0; f < m.n_free; ++f)
             for (int k = 0; k < 3; ++k)
                 q[3 * f + k] = m.X[3 * (size_t)m.free_vertex[f] + k] + U[4 * (size_t)m.free_vertex[f] + k];
@@ -671,6 +667,28 @@ lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double*
         if (ms_elem) *ms_elem = ms[1];
         if (ms_vjp) *ms_vjp = ms[2];
         if (ms_total) *ms_total = ms[3];
+    });
+}
+
+lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, double* eval_ms,
+                           double* out_fwd_ms, double* E) {
+    return run([&] {
+        check_ctx(ctx);
+        require(K >= 1 && Z && eval_ms && out_fwd_ms, "bench: bad arguments");
+        bench_evals(ctx->c, K, Z, flush_bytes, eval_ms, out_fwd_ms, E);
+    });
+}
+
+lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg, int quasi_static,
+                           size_t flush_bytes, double* step_ms, lsb_exit_report* reports) {
+    return run([&] {
+        check_ctx(ctx);
+        require(K >= 1 && step_ms, "bench: bad arguments");
+        Context& c = ctx->c;
+        prepare_steps(c, K, cfg, quasi_static);
+        bench_steps(c, K, flush_bytes, step_ms, reports);
+        get_state(c);
+        c.launches += 3LL * 0;
     });
 }
 

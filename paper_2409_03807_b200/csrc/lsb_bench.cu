@@ -1,0 +1,66 @@
+// Measurement hooks used by bench.py: per-step CUDA-event timing on the
+// context's stream, with an L2 flush (a write of a buffer larger than L2)
+// before every timed step so W_out is re-read from HBM each step.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "../../include/lipsub_b200.h"
+#include "lsb_context.hpp"
+
+namespace lsb {
+
+void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms,
+                 double* E) {
+    const int r = c.r;
+    double* dZ = nullptr;
+    cuda_check(cudaMalloc(&dZ, sizeof(double) * (size_t)K * r), "bench Z");
+    cuda_check(cudaMemcpy(dZ, Z, sizeof(double) * (size_t)K * r, cudaMemcpyHostToDevice), "bench Z");
+    void* flush = nullptr;
+    if (flush_bytes) cuda_check(cudaMalloc(&flush, flush_bytes), "bench flush");
+    cudaEvent_t ev[4];
+    for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+    for (int k = 0; k < K; ++k) {
+        if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
+        cuda_check(cudaMemcpyAsync(c.d_state->zt, dZ + (size_t)k * r, sizeof(double) * r, cudaMemcpyDeviceToDevice,
+                                   c.stream),
+                   "z");
+        c.impl->eval_timed(c, ev);
+        c.launches += 5;
+        cuda_check(cudaEventSynchronize(ev[3]), "bench sync");
+        float t0, t1;
+        cudaEventElapsedTime(&t0, ev[0], ev[3]);
+        cudaEventElapsedTime(&t1, ev[1], ev[2]);
+        eval_ms[k] = t0;
+        out_ms[k] = t1;
+        if (E) cuda_check(cudaMemcpy(&E[k], &c.d_state->f_eval, sizeof(double), cudaMemcpyDeviceToHost), "E");
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (flush) cudaFree(flush);
+    cudaFree(dZ);
+}
+
+void bench_steps(Context& c, int K, size_t flush_bytes, double* step_ms, lsb_exit_report* reps) {
+    void* flush = nullptr;
+    if (flush_bytes) cuda_check(cudaMalloc(&flush, flush_bytes), "bench flush");
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    for (int k = 0; k < K; ++k) {
+        if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
+        cuda_check(cudaEventRecord(e0, c.stream), "ev");
+        c.impl->step(c);
+        cuda_check(cudaEventRecord(e1, c.stream), "ev");
+        cuda_check(cudaEventSynchronize(e1), "bench sync");
+        float t;
+        cudaEventElapsedTime(&t, e0, e1);
+        step_ms[k] = t;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (flush) cudaFree(flush);
+    if (reps) cuda_check(cudaMemcpy(reps, c.d_reports, sizeof(lsb_exit_report) * K, cudaMemcpyDeviceToHost), "reports");
+}
+
+}  // namespace lsb

@@ -92,7 +92,7 @@ struct alignas(32) D4 { double v[4]; };
 
 __device__ __forceinline__ F8 ld_stream(const F8* p) {
     F8 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
                    "=f"(r.v[6]), "=f"(r.v[7])
                  : "l"(p));
@@ -100,10 +100,35 @@ __device__ __forceinline__ F8 ld_stream(const F8* p) {
 }
 __device__ __forceinline__ D4 ld_stream(const D4* p) {
     D4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
                  : "l"(p));
     return r;
+}
+
+// ---- asynchronous global -> shared staging (LDGSTS): issue everything, wait once ----------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// Block-cooperative copy of `count` doubles (8-byte aligned) into shared memory.
+__device__ __forceinline__ void stage_doubles(double* dst, const double* src, int count) {
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+    if (((sa ^ da) & 15u) == 0) {
+        const int head = (sa & 15u) ? 1 : 0;
+        if (head && threadIdx.x == 0 && count > 0) cp_async8(dst, src);
+        const int body = (count - head) / 2;
+        for (int k = threadIdx.x; k < body; k += blockDim.x) cp_async16(dst + head + 2 * k, src + head + 2 * k);
+        const int tail = head + 2 * body;
+        if (tail < count && threadIdx.x == 0) cp_async8(dst + tail, src + tail);
+    } else {
+        for (int k = threadIdx.x; k < count; k += blockDim.x) cp_async8(dst + k, src + k);
+    }
 }
 
 template <typename T> struct VecT;

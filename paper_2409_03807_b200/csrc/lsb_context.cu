@@ -37,16 +37,14 @@ void cuda_check(cudaError_t e, const char* what) {
 // ------------------------------------------------------------------ dynamics kernels
 // qbar - X for the step (reduced_solver.cpp:249-254), warm start z (:256).
 __global__ void prep_step_kernel(int n, const int* vfree, const double* u_state, const double* v_state,
-                                 const double* a_ext, const double* z_state, int r, DevState* st, void* ut_out,
-                                 int fp32) {
+                                 const double* a_ext, const double* z_state, int r, DevState* st, double* ut_out) {
     const double dt = st->dt;
     const int quasi = st->quasi_static;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int f = i / 3, c = i - 3 * f;
         const size_t vi = (size_t)vfree[f] * 3 + c;
         const double ut = u_state[vi] + dt * v_state[vi] + (dt * dt) * a_ext[i];
-        if (fp32) static_cast<float*>(ut_out)[i] = quasi ? 0.f : (float)ut;
-        else static_cast<double*>(ut_out)[i] = quasi ? 0.0 : ut;
+        ut_out[i] = quasi ? 0.0 : ut;
     }
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < r; i += blockDim.x) st->zt[i] = z_state[i];
@@ -58,7 +56,7 @@ __global__ void prep_step_kernel(int n, const int* vfree, const double* u_state,
 }
 
 // x' = unpack(decode(z*)), v' = (x' - x) / dt over all V rows (:266-276), report.
-__global__ void finalize_step_kernel(int V, const void* U, int fp32, const char* vpinned, const double* pin_disp,
+__global__ void finalize_step_kernel(int V, const double* U, const char* vpinned, const double* pin_disp,
                                      double* u_state, double* v_state, double* z_state, int r, DevState* st) {
     lsb_exit_report* reports = static_cast<lsb_exit_report*>(st->reports);
     double* z_traj = st->z_traj;
@@ -69,8 +67,7 @@ __global__ void finalize_step_kernel(int V, const void* U, int fp32, const char*
             const size_t k = (size_t)v * 3 + c;
             double un;
             if (vpinned[v]) un = pin_disp[k];
-            else un = fp32 ? (double)static_cast<const float*>(U)[(size_t)v * 4 + c]
-                           : static_cast<const double*>(U)[(size_t)v * 4 + c];
+            else un = U[(size_t)v * 4 + c];
             v_state[k] = quasi ? 0.0 : (un - u_state[k]) / dt;
             u_state[k] = un;
         }
@@ -98,45 +95,79 @@ __global__ void finalize_step_kernel(int V, const void* U, int fp32, const char*
 }
 
 __global__ void count_loop_kernel(const DevState* st, long long* acc) {
-    // device-side launch accounting for WHILE-loop bodies: 3 kernels per body
-    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += 3LL * st->loop_iters;
+    // device-side launch accounting for WHILE-loop bodies: 4 kernels per body
+    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += 4LL * st->loop_iters;
 }
 
-// ------------------------------------------------------------------ Impl<T>
-template <typename T>
+// ------------------------------------------------------------------ Impl<TS>
+template <typename TS>
 struct KernelSet {
-    void (*out_fwd)(const EvalParams<T>);
-    void (*vjp)(const EvalParams<T>);
+    void (*out_fwd)(const EvalParams<TS>);
+    void (*vjp)(const EvalParams<TS>);
 };
 
-template <typename T, int HP>
-KernelSet<T> kernels_for() {
-    return {out_fwd_kernel<T, HP>, vjp_ctrl_kernel<T, HP>};
+template <typename TS, int HP>
+KernelSet<TS> kernels_for() {
+    return {out_fwd_kernel<TS, HP>, vjp_kernel<TS, HP>};
 }
 
-template <typename T>
-KernelSet<T> select_kernels(int hp) {
+template <typename TS>
+KernelSet<TS> select_kernels(int hp) {
     switch (hp) {
-        case 32: return kernels_for<T, 32>();
-        case 64: return kernels_for<T, 64>();
-        case 128: return kernels_for<T, 128>();
-        case 256: return kernels_for<T, 256>();
-        case 512: return kernels_for<T, 512>();
+        case 32: return kernels_for<TS, 32>();
+        case 64: return kernels_for<TS, 64>();
+        case 128: return kernels_for<TS, 128>();
+        case 256: return kernels_for<TS, 256>();
+        case 512: return kernels_for<TS, 512>();
     }
     throw LsbError(LSB_EINVAL, "decoder: unsupported padded width");
 }
 
-template <typename T>
+using CtrlFn = void (*)(int, int, int);  // placeholder type for table entries
+
+template <typename TS>
 struct Impl final : ImplBase {
-    EvalParams<T> p{};
-    KernelSet<T> ks{};
-    size_t vjp_smem = 0, start_smem = 0;
-    cudaGraphExec_t g_min = nullptr, g_step = nullptr;
+    EvalParams<TS> p{};
+    KernelSet<TS> ks{};
+    void (*ctrl)(const EvalParams<TS>, int, int, int) = nullptr;
+    size_t vjp_smem = 0, ctrl_smem = 0;
+    int cs = 8;
+    cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_timed = nullptr;
+    cudaEvent_t timed_ev[4] = {};
     cudaGraphConditionalHandle h_min{}, h_step{};
 
     ~Impl() override {
         if (g_min) cudaGraphExecDestroy(g_min);
         if (g_step) cudaGraphExecDestroy(g_step);
+        if (g_timed) cudaGraphExecDestroy(g_timed);
+    }
+
+    void eval_timed(Context& c, cudaEvent_t* ev) override {
+        if (!g_timed || ev[0] != timed_ev[0]) {
+            if (g_timed) cudaGraphExecDestroy(g_timed);
+            for (int k = 0; k < 4; ++k) timed_ev[k] = ev[k];
+            cudaGraph_t g;
+            cuda_check(cudaGraphCreate(&g, 0), "graph create");
+            cudaGraphNode_t e0, e1, e2, e3;
+            cuda_check(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ev[0]), "event node");
+            int cm = kCtrlStart, mode = kModeEval, want = 1;
+            EvalParams<TS> pg = p;
+            void* sargs[] = {&pg, &cm, &mode, &want};
+            cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs);
+            cuda_check(cudaGraphAddEventRecordNode(&e1, g, &n0, 1, ev[1]), "event node");
+            void* a1[] = {&pg};
+            cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, 0, a1);
+            cuda_check(cudaGraphAddEventRecordNode(&e2, g, &n1, 1, ev[2]), "event node");
+            cudaGraphNode_t n2 = add_kernel(g, e2, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
+            cudaGraphNode_t n3 = add_kernel(g, n2, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1);
+            int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
+            void* a4[] = {&pg, &cm2, &z0, &z1};
+            cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4);
+            cuda_check(cudaGraphAddEventRecordNode(&e3, g, &n4, 1, ev[3]), "event node");
+            cuda_check(cudaGraphInstantiate(&g_timed, g, 0), "graph instantiate (timed eval)");
+            cudaGraphDestroy(g);
+        }
+        cuda_check(cudaGraphLaunch(g_timed, c.stream), "graph launch (timed eval)");
     }
 
     void setup(Context& c) override {
@@ -150,23 +181,22 @@ struct Impl final : ImplBase {
         p.h = c.h;
         p.hp = c.hp;
         p.out_act = c.out_act;
-        p.Wout = static_cast<const T*>(c.d_Wout);
-        p.bout = static_cast<const T*>(c.d_bout);
-        p.sout = static_cast<const T*>(c.d_sout);
-        p.cout = static_cast<const T*>(c.d_cout);
-        p.dsout = static_cast<T*>(c.d_dsout);
-        p.mass = static_cast<const T*>(c.d_mass);
-        p.ut = static_cast<const T*>(c.d_ut);
-        p.rin = static_cast<T*>(c.d_rin);
+        p.Wout = static_cast<const TS*>(c.d_Wout);
+        p.bout = c.d_bout;
+        p.sout = c.d_sout;
+        p.cout = c.d_cout;
+        p.dsout = c.d_dsout;
+        p.mass = c.d_mass;
+        p.ut = c.d_ut;
+        p.rin = c.d_rin;
         p.vfree = c.d_vfree;
         p.tets = reinterpret_cast<const int4*>(c.d_tets);
-        p.rec = static_cast<const T*>(c.d_rec);
-        p.U = static_cast<T*>(c.d_U);
-        p.forces = static_cast<T*>(c.d_forces);
+        p.rec = static_cast<const TS*>(c.d_rec);
+        p.U = c.d_U;
+        p.forces = c.d_forces;
         p.csr_ptr = c.d_csr_ptr;
         p.csr_ent = c.d_csr_ent;
         p.Wh = c.d_Wh;
-        p.WhT = c.d_WhT;
         p.bh = c.d_bh;
         for (int l = 0; l < c.nhid; ++l) {
             p.hoff[l] = c.hoff[l];
@@ -176,18 +206,20 @@ struct Impl final : ImplBase {
             p.hact[l] = c.hact[l];
         }
         p.a_hid = c.d_a_hid;
-        p.y_last = static_cast<T*>(c.d_y_last);
+        p.y_last = c.d_y_last;
         p.st = c.d_state;
-        ks = select_kernels<T>(c.hp);
+        ks = select_kernels<TS>(c.hp);
+        // W_out stays L2-resident when it fits in ~60% of L2, else it is streamed
+        const size_t wbytes = (size_t)c.n * c.hp * sizeof(TS);
+        p.w_resident = wbytes <= (size_t)(0.6 * c.l2_bytes) ? 1 : 0;
         // grid sizing: persistent grids of (SMs x resident blocks)
         int occ = 0;
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.out_fwd, 256, 0), "occupancy out_fwd");
         p.grid_out = std::max(1, c.num_sms * std::max(1, occ));
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<T>, 256, 0), "occupancy elem");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<TS>, 256, 0), "occupancy elem");
         p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.num_sms * std::max(1, occ)));
         p.vpb = 64;
-        vjp_smem = std::max<size_t>(8 * (size_t)c.hp * sizeof(double) + 3 * p.vpb * sizeof(T),
-                                    2 * kMaxHidden * sizeof(double));
+        vjp_smem = 8 * (size_t)c.hp * sizeof(double) + 3 * p.vpb * sizeof(double);
         cuda_check(cudaFuncSetAttribute(ks.vjp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjp_smem),
                    "smem attr vjp");
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, 256, vjp_smem), "occupancy vjp");
@@ -195,7 +227,32 @@ struct Impl final : ImplBase {
         p.grid_vjp = std::max(1, std::min(nslab, c.num_sms * std::max(1, occ)));
         p.group = 16;
         p.n_groups = (p.grid_vjp + p.group - 1) / p.group;
-        start_smem = 2 * kMaxHidden * sizeof(double);
+        // control cluster: hidden weights split in row slices over cs CTAs
+        size_t wtot = 0;
+        int maxrows = 0;
+        for (int l = 0; l < c.nhid; ++l) {
+            wtot += (size_t)c.hrows[l] * c.hcols[l];
+            maxrows = std::max(maxrows, c.hrows[l]);
+        }
+        const size_t fixed = (3 * kMaxHidden + 128 + 2 * kMaxLayers * 64) * sizeof(double) + sizeof(DevState) + 64;
+        auto slice_words = [&](int k) {
+            size_t w = 0;
+            for (int l = 0; l < c.nhid; ++l) w += (((size_t)((c.hrows[l] + k - 1) / k) * c.hcols[l] + 1) & ~(size_t)1);
+            return w;
+        };
+        cs = 8;
+        if (slice_words(8) * 8 + fixed > 200 * 1024 || (maxrows + 7) / 8 > 64) cs = 16;
+        if (slice_words(cs) * 8 + fixed > 220 * 1024 || (maxrows + cs - 1) / cs > 64)
+            throw LsbError(LSB_EINVAL, "decoder: hidden layers too large for the control cluster");
+        p.cs = cs;
+        p.ctrl_smem_w = (int)slice_words(cs);
+        ctrl_smem = p.ctrl_smem_w * sizeof(double) + fixed;
+        ctrl = cs == 8 ? ctrl_kernel<TS, 8> : ctrl_kernel<TS, 16>;
+        if (cs == 16)
+            cuda_check(cudaFuncSetAttribute(ctrl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
+        cuda_check(cudaFuncSetAttribute(ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem),
+                   "smem attr ctrl");
+        (void)wtot;
         c.grid_out = p.grid_out;
         c.grid_elem = p.grid_elem;
         c.grid_vjp = p.grid_vjp;
@@ -208,17 +265,22 @@ struct Impl final : ImplBase {
         p.in_graph = 0;
     }
 
+    void launch_ctrl(cudaStream_t s, int cmode, int smode, int want) {
+        ctrl<<<cs, 256, ctrl_smem, s>>>(p, cmode, smode, want);
+    }
+
     // One evaluation body, stream-launched (non-graph path).
     void launch_eval_body(cudaStream_t s, Context& c) {
         ks.out_fwd<<<p.grid_out, 256, 0, s>>>(p);
-        elem_kernel<T><<<p.grid_elem, 256, 0, s>>>(p);
+        elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
         ks.vjp<<<p.grid_vjp, 256, vjp_smem, s>>>(p);
-        c.launches += 3;
+        launch_ctrl(s, kCtrlAfterEval, 0, 0);
+        c.launches += 4;
     }
 
     void eval(Context& c, bool want_grad) override {
         cudaStream_t s = c.stream;
-        start_kernel<T><<<1, 256, start_smem, s>>>(p, kModeEval, want_grad ? 1 : 0);
+        launch_ctrl(s, kCtrlStart, kModeEval, want_grad ? 1 : 0);
         c.launches += 1;
         launch_eval_body(s, c);
         cuda_check(cudaGetLastError(), "eval launch");
@@ -226,21 +288,23 @@ struct Impl final : ImplBase {
 
     void profile(Context& c, int reps, float* ms) override {
         cudaStream_t s = c.stream;
-        cudaEvent_t ev[5];
+        cudaEvent_t ev[6];
         for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
-        double acc[4] = {0, 0, 0, 0};
+        double acc[5] = {0, 0, 0, 0, 0};
         for (int it = 0; it < reps; ++it) {
             cudaEventRecord(ev[0], s);
-            start_kernel<T><<<1, 256, start_smem, s>>>(p, kModeEval, 1);
+            launch_ctrl(s, kCtrlStart, kModeEval, 1);
             cudaEventRecord(ev[1], s);
             ks.out_fwd<<<p.grid_out, 256, 0, s>>>(p);
             cudaEventRecord(ev[2], s);
-            elem_kernel<T><<<p.grid_elem, 256, 0, s>>>(p);
+            elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
             cudaEventRecord(ev[3], s);
             ks.vjp<<<p.grid_vjp, 256, vjp_smem, s>>>(p);
             cudaEventRecord(ev[4], s);
-            c.launches += 4;
-            cuda_check(cudaEventSynchronize(ev[4]), "profile sync");
+            launch_ctrl(s, kCtrlAfterEval, 0, 0);
+            cudaEventRecord(ev[5], s);
+            c.launches += 5;
+            cuda_check(cudaEventSynchronize(ev[5]), "profile sync");
             float t;
             cudaEventElapsedTime(&t, ev[1], ev[2]);
             acc[0] += t;
@@ -248,14 +312,28 @@ struct Impl final : ImplBase {
             acc[1] += t;
             cudaEventElapsedTime(&t, ev[3], ev[4]);
             acc[2] += t;
-            cudaEventElapsedTime(&t, ev[0], ev[4]);
+            cudaEventElapsedTime(&t, ev[4], ev[5]);
             acc[3] += t;
+            cudaEventElapsedTime(&t, ev[0], ev[5]);
+            acc[4] += t;
         }
-        for (int k = 0; k < 4; ++k) ms[k] = (float)(acc[k] / reps);
+        for (int k = 0; k < 5; ++k) ms[k] = (float)(acc[k] / reps);
         for (auto& e : ev) cudaEventDestroy(e);
     }
 
-    // WHILE(cond){ out_fwd -> elem -> vjp_ctrl } appended after `dep`.
+    cudaGraphNode_t add_kernel(cudaGraph_t g, cudaGraphNode_t dep, void* fn, int grid, size_t smem, void** args) {
+        cudaKernelNodeParams kp = {};
+        kp.func = fn;
+        kp.gridDim = dim3(grid);
+        kp.blockDim = dim3(256);
+        kp.sharedMemBytes = (unsigned)smem;
+        kp.kernelParams = args;
+        cudaGraphNode_t nd;
+        cuda_check(cudaGraphAddKernelNode(&nd, g, dep ? &dep : nullptr, dep ? 1 : 0, &kp), "kernel node");
+        return nd;
+    }
+
+    // WHILE(cond){ out_fwd -> elem -> vjp -> ctrl } appended after `dep`.
     cudaGraphNode_t add_while(cudaGraph_t graph, cudaGraphNode_t dep, cudaGraphConditionalHandle* handle) {
         cuda_check(cudaGraphConditionalHandleCreate(handle, graph, 1, cudaGraphCondAssignDefault), "cond handle");
         cudaGraphNodeParams cp = {};
@@ -266,50 +344,31 @@ struct Impl final : ImplBase {
         cudaGraphNode_t wnode;
         cuda_check(cudaGraphAddNode(&wnode, graph, dep ? &dep : nullptr, dep ? 1 : 0, &cp), "while node");
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        EvalParams<T> pg = p;
+        EvalParams<TS> pg = p;
         pg.in_graph = 1;
         pg.cond = *handle;
-        // kernel params are copied at node creation
-        void* args[] = {&pg};
-        cudaKernelNodeParams kp = {};
-        kp.kernelParams = args;
-        kp.blockDim = dim3(256);
-        cudaGraphNode_t n1, n2, n3;
-        kp.func = (void*)ks.out_fwd;
-        kp.gridDim = dim3(p.grid_out);
-        kp.sharedMemBytes = 0;
-        cuda_check(cudaGraphAddKernelNode(&n1, body, nullptr, 0, &kp), "node out_fwd");
-        kp.func = (void*)elem_kernel<T>;
-        kp.gridDim = dim3(p.grid_elem);
-        cuda_check(cudaGraphAddKernelNode(&n2, body, &n1, 1, &kp), "node elem");
-        kp.func = (void*)ks.vjp;
-        kp.gridDim = dim3(p.grid_vjp);
-        kp.sharedMemBytes = (unsigned)vjp_smem;
-        cuda_check(cudaGraphAddKernelNode(&n3, body, &n2, 1, &kp), "node vjp");
+        void* a1[] = {&pg};
+        int cm = kCtrlAfterEval, z0 = 0, z1 = 0;
+        void* a4[] = {&pg, &cm, &z0, &z1};
+        cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, 0, a1);
+        cudaGraphNode_t n2 = add_kernel(body, n1, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
+        cudaGraphNode_t n3 = add_kernel(body, n2, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1);
+        add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4);
         return wnode;
     }
 
     cudaGraphNode_t add_start(cudaGraph_t graph, cudaGraphNode_t dep) {
-        int mode = kModeLbfgs, want = 1;
-        EvalParams<T> pg = p;
-        void* args[] = {&pg, &mode, &want};
-        cudaKernelNodeParams kp = {};
-        kp.func = (void*)start_kernel<T>;
-        kp.gridDim = dim3(1);
-        kp.blockDim = dim3(256);
-        kp.sharedMemBytes = (unsigned)start_smem;
-        kp.kernelParams = args;
-        cudaGraphNode_t nd;
-        cuda_check(cudaGraphAddKernelNode(&nd, graph, dep ? &dep : nullptr, dep ? 1 : 0, &kp), "node start");
-        return nd;
+        int cm = kCtrlStart, mode = kModeLbfgs, want = 1;
+        EvalParams<TS> pg = p;
+        void* args[] = {&pg, &cm, &mode, &want};
+        return add_kernel(graph, dep, (void*)ctrl, cs, ctrl_smem, args);
     }
 
     void build_min_graph(Context& c) {
         cudaGraph_t g;
         cuda_check(cudaGraphCreate(&g, 0), "graph create");
         cudaGraphNode_t st = add_start(g, nullptr);
-        cudaGraphNode_t w = add_while(g, st, &h_min);
-        (void)w;
+        add_while(g, st, &h_min);
         cuda_check(cudaGraphInstantiate(&g_min, g, 0), "graph instantiate (minimize)");
         cudaGraphDestroy(g);
     }
@@ -320,41 +379,30 @@ struct Impl final : ImplBase {
         const int threads = 256;
         const int grid_n = std::max(1, std::min((p.n + threads - 1) / threads, c.num_sms * 8));
         const int grid_v = std::max(1, std::min((p.V + threads - 1) / threads, c.num_sms * 8));
-        // prep
-        int n = p.n, r = p.r, fp32 = sizeof(T) == 4 ? 1 : 0, V = p.V;
+        int n = p.n, r = p.r, V = p.V;
         const int* vfree = p.vfree;
         const double* u_state = c.d_u_state;
         const double* v_state = c.d_v_state;
         const double* a_ext = c.d_a_ext;
         const double* z_state = c.d_z_state;
         DevState* st = c.d_state;
-        void* ut = c.d_ut;
-        void* a_prep[] = {&n, &vfree, &u_state, &v_state, &a_ext, &z_state, &r, &st, &ut, &fp32};
-        cudaKernelNodeParams kp = {};
-        kp.func = (void*)prep_step_kernel;
-        kp.gridDim = dim3(grid_n);
-        kp.blockDim = dim3(threads);
-        kp.kernelParams = a_prep;
-        cudaGraphNode_t n_prep;
-        cuda_check(cudaGraphAddKernelNode(&n_prep, g, nullptr, 0, &kp), "node prep");
+        double* ut = c.d_ut;
+        void* a_prep[] = {&n, &vfree, &u_state, &v_state, &a_ext, &z_state, &r, &st, &ut};
+        cudaGraphNode_t n_prep = add_kernel(g, nullptr, (void*)prep_step_kernel, grid_n, 0, a_prep);
         cudaGraphNode_t n_start = add_start(g, n_prep);
         cudaGraphNode_t n_while = add_while(g, n_start, &h_step);
-        // finalize
-        const void* U = c.d_U;
+        const double* U = c.d_U;
         const char* vpinned = c.d_vpinned;
         const double* pin_disp = c.d_pin_disp;
         double* u_st = c.d_u_state;
         double* v_st = c.d_v_state;
         double* z_st = c.d_z_state;
-        void* a_fin[] = {&V, &U, &fp32, &vpinned, &pin_disp, &u_st, &v_st, &z_st, &r, &st};
-        kp.func = (void*)finalize_step_kernel;
-        kp.gridDim = dim3(grid_v);
-        kp.kernelParams = a_fin;
-        cudaGraphNode_t n_fin;
-        cuda_check(cudaGraphAddKernelNode(&n_fin, g, &n_while, 1, &kp), "node finalize");
+        void* a_fin[] = {&V, &U, &vpinned, &pin_disp, &u_st, &v_st, &z_st, &r, &st};
+        cudaGraphNode_t n_fin = add_kernel(g, n_while, (void*)finalize_step_kernel, grid_v, 0, a_fin);
         long long* acc = c.d_launch_acc;
         const DevState* cst = c.d_state;
         void* a_cnt[] = {&cst, &acc};
+        cudaKernelNodeParams kp = {};
         kp.func = (void*)count_loop_kernel;
         kp.gridDim = dim3(1);
         kp.blockDim = dim3(32);
@@ -368,7 +416,7 @@ struct Impl final : ImplBase {
     void minimize(Context& c) override {
         if (!g_min) build_min_graph(c);
         cuda_check(cudaGraphLaunch(g_min, c.stream), "graph launch (minimize)");
-        c.launches += 1;  // start kernel; loop bodies are counted from st->loop_iters
+        c.launches += 1;  // start; loop bodies are counted from st->loop_iters
     }
 
     void step(Context& c) override {

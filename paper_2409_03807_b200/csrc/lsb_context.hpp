@@ -34,6 +34,9 @@ struct ImplBase {
     virtual void step(Context& c) = 0;
     virtual void profile(Context& c, int reps, float* ms) = 0;
     virtual void invalidate_graphs() = 0;
+    // One evaluation at st->zt as a graph with event-record nodes:
+    // ev[0] | ctrl(start) | ev[1] | out_fwd | ev[2] | elem, vjp, ctrl | ev[3]
+    virtual void eval_timed(Context& c, cudaEvent_t* ev) = 0;
 };
 std::unique_ptr<ImplBase> make_impl(int precision);
 
@@ -62,19 +65,20 @@ struct Context {
     bool has_qbar = false;
     double dt = 0.05;
 
-    // ---- device buffers (T = double or float per precision) ----
+    // ---- device buffers: W_out and rec in the storage precision (wsize), rest fp64 ----
     void* d_Wout = nullptr;  // n x hp
-    void *d_bout = nullptr, *d_sout = nullptr, *d_cout = nullptr, *d_dsout = nullptr;
-    void *d_mass = nullptr, *d_ut = nullptr, *d_rin = nullptr;
+    double *d_bout = nullptr, *d_sout = nullptr, *d_cout = nullptr, *d_dsout = nullptr;
+    double *d_mass = nullptr, *d_ut = nullptr, *d_rin = nullptr;
     int* d_vfree = nullptr;
     int* d_tets = nullptr;
     void* d_rec = nullptr;
-    void* d_U = nullptr;
-    void* d_forces = nullptr;
+    double* d_U = nullptr;
+    double* d_forces = nullptr;
     int *d_csr_ptr = nullptr, *d_csr_ent = nullptr;
-    double *d_Wh = nullptr, *d_WhT = nullptr, *d_bh = nullptr;
+    double *d_Wh = nullptr, *d_bh = nullptr;
     double* d_a_hid = nullptr;
-    void* d_y_last = nullptr;
+    double* d_y_last = nullptr;
+    size_t l2_bytes = 126u << 20;
     double *d_e_part_out = nullptr, *d_e_part_elem = nullptr, *d_ybar_part = nullptr, *d_ybar_grp = nullptr;
     unsigned int* d_grp_cnt = nullptr;
     DevState* d_state = nullptr;
