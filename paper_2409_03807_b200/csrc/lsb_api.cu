@@ -359,8 +359,25 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.d_dsout = static_cast<double*>(c.dmalloc(n * 8));
         c.d_mass = static_cast<double*>(c.dmalloc(n * 8));
         cuda_check(cudaMemcpy(c.d_mass, c.mass.data(), n * 8, cudaMemcpyHostToDevice), "mass");
-        c.d_ut = static_cast<double*>(c.dmalloc(n * 8));
+        c.d_ut = static_cast<double*>(c.dmalloc((n + 2) * 8));  // +2: 16-byte TMA tails
         c.d_rin = static_cast<double*>(c.dmalloc(n * 8));
+        c.d_tv = static_cast<double*>(c.dmalloc((n + 2) * 8));
+        {  // per-row side data staged with every W_out tile
+            std::vector<double> ep(6 * (size_t)n, 0.0);
+            const HostLayer& o = c.layers[L - 1];
+            for (int f = 0; f < m.n_free; ++f)
+                for (int k = 0; k < 3; ++k) {
+                    const int i = 3 * f + k;
+                    ep[6 * (size_t)i + 0] = o.b[i];
+                    ep[6 * (size_t)i + 1] = c.scale[i];
+                    ep[6 * (size_t)i + 2] = c.shift[i] - m.X[3 * (size_t)m.free_vertex[f] + k];
+                    ep[6 * (size_t)i + 3] = c.mass[i];
+                    ep[6 * (size_t)i + 4] = (double)(4 * m.free_vertex[f] + k);
+                }
+            c.h_eprow = ep;
+            c.d_eprow = static_cast<double*>(c.dmalloc(ep.size() * 8));
+            cuda_check(cudaMemcpy(c.d_eprow, ep.data(), ep.size() * 8, cudaMemcpyHostToDevice), "eprow");
+        }
         c.d_vfree = static_cast<int*>(c.dmalloc(sizeof(int) * m.n_free));
         cuda_check(cudaMemcpy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice), "vfree");
         c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * (size_t)m.E));
@@ -494,6 +511,8 @@ lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
                 for (int k = 0; k < 3; ++k)
                     ut[3 * f + k] = qbar[3 * f + k] - c.mesh.X[3 * (size_t)c.mesh.free_vertex[f] + k];
             cuda_check(cudaMemcpy(c.d_ut, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice), "ut");
+            for (int i = 0; i < c.n; ++i) c.h_eprow[6 * (size_t)i + 5] = ut[i];
+            cuda_check(cudaMemcpy(c.d_eprow, c.h_eprow.data(), c.h_eprow.size() * 8, cudaMemcpyHostToDevice), "eprow");
         }
         c.has_qbar = qbar != nullptr;
         c.dt = dt;

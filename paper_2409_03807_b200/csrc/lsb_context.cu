@@ -13,6 +13,7 @@
 
 #include "../../include/lipsub_b200.h"
 #include "lsb_context.hpp"
+#include "lsb_stream.cuh"
 
 namespace lsb {
 
@@ -37,7 +38,8 @@ void cuda_check(cudaError_t e, const char* what) {
 // ------------------------------------------------------------------ dynamics kernels
 // qbar - X for the step (reduced_solver.cpp:249-254), warm start z (:256).
 __global__ void prep_step_kernel(int n, const int* vfree, const double* u_state, const double* v_state,
-                                 const double* a_ext, const double* z_state, int r, DevState* st, double* ut_out) {
+                                 const double* a_ext, const double* z_state, int r, DevState* st, double* ut_out,
+                                 double* eprow) {
     const double dt = st->dt;
     const int quasi = st->quasi_static;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -45,6 +47,7 @@ __global__ void prep_step_kernel(int n, const int* vfree, const double* u_state,
         const size_t vi = (size_t)vfree[f] * 3 + c;
         const double ut = u_state[vi] + dt * v_state[vi] + (dt * dt) * a_ext[i];
         ut_out[i] = quasi ? 0.0 : ut;
+        eprow[6 * (size_t)i + 5] = quasi ? 0.0 : ut;
     }
     if (blockIdx.x == 0) {
         for (int i = threadIdx.x; i < r; i += blockDim.x) st->zt[i] = z_state[i];
@@ -95,8 +98,8 @@ __global__ void finalize_step_kernel(int V, const double* U, const char* vpinned
 }
 
 __global__ void count_loop_kernel(const DevState* st, long long* acc) {
-    // device-side launch accounting for WHILE-loop bodies: 4 kernels per body
-    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += 4LL * st->loop_iters;
+    // device-side launch accounting for WHILE-loop bodies: 5 kernels per body
+    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += 5LL * st->loop_iters;
 }
 
 // ------------------------------------------------------------------ Impl<TS>
@@ -104,21 +107,34 @@ template <typename TS>
 struct KernelSet {
     void (*out_fwd)(const EvalParams<TS>);
     void (*vjp)(const EvalParams<TS>);
+    size_t smem;      // dynamic smem of both streaming kernels (ring + scratch)
+    int tile_rows;
 };
 
 template <typename TS, int HP>
 KernelSet<TS> kernels_for() {
-    return {out_fwd_kernel<TS, HP>, vjp_kernel<TS, HP>};
+    return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
+            StreamCfg<TS, HP>::TR};
 }
 
 template <typename TS>
-KernelSet<TS> select_kernels(int hp) {
+KernelSet<TS> select_kernels(int hp);
+template <>
+KernelSet<float> select_kernels<float>(int hp) {
     switch (hp) {
-        case 32: return kernels_for<TS, 32>();
-        case 64: return kernels_for<TS, 64>();
-        case 128: return kernels_for<TS, 128>();
-        case 256: return kernels_for<TS, 256>();
-        case 512: return kernels_for<TS, 512>();
+        case 128: return kernels_for<float, 128>();
+        case 256: return kernels_for<float, 256>();
+        case 512: return kernels_for<float, 512>();
+    }
+    throw LsbError(LSB_EINVAL, "decoder: unsupported padded width");
+}
+template <>
+KernelSet<double> select_kernels<double>(int hp) {
+    switch (hp) {
+        case 64: return kernels_for<double, 64>();
+        case 128: return kernels_for<double, 128>();
+        case 256: return kernels_for<double, 256>();
+        case 512: return kernels_for<double, 512>();
     }
     throw LsbError(LSB_EINVAL, "decoder: unsupported padded width");
 }
@@ -130,7 +146,8 @@ struct Impl final : ImplBase {
     EvalParams<TS> p{};
     KernelSet<TS> ks{};
     void (*ctrl)(const EvalParams<TS>, int, int, int) = nullptr;
-    size_t vjp_smem = 0, ctrl_smem = 0;
+    size_t vjp_smem = 0, ctrl_smem = 0, out_smem = 0;
+    int grid_gather = 1;
     int cs = 8;
     cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_timed = nullptr;
     cudaEvent_t timed_ev[4] = {};
@@ -156,10 +173,11 @@ struct Impl final : ImplBase {
             cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs);
             cuda_check(cudaGraphAddEventRecordNode(&e1, g, &n0, 1, ev[1]), "event node");
             void* a1[] = {&pg};
-            cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, 0, a1);
+            cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
             cuda_check(cudaGraphAddEventRecordNode(&e2, g, &n1, 1, ev[2]), "event node");
             cudaGraphNode_t n2 = add_kernel(g, e2, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-            cudaGraphNode_t n3 = add_kernel(g, n2, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1);
+            cudaGraphNode_t n2b = add_kernel(g, n2, (void*)gather_kernel<TS>, grid_gather, 0, a1);
+            cudaGraphNode_t n3 = add_kernel(g, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
             int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
             void* a4[] = {&pg, &cm2, &z0, &z1};
             cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4);
@@ -189,6 +207,8 @@ struct Impl final : ImplBase {
         p.mass = c.d_mass;
         p.ut = c.d_ut;
         p.rin = c.d_rin;
+        p.eprow = c.d_eprow;
+        p.tv = c.d_tv;
         p.vfree = c.d_vfree;
         p.tets = reinterpret_cast<const int4*>(c.d_tets);
         p.rec = static_cast<const TS*>(c.d_rec);
@@ -214,17 +234,24 @@ struct Impl final : ImplBase {
         p.w_resident = wbytes <= (size_t)(0.6 * c.l2_bytes) ? 1 : 0;
         // grid sizing: persistent grids of (SMs x resident blocks)
         int occ = 0;
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.out_fwd, 256, 0), "occupancy out_fwd");
-        p.grid_out = std::max(1, c.num_sms * std::max(1, occ));
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<TS>, 256, 0), "occupancy elem");
-        p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.num_sms * std::max(1, occ)));
-        p.vpb = 64;
-        vjp_smem = 8 * (size_t)c.hp * sizeof(double) + 3 * p.vpb * sizeof(double);
+        p.vpb = 64;  // 192 rows per slab: a multiple of every tile height
+        out_smem = ks.smem;
+        vjp_smem = ks.smem + 8 * (size_t)c.hp * sizeof(double);
+        cuda_check(cudaFuncSetAttribute(ks.out_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)out_smem),
+                   "smem attr out_fwd");
         cuda_check(cudaFuncSetAttribute(ks.vjp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjp_smem),
                    "smem attr vjp");
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, 256, vjp_smem), "occupancy vjp");
-        const int nslab = (m.n_free + p.vpb - 1) / p.vpb;
-        p.grid_vjp = std::max(1, std::min(nslab, c.num_sms * std::max(1, occ)));
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.out_fwd, kStreamThreads, out_smem),
+                   "occupancy out_fwd");
+        const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
+        p.grid_out = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<TS>, 256, 0), "occupancy elem");
+        p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.num_sms * std::max(1, occ)));
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, kStreamThreads, vjp_smem),
+                   "occupancy vjp");
+        p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<TS>, 256, 0), "occupancy gather");
+        grid_gather = std::max(1, std::min((c.n + 255) / 256, c.num_sms * std::max(1, occ)));
         p.group = 16;
         p.n_groups = (p.grid_vjp + p.group - 1) / p.group;
         // control cluster: hidden weights split in row slices over cs CTAs
@@ -271,11 +298,12 @@ struct Impl final : ImplBase {
 
     // One evaluation body, stream-launched (non-graph path).
     void launch_eval_body(cudaStream_t s, Context& c) {
-        ks.out_fwd<<<p.grid_out, 256, 0, s>>>(p);
+        ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
         elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
-        ks.vjp<<<p.grid_vjp, 256, vjp_smem, s>>>(p);
+        gather_kernel<TS><<<grid_gather, 256, 0, s>>>(p);
+        ks.vjp<<<p.grid_vjp, kStreamThreads, vjp_smem, s>>>(p);
         launch_ctrl(s, kCtrlAfterEval, 0, 0);
-        c.launches += 4;
+        c.launches += 5;
     }
 
     void eval(Context& c, bool want_grad) override {
@@ -295,11 +323,12 @@ struct Impl final : ImplBase {
             cudaEventRecord(ev[0], s);
             launch_ctrl(s, kCtrlStart, kModeEval, 1);
             cudaEventRecord(ev[1], s);
-            ks.out_fwd<<<p.grid_out, 256, 0, s>>>(p);
+            ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
             cudaEventRecord(ev[2], s);
             elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
             cudaEventRecord(ev[3], s);
-            ks.vjp<<<p.grid_vjp, 256, vjp_smem, s>>>(p);
+            gather_kernel<TS><<<grid_gather, 256, 0, s>>>(p);
+            ks.vjp<<<p.grid_vjp, kStreamThreads, vjp_smem, s>>>(p);
             cudaEventRecord(ev[4], s);
             launch_ctrl(s, kCtrlAfterEval, 0, 0);
             cudaEventRecord(ev[5], s);
@@ -321,11 +350,12 @@ struct Impl final : ImplBase {
         for (auto& e : ev) cudaEventDestroy(e);
     }
 
-    cudaGraphNode_t add_kernel(cudaGraph_t g, cudaGraphNode_t dep, void* fn, int grid, size_t smem, void** args) {
+    cudaGraphNode_t add_kernel(cudaGraph_t g, cudaGraphNode_t dep, void* fn, int grid, size_t smem, void** args,
+                               int threads = 256) {
         cudaKernelNodeParams kp = {};
         kp.func = fn;
         kp.gridDim = dim3(grid);
-        kp.blockDim = dim3(256);
+        kp.blockDim = dim3(threads);
         kp.sharedMemBytes = (unsigned)smem;
         kp.kernelParams = args;
         cudaGraphNode_t nd;
@@ -350,9 +380,10 @@ struct Impl final : ImplBase {
         void* a1[] = {&pg};
         int cm = kCtrlAfterEval, z0 = 0, z1 = 0;
         void* a4[] = {&pg, &cm, &z0, &z1};
-        cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, 0, a1);
+        cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
         cudaGraphNode_t n2 = add_kernel(body, n1, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-        cudaGraphNode_t n3 = add_kernel(body, n2, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1);
+        cudaGraphNode_t n2b = add_kernel(body, n2, (void*)gather_kernel<TS>, grid_gather, 0, a1);
+        cudaGraphNode_t n3 = add_kernel(body, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
         add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4);
         return wnode;
     }
@@ -387,7 +418,8 @@ struct Impl final : ImplBase {
         const double* z_state = c.d_z_state;
         DevState* st = c.d_state;
         double* ut = c.d_ut;
-        void* a_prep[] = {&n, &vfree, &u_state, &v_state, &a_ext, &z_state, &r, &st, &ut};
+        double* eprow = c.d_eprow;
+        void* a_prep[] = {&n, &vfree, &u_state, &v_state, &a_ext, &z_state, &r, &st, &ut, &eprow};
         cudaGraphNode_t n_prep = add_kernel(g, nullptr, (void*)prep_step_kernel, grid_n, 0, a_prep);
         cudaGraphNode_t n_start = add_start(g, n_prep);
         cudaGraphNode_t n_while = add_while(g, n_start, &h_step);

@@ -69,6 +69,9 @@ struct Context {
     void* d_Wout = nullptr;  // n x hp
     double *d_bout = nullptr, *d_sout = nullptr, *d_cout = nullptr, *d_dsout = nullptr;
     double *d_mass = nullptr, *d_ut = nullptr, *d_rin = nullptr;
+    double* d_eprow = nullptr;  // n x 6 {b, s, shift - X, m, U slot, qbar - X}
+    std::vector<double> h_eprow;
+    double* d_tv = nullptr;     // n
     int* d_vfree = nullptr;
     int* d_tets = nullptr;
     void* d_rec = nullptr;

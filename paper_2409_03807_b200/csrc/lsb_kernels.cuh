@@ -88,6 +88,8 @@ struct EvalParams {
     const double* mass;
     const double* ut;    // qbar - X (free DOFs)
     double* rin;         // m (u - ut) / dt^2
+    double* eprow;       // n x 6: {b, s, shift - X, m, U slot, qbar - X} per output row (TMA-staged)
+    double* tv;          // n: s phi'(a) g (gathered full-space gradient, VJP input)
     // mesh
     const int* vfree;
     const int4* tets;
