@@ -1,16 +1,1016 @@
-// Batched evaluation / Hessians — see lsb_batched.hpp.
+// Batched evaluation of E(z) and grad E(z) for many latent vectors (config 4),
+// and the second-order path (subspace Hessians, Lipschitz loss; config 5).
+//
+// Layout per batch chunk of BC columns (fp32 storage, fp64 reductions):
+//   Y_l, A_l  [h][BC]      hidden activations / pre-activations
+//   U         [V][3][BC]   vertex displacements (pinned rows = pin displacement)
+//   T         [n][BC]      s * (gathered elastic forces + inertia residual)
+//   Ybar      [h][BC]      W_out^T T
+// Element pass: contiguous tet blocks (host-precomputed block -> touched free
+// vertices); one CTA per (block, 64-column tile); thread b owns column b and
+// accumulates the block's vertex forces in shared memory in ascending tet order
+// (deterministic, no atomics); block partials are combined per vertex in
+// ascending block order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <tuple>
+#include <vector>
+
 #include "lsb_batched.hpp"
+#include "lsb_tc.cuh"
 
 namespace lsb {
 
-void batched_eval(Context&, int, const double*, double*, double*) {
-    throw LsbError(LSB_EINVAL, "eval_batched: not implemented in this build");
+namespace {
+
+constexpr int kBC = 128;       // batch columns per chunk
+constexpr int kEcols = 64;     // columns per element CTA
+constexpr int kTB = 48;        // tets per element block
+
+__device__ __forceinline__ float act_f(int a, float x, int order) {
+    return (float)act_eval(a, (double)x, order);
 }
-void batched_hessian(Context&, int, const double*, double*) {
-    throw LsbError(LSB_EINVAL, "hessian_batched: not implemented in this build");
+
+// ---------------------------------------------------------------- small GEMMs (hidden layers)
+// C[M][N] = A[M][K] * B[K][N] (+ bias[M]); optional pre-activation store and activation.
+// transA: A given as [K][M] (computes A^T B).  Tile 32x32, 256 threads, 2x2 per thread.
+__global__ void __launch_bounds__(256) small_gemm_kernel(int M, int N, int K, const double* A, int transA,
+                                                         const float* B, const double* bias, float* C,
+                                                         float* pre, int act, const float* gate, int gate_act) {
+    __shared__ float As[16][33];
+    __shared__ float Bs[16][33];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+    float acc[2][2] = {{0, 0}, {0, 0}};
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int t = threadIdx.x; t < 16 * 32; t += 256) {
+            const int kk = t / 32, mm = t % 32;
+            const int m = m0 + mm, k = k0 + kk;
+            As[kk][mm] = (m < M && k < K) ? (float)(transA ? A[(size_t)k * M + m] : A[(size_t)m * K + k]) : 0.f;
+            const int n = n0 + mm;
+            Bs[kk][mm] = (n < N && k < K) ? B[(size_t)k * N + n] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) acc[i][j] = fmaf(As[kk][ty * 2 + i], Bs[kk][tx * 2 + j], acc[i][j]);
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int m = m0 + ty * 2 + i, n = n0 + tx * 2 + j;
+            if (m < M && n < N) {
+                float v = acc[i][j] + (bias ? (float)bias[m] : 0.f);
+                if (pre) pre[(size_t)m * N + n] = v;
+                if (gate) v *= act_f(gate_act, gate[(size_t)m * N + n], 1);  // backward: times phi'(pre)
+                C[(size_t)m * N + n] = act >= 0 ? act_f(act, v, 0) : v;
+            }
+        }
 }
-double lipschitz_loss(Context&, int, const double*, const double*) {
-    throw LsbError(LSB_EINVAL, "lipschitz_loss: not implemented in this build");
+
+// ---------------------------------------------------------------- output layer epilogue (CUDA-core path)
+// Ubuf[n][BC] = W_out[n][h] * Y[h][BC] (fp32 SGEMM, 128x128 tiles, 8x8 per thread).
+__global__ void __launch_bounds__(256) sgemm_nn_kernel(int M, int N, int K, const float* A, int lda, const float* B,
+                                                       int ldb, float* C, int ldc) {
+    __shared__ float As[16][128 + 4];
+    __shared__ float Bs[16][128 + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+        for (int t = threadIdx.x; t < 16 * 128; t += 256) {
+            const int mm = t / 16, kk = t % 16;
+            const int m = m0 + mm, k = k0 + kk;
+            As[kk][mm] = (m < M && k < K) ? A[(size_t)m * lda + k] : 0.f;
+            const int kb = t / 128, nn = t % 128;
+            const int n = n0 + nn, k2 = k0 + kb;
+            Bs[kb][nn] = (n < N && k2 < K) ? B[(size_t)k2 * ldb + n] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+            if (m < M && n < N) C[(size_t)m * ldc + n] = acc[i][j];
+        }
+}
+
+// Split-K Ybar partials: P[kc][h][BC] = W_out[k-range]^T T[k-range][BC] (fp32).
+__global__ void __launch_bounds__(256) sgemm_tn_splitk_kernel(int H, int N, int K, int kchunk, const float* W,
+                                                              int ldw, const float* T, int ldt, float* P) {
+    __shared__ float As[16][128 + 4];
+    __shared__ float Bs[16][128 + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
+    const int kb0 = blockIdx.z * kchunk, kb1 = min(K, kb0 + kchunk);
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int k0 = kb0; k0 < kb1; k0 += 16) {
+        for (int t = threadIdx.x; t < 16 * 128; t += 256) {
+            const int kk = t / 128, mm = t % 128;
+            const int m = m0 + mm, k = k0 + kk;
+            As[kk][mm] = (m < H && k < kb1) ? W[(size_t)k * ldw + m] : 0.f;
+            const int n = n0 + mm;
+            Bs[kk][mm] = (n < N && k < kb1) ? T[(size_t)k * ldt + n] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    float* out = P + (size_t)blockIdx.z * H * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+            if (m < H && n < N) out[(size_t)m * N + n] = acc[i][j];
+        }
+}
+
+// Deterministic split-K reduction: Ybar[h][N] = sum_kc P[kc][h][N] (fp64 accumulate).
+__global__ void splitk_reduce_kernel(int HN, int nk, const float* P, float* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HN; i += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nk; ++k) s += P[(size_t)k * HN + i];
+        out[i] = (float)s;
+    }
+}
+
+// u = s (C + b) + shift - X -> U[v][3][N]; inertia residual and energy partials per column.
+__global__ void __launch_bounds__(256) out_epilogue_kernel(int n, int N, const float* C, const double* eprow,
+                                                           const double* ut, int has_inertia, double inv_dt2,
+                                                           float* U, float* rin, double* epart) {
+    // block: 256 threads over (rows tile of 64) x (N columns), column-major partial sums
+    const int col = threadIdx.x % 64 + 64 * blockIdx.y;
+    const int rsub = threadIdx.x / 64;  // 4 row lanes
+    __shared__ double red[4][64];
+    double e = 0.0;
+    if (col < N) {
+        for (int row = blockIdx.x * 64 + rsub; row < min(n, (int)(blockIdx.x + 1) * 64); row += 4) {
+            const double* e6 = eprow + (size_t)row * 6;
+            const double u = e6[1] * ((double)C[(size_t)row * N + col] + e6[0]) + e6[2];
+            const int slot = (int)e6[4];  // 4 v + c
+            U[((size_t)(slot >> 2) * 3 + (slot & 3)) * N + col] = (float)u;
+            if (has_inertia) {
+                const double d = u - ut[row];
+                rin[(size_t)row * N + col] = (float)(inv_dt2 * e6[3] * d);
+                e += e6[3] * d * d;
+            }
+        }
+    }
+    red[rsub][threadIdx.x % 64] = e;
+    __syncthreads();
+    if (rsub == 0 && col < N)
+        epart[(size_t)blockIdx.x * N + col] = 0.5 * inv_dt2 * (red[0][threadIdx.x] + red[1][threadIdx.x] +
+                                                                red[2][threadIdx.x] + red[3][threadIdx.x]);
+}
+
+// ---------------------------------------------------------------- batched element pass
+// One CTA per (tet block, 64-column tile); thread = column.
+template <typename TR>
+__global__ void __launch_bounds__(kEcols) elem_batched_kernel(const int4* tets, const TR* rec, const int* blk_tet0,
+                                                             const int* blk_vptr, const short* tet_loc,
+                                                             const float* U, int N, float* partial,
+                                                             double* eblk) {
+    extern __shared__ float acc[];  // [nv][3][kEcols]
+    const int blk = blockIdx.x;
+    const int col = blockIdx.y * kEcols + threadIdx.x;
+    const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    for (int i = threadIdx.x; i < nv * 3 * kEcols; i += blockDim.x) acc[i] = 0.f;
+    __syncthreads();
+    double esum = 0.0;
+    if (col < N) {
+        for (int e = e0; e < e1; ++e) {
+            const int4 t = __ldg(tets + e);
+            double rd[12];
+            load_rec<TR>(rec, (size_t)e, rd);
+            float rc[12];
+#pragma unroll
+            for (int q = 0; q < 12; ++q) rc[q] = (float)rd[q];
+            const int vv[4] = {t.x, t.y, t.z, t.w};
+            float u[4][3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) u[k][c] = __ldg(U + ((size_t)vv[k] * 3 + c) * N + col);
+            float f[12];
+            esum += (double)tet_energy_forces_t<float>(u[0], u[1], u[2], u[3], rc, f);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int lv = tet_loc[(size_t)e * 4 + k];
+                if (lv >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[(lv * 3 + c) * kEcols + threadIdx.x] += f[k * 3 + c];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (col < N) {
+        for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + threadIdx.x];
+        eblk[(size_t)blk * N + col] = esum;
+    }
+}
+
+// T[row][N] = s (sum of the vertex's block partials in block order + inertia).
+__global__ void combine_kernel(int n, int N, const int* vslot_ptr, const int* vslot, const float* partial,
+                               const float* rin, int has_inertia, const double* eprow, float* T) {
+    const size_t total = (size_t)n * N;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int row = (int)(idx / N), col = (int)(idx % N);
+        const int f = row / 3, c = row - 3 * f;
+        double g = 0.0;
+        for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) g += partial[((size_t)vslot[k] * 3 + c) * N + col];
+        if (has_inertia) g += rin[idx];
+        T[idx] = (float)(g * eprow[(size_t)row * 6 + 1]);
+    }
+}
+
+// E[b] = sum of inertia partials + element block partials (fixed order, fp64):
+// block = column; 256 threads stride the partial rows, fixed-tree block sum.
+__global__ void __launch_bounds__(256) energy_reduce_kernel(int N, int nrow_tiles, const double* epart, int nblk,
+                                                            const double* eblk, int has_inertia, double* E) {
+    __shared__ double red[32];
+    const int col = blockIdx.x;
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += eblk[(size_t)b * N + col];
+    if (has_inertia)
+        for (int b = threadIdx.x; b < nrow_tiles; b += blockDim.x) s += epart[(size_t)b * N + col];
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) E[col] = tot;
+}
+
+
+// ================================================================ second order (config 5)
+// Hidden forward with first and second tangents.  Per point p the column block
+// of X is [y | P_1..P_r | S_(a,b), a <= b] (1 + r + r(r+1)/2 columns); after the
+// GEMM Q = W X, this applies the activation rule per row:
+//   y' = phi(a), P'_a = phi'(a) Q_a, S'_ab = phi''(a) Q_a Q_b + phi'(a) Q_ab.
+__global__ void tangent_act_kernel(int R, int P, int r, int cols, const float* Q, const double* bias, int act,
+                                   float* X) {
+    const int npair = r * (r + 1) / 2;
+    const int total = R * P;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int i = idx / P, p = idx % P;
+        const float* q = Q + (size_t)i * P * cols + (size_t)p * cols;
+        float* x = X + (size_t)i * P * cols + (size_t)p * cols;
+        const double a = (double)q[0] + bias[i];
+        const float d1 = (float)act_eval(act, a, 1), d2 = (float)act_eval(act, a, 2);
+        x[0] = (float)act_eval(act, a, 0);
+        for (int k = 0; k < r; ++k) x[1 + k] = d1 * q[1 + k];
+        int t = 0;
+        for (int aa = 0; aa < r; ++aa)
+            for (int bb = aa; bb < r; ++bb, ++t) x[1 + r + t] = d2 * q[1 + aa] * q[1 + bb] + d1 * q[1 + r + t];
+        (void)npair;
+    }
+}
+
+// X0 = [z | I | 0] per point.
+__global__ void tangent_init_kernel(int r, int P, int cols, const float* Zt /*[r][P]*/, float* X) {
+    const int total = r * P * cols;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int i = idx / (P * cols), rem = idx % (P * cols), p = rem / cols, j = rem % cols;
+        float v = 0.f;
+        if (j == 0) v = Zt[(size_t)i * P + p];
+        else if (j == 1 + i) v = 1.f;
+        X[idx] = v;
+    }
+}
+
+// B operand of the output GEMM: [h][P*(1+r)] = the y and P columns of X_L.
+__global__ void tangent_pack_kernel(int h, int P, int r, int cols, const float* X, float* B) {
+    const int w = 1 + r;
+    const int total = h * P * w;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int i = idx / (P * w), rem = idx % (P * w), p = rem / w, j = rem % w;
+        B[idx] = X[(size_t)i * P * cols + (size_t)p * cols + j];
+    }
+}
+
+// u -> U[v][3][P]; J_ia = s_i C_ia -> Jv[v][3][P][r] (pinned rows: pin displacement, zero J).
+__global__ void tangent_out_kernel(int n, int P, int r, const float* C, const double* eprow, float* U, float* Jv) {
+    const int w = 1 + r;
+    const int total = n * P;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int row = idx / P, p = idx % P;
+        const double* e6 = eprow + (size_t)row * 6;
+        const float* c = C + (size_t)row * P * w + (size_t)p * w;
+        const int slot = (int)e6[4];
+        const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
+        U[vc * P + p] = (float)(e6[1] * ((double)c[0] + e6[0]) + e6[2]);
+        for (int a = 0; a < r; ++a) Jv[(vc * P + p) * r + a] = (float)(e6[1] * c[1 + a]);
+    }
+}
+
+// Per-tet elastic Hessian contraction.  CTA = (tet block, group of GP points),
+// thread = (point, direction b).  Per tet: each thread forms dF_b, the
+// stress differential M_b = 2 psi_I dF_b + psi_J (dcof F)[dF_b] and the scalars
+// alpha_b = gI : dF_b, beta_b = cof F : dF_b, publishes them to shared memory;
+// then accumulates its share of the pairs (a <= b):
+//   C_ab += vol (dF_a : M_b + psi_II alpha_a alpha_b + psi_JJ beta_a beta_b).
+// Thread (point, 0) also accumulates the block's elastic forces (gradient).
+template <int R>
+__global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const float* rec, const int* blk_tet0,
+                                                        const int* blk_vptr, const short* tet_loc, const float* U,
+                                                        const float* Jv, int P, float* Cpart, float* gpart) {
+    constexpr int GP = 256 / R;                  // points per CTA
+    constexpr int NPAIR = R * (R + 1) / 2;
+    constexpr int PPT = (NPAIR * GP + 255) / 256;  // pairs per thread
+    __shared__ float sh_dF[GP][R][9];
+    __shared__ float sh_M[GP][R][9];
+    __shared__ float sh_ab[GP][R][2];
+    __shared__ float sh_sc[GP][3];               // vol psi_II, vol psi_JJ, vol
+    extern __shared__ float accg[];              // [nv][3][GP]
+    const int tid = threadIdx.x;
+    const int pl = tid / R, b = tid % R;
+    const int p = blockIdx.y * GP + pl;
+    const bool live = p < P;
+    const int blk = blockIdx.x;
+    const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    for (int i = tid; i < nv * 3 * GP; i += 256) accg[i] = 0.f;
+    // pair assignment: thread handles global pair-slots tid, tid + 256, ... over (point, pair)
+    float cacc[PPT];
+    int pa[PPT], pb[PPT], ppt[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        cacc[k] = 0.f;
+        const int slot = tid + 256 * k;
+        ppt[k] = -1;
+        pa[k] = pb[k] = 0;
+        if (slot < NPAIR * GP && blockIdx.y * GP + slot / NPAIR < P) {
+            int a = 0, rem = slot % NPAIR;
+            while (rem >= R - a) {
+                rem -= R - a;
+                ++a;
+            }
+            ppt[k] = slot / NPAIR;
+            pa[k] = a;
+            pb[k] = a + rem;
+        }
+    }
+    __syncthreads();
+    for (int e = e0; e < e1; ++e) {
+        const int4 t = __ldg(tets + e);
+        const int vv[4] = {t.x, t.y, t.z, t.w};
+        float rc[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) rc[q] = __ldg(rec + (size_t)e * 12 + q);
+        if (live) {
+            float u[4][3], du[4][3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const size_t vc = (size_t)vv[k] * 3 + c;
+                    u[k][c] = __ldg(U + vc * P + p);
+                    du[k][c] = __ldg(Jv + (vc * P + p) * R + b);
+                }
+            // base state: A, F, cof F, invariants
+            float A[9], dA[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int c2 = 0; c2 < 3; ++c2) {
+                    float s = 0.f, ds = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        s += (u[k + 1][a] - u[0][a]) * rc[k * 3 + c2];
+                        ds += (du[k + 1][a] - du[0][a]) * rc[k * 3 + c2];
+                    }
+                    A[a * 3 + c2] = s;
+                    dA[a * 3 + c2] = ds;
+                }
+            float F[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
+            // cof F columns: f1 x f2, f2 x f0, f0 x f1 (f_c = column c)
+            float cof[9];
+            cof[0] = F[4] * F[8] - F[7] * F[5];
+            cof[3] = F[7] * F[2] - F[1] * F[8];
+            cof[6] = F[1] * F[5] - F[4] * F[2];
+            cof[1] = F[5] * F[6] - F[8] * F[3];
+            cof[4] = F[8] * F[0] - F[2] * F[6];
+            cof[7] = F[2] * F[3] - F[5] * F[0];
+            cof[2] = F[3] * F[7] - F[6] * F[4];
+            cof[5] = F[6] * F[1] - F[0] * F[7];
+            cof[8] = F[0] * F[4] - F[3] * F[1];
+            const float vol = rc[9], mu = rc[10], lam = rc[11];
+            const float trA = A[0] + A[4] + A[8];
+            float q = 0.f;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) q += A[k] * A[k];
+            const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+            const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
+                               A[6] * (A[1] * A[5] - A[4] * A[2]);
+            const float jm1 = trA + m2 + detA;
+            const float uI = 4.f + 2.f * trA + q;  // I + 1
+            const float psiI = 0.5f * mu * (1.f - 1.f / uI);
+            const float psiII = 0.5f * mu / (uI * uI);
+            const float psiJ = lam * jm1 - 0.75f * mu;
+            // directional quantities for direction b
+            float alpha = 0.f, beta = 0.f;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                alpha += 2.f * F[k] * dA[k];
+                beta += cof[k] * dA[k];
+            }
+            // (dcof F)[dF]: column-wise d(f1 x f2) = df1 x f2 + f1 x df2, etc.
+            float dc[9];
+            {
+#define COL(M, c, r_) M[(r_) * 3 + (c)]
+                float f[3][3], df[3][3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int r_ = 0; r_ < 3; ++r_) {
+                        f[c][r_] = COL(F, c, r_);
+                        df[c][r_] = COL(dA, c, r_);
+                    }
+                const int ci[3] = {1, 2, 0}, cj[3] = {2, 0, 1};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const float* a1 = f[ci[c]];
+                    const float* a2 = f[cj[c]];
+                    const float* d1 = df[ci[c]];
+                    const float* d2 = df[cj[c]];
+                    COL(dc, c, 0) = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
+                    COL(dc, c, 1) = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
+                    COL(dc, c, 2) = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
+                }
+#undef COL
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                sh_dF[pl][b][k] = dA[k];
+                sh_M[pl][b][k] = 2.f * psiI * dA[k] + psiJ * dc[k];
+            }
+            sh_ab[pl][b][0] = alpha;
+            sh_ab[pl][b][1] = beta;
+            if (b == 0) {
+                sh_sc[pl][0] = vol * psiII;
+                sh_sc[pl][1] = vol * lam;
+                sh_sc[pl][2] = vol;
+                // elastic forces of this tet at point p (gradient of P)
+                float Pst[9];
+                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
+                float cA[9];
+                cA[0] = A[4] * A[8] - A[7] * A[5];
+                cA[3] = A[7] * A[2] - A[1] * A[8];
+                cA[6] = A[1] * A[5] - A[4] * A[2];
+                cA[1] = A[5] * A[6] - A[8] * A[3];
+                cA[4] = A[8] * A[0] - A[2] * A[6];
+                cA[7] = A[2] * A[3] - A[5] * A[0];
+                cA[2] = A[3] * A[7] - A[6] * A[4];
+                cA[5] = A[6] * A[1] - A[0] * A[7];
+                cA[8] = A[0] * A[4] - A[3] * A[1];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int bb = 0; bb < 3; ++bb) {
+                        const float id = a == bb ? 1.f : 0.f;
+                        Pst[a * 3 + bb] = c1 * (A[a * 3 + bb] + A[bb * 3 + a] - trA * id - cA[a * 3 + bb]) +
+                                          c2 * F[a * 3 + bb] + c3 * cof[a * 3 + bb];
+                    }
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    float s0 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float hv = vol * (Pst[a * 3 + 0] * rc[c * 3 + 0] + Pst[a * 3 + 1] * rc[c * 3 + 1] +
+                                                Pst[a * 3 + 2] * rc[c * 3 + 2]);
+                        const int lv = tet_loc[(size_t)e * 4 + c + 1];
+                        if (lv >= 0) accg[(lv * 3 + a) * GP + pl] += hv;
+                        s0 += hv;
+                    }
+                    const int lv0 = tet_loc[(size_t)e * 4];
+                    if (lv0 >= 0) accg[(lv0 * 3 + a) * GP + pl] -= s0;
+                }
+            }
+        }
+        __syncthreads();
+        // pair contractions
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            {
+                const int pp = ppt[k];
+                if (pp >= 0) {
+                    const int a = pa[k], bb = pb[k];
+                    float s = 0.f;
+#pragma unroll
+                    for (int k9 = 0; k9 < 9; ++k9) s += sh_dF[pp][a][k9] * sh_M[pp][bb][k9];
+                    s = sh_sc[pp][2] * s + sh_sc[pp][0] * sh_ab[pp][a][0] * sh_ab[pp][bb][0] +
+                        sh_sc[pp][1] * sh_ab[pp][a][1] * sh_ab[pp][bb][1];
+                    cacc[k] += s;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // block partials
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const int slot = tid + 256 * k;
+        if (slot < NPAIR * GP) {
+            const int pp = slot / NPAIR, pr = slot % NPAIR;
+            const int pg = blockIdx.y * GP + pp;
+            if (pg < P) Cpart[((size_t)blk * P + pg) * NPAIR + pr] = cacc[k];
+        }
+    }
+    for (int i = tid; i < nv * 3 * GP; i += 256) {
+        const int pp = i % GP;
+        const int pg = blockIdx.y * GP + pp;
+        if (pg < P) gpart[((size_t)(v0 * 3) + i / GP) * P + pg] = accg[i];
+    }
+}
+
+// C[p][pair] = sum over blocks (fixed order, fp64).
+__global__ void hess_reduce_kernel(int nblk, int P, int npair, const float* Cpart, double* C) {
+    const int total = P * npair;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nblk; ++b) s += Cpart[(size_t)b * total + idx];
+        C[idx] = s;
+    }
+}
+
+// H[p][a][b] = C_ab + sum_j ybar[j][p] S_L[j][p, ab]  (symmetric fill).
+__global__ void hess_final_kernel(int h, int P, int r, int cols, const double* C, const float* Ybar, const float* X,
+                                  double* H) {
+    const int npair = r * (r + 1) / 2;
+    const int total = P * npair;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int p = idx / npair, pr = idx % npair;
+        double s = C[idx];
+        for (int j = 0; j < h; ++j)
+            s += (double)Ybar[(size_t)j * P + p] * (double)X[(size_t)j * P * cols + (size_t)p * cols + 1 + r + pr];
+        int a = 0, rem = pr;
+        while (rem >= r - a) {
+            rem -= r - a;
+            ++a;
+        }
+        const int b = a + rem;
+        H[((size_t)p * r + a) * r + b] = s;
+        H[((size_t)p * r + b) * r + a] = s;
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- engine
+struct BatchedEngine : BatchedBase {
+    int BC = kBC;
+    // tet blocks
+    int nblk = 0, nslots = 0;
+    int *d_blk_tet0 = nullptr, *d_blk_vptr = nullptr, *d_vslot_ptr = nullptr, *d_vslot = nullptr;
+    short* d_tet_loc = nullptr;
+    int max_nv = 0;
+    // buffers
+    float *d_W = nullptr;  // W_out fp32 [n][h] (unpadded)
+    float *d_Z = nullptr, *d_Y[kMaxLayers + 1] = {}, *d_A[kMaxLayers] = {};
+    float *d_C = nullptr, *d_U = nullptr, *d_rin = nullptr, *d_T = nullptr, *d_part = nullptr, *d_P = nullptr;
+    float *d_Ybar = nullptr, *d_Gb[2] = {};
+    double *d_epart = nullptr, *d_eblk = nullptr, *d_E = nullptr;
+    int nk = 1, kchunk = 1, nrow_tiles = 1;
+    std::vector<void*> allocs;
+    TcGemm tc;  // tcgen05 GEMM engine (lsb_tc.cuh)
+    // second order (config 5)
+    static constexpr int PH = 16;  // points per Hessian chunk
+    bool hess_ready = false;
+    float *d_Whf = nullptr;  // hidden weights fp32 (concatenated, row-major)
+    float *d_X[2] = {}, *d_Q = nullptr, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
+    float *d_Cpart = nullptr, *d_gpart = nullptr, *d_Th = nullptr, *d_Yh = nullptr, *d_Ph = nullptr, *d_Zh = nullptr;
+    double *d_Ch = nullptr, *d_H = nullptr;
+    int hcols = 0;
+
+    ~BatchedEngine() override {
+        for (void* p : allocs) cudaFree(p);
+    }
+    template <typename X>
+    X* alloc(size_t count) {
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, std::max<size_t>(count * sizeof(X), 16)), "batched malloc");
+        allocs.push_back(p);
+        return static_cast<X*>(p);
+    }
+
+    void init(Context& c) {
+        const HostMesh& m = c.mesh;
+        // --- tet blocks of kTB consecutive tets; touched free vertices, local indices
+        nblk = (m.E + kTB - 1) / kTB;
+        std::vector<int> tet0(nblk + 1), vptr(nblk + 1, 0);
+        std::vector<short> loc(4 * (size_t)m.E, -1);
+        std::vector<int> slot_vertex;  // global slot -> free vertex slot f
+        for (int b = 0; b < nblk; ++b) {
+            tet0[b] = b * kTB;
+            const int e1 = std::min(m.E, (b + 1) * kTB);
+            std::vector<int> verts;
+            for (int e = b * kTB; e < e1; ++e)
+                for (int k = 0; k < 4; ++k) {
+                    const int f = m.free_index[m.T[4 * (size_t)e + k]];
+                    if (f >= 0) verts.push_back(f);
+                }
+            std::sort(verts.begin(), verts.end());
+            verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+            for (int e = b * kTB; e < e1; ++e)
+                for (int k = 0; k < 4; ++k) {
+                    const int f = m.free_index[m.T[4 * (size_t)e + k]];
+                    if (f >= 0)
+                        loc[4 * (size_t)e + k] =
+                            (short)(std::lower_bound(verts.begin(), verts.end(), f) - verts.begin());
+                }
+            vptr[b + 1] = vptr[b] + (int)verts.size();
+            max_nv = std::max(max_nv, (int)verts.size());
+            slot_vertex.insert(slot_vertex.end(), verts.begin(), verts.end());
+        }
+        tet0[nblk] = m.E;
+        nslots = vptr[nblk];
+        // vertex -> slots (ascending block order)
+        std::vector<int> cnt(m.n_free + 1, 0);
+        for (int s = 0; s < nslots; ++s) cnt[slot_vertex[s] + 1]++;
+        std::vector<int> sptr(m.n_free + 1, 0);
+        for (int f = 0; f < m.n_free; ++f) sptr[f + 1] = sptr[f] + cnt[f + 1];
+        std::vector<int> slots(nslots), fill(sptr.begin(), sptr.end() - 1);
+        for (int s = 0; s < nslots; ++s) slots[fill[slot_vertex[s]]++] = s;
+        d_blk_tet0 = alloc<int>(nblk + 1);
+        d_blk_vptr = alloc<int>(nblk + 1);
+        d_tet_loc = alloc<short>(4 * (size_t)m.E);
+        d_vslot_ptr = alloc<int>(m.n_free + 1);
+        d_vslot = alloc<int>(nslots);
+        cuda_check(cudaMemcpy(d_blk_tet0, tet0.data(), 4 * tet0.size(), cudaMemcpyHostToDevice), "blk");
+        cuda_check(cudaMemcpy(d_blk_vptr, vptr.data(), 4 * vptr.size(), cudaMemcpyHostToDevice), "blk");
+        cuda_check(cudaMemcpy(d_tet_loc, loc.data(), 2 * loc.size(), cudaMemcpyHostToDevice), "blk");
+        cuda_check(cudaMemcpy(d_vslot_ptr, sptr.data(), 4 * sptr.size(), cudaMemcpyHostToDevice), "blk");
+        cuda_check(cudaMemcpy(d_vslot, slots.data(), 4 * slots.size(), cudaMemcpyHostToDevice), "blk");
+        // --- decoder output layer (fp32, unpadded [n][h])
+        const HostLayer& o = c.layers[c.nhid];
+        std::vector<float> W(o.W.size());
+        for (size_t i = 0; i < W.size(); ++i) W[i] = (float)o.W[i];
+        d_W = alloc<float>(W.size());
+        cuda_check(cudaMemcpy(d_W, W.data(), 4 * W.size(), cudaMemcpyHostToDevice), "batched W");
+        // --- chunk buffers
+        const int n = c.n, h = c.h, V = m.V;
+        int hmax = c.r;
+        for (int l = 0; l < c.nhid; ++l) hmax = std::max(hmax, c.hrows[l]);
+        d_Z = alloc<float>((size_t)c.r * BC);
+        for (int l = 0; l < c.nhid; ++l) {
+            d_Y[l + 1] = alloc<float>((size_t)c.hrows[l] * BC);
+            d_A[l] = alloc<float>((size_t)c.hrows[l] * BC);
+        }
+        d_Y[0] = d_Z;
+        d_C = alloc<float>((size_t)n * BC);
+        d_U = alloc<float>((size_t)V * 3 * BC);
+        d_rin = alloc<float>((size_t)n * BC);
+        d_T = alloc<float>((size_t)n * BC);
+        d_part = alloc<float>((size_t)nslots * 3 * BC);
+        kchunk = 256;
+        nk = (n + kchunk - 1) / kchunk;
+        d_P = alloc<float>((size_t)nk * h * BC);
+        d_Ybar = alloc<float>((size_t)h * BC);
+        d_Gb[0] = alloc<float>((size_t)hmax * BC);
+        d_Gb[1] = alloc<float>((size_t)hmax * BC);
+        nrow_tiles = (n + 63) / 64;
+        d_epart = alloc<double>((size_t)nrow_tiles * BC);
+        d_eblk = alloc<double>((size_t)nblk * BC);
+        d_E = alloc<double>(BC);
+        // pinned rows of U: pin displacement, constant across columns
+        std::vector<float> U0((size_t)V * 3 * BC, 0.f);
+        for (int v : m.pinned)
+            for (int k = 0; k < 3; ++k) {
+                const float d = (float)(c.pin_positions[3 * (size_t)v + k] - m.X[3 * (size_t)v + k]);
+                for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
+            }
+        cuda_check(cudaMemcpy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice), "U pins");
+        const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
+        if (c.precision == LSB_FP64)
+            cuda_check(cudaFuncSetAttribute(elem_batched_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)esmem), "elem smem");
+        else
+            cuda_check(cudaFuncSetAttribute(elem_batched_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)esmem), "elem smem");
+        tc.init(c, d_W, n, h, BC);
+    }
+
+    // One chunk of N <= BC columns; Z (N x r, host) -> E (N), G (N x r or null).
+    void run_chunk(Context& c, int N, const double* Z, double* E, double* G) {
+        cudaStream_t s = c.stream;
+        const int n = c.n, h = c.h, r = c.r, V = c.mesh.V;
+        (void)V;
+        // objective parameters from the single-instance state (host mirror)
+        DevState* hs = c.h_state;
+        cuda_check(cudaMemcpyAsync(hs, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s), "state");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        const int has_inertia = hs->has_inertia;
+        const double inv_dt2 = hs->inv_dt2;
+        // Z^T -> [r][BC] (columns beyond N are zero)
+        std::vector<float> zt((size_t)r * BC, 0.f);
+        for (int b = 0; b < N; ++b)
+            for (int k = 0; k < r; ++k) zt[(size_t)k * BC + b] = (float)Z[(size_t)b * r + k];
+        cuda_check(cudaMemcpyAsync(d_Z, zt.data(), 4 * zt.size(), cudaMemcpyHostToDevice, s), "Z");
+        // hidden forward
+        for (int l = 0; l < c.nhid; ++l) {
+            const int M = c.hrows[l], K = c.hcols[l];
+            dim3 grid((BC + 31) / 32, (M + 31) / 32);
+            small_gemm_kernel<<<grid, 256, 0, s>>>(M, BC, K, c.d_Wh + c.hoff[l], 0, d_Y[l], c.d_bh + c.boff[l],
+                                                   d_Y[l + 1], d_A[l], c.hact[l], nullptr, 0);
+        }
+        // output layer: C = W_out Y_L (tcgen05 when available, else SGEMM)
+        if (!tc.gemm_out(s, d_Y[c.nhid], d_C)) {
+            dim3 g1((BC + 127) / 128, (n + 127) / 128);
+            sgemm_nn_kernel<<<g1, 256, 0, s>>>(n, BC, h, d_W, h, d_Y[c.nhid], BC, d_C, BC);
+        }
+        {
+            dim3 g((n + 63) / 64, (BC + 63) / 64);
+            out_epilogue_kernel<<<g, 256, 0, s>>>(n, BC, d_C, c.d_eprow, c.d_ut, has_inertia, inv_dt2, d_U, d_rin,
+                                                  d_epart);
+        }
+        // element pass
+        {
+            dim3 g(nblk, (BC + kEcols - 1) / kEcols);
+            const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
+            if (c.precision == LSB_FP64)
+                elem_batched_kernel<double><<<g, kEcols, esmem, s>>>(
+                    reinterpret_cast<const int4*>(c.d_tets), static_cast<const double*>(c.d_rec), d_blk_tet0,
+                    d_blk_vptr, d_tet_loc, d_U, BC, d_part, d_eblk);
+            else
+                elem_batched_kernel<float><<<g, kEcols, esmem, s>>>(
+                    reinterpret_cast<const int4*>(c.d_tets), static_cast<const float*>(c.d_rec), d_blk_tet0,
+                    d_blk_vptr, d_tet_loc, d_U, BC, d_part, d_eblk);
+        }
+        energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, nrow_tiles, d_epart, nblk, d_eblk, has_inertia, d_E);
+        c.batched_launches += 5 + c.nhid;
+        if (G) {
+            combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, d_vslot_ptr, d_vslot, d_part, d_rin, has_inertia,
+                                                         c.d_eprow, d_T);
+            // Ybar = W_out^T T
+            if (!tc.gemm_vjp(s, d_T, d_Ybar)) {
+                dim3 g2((BC + 127) / 128, (h + 127) / 128, nk);
+                sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, BC, n, kchunk, d_W, h, d_T, BC, d_P);
+                splitk_reduce_kernel<<<c.num_sms, 256, 0, s>>>(h * BC, nk, d_P, d_Ybar);
+            }
+            // hidden backward: g_{l-1} = W_l^T (g_l * phi'(A_l))
+            const float* gin = d_Ybar;
+            int buf = 0;
+            for (int l = c.nhid - 1; l >= 0; --l) {
+                const int R = c.hrows[l], C = c.hcols[l];
+                // out[C][BC] = W_l^T [C x R] * (gin * phi'(A_l)) ; gating applied on the input side:
+                // precompute gated input in place via small_gemm with identity W? simpler: gate kernel
+                dim3 grid((BC + 31) / 32, (C + 31) / 32);
+                gate_mul(s, R, gin, d_A[l], c.hact[l], d_Gb[buf]);
+                small_gemm_kernel<<<grid, 256, 0, s>>>(C, BC, R, c.d_Wh + c.hoff[l], 1, d_Gb[buf], nullptr,
+                                                       d_Gb[buf ^ 1], nullptr, -1, nullptr, 0);
+                gin = d_Gb[buf ^ 1];
+                buf ^= 1;
+                c.batched_launches += 2;
+            }
+            c.batched_launches += 3;
+            std::vector<float> gz((size_t)r * BC);
+            cuda_check(cudaMemcpyAsync(gz.data(), gin, 4 * gz.size(), cudaMemcpyDeviceToHost, s), "G");
+            std::vector<double> e(BC);
+            cuda_check(cudaMemcpyAsync(e.data(), d_E, 8 * BC, cudaMemcpyDeviceToHost, s), "E");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+            for (int b = 0; b < N; ++b) {
+                E[b] = e[b];
+                for (int k = 0; k < r; ++k) G[(size_t)b * r + k] = gz[(size_t)k * BC + b];
+            }
+        } else {
+            std::vector<double> e(BC);
+            cuda_check(cudaMemcpyAsync(e.data(), d_E, 8 * BC, cudaMemcpyDeviceToHost, s), "E");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+            for (int b = 0; b < N; ++b) E[b] = e[b];
+        }
+    }
+
+    static void gate_mul(cudaStream_t s, int R, const float* g, const float* A, int act, float* out);
+
+    void init_hessian(Context& c) {
+        const int r = c.r, h = c.h, n = c.n;
+        if (c.out_act != kIdentity) throw LsbError(LSB_EINVAL, "hessian: device path requires an identity output layer");
+        if (r != 8 && r != 16 && r != 32)
+            throw LsbError(LSB_EINVAL, "hessian: device path supports latent dims 8, 16, 32");
+        const int npair = r * (r + 1) / 2;
+        hcols = 1 + r + npair;
+        int hmax = r;
+        for (int l = 0; l < c.nhid; ++l) hmax = std::max(hmax, c.hrows[l]);
+        size_t wtot = 0;
+        for (int l = 0; l < c.nhid; ++l) wtot += (size_t)c.hrows[l] * c.hcols[l];
+        std::vector<float> wf(wtot);
+        size_t off = 0;
+        for (int l = 0; l < c.nhid; ++l)
+            for (double v : c.layers[l].W) wf[off++] = (float)v;
+        d_Whf = alloc<float>(std::max<size_t>(1, wtot));
+        if (wtot) cuda_check(cudaMemcpy(d_Whf, wf.data(), 4 * wtot, cudaMemcpyHostToDevice), "Whf");
+        d_X[0] = alloc<float>((size_t)hmax * PH * hcols);
+        d_X[1] = alloc<float>((size_t)hmax * PH * hcols);
+        d_Q = alloc<float>((size_t)hmax * PH * hcols);
+        d_Bt = alloc<float>((size_t)h * PH * (1 + r));
+        d_Ct = alloc<float>((size_t)n * PH * (1 + r));
+        d_Uh = alloc<float>((size_t)c.mesh.V * 3 * PH);
+        d_Jv = alloc<float>((size_t)c.mesh.V * 3 * PH * r);
+        d_Cpart = alloc<float>((size_t)nblk * PH * npair);
+        d_gpart = alloc<float>((size_t)nslots * 3 * PH);
+        d_Th = alloc<float>((size_t)n * PH);
+        d_Yh = alloc<float>((size_t)h * PH);
+        d_Ph = alloc<float>((size_t)nk * h * PH);
+        d_Zh = alloc<float>((size_t)r * PH);
+        d_Ch = alloc<double>((size_t)PH * npair);
+        d_H = alloc<double>((size_t)PH * r * r);
+        // pinned rows: pin displacement in U, zero J
+        std::vector<float> U0((size_t)c.mesh.V * 3 * PH, 0.f);
+        for (int v : c.mesh.pinned)
+            for (int k = 0; k < 3; ++k) {
+                const float d = (float)(c.pin_positions[3 * (size_t)v + k] - c.mesh.X[3 * (size_t)v + k]);
+                for (int p = 0; p < PH; ++p) U0[((size_t)v * 3 + k) * PH + p] = d;
+            }
+        cuda_check(cudaMemcpy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice), "Uh");
+        cuda_check(cudaMemset(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r), "Jv");
+        const size_t gsmem = (size_t)max_nv * 3 * (256 / r) * sizeof(float);
+        if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        hess_ready = true;
+    }
+
+    // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
+    void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout) {
+        if (!hess_ready) init_hessian(c);
+        cudaStream_t s = c.stream;
+        const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols, npair = r * (r + 1) / 2;
+        std::vector<float> zt((size_t)r * P, 0.f);
+        for (int p = 0; p < N; ++p)
+            for (int k = 0; k < r; ++k) zt[(size_t)k * P + p] = (float)Z[(size_t)p * r + k];
+        cuda_check(cudaMemcpyAsync(d_Zh, zt.data(), 4 * zt.size(), cudaMemcpyHostToDevice, s), "Zh");
+        tangent_init_kernel<<<c.num_sms, 256, 0, s>>>(r, P, cols, d_Zh, d_X[0]);
+        int cur = 0;
+        size_t woff = 0;
+        for (int l = 0; l < c.nhid; ++l) {
+            const int R = c.hrows[l], K = c.hcols[l];
+            dim3 g((P * cols + 127) / 128, (R + 127) / 128);
+            sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_X[cur], P * cols, d_Q, P * cols);
+            tangent_act_kernel<<<c.num_sms, 256, 0, s>>>(R, P, r, cols, d_Q, c.d_bh + c.boff[l], c.hact[l], d_X[cur ^ 1]);
+            woff += (size_t)R * K;
+            cur ^= 1;
+        }
+        const float* XL = d_X[cur];
+        tangent_pack_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, XL, d_Bt);
+        {
+            dim3 g((P * (1 + r) + 127) / 128, (n + 127) / 128);
+            sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (1 + r), h, d_W, h, d_Bt, P * (1 + r), d_Ct, P * (1 + r));
+        }
+        tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv);
+        {
+            const int gp = 256 / r;
+            dim3 g(nblk, (P + gp - 1) / gp);
+            const size_t gsmem = (size_t)max_nv * 3 * gp * sizeof(float);
+            const float* recf = static_cast<const float*>(rec_f32(c));
+            auto args = std::make_tuple(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0, d_blk_vptr,
+                                        d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+            (void)args;
+            if (r == 8)
+                elem_hess_kernel<8><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
+                                                         d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+            else if (r == 16)
+                elem_hess_kernel<16><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
+                                                          d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+            else
+                elem_hess_kernel<32><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
+                                                          d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+        }
+        hess_reduce_kernel<<<c.num_sms, 256, 0, s>>>(nblk, P, npair, d_Cpart, d_Ch);
+        // gradient of the elastic potential (no inertia), times s
+        combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, d_vslot_ptr, d_vslot, d_gpart, nullptr, 0, c.d_eprow, d_Th);
+        {
+            dim3 g2((P + 127) / 128, (h + 127) / 128, nk);
+            sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, P, n, kchunk, d_W, h, d_Th, P, d_Ph);
+            splitk_reduce_kernel<<<c.num_sms, 256, 0, s>>>(h * P, nk, d_Ph, d_Yh);
+        }
+        hess_final_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, d_Ch, d_Yh, XL, d_H);
+        c.batched_launches += 10 + 2 * c.nhid;
+        std::vector<double> Hh((size_t)P * r * r);
+        cuda_check(cudaMemcpyAsync(Hh.data(), d_H, 8 * Hh.size(), cudaMemcpyDeviceToHost, s), "H");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        std::memcpy(Hout, Hh.data(), 8 * (size_t)N * r * r);
+    }
+
+    // fp32 copy of the element records (the fp64 context stores them in fp64)
+    float* d_recf = nullptr;
+    const void* rec_f32(Context& c) {
+        if (c.precision == LSB_FP32) return c.d_rec;
+        if (!d_recf) {
+            const HostMesh& m = c.mesh;
+            std::vector<float> rec(12 * (size_t)m.E);
+            for (int e = 0; e < m.E; ++e) {
+                for (int k = 0; k < 9; ++k) rec[12 * (size_t)e + k] = (float)m.Dminv[9 * (size_t)e + k];
+                rec[12 * (size_t)e + 9] = (float)m.vol[e];
+                rec[12 * (size_t)e + 10] = (float)c.mu[e];
+                rec[12 * (size_t)e + 11] = (float)c.lambda[e];
+            }
+            d_recf = alloc<float>(rec.size());
+            cuda_check(cudaMemcpy(d_recf, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice), "recf");
+        }
+        return d_recf;
+    }
+};
+
+namespace {
+__global__ void gate_kernel(int total, const float* g, const float* A, int act, float* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x)
+        out[i] = g[i] * act_f(act, A[i], 1);
+}
+}  // namespace
+
+void BatchedEngine::gate_mul(cudaStream_t s, int R, const float* g, const float* A, int act, float* out) {
+    const int total = R * kBC;
+    gate_kernel<<<(total + 255) / 256, 256, 0, s>>>(total, g, A, act, out);
+}
+
+static BatchedEngine& engine(Context& c) {
+    if (!c.batched) {
+        auto* e = new BatchedEngine();
+        c.batched.reset(e);
+        e->init(c);
+    }
+    return *static_cast<BatchedEngine*>(c.batched.get());
+}
+
+void batched_eval(Context& c, int B, const double* Z, double* E, double* G) {
+    BatchedEngine& eng = engine(c);
+    for (int b0 = 0; b0 < B; b0 += eng.BC) {
+        const int N = std::min(eng.BC, B - b0);
+        eng.run_chunk(c, N, Z + (size_t)b0 * c.r, E + b0, G ? G + (size_t)b0 * c.r : nullptr);
+    }
+}
+
+void batched_hessian(Context& c, int B, const double* Z, double* H) {
+    BatchedEngine& eng = engine(c);
+    const int r = c.r;
+    for (int b0 = 0; b0 < B; b0 += BatchedEngine::PH) {
+        const int N = std::min(BatchedEngine::PH, B - b0);
+        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, H + (size_t)b0 * r * r);
+    }
+}
+
+// mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2 (losses.cpp:196-213, order 2), fp64 combine.
+double lipschitz_loss(Context& c, int P, const double* Z1, const double* Z2) {
+    const int r = c.r;
+    std::vector<double> Z(2 * (size_t)P * r), H(2 * (size_t)P * r * r);
+    for (int p = 0; p < P; ++p) {  // interleave z1, z2 so both Hessians of a pair share a chunk
+        std::memcpy(&Z[(2 * (size_t)p) * r], Z1 + (size_t)p * r, 8 * r);
+        std::memcpy(&Z[(2 * (size_t)p + 1) * r], Z2 + (size_t)p * r, 8 * r);
+    }
+    batched_hessian(c, 2 * P, Z.data(), H.data());
+    double total = 0.0;
+    for (int p = 0; p < P; ++p) {
+        double d2 = 0.0, dz2 = 0.0;
+        const double* H1 = &H[(2 * (size_t)p) * r * r];
+        const double* H2 = &H[(2 * (size_t)p + 1) * r * r];
+        for (int k = 0; k < r * r; ++k) d2 += (H1[k] - H2[k]) * (H1[k] - H2[k]);
+        for (int k = 0; k < r; ++k) dz2 += (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]) * (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]);
+        total += d2 / dz2;
+    }
+    return total / P;
 }
 
 }  // namespace lsb

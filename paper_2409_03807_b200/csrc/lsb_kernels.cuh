@@ -445,30 +445,31 @@ __device__ __forceinline__ void load_u(const double* U, int v, double* o) {
 // Energy and 12 local forces of one tet from vertex displacements.
 // A = (Ds - Ds_rest) Dm^-1 (reference element_frame, energy.cpp:163-175);
 // forces = vol P Dm^-T (= vol B^T vec(P), energy.cpp:290-291).
-__device__ __forceinline__ double tet_energy_forces(const double* u0, const double* u1, const double* u2,
-                                                    const double* u3, const double* rec, double* f) {
-    double D[9];
+template <typename T>
+__device__ __forceinline__ T tet_energy_forces_t(const T* u0, const T* u1, const T* u2, const T* u3, const T* rec,
+                                                 T* f) {
+    T D[9];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         D[a * 3 + 0] = u1[a] - u0[a];
         D[a * 3 + 1] = u2[a] - u0[a];
         D[a * 3 + 2] = u3[a] - u0[a];
     }
-    double A[9];
+    T A[9];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int b = 0; b < 3; ++b)
             A[a * 3 + b] = D[a * 3 + 0] * rec[0 * 3 + b] + D[a * 3 + 1] * rec[1 * 3 + b] + D[a * 3 + 2] * rec[2 * 3 + b];
-    double P[9];
-    const double vol = rec[9];
-    const double psi = snh_psi_P(A, rec[10], rec[11], P);
+    T P[9];
+    const T vol = rec[9];
+    const T psi = snh_psi_P(A, rec[10], rec[11], P);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        double s0 = 0;
+        T s0 = 0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double hv =
+            const T hv =
                 vol * (P[a * 3 + 0] * rec[c * 3 + 0] + P[a * 3 + 1] * rec[c * 3 + 1] + P[a * 3 + 2] * rec[c * 3 + 2]);
             f[(c + 1) * 3 + a] = hv;
             s0 += hv;
@@ -476,6 +477,10 @@ __device__ __forceinline__ double tet_energy_forces(const double* u0, const doub
         f[a] = -s0;
     }
     return vol * psi;
+}
+__device__ __forceinline__ double tet_energy_forces(const double* u0, const double* u1, const double* u2,
+                                                    const double* u3, const double* rec, double* f) {
+    return tet_energy_forces_t<double>(u0, u1, u2, u3, rec, f);
 }
 
 template <typename TS>

@@ -1,0 +1,67 @@
+"""GPU parity of the subspace Hessian of the elastic potential
+(reference reduced_potential_hessian, losses.cpp:301-316) and of the order-2
+Lipschitz loss (lipschitz_loss(model, pairs, 2, pot), losses.cpp:196-213,237-244)
+against the CPU oracle.  Device path: fp32 with fp64 reductions; tolerance
+1e-4 relative (north star, config 5)."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_hessian_matches_oracle_c1(precision, oracle, product):
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system(precision)
+    ob = oracle.problem("c1")
+    Z1, Z2 = configs.latent_pairs_c5(pr.model.r, 12)
+    Z = np.concatenate([Z1, Z2])
+    H = sysm.hessian_batched(Z)
+    for k in range(0, Z.shape[0], 5):
+        Ho = ob.reduced_potential_hessian(Z[k])
+        assert rel_err(H[k], Ho) < 1e-4, (k, rel_err(H[k], Ho))
+        assert np.array_equal(H[k], H[k].T)
+
+
+def test_lipschitz_loss_matches_oracle_c1(oracle, product):
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    ob = oracle.problem("c1")
+    Z1, Z2 = configs.latent_pairs_c5(pr.model.r, 24)
+    loss = product.lipschitz_loss(sysm, list(zip(Z1, Z2)))
+    ref = ob.lipschitz_loss2(Z1, Z2, threads=8)
+    assert rel_err(loss, ref) < 1e-4, (loss, ref)
+    assert product.lipschitz_loss(sysm, list(zip(Z2, Z1))) == pytest.approx(loss, rel=1e-12)
+    with pytest.raises(ValueError, match="coincident"):
+        sysm.lipschitz_loss(Z1[:1], Z1[:1].copy())
+
+
+def test_hessian_general_decoder(oracle, product):
+    """Non-ELU activation, biases, scale != 1, pinned-vertex mesh (r = 8)."""
+    P = product
+    mesh = P.make_bar_mesh(3, 2, 2, 1.0, 0.4, 0.5, jitter_frac=0.05, seed=3)
+    rng = np.random.default_rng(4)
+    n = mesh.num_dofs()
+    dims = [8, 16, 16, n]
+    layers = []
+    for i in range(3):
+        W = rng.standard_normal((dims[i + 1], dims[i])) * (0.4 if i < 2 else 0.05)
+        b = 0.1 * rng.standard_normal(dims[i + 1])
+        layers.append(P.Layer(W, b, P.Activation.Silu if i < 2 else P.Activation.Identity))
+    shift = P.dof_pack(mesh, mesh.vertices)
+    scale = 0.3 + 0.1 * rng.random(n)
+    model = P.SubspaceModel(8, n, layers, shift, scale)
+    mu = 2.0 + rng.random(mesh.num_elements())
+    lam = 1.0 + rng.random(mesh.num_elements())
+    sysm = P.ReducedSystem(mesh, mu, lam, 3.0, model, "fp64")
+    o = oracle.Oracle.from_mesh(mesh.vertices, mesh.elements, mesh.pinned)
+    o.set_material(mu, lam, 3.0)
+    o.set_decoder([(l.W, l.b, int(l.act)) for l in layers], shift, scale, 8)
+    Z = 0.5 * rng.standard_normal((5, 8))
+    H = sysm.hessian_batched(Z)
+    for k in range(5):
+        assert rel_err(H[k], o.reduced_potential_hessian(Z[k])) < 1e-4
