@@ -290,20 +290,28 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(int N, int nrow_tile
 //   y' = phi(a), P'_a = phi'(a) Q_a, S'_ab = phi''(a) Q_a Q_b + phi'(a) Q_ab.
 __global__ void tangent_act_kernel(int R, int P, int r, int cols, const float* Q, const double* bias, int act,
                                    float* X) {
-    const int npair = r * (r + 1) / 2;
-    const int total = R * P;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const int i = idx / P, p = idx % P;
-        const float* q = Q + (size_t)i * P * cols + (size_t)p * cols;
-        float* x = X + (size_t)i * P * cols + (size_t)p * cols;
+    const size_t total = (size_t)R * P * cols;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx % cols);
+        const size_t ip = idx / cols;
+        const int i = (int)(ip / P);
+        const float* q = Q + ip * cols;
         const double a = (double)q[0] + bias[i];
-        const float d1 = (float)act_eval(act, a, 1), d2 = (float)act_eval(act, a, 2);
-        x[0] = (float)act_eval(act, a, 0);
-        for (int k = 0; k < r; ++k) x[1 + k] = d1 * q[1 + k];
-        int t = 0;
-        for (int aa = 0; aa < r; ++aa)
-            for (int bb = aa; bb < r; ++bb, ++t) x[1 + r + t] = d2 * q[1 + aa] * q[1 + bb] + d1 * q[1 + r + t];
-        (void)npair;
+        float v;
+        if (j == 0) {
+            v = (float)act_eval(act, a, 0);
+        } else if (j <= r) {
+            v = (float)act_eval(act, a, 1) * q[j];
+        } else {
+            int aa = 0, rem = j - 1 - r;
+            while (rem >= r - aa) {
+                rem -= r - aa;
+                ++aa;
+            }
+            const int bb = aa + rem;
+            v = (float)act_eval(act, a, 2) * q[1 + aa] * q[1 + bb] + (float)act_eval(act, a, 1) * q[j];
+        }
+        X[idx] = v;
     }
 }
 
@@ -345,42 +353,63 @@ __global__ void tangent_out_kernel(int n, int P, int r, const float* C, const do
 }
 
 // Per-tet elastic Hessian contraction.  CTA = (tet block, group of GP points),
-// thread = (point, direction b).  Per tet: each thread forms dF_b, the
-// stress differential M_b = 2 psi_I dF_b + psi_J (dcof F)[dF_b] and the scalars
-// alpha_b = gI : dF_b, beta_b = cof F : dF_b, publishes them to shared memory;
-// then accumulates its share of the pairs (a <= b):
-//   C_ab += vol (dF_a : M_b + psi_II alpha_a alpha_b + psi_JJ beta_a beta_b).
-// Thread (point, 0) also accumulates the block's elastic forces (gradient).
+// thread = (point, direction b).  The block's vertex displacements and
+// Jacobian rows for the CTA's points are staged in shared memory once
+// (cp.async, all in flight).  Per tet each thread forms dF_b, the stress
+// differential M_b = 2 psi_I dF_b + psi_J (dcof F)[dF_b] and the scalars
+// alpha_b = 2F : dF_b, beta_b = cof F : dF_b, publishes them (double-buffered,
+// one barrier per tet) and accumulates its share of the pairs (a <= b):
+//   C_ab += vol (dF_a : M_b + psi_II alpha_a alpha_b + lambda beta_a beta_b)
+// (= J^T hess(P) J restricted to the tet).  Thread (point, 0) also accumulates
+// the block's elastic forces (gradient of P) for the decoder-curvature term.
 template <int R>
-__global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const float* rec, const int* blk_tet0,
-                                                        const int* blk_vptr, const short* tet_loc, const float* U,
-                                                        const float* Jv, int P, float* Cpart, float* gpart) {
-    constexpr int GP = 256 / R;                  // points per CTA
+__global__ void __launch_bounds__(128, 3) elem_hess_kernel(const int4* tets, const float* rec, const int* blk_tet0,
+                                                           const int* blk_vptr, const short* tet_loc,
+                                                           const int* blk_aptr, const int* blk_avert,
+                                                           const short* tet_aloc, const float* U, const float* Jv,
+                                                           int P, float* Cpart, float* gpart) {
+    constexpr int GP = 128 / R;                  // points per CTA
     constexpr int NPAIR = R * (R + 1) / 2;
-    constexpr int PPT = (NPAIR * GP + 255) / 256;  // pairs per thread
-    __shared__ float sh_dF[GP][R][9];
-    __shared__ float sh_M[GP][R][9];
-    __shared__ float sh_ab[GP][R][2];
-    __shared__ float sh_sc[GP][3];               // vol psi_II, vol psi_JJ, vol
-    extern __shared__ float accg[];              // [nv][3][GP]
+    constexpr int PPT = (NPAIR * GP + 127) / 128;  // pairs per thread
+    __shared__ float sh_dF[2][GP][R][9];
+    __shared__ float sh_M[2][GP][R][9];
+    __shared__ float sh_ab[2][GP][R][2];
+    __shared__ float sh_sc[2][GP][3];
+    extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
     const int pl = tid / R, b = tid % R;
-    const int p = blockIdx.y * GP + pl;
-    const bool live = p < P;
+    const int p0 = blockIdx.y * GP;
     const int blk = blockIdx.x;
     const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
     const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
-    for (int i = tid; i < nv * 3 * GP; i += 256) accg[i] = 0.f;
-    // pair assignment: thread handles global pair-slots tid, tid + 256, ... over (point, pair)
+    const int a0 = blk_aptr[blk], nva = blk_aptr[blk + 1] - a0;
+    float* Js = dyn;                                 // [nva][3][GP][R]
+    float* Us = Js + (size_t)nva * 3 * GP * R;       // [nva][3][GP]
+    float* accg = Us + (size_t)nva * 3 * GP;         // [nv][3][GP]
+    // ---- stage (all copies in flight, one wait)
+    for (int i = tid; i < nva * 3; i += 128) {
+        const int va = __ldg(blk_avert + a0 + i / 3), c = i % 3;
+        const size_t vc = (size_t)va * 3 + c;
+        const float* src = Jv + (vc * P + p0) * R;
+        float* dst = Js + (size_t)i * GP * R;
+        for (int k = 0; k < GP * R; k += 4) cp_async16(dst + k, src + k);
+    }
+    static_assert(GP % 4 == 0, "16-byte staging of U");
+    for (int i = tid; i < nva * 3 * (GP / 4); i += 128) {
+        const int vcl = i / (GP / 4), k4 = i % (GP / 4);
+        const int va = __ldg(blk_avert + a0 + vcl / 3), c = vcl % 3;
+        cp_async16(Us + (size_t)vcl * GP + 4 * k4, U + ((size_t)va * 3 + c) * P + p0 + 4 * k4);
+    }
+    for (int i = tid; i < nv * 3 * GP; i += 128) accg[i] = 0.f;
     float cacc[PPT];
     int pa[PPT], pb[PPT], ppt[PPT];
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         cacc[k] = 0.f;
-        const int slot = tid + 256 * k;
+        const int slot = tid + 128 * k;
         ppt[k] = -1;
         pa[k] = pb[k] = 0;
-        if (slot < NPAIR * GP && blockIdx.y * GP + slot / NPAIR < P) {
+        if (slot < NPAIR * GP && p0 + slot / NPAIR < P) {
             int a = 0, rem = slot % NPAIR;
             while (rem >= R - a) {
                 rem -= R - a;
@@ -391,42 +420,44 @@ __global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const 
             pb[k] = a + rem;
         }
     }
+    cp_async_wait_all();
     __syncthreads();
+    const bool live = p0 + pl < P;
     for (int e = e0; e < e1; ++e) {
+        const int buf = (e - e0) & 1;
         const int4 t = __ldg(tets + e);
-        const int vv[4] = {t.x, t.y, t.z, t.w};
         float rc[12];
-#pragma unroll
-        for (int q = 0; q < 12; ++q) rc[q] = __ldg(rec + (size_t)e * 12 + q);
+        {
+            const float4* r4 = reinterpret_cast<const float4*>(rec + (size_t)e * 12);
+            const float4 x0 = __ldg(r4), x1 = __ldg(r4 + 1), x2 = __ldg(r4 + 2);
+            rc[0] = x0.x; rc[1] = x0.y; rc[2] = x0.z; rc[3] = x0.w;
+            rc[4] = x1.x; rc[5] = x1.y; rc[6] = x1.z; rc[7] = x1.w;
+            rc[8] = x2.x; rc[9] = x2.y; rc[10] = x2.z; rc[11] = x2.w;
+        }
         if (live) {
-            float u[4][3], du[4][3];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const size_t vc = (size_t)vv[k] * 3 + c;
-                    u[k][c] = __ldg(U + vc * P + p);
-                    du[k][c] = __ldg(Jv + (vc * P + p) * R + b);
-                }
-            // base state: A, F, cof F, invariants
+            int la[4];
+            la[0] = tet_aloc[(size_t)e * 4 + 0];
+            la[1] = tet_aloc[(size_t)e * 4 + 1];
+            la[2] = tet_aloc[(size_t)e * 4 + 2];
+            la[3] = tet_aloc[(size_t)e * 4 + 3];
             float A[9], dA[9];
 #pragma unroll
-            for (int a = 0; a < 3; ++a)
+            for (int a = 0; a < 3; ++a) {
+                float du[4], uu[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uu[k] = Us[(la[k] * 3 + a) * GP + pl];
+                    du[k] = Js[((size_t)(la[k] * 3 + a) * GP + pl) * R + b];
+                }
 #pragma unroll
                 for (int c2 = 0; c2 < 3; ++c2) {
-                    float s = 0.f, ds = 0.f;
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        s += (u[k + 1][a] - u[0][a]) * rc[k * 3 + c2];
-                        ds += (du[k + 1][a] - du[0][a]) * rc[k * 3 + c2];
-                    }
-                    A[a * 3 + c2] = s;
-                    dA[a * 3 + c2] = ds;
+                    A[a * 3 + c2] = (uu[1] - uu[0]) * rc[c2] + (uu[2] - uu[0]) * rc[3 + c2] + (uu[3] - uu[0]) * rc[6 + c2];
+                    dA[a * 3 + c2] = (du[1] - du[0]) * rc[c2] + (du[2] - du[0]) * rc[3 + c2] + (du[3] - du[0]) * rc[6 + c2];
                 }
+            }
             float F[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
-            // cof F columns: f1 x f2, f2 x f0, f0 x f1 (f_c = column c)
             float cof[9];
             cof[0] = F[4] * F[8] - F[7] * F[5];
             cof[3] = F[7] * F[2] - F[1] * F[8];
@@ -450,52 +481,35 @@ __global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const 
             const float psiI = 0.5f * mu * (1.f - 1.f / uI);
             const float psiII = 0.5f * mu / (uI * uI);
             const float psiJ = lam * jm1 - 0.75f * mu;
-            // directional quantities for direction b
             float alpha = 0.f, beta = 0.f;
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 alpha += 2.f * F[k] * dA[k];
                 beta += cof[k] * dA[k];
             }
-            // (dcof F)[dF]: column-wise d(f1 x f2) = df1 x f2 + f1 x df2, etc.
+            // (dcof F)[dF]: column c of cof is f_i x f_j, (i, j) = (1,2), (2,0), (0,1)
             float dc[9];
-            {
-#define COL(M, c, r_) M[(r_) * 3 + (c)]
-                float f[3][3], df[3][3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                    for (int r_ = 0; r_ < 3; ++r_) {
-                        f[c][r_] = COL(F, c, r_);
-                        df[c][r_] = COL(dA, c, r_);
-                    }
-                const int ci[3] = {1, 2, 0}, cj[3] = {2, 0, 1};
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float* a1 = f[ci[c]];
-                    const float* a2 = f[cj[c]];
-                    const float* d1 = df[ci[c]];
-                    const float* d2 = df[cj[c]];
-                    COL(dc, c, 0) = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
-                    COL(dc, c, 1) = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
-                    COL(dc, c, 2) = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
-                }
-#undef COL
+            for (int c = 0; c < 3; ++c) {
+                const int ci = (c + 1) % 3, cj = (c + 2) % 3;
+                const float a1[3] = {F[ci], F[3 + ci], F[6 + ci]}, a2[3] = {F[cj], F[3 + cj], F[6 + cj]};
+                const float d1[3] = {dA[ci], dA[3 + ci], dA[6 + ci]}, d2[3] = {dA[cj], dA[3 + cj], dA[6 + cj]};
+                dc[0 * 3 + c] = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
+                dc[1 * 3 + c] = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
+                dc[2 * 3 + c] = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
             }
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
-                sh_dF[pl][b][k] = dA[k];
-                sh_M[pl][b][k] = 2.f * psiI * dA[k] + psiJ * dc[k];
+                sh_dF[buf][pl][b][k] = dA[k];
+                sh_M[buf][pl][b][k] = 2.f * psiI * dA[k] + psiJ * dc[k];
             }
-            sh_ab[pl][b][0] = alpha;
-            sh_ab[pl][b][1] = beta;
+            sh_ab[buf][pl][b][0] = alpha;
+            sh_ab[buf][pl][b][1] = beta;
             if (b == 0) {
-                sh_sc[pl][0] = vol * psiII;
-                sh_sc[pl][1] = vol * lam;
-                sh_sc[pl][2] = vol;
-                // elastic forces of this tet at point p (gradient of P)
-                float Pst[9];
-                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
+                sh_sc[buf][pl][0] = vol * psiII;
+                sh_sc[buf][pl][1] = vol * lam;
+                sh_sc[buf][pl][2] = vol;
+                // elastic forces of this tet at this point (cancellation-free P)
                 float cA[9];
                 cA[0] = A[4] * A[8] - A[7] * A[5];
                 cA[3] = A[7] * A[2] - A[1] * A[8];
@@ -506,6 +520,8 @@ __global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const 
                 cA[2] = A[3] * A[7] - A[6] * A[4];
                 cA[5] = A[6] * A[1] - A[0] * A[7];
                 cA[8] = A[0] * A[4] - A[3] * A[1];
+                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
+                float Pst[9];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -531,48 +547,48 @@ __global__ void __launch_bounds__(256) elem_hess_kernel(const int4* tets, const 
             }
         }
         __syncthreads();
-        // pair contractions
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-            {
-                const int pp = ppt[k];
-                if (pp >= 0) {
-                    const int a = pa[k], bb = pb[k];
-                    float s = 0.f;
+            const int pp = ppt[k];
+            if (pp >= 0) {
+                const int a = pa[k], bb = pb[k];
+                float s = 0.f;
 #pragma unroll
-                    for (int k9 = 0; k9 < 9; ++k9) s += sh_dF[pp][a][k9] * sh_M[pp][bb][k9];
-                    s = sh_sc[pp][2] * s + sh_sc[pp][0] * sh_ab[pp][a][0] * sh_ab[pp][bb][0] +
-                        sh_sc[pp][1] * sh_ab[pp][a][1] * sh_ab[pp][bb][1];
-                    cacc[k] += s;
-                }
+                for (int k9 = 0; k9 < 9; ++k9) s += sh_dF[buf][pp][a][k9] * sh_M[buf][pp][bb][k9];
+                cacc[k] += sh_sc[buf][pp][2] * s + sh_sc[buf][pp][0] * sh_ab[buf][pp][a][0] * sh_ab[buf][pp][bb][0] +
+                           sh_sc[buf][pp][1] * sh_ab[buf][pp][a][1] * sh_ab[buf][pp][bb][1];
             }
         }
-        __syncthreads();
     }
-    // block partials
+    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-        const int slot = tid + 256 * k;
-        if (slot < NPAIR * GP) {
-            const int pp = slot / NPAIR, pr = slot % NPAIR;
-            const int pg = blockIdx.y * GP + pp;
-            if (pg < P) Cpart[((size_t)blk * P + pg) * NPAIR + pr] = cacc[k];
+    for (int k = 0; k < PPT; ++k)
+        if (ppt[k] >= 0) {
+            const int pr = (tid + 128 * k) % NPAIR;
+            Cpart[((size_t)blk * P + p0 + ppt[k]) * NPAIR + pr] = cacc[k];
         }
-    }
-    for (int i = tid; i < nv * 3 * GP; i += 256) {
+    for (int i = tid; i < nv * 3 * GP; i += 128) {
         const int pp = i % GP;
-        const int pg = blockIdx.y * GP + pp;
-        if (pg < P) gpart[((size_t)(v0 * 3) + i / GP) * P + pg] = accg[i];
+        if (p0 + pp < P) gpart[((size_t)(v0 * 3) + i / GP) * P + p0 + pp] = accg[i];
     }
 }
 
-// C[p][pair] = sum over blocks (fixed order, fp64).
-__global__ void hess_reduce_kernel(int nblk, int P, int npair, const float* Cpart, double* C) {
+// C[p][pair] = sum over blocks (fixed order, fp64): CTA per 32 (p, pair) entries,
+// 8 warps stride the blocks, fixed combine order.
+__global__ void __launch_bounds__(256) hess_reduce_kernel(int nblk, int P, int npair, const float* Cpart, double* C) {
+    __shared__ double red[8][33];
     const int total = P * npair;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nblk; ++b) s += Cpart[(size_t)b * total + idx];
-        C[idx] = s;
+    const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int w = threadIdx.x >> 5;
+    double s = 0.0;
+    if (idx < total)
+        for (int b = w; b < nblk; b += 8) s += Cpart[(size_t)b * total + idx];
+    red[w][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (w == 0 && idx < total) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+        C[idx] = t;
     }
 }
 
@@ -607,6 +623,10 @@ struct BatchedEngine : BatchedBase {
     int *d_blk_tet0 = nullptr, *d_blk_vptr = nullptr, *d_vslot_ptr = nullptr, *d_vslot = nullptr;
     short* d_tet_loc = nullptr;
     int max_nv = 0;
+    // all touched vertices (free and pinned) per block, for shared-memory staging
+    int *d_blk_aptr = nullptr, *d_blk_avert = nullptr;
+    short* d_tet_aloc = nullptr;
+    int max_nva = 0;
     // buffers
     float *d_W = nullptr;  // W_out fp32 [n][h] (unpadded)
     float *d_Z = nullptr, *d_Y[kMaxLayers + 1] = {}, *d_A[kMaxLayers] = {};
@@ -617,7 +637,7 @@ struct BatchedEngine : BatchedBase {
     std::vector<void*> allocs;
     TcGemm tc;  // tcgen05 GEMM engine (lsb_tc.cuh)
     // second order (config 5)
-    static constexpr int PH = 16;  // points per Hessian chunk
+    static constexpr int PH = 64;  // points per Hessian chunk
     bool hess_ready = false;
     float *d_Whf = nullptr;  // hidden weights fp32 (concatenated, row-major)
     float *d_X[2] = {}, *d_Q = nullptr, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
@@ -667,6 +687,31 @@ struct BatchedEngine : BatchedBase {
         }
         tet0[nblk] = m.E;
         nslots = vptr[nblk];
+        {
+            std::vector<int> aptr(nblk + 1, 0), avert;
+            std::vector<short> aloc(4 * (size_t)m.E, -1);
+            for (int bk = 0; bk < nblk; ++bk) {
+                const int e1 = std::min(m.E, (bk + 1) * kTB);
+                std::vector<int> verts;
+                for (int e = bk * kTB; e < e1; ++e)
+                    for (int k = 0; k < 4; ++k) verts.push_back(m.T[4 * (size_t)e + k]);
+                std::sort(verts.begin(), verts.end());
+                verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+                for (int e = bk * kTB; e < e1; ++e)
+                    for (int k = 0; k < 4; ++k)
+                        aloc[4 * (size_t)e + k] = (short)(std::lower_bound(verts.begin(), verts.end(),
+                                                                           m.T[4 * (size_t)e + k]) - verts.begin());
+                aptr[bk + 1] = aptr[bk] + (int)verts.size();
+                max_nva = std::max(max_nva, (int)verts.size());
+                avert.insert(avert.end(), verts.begin(), verts.end());
+            }
+            d_blk_aptr = alloc<int>(nblk + 1);
+            d_blk_avert = alloc<int>(avert.size());
+            d_tet_aloc = alloc<short>(aloc.size());
+            cuda_check(cudaMemcpy(d_blk_aptr, aptr.data(), 4 * aptr.size(), cudaMemcpyHostToDevice), "blk");
+            cuda_check(cudaMemcpy(d_blk_avert, avert.data(), 4 * avert.size(), cudaMemcpyHostToDevice), "blk");
+            cuda_check(cudaMemcpy(d_tet_aloc, aloc.data(), 2 * aloc.size(), cudaMemcpyHostToDevice), "blk");
+        }
         // vertex -> slots (ascending block order)
         std::vector<int> cnt(m.n_free + 1, 0);
         for (int s = 0; s < nslots; ++s) cnt[slot_vertex[s] + 1]++;
@@ -866,11 +911,16 @@ struct BatchedEngine : BatchedBase {
             }
         cuda_check(cudaMemcpy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice), "Uh");
         cuda_check(cudaMemset(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r), "Jv");
-        const size_t gsmem = (size_t)max_nv * 3 * (256 / r) * sizeof(float);
+        const size_t gsmem = hess_smem(r);
         if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         hess_ready = true;
+    }
+
+    size_t hess_smem(int r) const {
+        const int gp = 128 / r;
+        return ((size_t)max_nva * 3 * gp * r + (size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;
     }
 
     // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
@@ -889,7 +939,7 @@ struct BatchedEngine : BatchedBase {
             const int R = c.hrows[l], K = c.hcols[l];
             dim3 g((P * cols + 127) / 128, (R + 127) / 128);
             sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_X[cur], P * cols, d_Q, P * cols);
-            tangent_act_kernel<<<c.num_sms, 256, 0, s>>>(R, P, r, cols, d_Q, c.d_bh + c.boff[l], c.hact[l], d_X[cur ^ 1]);
+            tangent_act_kernel<<<c.num_sms * 8, 256, 0, s>>>(R, P, r, cols, d_Q, c.d_bh + c.boff[l], c.hact[l], d_X[cur ^ 1]);
             woff += (size_t)R * K;
             cur ^= 1;
         }
@@ -901,24 +951,22 @@ struct BatchedEngine : BatchedBase {
         }
         tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv);
         {
-            const int gp = 256 / r;
+            const int gp = 128 / r;
             dim3 g(nblk, (P + gp - 1) / gp);
-            const size_t gsmem = (size_t)max_nv * 3 * gp * sizeof(float);
+            const size_t gsmem = hess_smem(r);
             const float* recf = static_cast<const float*>(rec_f32(c));
-            auto args = std::make_tuple(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0, d_blk_vptr,
-                                        d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
-            (void)args;
+            const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
             if (r == 8)
-                elem_hess_kernel<8><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
-                                                         d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+                elem_hess_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                                                         d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
             else if (r == 16)
-                elem_hess_kernel<16><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
-                                                          d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+                elem_hess_kernel<16><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                                                          d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
             else
-                elem_hess_kernel<32><<<g, 256, gsmem, s>>>(reinterpret_cast<const int4*>(c.d_tets), recf, d_blk_tet0,
-                                                          d_blk_vptr, d_tet_loc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+                elem_hess_kernel<32><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                                                          d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
         }
-        hess_reduce_kernel<<<c.num_sms, 256, 0, s>>>(nblk, P, npair, d_Cpart, d_Ch);
+        hess_reduce_kernel<<<(P * npair + 31) / 32, 256, 0, s>>>(nblk, P, npair, d_Cpart, d_Ch);
         // gradient of the elastic potential (no inertia), times s
         combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, d_vslot_ptr, d_vslot, d_gpart, nullptr, 0, c.d_eprow, d_Th);
         {
