@@ -83,3 +83,15 @@ def test_reduced_step_api_teacher_forced_c2(oracle, product):
     assert rep.iterations == res3["iterations"][0]
     assert np.max(np.abs(state.z - res3["z"])) < 1e-7
     assert rel_err(state.positions, res3["positions"]) < 1e-9
+
+
+def test_cpp_api_binary():
+    """The C++ mirror of the reference interface (include/lipsub_b200/lipsub.hpp)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "paper_2409_03807_b200", "_lib", "test_cpp_api")
+    assert os.path.exists(exe), "run __graft_entry__.build()"
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert res.stdout.startswith("ok")
