@@ -34,6 +34,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLUSH_BYTES = 512 << 20
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the reported kernel, from the
+# committed ncu --set full captures (profiles/); None until captured for that path.
+TRAFFIC = {}
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -252,14 +255,22 @@ def main():
         e2e_t += time.perf_counter() - t0
     e2e_value = ws * K / e2e_t if e2e_t > 0 else None
 
-    # ---- roofline of the dominant kernel (output layer: the first W_out stream)
+    # ---- roofline of the dominant kernel
     hbm, peak_kind = peaks()
     alg_total, alg_out = algorithmic_bytes(n, h, E, w, per_tet_material=spec.young[1] > spec.young[0])
-    of_avg_s = float(of_ms.mean()) * 1e-3
-    achieved = alg_out / of_avg_s / 1e9
+    solve = sysm.solve_kernel_info()
+    if solve["in_use"]:
+        # one persistent launch per evaluation: the kernel IS the evaluation
+        kname, alg, dur_s = "solve_kernel (persistent, cooperative clusters)", alg_total, float(of_ms.mean()) * 1e-3
+    else:
+        kname, alg, dur_s = "out_fwd_tma_kernel", alg_out, float(of_ms.mean()) * 1e-3
+    achieved = alg / dur_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "kernel": "out_fwd_kernel", "peak_kind": peak_kind,
-            "algorithmic_bytes_per_launch": alg_out,
+            "traffic": TRAFFIC.get((args.config, solve["in_use"])), "kernel": kname, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": alg,
+            "algorithmic_formula": "w(2nh+9n)+E(16+10w)[+2wE] per E+grad eval (SURVEY 8d)" if solve["in_use"]
+            else "n h w + 56 n (W_out stream + per-row operands)",
+            "solve_grid": solve["grid"],
             "eval_frac": (alg_total / (t_total_ms * 1e-3 / K)) / 1e9 / hbm}
 
     cpu = None

@@ -163,6 +163,16 @@ lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double*
 /* Second-order Lipschitz loss mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2. */
 lsb_status lsb_lipschitz_loss(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss);
 
+/* Persistent solve kernel (one cooperative launch of thread-block clusters per
+ * evaluation / solve / step).  lsb_get_solve_info reports its grid (0 = not
+ * available for this problem, the multi-kernel CUDA-graph path is used) and whether
+ * it is in use; lsb_set_solve_kernel(ctx, 0) forces the graph path. */
+lsb_status lsb_get_solve_info(const lsb_context* ctx, int* solve_grid, int* in_use);
+lsb_status lsb_set_solve_kernel(lsb_context* ctx, int enable);
+/* Phase timestamps of the last solve-kernel launch (contexts created with LSB_TRACE=1):
+ * pairs (tag, globaltimer ns), count pairs. */
+lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int cap, int* count);
+
 /* ---- measurement hooks (bench.py) ------------------------------------------------------------ */
 /* Number of kernels this library launched since creation (every launch, graph node
  * executions counted per execution as reported by the device counters). */

@@ -100,6 +100,9 @@ SIGNATURES = [
     ("lsb_bench_evals", C.c_int, [_CTX, C.c_int, _D, C.c_size_t, _D, _D, _D]),
     ("lsb_bench_steps", C.c_int, [_CTX, C.c_int, C.POINTER(lsb_solver_config), C.c_int, C.c_size_t, _D,
                                   C.POINTER(lsb_exit_report)]),
+    ("lsb_get_solve_info", C.c_int, [_CTX, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("lsb_set_solve_kernel", C.c_int, [_CTX, C.c_int]),
+    ("lsb_get_trace", C.c_int, [_CTX, C.POINTER(C.c_ulonglong), C.c_int, C.POINTER(C.c_int)]),
     ("lsb_get_launch_count", C.c_int, [_CTX, C.POINTER(C.c_longlong)]),
     ("lsb_profile_eval", C.c_int, [_CTX, _D, C.c_int, _D, _D, _D, _D]),
 ]

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -395,7 +396,14 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             c.upload_real(c.d_rec, rec.data(), rec.size());
         }
         c.d_U = static_cast<double*>(c.dmalloc(4 * (size_t)m.V * 8));
-        c.d_forces = static_cast<double*>(c.dmalloc(12 * (size_t)m.E * 8));
+        c.d_forces = static_cast<double*>(c.dmalloc(4 * std::max<size_t>(1, m.csr_ent.size()) * 8));
+        {  // CSR position of each (tet, slot) force; -1 for pinned vertices
+            std::vector<int> fpos(4 * (size_t)m.E, -1);
+            for (int f = 0; f < m.n_free; ++f)
+                for (int k = m.csr_ptr[f]; k < m.csr_ptr[f + 1]; ++k) fpos[m.csr_ent[k]] = k;
+            c.d_fpos = static_cast<int*>(c.dmalloc(fpos.size() * 4));
+            cuda_check(cudaMemcpy(c.d_fpos, fpos.data(), fpos.size() * 4, cudaMemcpyHostToDevice), "fpos");
+        }
         c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
         cuda_check(cudaMemcpy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice), "csr");
         c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
@@ -439,6 +447,10 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.d_launch_acc = static_cast<long long*>(c.dmalloc(sizeof(long long)));
         cuda_check(cudaStreamSynchronize(c.stream), "sync");
         upload_pins(c);
+        {
+            const char* tr = getenv("LSB_TRACE");
+            if (tr && tr[0] == '1') c.d_trace = static_cast<unsigned long long*>(c.dmalloc(8 * 512));
+        }
         c.impl = make_impl(precision);
         c.impl->setup(c);
         // defaults: dt 0.05 (SolverConfig), history 8, no inertia
@@ -566,7 +578,7 @@ lsb_status lsb_lbfgs(lsb_context* ctx, double* z, const lsb_solver_config* cfg, 
         c.impl->minimize(c);
         get_state(c);
         const DevState* s = c.h_state;
-        c.launches += 3LL * s->loop_iters;
+        if (!(c.use_solve && c.impl->has_solve())) c.launches += 5LL * s->loop_iters;
         if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
         std::memcpy(z, s->x, sizeof(double) * c.r);
         fill_report(s, report);
@@ -660,6 +672,38 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
         cuda_check(cudaMemcpy(tmp.data(), c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost), "reports");
         for (int s = 0; s < steps; ++s)
             if (tmp[s].code == -kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+    });
+}
+
+lsb_status lsb_get_solve_info(const lsb_context* ctx, int* solve_grid, int* use_solve) {
+    return run([&] {
+        check_ctx(ctx);
+        if (solve_grid) *solve_grid = ctx->c.impl->has_solve() ? ctx->c.solve_grid : 0;
+        g_last_error = ctx->c.solve_reason;
+        if (use_solve) *use_solve = (ctx->c.use_solve && ctx->c.impl->has_solve()) ? 1 : 0;
+    });
+}
+
+lsb_status lsb_set_solve_kernel(lsb_context* ctx, int enable) {
+    return run([&] {
+        check_ctx(ctx);
+        ctx->c.use_solve = enable != 0;
+    });
+}
+
+lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int cap, int* count) {
+    return run([&] {
+        check_ctx(ctx);
+        *count = 0;
+        if (!ctx->c.d_trace) return;
+        std::vector<unsigned long long> t(512);
+        cuda_check(cudaMemcpy(t.data(), ctx->c.d_trace, 8 * 512, cudaMemcpyDeviceToHost), "trace");
+        const int n = (int)std::min<unsigned long long>(t[0], 255);
+        for (int i = 0; i < n && 2 * i + 1 < cap; ++i) {
+            out[2 * i] = t[1 + 2 * i];
+            out[2 * i + 1] = t[2 + 2 * i];
+        }
+        *count = n;
     });
 }
 

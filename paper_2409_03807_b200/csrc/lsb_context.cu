@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -13,7 +14,7 @@
 
 #include "../../include/lipsub_b200.h"
 #include "lsb_context.hpp"
-#include "lsb_stream.cuh"
+#include "lsb_solve.cuh"
 
 namespace lsb {
 
@@ -109,12 +110,60 @@ struct KernelSet {
     void (*vjp)(const EvalParams<TS>);
     size_t smem;      // dynamic smem of both streaming kernels (ring + scratch)
     int tile_rows;
+    size_t stage_bytes;  // one ring stage (tile + side records)
 };
 
 template <typename TS, int HP>
 KernelSet<TS> kernels_for() {
     return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
-            StreamCfg<TS, HP>::TR};
+            StreamCfg<TS, HP>::TR, (size_t)StreamCfg<TS, HP>::STAGEB};
+}
+
+using SolveFnD = void (*)(const EvalParams<double>, const SolveParams);
+using SolveFnF = void (*)(const EvalParams<float>, const SolveParams);
+template <typename TS>
+struct SolveFn {
+    using type = void (*)(const EvalParams<TS>, const SolveParams);
+};
+template <typename TS, int CS>
+typename SolveFn<TS>::type select_solve(int hp);
+template <>
+SolveFn<double>::type select_solve<double, 8>(int hp) {
+    switch (hp) {
+        case 64: return solve_kernel<double, 64, 8>;
+        case 128: return solve_kernel<double, 128, 8>;
+        case 256: return solve_kernel<double, 256, 8>;
+        case 512: return solve_kernel<double, 512, 8>;
+    }
+    return nullptr;
+}
+template <>
+SolveFn<double>::type select_solve<double, 16>(int hp) {
+    switch (hp) {
+        case 64: return solve_kernel<double, 64, 16>;
+        case 128: return solve_kernel<double, 128, 16>;
+        case 256: return solve_kernel<double, 256, 16>;
+        case 512: return solve_kernel<double, 512, 16>;
+    }
+    return nullptr;
+}
+template <>
+SolveFn<float>::type select_solve<float, 8>(int hp) {
+    switch (hp) {
+        case 128: return solve_kernel<float, 128, 8>;
+        case 256: return solve_kernel<float, 256, 8>;
+        case 512: return solve_kernel<float, 512, 8>;
+    }
+    return nullptr;
+}
+template <>
+SolveFn<float>::type select_solve<float, 16>(int hp) {
+    switch (hp) {
+        case 128: return solve_kernel<float, 128, 16>;
+        case 256: return solve_kernel<float, 256, 16>;
+        case 512: return solve_kernel<float, 512, 16>;
+    }
+    return nullptr;
 }
 
 template <typename TS>
@@ -148,6 +197,13 @@ struct Impl final : ImplBase {
     void (*ctrl)(const EvalParams<TS>, int, int, int) = nullptr;
     size_t vjp_smem = 0, ctrl_smem = 0, out_smem = 0;
     int grid_gather = 1;
+    // persistent solve kernel (cooperative launch of thread-block clusters)
+    typename SolveFn<TS>::type solve = nullptr;
+    size_t solve_smem = 0;
+    int solve_stages = 8;
+    int solve_grid = 0;
+    EvalParams<TS> ps{};  // params with solve-sized partial buffers
+    SolveShared* d_sh = nullptr;
     int cs = 8;
     cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_timed = nullptr;
     cudaEvent_t timed_ev[4] = {};
@@ -160,6 +216,14 @@ struct Impl final : ImplBase {
     }
 
     void eval_timed(Context& c, cudaEvent_t* ev) override {
+        if (solve && c.use_solve) {
+            cuda_check(cudaEventRecord(ev[0], c.stream), "ev");
+            cuda_check(cudaEventRecord(ev[1], c.stream), "ev");
+            launch_solve(c, 0, 0, 1);
+            cuda_check(cudaEventRecord(ev[2], c.stream), "ev");
+            cuda_check(cudaEventRecord(ev[3], c.stream), "ev");
+            return;
+        }
         if (!g_timed || ev[0] != timed_ev[0]) {
             if (g_timed) cudaGraphExecDestroy(g_timed);
             for (int k = 0; k < 4; ++k) timed_ev[k] = ev[k];
@@ -216,6 +280,7 @@ struct Impl final : ImplBase {
         p.forces = c.d_forces;
         p.csr_ptr = c.d_csr_ptr;
         p.csr_ent = c.d_csr_ent;
+        p.fpos = reinterpret_cast<const int4*>(c.d_fpos);
         p.Wh = c.d_Wh;
         p.bh = c.d_bh;
         for (int l = 0; l < c.nhid; ++l) {
@@ -251,7 +316,7 @@ struct Impl final : ImplBase {
                    "occupancy vjp");
         p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<TS>, 256, 0), "occupancy gather");
-        grid_gather = std::max(1, std::min((c.n + 255) / 256, c.num_sms * std::max(1, occ)));
+        grid_gather = std::max(1, std::min((m.n_free + 255) / 256, c.num_sms * std::max(1, occ)));
         p.group = 16;
         p.n_groups = (p.grid_vjp + p.group - 1) / p.group;
         // control cluster: hidden weights split in row slices over cs CTAs
@@ -290,7 +355,109 @@ struct Impl final : ImplBase {
         p.ybar_grp = c.d_ybar_grp;
         p.grp_cnt = c.d_grp_cnt;
         p.in_graph = 0;
+        setup_solve(c);
     }
+
+    void setup_solve(Context& c) {
+        const char* env = getenv("LSB_DISABLE_SOLVE_KERNEL");
+        if (env && env[0] == '1') {
+            c.solve_reason = "disabled by LSB_DISABLE_SOLVE_KERNEL";
+            return;
+        }
+        solve = cs == 8 ? select_solve<TS, 8>(c.hp) : select_solve<TS, 16>(c.hp);
+        if (!solve) {
+            c.solve_reason = "no solve kernel instantiated for this width";
+            return;
+        }
+        // ring of 16 stages when it fits beside the control-cluster area, else 8 (multiple of 8, see
+        // kStreamStages)
+        solve_stages = 16;
+        solve_smem = solve_stages * (ks.stage_bytes + 16) + ctrl_smem + 256;
+        if (solve_smem > 227 * 1024) {
+            solve_stages = 8;
+            solve_smem = solve_stages * (ks.stage_bytes + 16) + ctrl_smem + 256;
+        }
+        if (solve_smem > 227 * 1024) {
+            c.solve_reason = "shared memory " + std::to_string(solve_smem) + " B exceeds 227 KB";
+            solve = nullptr;
+            return;
+        }
+        if (cudaFuncSetAttribute(solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem) != cudaSuccess ||
+            (cs == 16 && cudaFuncSetAttribute(solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+            c.solve_reason = std::string("attribute: ") + cudaGetErrorString(cudaGetLastError());
+            solve = nullptr;
+            return;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(kStreamThreads);
+        cfg.dynamicSmemBytes = solve_smem;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)solve, &cfg) != cudaSuccess || nclusters < 1) {
+            c.solve_reason = std::string("occupancy: ") + cudaGetErrorString(cudaGetLastError());
+            solve = nullptr;
+            return;
+        }
+        solve_grid = nclusters * cs;
+        ps = p;
+        ps.e_part_out = static_cast<double*>(c.dmalloc(sizeof(double) * solve_grid));
+        ps.e_part_elem = static_cast<double*>(c.dmalloc(sizeof(double) * solve_grid));
+        ps.ybar_part = static_cast<double*>(c.dmalloc(sizeof(double) * (size_t)solve_grid * c.hp));
+        d_sh = static_cast<SolveShared*>(c.dmalloc(sizeof(SolveShared)));
+        c.solve_grid = solve_grid;
+    }
+
+    SolveParams solve_params(Context& c, int task, int quasi, int want_grad = 1) {
+        SolveParams sp{};
+        sp.task = task;
+        sp.quasi = quasi;
+        sp.nst = solve_stages;
+        sp.want_grad = want_grad;
+        sp.u_state = c.d_u_state;
+        sp.v_state = c.d_v_state;
+        sp.a_ext = c.d_a_ext;
+        sp.z_state = c.d_z_state;
+        sp.u_state_w = c.d_u_state;
+        sp.v_state_w = c.d_v_state;
+        sp.vpinned = c.d_vpinned;
+        sp.pin_disp = c.d_pin_disp;
+        sp.sh = d_sh;
+        sp.launch_acc = nullptr;
+        sp.trace = c.d_trace;
+        return sp;
+    }
+
+    void launch_solve(Context& c, int task, int quasi, int want_grad = 1) {
+        SolveParams sp = solve_params(c, task, quasi, want_grad);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.gridDim = dim3(solve_grid);
+        cfg.blockDim = dim3(kStreamThreads);
+        cfg.dynamicSmemBytes = solve_smem;
+        cfg.stream = c.stream;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        cuda_check(cudaLaunchKernelEx(&cfg, solve, ps, sp), "solve kernel launch");
+        c.launches += 1;
+    }
+
+    bool has_solve() const override { return solve != nullptr; }
+    void solve_eval(Context& c) override { launch_solve(c, 0, 0, 1); }
+    void solve_minimize(Context& c) override { launch_solve(c, 1, 0); }
+    void solve_step(Context& c, int quasi) override { launch_solve(c, 2, quasi); }
 
     void launch_ctrl(cudaStream_t s, int cmode, int smode, int want) {
         ctrl<<<cs, 256, ctrl_smem, s>>>(p, cmode, smode, want);
@@ -307,6 +474,10 @@ struct Impl final : ImplBase {
     }
 
     void eval(Context& c, bool want_grad) override {
+        if (solve && c.use_solve) {
+            launch_solve(c, 0, 0, want_grad ? 1 : 0);
+            return;
+        }
         cudaStream_t s = c.stream;
         launch_ctrl(s, kCtrlStart, kModeEval, want_grad ? 1 : 0);
         c.launches += 1;
@@ -446,12 +617,20 @@ struct Impl final : ImplBase {
     }
 
     void minimize(Context& c) override {
+        if (solve && c.use_solve) {
+            launch_solve(c, 1, 0);
+            return;
+        }
         if (!g_min) build_min_graph(c);
         cuda_check(cudaGraphLaunch(g_min, c.stream), "graph launch (minimize)");
         c.launches += 1;  // start; loop bodies are counted from st->loop_iters
     }
 
     void step(Context& c) override {
+        if (solve && c.use_solve) {
+            launch_solve(c, 2, c.h_state->quasi_static);
+            return;
+        }
         if (!g_step) {
             c.ensure_step_buffers(1);
             build_step_graph(c);

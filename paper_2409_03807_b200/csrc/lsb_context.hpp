@@ -37,6 +37,11 @@ struct ImplBase {
     // One evaluation at st->zt as a graph with event-record nodes:
     // ev[0] | ctrl(start) | ev[1] | out_fwd | ev[2] | elem, vjp, ctrl | ev[3]
     virtual void eval_timed(Context& c, cudaEvent_t* ev) = 0;
+    // persistent solve kernel (one cooperative cluster launch per eval / solve / step)
+    virtual bool has_solve() const = 0;
+    virtual void solve_eval(Context& c) = 0;
+    virtual void solve_minimize(Context& c) = 0;
+    virtual void solve_step(Context& c, int quasi) = 0;
 };
 std::unique_ptr<ImplBase> make_impl(int precision);
 
@@ -78,6 +83,7 @@ struct Context {
     double* d_U = nullptr;
     double* d_forces = nullptr;
     int *d_csr_ptr = nullptr, *d_csr_ent = nullptr;
+    int* d_fpos = nullptr;  // E x 4 CSR positions of tet-slot forces
     double *d_Wh = nullptr, *d_bh = nullptr;
     double* d_a_hid = nullptr;
     double* d_y_last = nullptr;
@@ -96,7 +102,10 @@ struct Context {
     bool state_set = false;
     long long* d_launch_acc = nullptr;
     long long launches = 0;
-    int grid_out = 0, grid_elem = 0, grid_vjp = 0;
+    int grid_out = 0, grid_elem = 0, grid_vjp = 0, solve_grid = 0;
+    bool use_solve = true;
+    std::string solve_reason;
+    unsigned long long* d_trace = nullptr;  // solve-kernel phase trace (LSB_TRACE=1)  // route eval/minimize/step through the persistent kernel when available
 
     std::unique_ptr<ImplBase> impl;
     std::unique_ptr<BatchedBase> batched;

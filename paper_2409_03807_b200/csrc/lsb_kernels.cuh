@@ -95,9 +95,10 @@ struct EvalParams {
     const int4* tets;
     const TS* rec;       // E x 12: Dminv (row-major 9), vol, mu, lambda
     double* U;           // V x 4 displacement (w unused)
-    double* forces;      // E x 12: local vertex forces (slot-major, xyz)
+    double* forces;      // nnz x 4: per (tet, free slot) force vectors in CSR order (xyz, pad)
     const int* csr_ptr;
     const int* csr_ent;
+    const int4* fpos;    // E: CSR position of each tet slot's force (-1 = pinned vertex)
     // hidden layers (fp64)
     const double* Wh;    // row-major, concatenated
     const double* bh;
@@ -483,6 +484,18 @@ __device__ __forceinline__ double tet_energy_forces(const double* u0, const doub
     return tet_energy_forces_t<double>(u0, u1, u2, u3, rec, f);
 }
 
+// Scatter one tet's 12 local forces to their vertices' CSR slots (32-byte vectors).
+__device__ __forceinline__ void store_forces_csr(double* F, int4 pos, const double* f) {
+    const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (ps[k] >= 0) {
+            double2* o = reinterpret_cast<double2*>(F + (size_t)ps[k] * 4);
+            __stcg(o, make_double2(f[3 * k], f[3 * k + 1]));
+            __stcg(o + 1, make_double2(f[3 * k + 2], 0.0));
+        }
+}
+
 template <typename TS>
 __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
     __shared__ double red[32];
@@ -513,9 +526,7 @@ __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
             load_rec<TS>(p.rec, (size_t)e, rec);
             double f[12];
             eacc += tet_energy_forces(u[q][0], u[q][1], u[q][2], u[q][3], rec, f);
-            double2* out = reinterpret_cast<double2*>(p.forces + (size_t)e * 12);
-#pragma unroll
-            for (int k = 0; k < 6; ++k) __stcg(out + k, make_double2(f[2 * k], f[2 * k + 1]));
+            store_forces_csr(p.forces, __ldg(p.fpos + e), f);
         }
     }
     const double tot = block_sum(eacc, red);

@@ -15,7 +15,7 @@ namespace lsb {
 template <typename TS, int HP>
 struct StreamCfg {
     static constexpr int ROWB = HP * (int)sizeof(TS);
-    static constexpr int TR = (16384 / ROWB) < 8 ? 8 : (16384 / ROWB);  // rows per tile
+    static constexpr int TR = (8192 / ROWB) < 8 ? 8 : (8192 / ROWB);  // rows per tile (8 KB)
     static constexpr int TILEB = TR * ROWB;
     static constexpr int V4 = 16 / (int)sizeof(TS);  // elements per 16-byte chunk
     static constexpr int NPL = HP / 32;              // elements per lane per row
@@ -28,7 +28,11 @@ struct StreamCfg {
     static_assert(TILEB % 16 == 0 && STAGEB % 16 == 0, "stage alignment");
 };
 
-constexpr int kStreamStages = 6;
+// Stage count of the streaming kernels' rings.  Tiles are consumed warp-per-tile
+// (tile i by consumer warp i % 8), so the stage count MUST be a multiple of 8:
+// then the previous user of a stage is the same warp, and a warp can never wait
+// on a phase two behind (mbarrier parity aliasing).
+constexpr int kStreamStages = 8;
 constexpr int kStreamThreads = 288;  // 8 consumer warps + 1 producer warp
 
 template <typename TS, int HP>
@@ -82,6 +86,86 @@ __device__ __forceinline__ void stream_producer(const EvalParams<TS>& p, int t0,
     }
 }
 
+// One warp computes every row of a forward tile: TR independent dot products,
+// interleaved butterfly reductions, lane j runs the epilogue of row j.
+template <typename TS, int HP>
+__device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
+                                           const double (&y)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4],
+                                           int has_inertia, double inv_dt2, bool ident) {
+    using C = StreamCfg<TS, HP>;
+    const int lane = threadIdx.x & 31;
+    const int rows = min(C::TR, p.n - t * C::TR);
+    const TS* tile = reinterpret_cast<const TS*>(st);
+    const double* ep = reinterpret_cast<const double*>(st + C::TILEB);
+    double acc[C::TR];
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j) {
+        acc[j] = 0.0;
+        if (j < rows) {
+            const TS* rowp = tile + (size_t)j * HP;
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c) {
+                double w[C::V4];
+                lds_chunk<TS>(rowp, c * 32 + lane, w);
+#pragma unroll
+                for (int q = 0; q < C::V4; ++q) acc[j] = fma(w[q], y[c][q], acc[j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int j = 0; j < C::TR; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    double mine = 0.0;
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j)
+        if (lane == j) mine = acc[j];
+    double e = 0.0;
+    if (lane < rows) {
+        const int row = t * C::TR + lane;
+        const double* e6 = ep + lane * 6;
+        const double a = mine + e6[0];
+        double phi = a;
+        if (!ident) {
+            phi = act_eval(p.out_act, a, 0);
+            p.dsout[row] = e6[1] * act_eval(p.out_act, a, 1);
+        }
+        const double uval = e6[1] * phi + e6[2];
+        p.U[(int)e6[4]] = uval;
+        if (has_inertia) {
+            const double diff = uval - e6[5];
+            p.rin[row] = inv_dt2 * (e6[3] * diff);
+            e = e6[3] * diff * diff;
+        }
+    }
+    return e;
+}
+
+// One warp accumulates a VJP tile into its per-lane column accumulators.
+template <typename TS, int HP>
+__device__ __forceinline__ void vjp_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
+                                         double (&acc)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4]) {
+    using C = StreamCfg<TS, HP>;
+    const int lane = threadIdx.x & 31;
+    const int rows = min(C::TR, p.n - t * C::TR);
+    const TS* tile = reinterpret_cast<const TS*>(st);
+    const double* tv = reinterpret_cast<const double*>(st + C::TILEB);
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j) {
+        if (j < rows) {
+            const double tval = tv[j];
+            const TS* rowp = tile + (size_t)j * HP;
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c) {
+                double w[C::V4];
+                lds_chunk<TS>(rowp, c * 32 + lane, w);
+#pragma unroll
+                for (int q = 0; q < C::V4; ++q) acc[c][q] = fma(w[q], tval, acc[c][q]);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- K2 (TMA): output layer forward
 template <typename TS, int HP>
 __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalParams<TS> p) {
@@ -95,7 +179,7 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
     if (tid == 0) {
         for (int s = 0; s < kStreamStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 8);
+            mbar_init(&empty[s], 1);
         }
         mbar_fence_init();
     }
@@ -115,44 +199,12 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
             for (int q = 0; q < C::V4; ++q) y[c][q] = p.y_last[(c * 32 + lane) * C::V4 + q];
         const int has_inertia = p.st->has_inertia;
         const bool ident = p.out_act == kIdentity;
-        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        // warp-per-tile: tile i is consumed entirely by warp i % 8
+        for (int t = t0 + warp, i = warp; t < t1; t += 8, i += 8) {
             const int s = i % kStreamStages, k = i / kStreamStages;
-            const int rows = min(C::TR, p.n - t * C::TR);
             mbar_wait(&full[s], k & 1);
             const unsigned char* st = ring + (size_t)s * C::STAGEB;
-            const TS* tile = reinterpret_cast<const TS*>(st);
-            const double* ep = reinterpret_cast<const double*>(st + C::TILEB);
-            for (int rr = warp; rr < rows; rr += 8) {
-                const TS* rowp = tile + (size_t)rr * HP;
-                double acc = 0.0;
-#pragma unroll
-                for (int c = 0; c < C::NCH; ++c) {
-                    double w[C::V4];
-                    lds_chunk<TS>(rowp, c * 32 + lane, w);
-#pragma unroll
-                    for (int q = 0; q < C::V4; ++q) acc = fma(w[q], y[c][q], acc);
-                }
-                acc = warp_sum(acc);
-                if (lane == 0) {
-                    const int row = t * C::TR + rr;
-                    const double* e6 = ep + rr * 6;
-                    const double a = acc + e6[0];
-                    const double es = e6[1];
-                    double phi = a;
-                    if (!ident) {
-                        phi = act_eval(p.out_act, a, 0);
-                        p.dsout[row] = es * act_eval(p.out_act, a, 1);
-                    }
-                    const double uval = es * phi + e6[2];
-                    p.U[(int)e6[4]] = uval;
-                    if (has_inertia) {
-                        const double em = e6[3];
-                        const double diff = uval - e6[5];
-                        p.rin[row] = inv_dt2 * (em * diff);
-                        eacc += em * diff * diff;
-                    }
-                }
-            }
+            eacc += fwd_tile<TS, HP>(p, st, t, y, has_inertia, inv_dt2, ident);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
@@ -164,21 +216,51 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
 // ---------------------------------------------------------------- K3b: vertex gather (+ inertia)
 // tv_i = s_i phi'(a_i) (sum of the per-tet forces on DOF i in ascending tet id
 // + inertia residual) -- the full-space gradient times the output scaling.
+// One free vertex, 4 cooperating lanes: lane q sums segment entries k = b + q,
+// b + q + 4, ... of the vertex's CSR force vectors (ascending tet id), the four
+// partials are combined in fixed lane order; + inertia, times s -> tv (3 rows).
+// Must be called by all lanes of the warp (lanes 4v..4v+3 share vertex v).
+template <typename TS>
+__device__ __forceinline__ void gather_vertex4(const EvalParams<TS>& p, int f, int has_inertia, bool ident) {
+    const int lane = threadIdx.x & 31, q = lane & 3;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (f < p.n_free) {
+        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
+        const double2* F = reinterpret_cast<const double2*>(p.forces);
+#pragma unroll 4
+        for (int k = b + q; k < e; k += 4) {
+            const double2 a = __ldcg(F + 2 * (size_t)k);
+            const double2 c = __ldcg(F + 2 * (size_t)k + 1);
+            gx += a.x;
+            gy += a.y;
+            gz += c.x;
+        }
+    }
+    // fixed-order combine: (q0 + q1) + (q2 + q3)
+    gx += __shfl_xor_sync(0xffffffffu, gx, 1);
+    gy += __shfl_xor_sync(0xffffffffu, gy, 1);
+    gz += __shfl_xor_sync(0xffffffffu, gz, 1);
+    gx += __shfl_xor_sync(0xffffffffu, gx, 2);
+    gy += __shfl_xor_sync(0xffffffffu, gy, 2);
+    gz += __shfl_xor_sync(0xffffffffu, gz, 2);
+    if (f < p.n_free && q < 3) {
+        const int row = 3 * f + q;
+        double g = q == 0 ? gx : (q == 1 ? gy : gz);
+        if (has_inertia) g += __ldcg(p.rin + row);
+        p.tv[row] = g * (ident ? p.eprow[6 * (size_t)row + 1] : __ldcg(p.dsout + row));
+    }
+}
+
 template <typename TS>
 __global__ void __launch_bounds__(256) gather_kernel(const EvalParams<TS> p) {
     const DevState* st = p.st;
     if (!st->need_grad) return;
     const bool ident = p.out_act == kIdentity;
     const int has_inertia = st->has_inertia;
-    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < p.n; row += gridDim.x * blockDim.x) {
-        const int f = row / 3, c = row - 3 * f;
-        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
-        double g = 0;
-#pragma unroll 8
-        for (int k = b; k < e; ++k) g += __ldcg(p.forces + (size_t)__ldg(p.csr_ent + k) * 3 + c);
-        if (has_inertia) g += p.rin[row];
-        p.tv[row] = g * (ident ? __ldg(p.sout + row) : p.dsout[row]);
-    }
+    const int nthr = gridDim.x * blockDim.x;
+    // warp-uniform trip count: gather_vertex4 shuffles across the whole warp
+    for (int wb = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; wb < 4 * p.n_free; wb += nthr)
+        gather_vertex4(p, (wb + (threadIdx.x & 31)) >> 2, has_inertia, ident);
 }
 
 // ---------------------------------------------------------------- K4 (TMA): VJP partials
@@ -197,7 +279,7 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_tma_kernel(const EvalParam
     if (tid == 0) {
         for (int s = 0; s < kStreamStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 8);
+            mbar_init(&empty[s], 1);
         }
         mbar_fence_init();
     }
@@ -213,24 +295,10 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_tma_kernel(const EvalParam
     if (warp == 8) {
         if (lane == 0) stream_producer<TS, HP, false>(p, t0, t1, ring, full, empty);
     } else {
-        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        for (int t = t0 + warp, i = warp; t < t1; t += 8, i += 8) {
             const int s = i % kStreamStages, k = i / kStreamStages;
-            const int rows = min(C::TR, p.n - t * C::TR);
             mbar_wait(&full[s], k & 1);
-            const unsigned char* stg = ring + (size_t)s * C::STAGEB;
-            const TS* tile = reinterpret_cast<const TS*>(stg);
-            const double* tv = reinterpret_cast<const double*>(stg + C::TILEB);
-            for (int rr = warp; rr < rows; rr += 8) {
-                const double tval = tv[rr];
-                const TS* rowp = tile + (size_t)rr * HP;
-#pragma unroll
-                for (int c = 0; c < C::NCH; ++c) {
-                    double w[C::V4];
-                    lds_chunk<TS>(rowp, c * 32 + lane, w);
-#pragma unroll
-                    for (int q = 0; q < C::V4; ++q) acc[c][q] = fma(w[q], tval, acc[c][q]);
-                }
-            }
+            vjp_tile<TS, HP>(p, ring + (size_t)s * C::STAGEB, t, acc);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }

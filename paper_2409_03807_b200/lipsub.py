@@ -406,6 +406,15 @@ class ReducedSystem:
         check(lib().lsb_lipschitz_loss(self._h, Z1.shape[0], dptr(Z1), dptr(Z2), C.byref(out)))
         return out.value
 
+    # --- execution path
+    def solve_kernel_info(self):
+        g, u = C.c_int(), C.c_int()
+        check(lib().lsb_get_solve_info(self._h, C.byref(g), C.byref(u)))
+        return {"grid": g.value, "in_use": bool(u.value), "reason": lib().lsb_last_error().decode()}
+
+    def use_solve_kernel(self, enable: bool):
+        check(lib().lsb_set_solve_kernel(self._h, int(enable)))
+
     # --- measurement hooks
     def launch_count(self) -> int:
         v = C.c_longlong()

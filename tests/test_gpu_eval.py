@@ -21,10 +21,14 @@ def _pair(name, precision, oracle, product):
     return pr, sysm, ob
 
 
+@pytest.mark.parametrize("path", ["solve", "graph"])
 @pytest.mark.parametrize("name,precision", [("c1", "fp64"), ("c1", "fp32"), ("c2", "fp64"), ("c2", "fp32")])
-def test_eval_matches_oracle(name, precision, oracle, product):
+def test_eval_matches_oracle(name, precision, path, oracle, product):
     from paper_2409_03807_b200 import configs
     pr, sysm, ob = _pair(name, precision, oracle, product)
+    sysm.use_solve_kernel(path == "solve")
+    if path == "solve":
+        assert sysm.solve_kernel_info()["in_use"]
     assert np.allclose(sysm.mass, ob.mass, rtol=1e-15, atol=0)
     qbar = configs.timestep0_qbar(pr, ob.mass)
     obj = product.ReducedObjective(sysm, qbar, configs.DT)

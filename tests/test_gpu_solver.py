@@ -12,11 +12,13 @@ from conftest import rel_err
 pytestmark = pytest.mark.gpu
 
 
-def test_lbfgs_device_matches_oracle_c1(oracle, product):
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_lbfgs_device_matches_oracle_c1(path, oracle, product):
     from paper_2409_03807_b200 import configs
     P = product
     pr = configs.build("c1")
     sysm = pr.system("fp64")
+    sysm.use_solve_kernel(path == "solve")
     ob = oracle.problem("c1")
     qbar = configs.timestep0_qbar(pr, ob.mass)
     cfg = configs.solver_config()
@@ -40,10 +42,12 @@ def _ofun(ob, qbar, x, g):
     return v
 
 
-def test_simulate_c1_free_running(oracle, product):
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_simulate_c1_free_running(path, oracle, product):
     from paper_2409_03807_b200 import configs
     pr = configs.build("c1")
     sysm = pr.system("fp64")
+    sysm.use_solve_kernel(path == "solve")
     ob = oracle.problem("c1")
     cfg = configs.solver_config()
     steps = 100

@@ -1,0 +1,32 @@
+"""Phase trace of one solve-kernel evaluation (LSB_TRACE=1)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+os.environ["LSB_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2409_03807_b200 as P  # noqa: E402
+from paper_2409_03807_b200 import configs  # noqa: E402
+
+names = {0: "enter", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
+         30: "gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid"}
+for name in sys.argv[1:] or ["c2"]:
+    pr = configs.build(name)
+    sysm = pr.system()
+    sysm.set_inertia(configs.timestep0_qbar(pr, sysm.mass), configs.DT)
+    z = 0.5 * np.random.default_rng(0).standard_normal(pr.model.r)
+    for rep in range(3):
+        sysm.eval(z)
+    buf = (C.c_ulonglong * 512)()
+    cnt = C.c_int()
+    P.check(P.lib().lsb_get_trace(sysm.handle, buf, 512, C.byref(cnt)))
+    t0 = buf[1]
+    prev = t0
+    out = []
+    for i in range(cnt.value):
+        tag, t = buf[2 * i], buf[2 * i + 1]
+        out.append(f"{names.get(tag, tag)}:{(t - prev) / 1000:.1f}")
+        prev = t
+    print(name, sysm.solve_kernel_info(), f"total {(prev - t0) / 1000:.1f} us |", " ".join(out))
