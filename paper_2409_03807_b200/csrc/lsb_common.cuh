@@ -168,6 +168,9 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// Order this thread's generic-proxy global writes before later async-proxy
+// (cp.async.bulk) reads of them; used before the barrier that publishes them.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -200,7 +200,7 @@ struct Impl final : ImplBase {
     // persistent solve kernel (cooperative launch of thread-block clusters)
     typename SolveFn<TS>::type solve = nullptr;
     size_t solve_smem = 0;
-    int solve_stages = 8;
+    int solve_spw = 1, solve_spw_ctrl = 1;
     int solve_grid = 0;
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
     SolveShared* d_sh = nullptr;
@@ -369,14 +369,20 @@ struct Impl final : ImplBase {
             c.solve_reason = "no solve kernel instantiated for this width";
             return;
         }
-        // ring of 16 stages when it fits beside the control-cluster area, else 8 (multiple of 8, see
-        // kStreamStages)
-        solve_stages = 16;
-        solve_smem = solve_stages * (ks.stage_bytes + 16) + ctrl_smem + 256;
-        if (solve_smem > 227 * 1024) {
-            solve_stages = 8;
-            solve_smem = solve_stages * (ks.stage_bytes + 16) + ctrl_smem + 256;
-        }
+        // self-issued rings: 9 warps x spw stages each, as many as fit (control CTAs: their
+        // control area follows the ring)
+        const size_t cap = 227 * 1024 - 256;
+        const size_t ctrl_area = ((size_t)p.ctrl_smem_w + ctrl_fixed_words()) * sizeof(double);
+        const int nw = kSolveThreads / 32;
+        solve_spw_ctrl = 0;
+        for (int k = 1; k * nw <= kSolveMaxStages && k <= 3; ++k)
+            if (kSolveBarBytes + k * nw * ks.stage_bytes + ctrl_area <= cap) solve_spw_ctrl = k;
+        solve_spw = std::max(solve_spw_ctrl, 1);
+        for (int k = 1; k * nw <= kSolveMaxStages && k <= 2; ++k)
+            if (kSolveBarBytes + k * nw * ks.stage_bytes <= cap) solve_spw = std::max(solve_spw, k);
+        solve_smem = std::max(kSolveBarBytes + solve_spw_ctrl * nw * ks.stage_bytes + ctrl_area,
+                              kSolveBarBytes + solve_spw * nw * ks.stage_bytes);
+        if (solve_spw_ctrl == 0) solve_smem = cap + 1;
         if (solve_smem > 227 * 1024) {
             c.solve_reason = "shared memory " + std::to_string(solve_smem) + " B exceeds 227 KB";
             solve = nullptr;
@@ -395,7 +401,7 @@ struct Impl final : ImplBase {
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3(cs);
-        cfg.blockDim = dim3(kStreamThreads);
+        cfg.blockDim = dim3(kSolveThreads);
         cfg.dynamicSmemBytes = solve_smem;
         cfg.attrs = at;
         cfg.numAttrs = 1;
@@ -412,13 +418,17 @@ struct Impl final : ImplBase {
         ps.ybar_part = static_cast<double*>(c.dmalloc(sizeof(double) * (size_t)solve_grid * c.hp));
         d_sh = static_cast<SolveShared*>(c.dmalloc(sizeof(SolveShared)));
         c.solve_grid = solve_grid;
+        c.solve_reason = "ring stages/warp " + std::to_string(solve_spw) + " (control CTAs " +
+                         std::to_string(solve_spw_ctrl) + "), smem " + std::to_string(solve_smem) + " B";
     }
 
     SolveParams solve_params(Context& c, int task, int quasi, int want_grad = 1) {
         SolveParams sp{};
         sp.task = task;
         sp.quasi = quasi;
-        sp.nst = solve_stages;
+        sp.spw = solve_spw;
+        sp.spw_ctrl = solve_spw_ctrl;
+        if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);
         sp.want_grad = want_grad;
         sp.u_state = c.d_u_state;
         sp.v_state = c.d_v_state;
@@ -445,7 +455,7 @@ struct Impl final : ImplBase {
         at[1].id = cudaLaunchAttributeCooperative;
         at[1].val.cooperative = 1;
         cfg.gridDim = dim3(solve_grid);
-        cfg.blockDim = dim3(kStreamThreads);
+        cfg.blockDim = dim3(kSolveThreads);
         cfg.dynamicSmemBytes = solve_smem;
         cfg.stream = c.stream;
         cfg.attrs = at;

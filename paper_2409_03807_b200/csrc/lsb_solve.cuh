@@ -15,6 +15,10 @@
 
 namespace lsb {
 
+constexpr int kSolveThreads = 288;  // 9 warps: all stream (self-issued rings) and all compute
+constexpr int kSolveMaxStages = 36;
+constexpr int kSolveBarBytes = 512;  // full barriers (kSolveMaxStages x 8 B, padded)
+
 // Launch-wide scalars the non-control CTAs need (written by the control CTA).
 struct SolveShared {
     int mode, phase, want_grad, done;
@@ -26,7 +30,9 @@ struct SolveParams {
     int task;         // 0 = eval (ctrl start + one evaluation), 1 = minimize, 2 = step
     int quasi;        // step: quasi-static
     int want_grad;    // eval: gradient wanted
-    int nst;          // ring stages (8 or 16: a multiple of the 8 consumer warps)
+    int spw;          // ring stages per warp, non-control CTAs
+    int spw_ctrl;     // ring stages per warp, control CTAs (their control area follows the ring)
+    int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
     // dynamics
     const double* u_state;
     const double* v_state;
@@ -43,20 +49,36 @@ struct SolveParams {
 
 
 // ---- control-cluster helpers (weights resident in smem) -------------------------------------------
+// The hidden MLP is row-partitioned over the CS CTAs of cluster 0 (part_lo).  Both
+// directions are push-based: a CTA stores what other CTAs need straight into their
+// shared memory (DSMEM), then one cluster barrier per layer publishes it, so every
+// operand read is local.
+constexpr int kCtrlRecv = 1024;  // CS x (rows per CTA) receive slots (<= 16 x 64)
 struct CtrlSmem {
     double* wsl;      // staged W row slices
-    double* ybuf;     // kMaxHidden
-    double* slice[2]; // 64 each
-    double* part[2];  // kMaxHidden each
+    double* xin[2];   // layer inputs (kMaxHidden each), double-buffered across layers
+    double* rbuf[2];  // backward receive buffers [src CTA][own row] (kCtrlRecv each)
+    double* tmp;      // ybar reduction scratch (kSolveThreads)
     double* bsl;      // kMaxLayers * 64
     double* asl;      // kMaxLayers * 64
     DevState* sst;
     int woff[kMaxLayers];
 };
+constexpr size_t ctrl_fixed_words() {
+    return 2 * kMaxHidden + 2 * kCtrlRecv + kSolveThreads + 2 * kMaxLayers * 64 + sizeof(DevState) / sizeof(double) + 8;
+}
+
+// owner CTA of row j under part_lo(R, CS, .) (32-bit arithmetic; R <= kMaxHidden)
+template <int CS>
+__device__ __forceinline__ int part_owner(int j, int R) {
+    int q = (j * CS) / R;
+    if (q < CS - 1 && (R * (q + 1)) / CS <= j) ++q;
+    if ((R * q) / CS > j) --q;
+    return q;
+}
 
 template <typename TS, int CS>
 __device__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state) {
-    const int tid = threadIdx.x;
     int off = 0;
     for (int l = 0; l < p.nhid; ++l) {
         const int R = p.hrows[l], C = p.hcols[l];
@@ -70,19 +92,21 @@ __device__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool wi
         stage_doubles(reinterpret_cast<double*>(cs.sst), reinterpret_cast<const double*>(p.st),
                       (int)(sizeof(DevState) / sizeof(double)));
     cp_async_wait_all();
-    (void)tid;
     __syncthreads();
 }
 
-// Backward through the hidden layers; ybar of the last hidden layer is the
-// fixed-order sum of the per-CTA partials (G x hp).  Result -> sst->gz (CTA 0).
-template <typename TS, int CS>
+// Backward through the hidden layers.  ybar of the last hidden layer is the
+// fixed-order sum of the per-CTA partials (G x hp); each CTA reduces its own
+// rows.  Layer l: partial p_c[j] = sum_{own i} W[i][j] gy[i] is pushed to the owner
+// of j (layer l-1 rows; CTA 0 for l = 0), which sums the CS partials in CTA order.
+// Result -> sst->gz (CTA 0).  Ends with __syncthreads.
+template <typename TS, int CS, typename Stamp>
 __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
-                              const double* ypart) {
-    const int tid = threadIdx.x;
+                              const double* ypart, Stamp& stamp) {
+    const int tid = threadIdx.x, nt = blockDim.x;
     if (p.nhid == 0) {
         if (c == 0)
-            for (int j = tid; j < p.r; j += blockDim.x) {
+            for (int j = tid; j < p.r; j += nt) {
                 double s = 0.0;
                 for (int b = 0; b < G; ++b) s += __ldcg(ypart + (size_t)b * p.hp + j);
                 cs.sst->gz[j] = s;
@@ -90,144 +114,144 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
         __syncthreads();
         return;
     }
-    const int Rl = p.hrows[p.nhid - 1];
+    double gy[2];  // this thread's own-row gradients (rows tid, tid + nt), layer being processed
     {
-        // own columns j0..j1 of ybar: threads split (column, partial chunk), fixed combine order
-        const int j0 = part_lo(Rl, CS, c), j1 = part_lo(Rl, CS, c + 1);
-        const int ncol = j1 - j0;
-        const int per = ncol > 0 ? max(1, (int)blockDim.x / ncol) : 1;  // threads per column
-        const int chunk = (G + per - 1) / per;
-        double* tmp = cs.part[0];  // ncol x per partial sums (<= blockDim.x)
-        const int col = tid / per, q = tid % per;
-        if (col < ncol) {
+        const int Rl = p.hrows[p.nhid - 1];
+        const int j0 = part_lo(Rl, CS, c), ncol = part_lo(Rl, CS, c + 1) - j0;
+        const int per = max(1, nt / max(ncol, 1));  // threads per column
+        const int col = tid % max(ncol, 1), q = tid / max(ncol, 1);
+        if (q < per && col < ncol) {
             double s = 0.0;
-            const int b0 = q * chunk, b1 = min(G, b0 + chunk);
-#pragma unroll 4
-            for (int b = b0; b < b1; ++b) s += __ldcg(ypart + (size_t)b * p.hp + j0 + col);
-            tmp[col * per + q] = s;
+            for (int b0 = q; b0 < G; b0 += 8 * per) {
+                double v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int b = b0 + k * per;
+                    v[k] = b < G ? __ldcg(ypart + (size_t)b * p.hp + j0 + col) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s += v[k];
+            }
+            cs.tmp[q * ncol + col] = s;
         }
         __syncthreads();
-        for (int j = tid; j < ncol; j += blockDim.x) {
+        for (int k = 0; k < 2; ++k) {
+            const int i = tid + k * nt;
             double s = 0.0;
-            for (int k = 0; k < per; ++k) s += tmp[j * per + k];
-            cs.slice[0][j] = s;
+            if (i < ncol)
+                for (int qq = 0; qq < per; ++qq) s += cs.tmp[qq * ncol + i];
+            gy[k] = s;
         }
+        __syncthreads();  // tmp is reused below
     }
-    __syncthreads();
+    stamp(90);
     for (int l = p.nhid - 1; l >= 0; --l) {
         const int R = p.hrows[l], C = p.hcols[l];
-        const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-        double* pt = cs.part[l & 1];
-        for (int i = tid; i < i1 - i0; i += blockDim.x)
-            cs.slice[0][i] *= act_eval(p.hact[l], cs.asl[l * 64 + i], 1);
+        const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
+        double* gys = cs.tmp;  // own-row gradient times act' (nrow <= 64)
+        for (int k = 0; k < 2; ++k) {
+            const int i = tid + k * nt;
+            if (i < nrow) gys[i] = gy[k] * act_eval(p.hact[l], cs.asl[l * 64 + i], 1);
+        }
         __syncthreads();
         const double* Ws = cs.wsl + cs.woff[l];
-        for (int j = tid; j < C; j += blockDim.x) {
-            double s = 0.0;
-            for (int i = 0; i < i1 - i0; ++i) s = fma(Ws[i * C + j], cs.slice[0][i], s);
-            pt[j] = s;
+        double* rb = cs.rbuf[l & 1];
+        const int Rp = l > 0 ? p.hrows[l - 1] : C;
+        for (int j = tid; j < C; j += nt) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int i = 0;
+            for (; i + 4 <= nrow; i += 4) {
+                s0 = fma(Ws[i * C + j], gys[i], s0);
+                s1 = fma(Ws[(i + 1) * C + j], gys[i + 1], s1);
+                s2 = fma(Ws[(i + 2) * C + j], gys[i + 2], s2);
+                s3 = fma(Ws[(i + 3) * C + j], gys[i + 3], s3);
+            }
+            for (; i < nrow; ++i) s0 = fma(Ws[i * C + j], gys[i], s0);
+            const double s = (s0 + s1) + (s2 + s3);
+            const int o = l > 0 ? part_owner<CS>(j, Rp) : 0;
+            const int jl = l > 0 ? j - part_lo(Rp, CS, o) : j;
+            cluster.map_shared_rank(rb, o)[c * 64 + jl] = s;
         }
+        stamp(130 + l);
         cluster.sync();
-        if (l > 0) {
-            const int Rp = p.hrows[l - 1];
-            const int k0 = part_lo(Rp, CS, c), k1 = part_lo(Rp, CS, c + 1);
-            for (int j = k0 + tid; j < k1; j += blockDim.x) {
-                double vals[CS];
+        stamp(140 + l);
+        // own rows of layer l-1 (or z for l = 0 on CTA 0): fixed CTA-order sum
+        const int nown = l > 0 ? part_lo(Rp, CS, c + 1) - part_lo(Rp, CS, c) : (c == 0 ? C : 0);
+        for (int k = 0; k < 2; ++k) {
+            const int i = tid + k * nt;
+            double s = 0.0;
+            if (i < nown) {
 #pragma unroll
-                for (int q = 0; q < CS; ++q) vals[q] = cluster.map_shared_rank(pt, q)[j];
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < CS; ++q) s += vals[q];
-                cs.slice[0][j - k0] = s;
+                for (int q = 0; q < CS; ++q) s += rb[q * 64 + i];
             }
-        } else if (c == 0) {
-            for (int j = tid; j < C; j += blockDim.x) {
-                double vals[CS];
-#pragma unroll
-                for (int q = 0; q < CS; ++q) vals[q] = cluster.map_shared_rank(pt, q)[j];
-                double s = 0.0;
-#pragma unroll
-                for (int q = 0; q < CS; ++q) s += vals[q];
-                cs.sst->gz[j] = s;
-            }
+            gy[k] = s;
+            if (l == 0 && i < nown) cs.sst->gz[i] = s;
         }
-        __syncthreads();
     }
+    __syncthreads();
 }
 
-// Hidden forward at zt (broadcast from CTA 0's state through DSMEM); keeps
-// own-row pre-activations in smem (asl) for the next backward; CTA 0 writes y_last.
-template <typename TS, int CS>
-__device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c) {
+// Forward through the hidden layers at sst->zt (CTA 0); the owner of each output
+// row pushes it into every CTA's next-layer input buffer.  y_last -> p.y_last.
+template <typename TS, int CS, typename Stamp>
+__device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, Stamp& stamp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nw = blockDim.x >> 5;
-    const double* zsrc = cluster.map_shared_rank(cs.sst->zt, 0);
-    for (int j = tid; j < p.r; j += blockDim.x) cs.ybuf[j] = zsrc[j];
+    {
+        const double* zsrc = cluster.map_shared_rank(cs.sst->zt, 0);
+        for (int j = tid; j < p.r; j += blockDim.x) cs.xin[0][j] = zsrc[j];
+    }
     __syncthreads();
-    // layer inputs: ybuf (layer 0) or the previous layer's slices in every CTA (DSMEM)
     for (int l = 0; l < p.nhid; ++l) {
         const int R = p.hrows[l], C = p.hcols[l];
-        const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-        double* out = cs.slice[l & 1];
-        const double* in_prev = cs.slice[(l & 1) ^ 1];
+        const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
+        const double* x = cs.xin[l & 1];
+        double* xn = cs.xin[(l & 1) ^ 1];
         const double* Ws = cs.wsl + cs.woff[l];
-        // operand fetch: lane j's inputs y[j], y[j+32], ... from their owners
-        double yin[kMaxHidden / 32];
+        double xr[kMaxHidden / 32];
 #pragma unroll
-        for (int k = 0; k < kMaxHidden / 32; ++k) {
-            const int j = lane + 32 * k;
-            double v = 0.0;
-            if (j < C) {
-                if (l == 0) {
-                    v = cs.ybuf[j];
-                } else {
-                    const int Rp = p.hrows[l - 1];
-                    int q = (int)(((long long)j * CS) / Rp);
-                    while (q + 1 < CS && part_lo(Rp, CS, q + 1) <= j) ++q;
-                    while (part_lo(Rp, CS, q) > j) --q;
-                    v = cluster.map_shared_rank(in_prev, q)[j - part_lo(Rp, CS, q)];
-                }
-            }
-            yin[k] = v;
-        }
-        for (int i = warp; i < i1 - i0; i += nw) {
-            double s = 0.0;
+        for (int k = 0; k < kMaxHidden / 32; ++k) xr[k] = lane + 32 * k < C ? x[lane + 32 * k] : 0.0;
+        for (int i = warp; i < nrow; i += 2 * nw) {
+            const int i2 = i + nw;
+            const bool two = i2 < nrow;
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
             for (int k = 0; k < kMaxHidden / 32; ++k) {
                 const int j = lane + 32 * k;
-                if (j < C) s = fma(Ws[i * C + j], yin[k], s);
+                if (j < C) {
+                    s0 = fma(Ws[i * C + j], xr[k], s0);
+                    if (two) s1 = fma(Ws[i2 * C + j], xr[k], s1);
+                }
             }
-            s = warp_sum(s);
-            if (lane == 0) {
-                const double a = s + cs.bsl[l * 64 + i];
-                cs.asl[l * 64 + i] = a;
-                out[i] = act_eval(p.hact[l], a, 0);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            }
+            const double a0 = s0 + cs.bsl[l * 64 + i];
+            const double y0 = act_eval(p.hact[l], a0, 0);
+            if (lane < CS) cluster.map_shared_rank(xn, lane)[i0 + i] = y0;
+            if (lane == 0) cs.asl[l * 64 + i] = a0;
+            if (two) {
+                const double a1 = s1 + cs.bsl[l * 64 + i2];
+                const double y1 = act_eval(p.hact[l], a1, 0);
+                if (lane < CS) cluster.map_shared_rank(xn, lane)[i0 + i2] = y1;
+                if (lane == 0) cs.asl[l * 64 + i2] = a1;
             }
         }
+        stamp(120 + l);
         cluster.sync();
     }
-    if (p.nhid > 0) {  // gather the last layer for y_last (CTA 0)
-        const int l = p.nhid - 1, R = p.hrows[l];
-        const double* lastv = cs.slice[l & 1];
-        if (c == 0)
-            for (int j = tid; j < p.hp; j += blockDim.x) {
-                double v = 0.0;
-                if (j < R) {
-                    int q = (int)(((long long)j * CS) / R);
-                    while (q + 1 < CS && part_lo(R, CS, q + 1) <= j) ++q;
-                    while (part_lo(R, CS, q) > j) --q;
-                    v = cluster.map_shared_rank(lastv, q)[j - part_lo(R, CS, q)];
-                }
-                p.y_last[j] = v;
-            }
-    } else if (c == 0) {
-        for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < p.r ? cs.ybuf[j] : 0.0;
+    if (c == 0) {
+        const double* x = cs.xin[p.nhid & 1];
+        const int R = p.nhid > 0 ? p.hrows[p.nhid - 1] : p.r;
+        for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < R ? x[j] : 0.0;
     }
 }
 
 // ---- the persistent kernel ---------------------------------------------------------------------------
 template <typename TS, int HP, int CS>
-__global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalParams<TS> p, const SolveParams sp) {
+__global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParams<TS> p, const SolveParams sp) {
     using C = StreamCfg<TS, HP>;
     extern __shared__ __align__(128) unsigned char smem[];
     cg::grid_group grid = cg::this_grid();
@@ -236,36 +260,39 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool is_ctrl = cta < CS;  // cluster 0 (clusters are contiguous block ranges)
     const int crank = (int)cluster.block_rank();
-    // ---- shared memory carve-up
-    unsigned char* ring = smem;
-    const int NS = sp.nst;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * C::STAGEB);
-    uint64_t* empty = full + NS;
-    double* cbase = reinterpret_cast<double*>(empty + NS);
+    // ---- shared memory carve-up: [barriers | ring (9 x spw stages) | control area (cluster 0)]
+    // Control CTAs run a shorter ring (the control area follows it); the others use
+    // the whole allocation.
+    constexpr int NW = kSolveThreads / 32;
+    WarpRing ring{smem + kSolveBarBytes, reinterpret_cast<uint64_t*>(smem), NW, is_ctrl ? sp.spw_ctrl : sp.spw,
+                  C::STAGEB, 0u};
+    double* cbase = reinterpret_cast<double*>(smem + kSolveBarBytes + (size_t)NW * sp.spw_ctrl * C::STAGEB);
     CtrlSmem cs;
     cs.wsl = cbase;
-    cs.ybuf = cbase + p.ctrl_smem_w;
-    cs.slice[0] = cs.ybuf + kMaxHidden;
-    cs.slice[1] = cs.ybuf + kMaxHidden + 64;
-    cs.part[0] = cs.ybuf + kMaxHidden + 128;
-    cs.part[1] = cs.ybuf + 2 * kMaxHidden + 128;
-    cs.bsl = cs.ybuf + 3 * kMaxHidden + 128;
+    cs.xin[0] = cbase + p.ctrl_smem_w;
+    cs.xin[1] = cs.xin[0] + kMaxHidden;
+    cs.rbuf[0] = cs.xin[1] + kMaxHidden;
+    cs.rbuf[1] = cs.rbuf[0] + kCtrlRecv;
+    cs.tmp = cs.rbuf[1] + kCtrlRecv;
+    cs.bsl = cs.tmp + kSolveThreads;
     cs.asl = cs.bsl + kMaxLayers * 64;
     cs.sst = reinterpret_cast<DevState*>(cs.asl + kMaxLayers * 64);
     __shared__ double red[32];
     __shared__ int s_flag;
-    if (tid == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_fence_init();
-    }
+    ring_init(ring.full, NW * ring.spw);
     __syncthreads();
-    int ring_i = 0;  // tiles passed through this CTA's ring (producer and consumers agree)
     const int ntiles = (p.n + C::TR - 1) / C::TR;
     const int t0 = (int)(((long long)ntiles * cta) / G);
     const int t1 = (int)(((long long)ntiles * (cta + 1)) / G);
+    const uint64_t pol_w = l2_policy(p.w_resident), pol_keep = l2_policy(1);
+    auto issue_f = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep); };
+    auto issue_v = [&](int t, unsigned char* b, uint64_t* bar) {
+        issue_vjp_w<TS, HP>(p, t, b, bar, pol_w);
+        issue_vjp_tv<TS, HP>(p, t, b, bar, pol_keep);
+    };
+    // the first forward tiles do not depend on z: prefetch now (a step rewrites the
+    // qbar column of the row records first, so it prefetches after that)
+    if (sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     int tr = 0;
@@ -332,48 +359,31 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
             st->inv_dt2 = s->inv_dt2;
         }
         cluster.sync();
-        ctrl_forward<TS, CS>(p, cs, cluster, crank);
+        ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
     }
     stamp(2);
+    fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
     grid.sync();
     stamp(3);
+    if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
 
     double inv_dt2 = __ldcg(&st->inv_dt2);
     int has_inertia = __ldcg(&st->has_inertia);
     for (;;) {
-        // ================= out_fwd (TMA ring)
+        // ================= out_fwd (self-issued TMA rings; first tiles already in flight)
         {
             double eacc = 0.0;
-            if (warp == 8) {
-                if (lane == 0) {
-                    const uint64_t pol = l2_policy(p.w_resident), keep = l2_policy(1);
-                    for (int t = t0, i = ring_i; t < t1; ++t, ++i) {
-                        const int s = i % NS, k = i / NS;
-                        if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-                        const int r0 = t * C::TR, rows = min(C::TR, p.n - r0);
-                        unsigned char* stg = ring + (size_t)s * C::STAGEB;
-                        mbar_expect_tx(&full[s], rows * C::ROWB + rows * 48);
-                        tma_load_1d(stg, p.Wout + (size_t)r0 * HP, rows * C::ROWB, &full[s], pol);
-                        tma_load_1d(stg + C::TILEB, p.eprow + (size_t)r0 * 6, rows * 48, &full[s], keep);
-                    }
-                }
-            } else {
+            {
                 double y[C::NCH][C::V4];
 #pragma unroll
                 for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
                     for (int q = 0; q < C::V4; ++q) y[c][q] = __ldcg(p.y_last + (c * 32 + lane) * C::V4 + q);
                 const bool ident = p.out_act == kIdentity;
-                for (int t = t0 + warp, i = ring_i + warp; t < t1; t += 8, i += 8) {
-                    const int s = i % NS, k = i / NS;
-                    mbar_wait(&full[s], k & 1);
-                    eacc += fwd_tile<TS, HP>(p, ring + (size_t)s * C::STAGEB, t, y, has_inertia, inv_dt2, ident);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s]);
-                }
+                ring_run(ring, t0, t1, issue_f, [&](int t, const unsigned char* b) {
+                    if (!(sp.exp & 1)) eacc += fwd_tile<TS, HP>(p, b, t, y, has_inertia, inv_dt2, ident);
+                });
             }
-            __syncwarp();
-            ring_i += t1 - t0;
             const double tot = block_sum(eacc, red);
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
@@ -421,6 +431,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
             else need = E <= __ldcg(&sh->f) + __ldcg(&sh->armijo_slope);
         }
         if (need) {
+            // the VJP's W tiles do not depend on tv: put them in flight now
+            if (lane == 0) {
+                const int n = min(ring.spw, ring.count(t0, t1));
+                for (int j = 0; j < n; ++j) issue_vjp_w<TS, HP>(p, t0 + warp + NW * j, ring.buf(j), ring.bar(j), pol_w);
+            }
             // ================= gather (4 lanes per vertex, contiguous CSR segments)
             {
                 const bool ident = p.out_act == kIdentity;
@@ -429,55 +444,36 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
                     gather_vertex4(p, (wb + lane) >> 2, has_inertia, ident);
             }
             stamp(30);
+            fence_proxy_async();  // tv (generic writes) -> bulk copies below
             grid.sync();
             stamp(31);
-            // ================= vjp (TMA ring)
+            // ================= vjp (self-issued TMA rings)
             {
+                if (lane == 0) {
+                    const int n = min(ring.spw, ring.count(t0, t1));
+                    for (int j = 0; j < n; ++j) issue_vjp_tv<TS, HP>(p, t0 + warp + NW * j, ring.buf(j), ring.bar(j), pol_keep);
+                }
                 double acc[C::NCH][C::V4];
 #pragma unroll
                 for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
                     for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
-                if (warp == 8) {
-                    if (lane == 0) {
-                        const uint64_t pol = l2_policy(p.w_resident), keep = l2_policy(1);
-                        for (int t = t0, i = ring_i; t < t1; ++t, ++i) {
-                            const int s = i % NS, k = i / NS;
-                            if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-                            const int r0 = t * C::TR, rows = min(C::TR, p.n - r0);
-                            const unsigned ub = ((unsigned)rows * 8 + 15) & ~15u;
-                            unsigned char* stg = ring + (size_t)s * C::STAGEB;
-                            mbar_expect_tx(&full[s], rows * C::ROWB + ub);
-                            tma_load_1d(stg, p.Wout + (size_t)r0 * HP, rows * C::ROWB, &full[s], pol);
-                            tma_load_1d(stg + C::TILEB, p.tv + r0, ub, &full[s], keep);
-                        }
-                    }
-                } else {
-                    for (int t = t0 + warp, i = ring_i + warp; t < t1; t += 8, i += 8) {
-                        const int s = i % NS, k = i / NS;
-                        mbar_wait(&full[s], k & 1);
-                        vjp_tile<TS, HP>(p, ring + (size_t)s * C::STAGEB, t, acc);
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&empty[s]);
-                    }
-                }
-                ring_i += t1 - t0;
+                ring_run(ring, t0, t1, issue_v, [&](int t, const unsigned char* b) {
+                    if (!(sp.exp & 1)) vjp_tile<TS, HP>(p, b, t, acc);
+                });
                 // per-warp partials -> this CTA's ybar partial (fixed warp order); the
                 // ring is idle now (every issued tile has been consumed)
-                __syncwarp();
-                double* wred = reinterpret_cast<double*>(ring);  // 8 x HP doubles <= ring bytes
+                double* wred = reinterpret_cast<double*>(ring.ring);  // NW x HP doubles <= ring bytes
                 __syncthreads();
-                if (warp < 8) {
 #pragma unroll
-                    for (int c = 0; c < C::NCH; ++c)
+                for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
-                        for (int q = 0; q < C::V4; ++q) wred[warp * HP + (c * 32 + lane) * C::V4 + q] = acc[c][q];
-                }
+                    for (int q = 0; q < C::V4; ++q) wred[warp * HP + (c * 32 + lane) * C::V4 + q] = acc[c][q];
                 __syncthreads();
                 for (int j = tid; j < HP; j += blockDim.x) {
                     double s = 0.0;
 #pragma unroll
-                    for (int w = 0; w < 8; ++w) s += wred[w * HP + j];
+                    for (int w = 0; w < NW; ++w) s += wred[w * HP + j];
                     p.ybar_part[(size_t)cta * HP + j] = s;
                 }
             }
@@ -485,6 +481,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
             grid.sync();
             stamp(41);
         }
+        // next forward's first tiles (drained at exit if there is no next forward)
+        ring_prefetch(ring, t0, t1, issue_f);
         // ================= control cluster: gradient, L-BFGS, next hidden forward
         if (is_ctrl) {
             DevState* s = cs.sst;
@@ -499,7 +497,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
             }
             // pre-activations of the point just evaluated are in asl (own rows)
             cluster.sync();
-            if (need) ctrl_backward<TS, CS>(p, cs, cluster, crank, G, p.ybar_part);
+            if (need) ctrl_backward<TS, CS>(p, cs, cluster, crank, G, p.ybar_part, stamp);
             if (crank == 0) {
                 if (warp == 0) {
                     int m = 0;
@@ -523,13 +521,14 @@ __global__ void __launch_bounds__(kStreamThreads, 1) solve_kernel(const EvalPara
             }
             cluster.sync();
             const int more = *cluster.map_shared_rank(&s_flag, 0);
-            if (more) ctrl_forward<TS, CS>(p, cs, cluster, crank);
+            if (more) ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
         }
         stamp(50);
         grid.sync();
         stamp(51);
         if (__ldcg(&sh->done)) break;
     }
+    ring_drain(ring, t0, t1);
     // ---- epilogue: publish state; step finalize (reference reduced_step :266-276)
     if (is_ctrl && crank == 0) {
         __syncthreads();
