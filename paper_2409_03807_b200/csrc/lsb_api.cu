@@ -39,13 +39,21 @@ void* Context::dmalloc(size_t bytes) {
     return p;
 }
 
+// Every host<->device copy of a context goes through its (non-blocking) stream and
+// waits for it: copies are then ordered after the allocation memsets and kernels
+// queued on that stream (a legacy-stream cudaMemcpy is not).
+void Context::copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) const {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, stream), what);
+    cuda_check(cudaStreamSynchronize(stream), what);
+}
+
 void Context::upload_real(void* dst, const double* src, size_t count) {
     if (wsize == 8) {
-        cuda_check(cudaMemcpy(dst, src, count * 8, cudaMemcpyHostToDevice), "upload");
+        copy(dst, src, count * 8, cudaMemcpyHostToDevice, "upload");
     } else {
         std::vector<float> tmp(count);
         for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(src[i]);
-        cuda_check(cudaMemcpy(dst, tmp.data(), count * 4, cudaMemcpyHostToDevice), "upload");
+        copy(dst, tmp.data(), count * 4, cudaMemcpyHostToDevice, "upload");
     }
 }
 
@@ -151,13 +159,13 @@ void upload_pins(Context& c) {
     std::vector<double> disp(3 * (size_t)m.V, 0.0);
     for (int v : m.pinned)
         for (int k = 0; k < 3; ++k) disp[3 * (size_t)v + k] = c.pin_positions[3 * (size_t)v + k] - m.X[3 * (size_t)v + k];
-    cuda_check(cudaMemcpy(c.d_pin_disp, disp.data(), disp.size() * 8, cudaMemcpyHostToDevice), "pins");
+    c.copy(c.d_pin_disp, disp.data(), disp.size() * 8, cudaMemcpyHostToDevice, "pins");
     std::vector<double> U4(4 * (size_t)m.V, 0.0);
     for (int v : m.pinned)
         for (int k = 0; k < 3; ++k) U4[4 * (size_t)v + k] = disp[3 * (size_t)v + k];
     // free rows: keep whatever the last decode wrote (re-uploading zeros is harmless
     // because every evaluation rewrites them before the element pass).
-    cuda_check(cudaMemcpy(c.d_U, U4.data(), U4.size() * 8, cudaMemcpyHostToDevice), "U pins");
+    c.copy(c.d_U, U4.data(), U4.size() * 8, cudaMemcpyHostToDevice, "U pins");
 }
 
 }  // namespace
@@ -345,21 +353,21 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             c.d_Wout = c.dmalloc(Wp.size() * w);
             c.upload_real(c.d_Wout, Wp.data(), Wp.size());
             c.d_bout = static_cast<double*>(c.dmalloc(n * 8));
-            cuda_check(cudaMemcpy(c.d_bout, o.b.data(), n * 8, cudaMemcpyHostToDevice), "bout");
+            c.copy(c.d_bout, o.b.data(), n * 8, cudaMemcpyHostToDevice, "bout");
         }
         c.d_sout = static_cast<double*>(c.dmalloc(n * 8));
-        cuda_check(cudaMemcpy(c.d_sout, c.scale.data(), n * 8, cudaMemcpyHostToDevice), "sout");
+        c.copy(c.d_sout, c.scale.data(), n * 8, cudaMemcpyHostToDevice, "sout");
         {
             std::vector<double> cs(n);
             for (int f = 0; f < m.n_free; ++f)
                 for (int k = 0; k < 3; ++k)
                     cs[3 * f + k] = c.shift[3 * f + k] - m.X[3 * (size_t)m.free_vertex[f] + k];
             c.d_cout = static_cast<double*>(c.dmalloc(n * 8));
-            cuda_check(cudaMemcpy(c.d_cout, cs.data(), n * 8, cudaMemcpyHostToDevice), "cout");
+            c.copy(c.d_cout, cs.data(), n * 8, cudaMemcpyHostToDevice, "cout");
         }
         c.d_dsout = static_cast<double*>(c.dmalloc(n * 8));
         c.d_mass = static_cast<double*>(c.dmalloc(n * 8));
-        cuda_check(cudaMemcpy(c.d_mass, c.mass.data(), n * 8, cudaMemcpyHostToDevice), "mass");
+        c.copy(c.d_mass, c.mass.data(), n * 8, cudaMemcpyHostToDevice, "mass");
         c.d_ut = static_cast<double*>(c.dmalloc((n + 2) * 8));  // +2: 16-byte TMA tails
         c.d_rin = static_cast<double*>(c.dmalloc(n * 8));
         c.d_tv = static_cast<double*>(c.dmalloc((n + 2) * 8));
@@ -377,12 +385,12 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
                 }
             c.h_eprow = ep;
             c.d_eprow = static_cast<double*>(c.dmalloc(ep.size() * 8));
-            cuda_check(cudaMemcpy(c.d_eprow, ep.data(), ep.size() * 8, cudaMemcpyHostToDevice), "eprow");
+            c.copy(c.d_eprow, ep.data(), ep.size() * 8, cudaMemcpyHostToDevice, "eprow");
         }
         c.d_vfree = static_cast<int*>(c.dmalloc(sizeof(int) * m.n_free));
-        cuda_check(cudaMemcpy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice), "vfree");
+        c.copy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice, "vfree");
         c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * (size_t)m.E));
-        cuda_check(cudaMemcpy(c.d_tets, m.T.data(), sizeof(int) * 4 * (size_t)m.E, cudaMemcpyHostToDevice), "tets");
+        c.copy(c.d_tets, m.T.data(), sizeof(int) * 4 * (size_t)m.E, cudaMemcpyHostToDevice, "tets");
         {
             std::vector<double> rec(12 * (size_t)m.E);
             for (int e = 0; e < m.E; ++e) {
@@ -402,12 +410,12 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             for (int f = 0; f < m.n_free; ++f)
                 for (int k = m.csr_ptr[f]; k < m.csr_ptr[f + 1]; ++k) fpos[m.csr_ent[k]] = k;
             c.d_fpos = static_cast<int*>(c.dmalloc(fpos.size() * 4));
-            cuda_check(cudaMemcpy(c.d_fpos, fpos.data(), fpos.size() * 4, cudaMemcpyHostToDevice), "fpos");
+            c.copy(c.d_fpos, fpos.data(), fpos.size() * 4, cudaMemcpyHostToDevice, "fpos");
         }
         c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
-        cuda_check(cudaMemcpy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice), "csr");
+        c.copy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice, "csr");
         c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
-        cuda_check(cudaMemcpy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice), "csr");
+        c.copy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice, "csr");
         {  // hidden layers, fp64, row-major and transposed
             std::vector<double> Wh, bh;
             for (int l = 0; l < c.nhid; ++l) {
@@ -423,8 +431,8 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             c.d_Wh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, Wh.size())));
             c.d_bh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, bh.size())));
             if (!Wh.empty()) {
-                cuda_check(cudaMemcpy(c.d_Wh, Wh.data(), 8 * Wh.size(), cudaMemcpyHostToDevice), "Wh");
-                cuda_check(cudaMemcpy(c.d_bh, bh.data(), 8 * bh.size(), cudaMemcpyHostToDevice), "bh");
+                c.copy(c.d_Wh, Wh.data(), 8 * Wh.size(), cudaMemcpyHostToDevice, "Wh");
+                c.copy(c.d_bh, bh.data(), 8 * bh.size(), cudaMemcpyHostToDevice, "bh");
             }
         }
         c.d_a_hid = static_cast<double*>(c.dmalloc(sizeof(double) * kMaxHidden * std::max(1, c.nhid)));
@@ -442,7 +450,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             std::vector<char> vp(m.V, 0);
             for (int v : m.pinned) vp[v] = 1;
             c.d_vpinned = static_cast<char*>(c.dmalloc(m.V));
-            cuda_check(cudaMemcpy(c.d_vpinned, vp.data(), m.V, cudaMemcpyHostToDevice), "vpinned");
+            c.copy(c.d_vpinned, vp.data(), m.V, cudaMemcpyHostToDevice, "vpinned");
         }
         c.d_launch_acc = static_cast<long long*>(c.dmalloc(sizeof(long long)));
         cuda_check(cudaStreamSynchronize(c.stream), "sync");
@@ -464,7 +472,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         h->max_ls = 128;
         h->hist_cap = 8;
         h->phase = kPhaseDone;
-        cuda_check(cudaMemcpy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice), "state init");
+        c.copy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice, "state init");
         c.ensure_step_buffers(16);
         cuda_check(cudaDeviceSynchronize(), "create sync");
         *out = holder.release();
@@ -522,13 +530,13 @@ lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
             for (int f = 0; f < c.mesh.n_free; ++f)
                 for (int k = 0; k < 3; ++k)
                     ut[3 * f + k] = qbar[3 * f + k] - c.mesh.X[3 * (size_t)c.mesh.free_vertex[f] + k];
-            cuda_check(cudaMemcpy(c.d_ut, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice), "ut");
+            c.copy(c.d_ut, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice, "ut");
             for (int i = 0; i < c.n; ++i) c.h_eprow[6 * (size_t)i + 5] = ut[i];
-            cuda_check(cudaMemcpy(c.d_eprow, c.h_eprow.data(), c.h_eprow.size() * 8, cudaMemcpyHostToDevice), "eprow");
+            c.copy(c.d_eprow, c.h_eprow.data(), c.h_eprow.size() * 8, cudaMemcpyHostToDevice, "eprow");
         }
         c.has_qbar = qbar != nullptr;
         c.dt = dt;
-        cuda_check(cudaMemcpy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice), "state put");
+        c.copy(c.d_state, h, sizeof(DevState), cudaMemcpyHostToDevice, "state put");
     });
 }
 
@@ -561,7 +569,7 @@ lsb_status lsb_decode(lsb_context* ctx, const double* z, double* q) {
         sync(c);
         const HostMesh& m = c.mesh;
         std::vector<double> U(4 * (size_t)m.V);
-        cuda_check(cudaMemcpy(U.data(), c.d_U, U.size() * 8, cudaMemcpyDeviceToHost), "U");
+        c.copy(U.data(), c.d_U, U.size() * 8, cudaMemcpyDeviceToHost, "U");
         for (int f = 0; f < m.n_free; ++f)
             for (int k = 0; k < 3; ++k)
                 q[3 * f + k] = m.X[3 * (size_t)m.free_vertex[f] + k] + U[4 * (size_t)m.free_vertex[f] + k];
@@ -594,9 +602,9 @@ lsb_status lsb_set_state(lsb_context* ctx, const double* positions, const double
         const HostMesh& m = c.mesh;
         std::vector<double> u(3 * (size_t)m.V);
         for (size_t i = 0; i < u.size(); ++i) u[i] = positions[i] - m.X[i];
-        cuda_check(cudaMemcpy(c.d_u_state, u.data(), u.size() * 8, cudaMemcpyHostToDevice), "state u");
-        cuda_check(cudaMemcpy(c.d_v_state, velocities, u.size() * 8, cudaMemcpyHostToDevice), "state v");
-        cuda_check(cudaMemcpy(c.d_z_state, z, c.r * 8, cudaMemcpyHostToDevice), "state z");
+        c.copy(c.d_u_state, u.data(), u.size() * 8, cudaMemcpyHostToDevice, "state u");
+        c.copy(c.d_v_state, velocities, u.size() * 8, cudaMemcpyHostToDevice, "state v");
+        c.copy(c.d_z_state, z, c.r * 8, cudaMemcpyHostToDevice, "state z");
         put_state(c, &DevState::t, 0.0);
         c.state_set = true;
     });
@@ -610,11 +618,11 @@ lsb_status lsb_get_state(lsb_context* ctx, double* positions, double* velocities
         sync(c);
         const HostMesh& m = c.mesh;
         if (positions) {
-            cuda_check(cudaMemcpy(positions, c.d_u_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost), "state u");
+            c.copy(positions, c.d_u_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost, "state u");
             for (size_t i = 0; i < 3 * (size_t)m.V; ++i) positions[i] += m.X[i];
         }
-        if (velocities) cuda_check(cudaMemcpy(velocities, c.d_v_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost), "state v");
-        if (z) cuda_check(cudaMemcpy(z, c.d_z_state, 8 * (size_t)c.r, cudaMemcpyDeviceToHost), "state z");
+        if (velocities) c.copy(velocities, c.d_v_state, 24 * (size_t)m.V, cudaMemcpyDeviceToHost, "state v");
+        if (z) c.copy(z, c.d_z_state, 8 * (size_t)c.r, cudaMemcpyDeviceToHost, "state z");
         if (t) {
             get_state(c);
             *t = c.h_state->t;
@@ -630,7 +638,7 @@ lsb_status lsb_set_external_force(lsb_context* ctx, const double* force) {
         sync(c);
         std::vector<double> a(c.n);
         for (int i = 0; i < c.n; ++i) a[i] = force[i] / c.mass[i];  // f / m (reduced_solver.cpp:253)
-        cuda_check(cudaMemcpy(c.d_a_ext, a.data(), a.size() * 8, cudaMemcpyHostToDevice), "force");
+        c.copy(c.d_a_ext, a.data(), a.size() * 8, cudaMemcpyHostToDevice, "force");
     });
 }
 
@@ -641,7 +649,7 @@ static void prepare_steps(Context& c, int steps, const lsb_solver_config* cfg, i
     get_state(c);
     c.h_state->quasi_static = quasi_static ? 1 : 0;
     c.h_state->step_idx = 0;
-    cuda_check(cudaMemcpy(c.d_state, c.h_state, sizeof(DevState), cudaMemcpyHostToDevice), "state put");
+    c.copy(c.d_state, c.h_state, sizeof(DevState), cudaMemcpyHostToDevice, "state put");
     c.ensure_step_buffers(std::max(1, steps));
 }
 
@@ -653,7 +661,7 @@ lsb_status lsb_step(lsb_context* ctx, const lsb_solver_config* cfg, int quasi_st
         c.impl->step(c);
         get_state(c);
         if (c.h_state->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
-        if (report) cuda_check(cudaMemcpy(report, c.d_reports, sizeof(lsb_exit_report), cudaMemcpyDeviceToHost), "report");
+        if (report) c.copy(report, c.d_reports, sizeof(lsb_exit_report), cudaMemcpyDeviceToHost, "report");
     });
 }
 
@@ -666,10 +674,10 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
         for (int s = 0; s < steps; ++s) c.impl->step(c);
         sync(c);
         get_state(c);
-        if (reports) cuda_check(cudaMemcpy(reports, c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost), "reports");
-        if (z_traj) cuda_check(cudaMemcpy(z_traj, c.d_z_traj, sizeof(double) * (size_t)steps * c.r, cudaMemcpyDeviceToHost), "z traj");
+        if (reports) c.copy(reports, c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost, "reports");
+        if (z_traj) c.copy(z_traj, c.d_z_traj, sizeof(double) * (size_t)steps * c.r, cudaMemcpyDeviceToHost, "z traj");
         std::vector<lsb_exit_report> tmp(steps);
-        cuda_check(cudaMemcpy(tmp.data(), c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost), "reports");
+        c.copy(tmp.data(), c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost, "reports");
         for (int s = 0; s < steps; ++s)
             if (tmp[s].code == -kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
     });
@@ -697,7 +705,7 @@ lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int ca
         *count = 0;
         if (!ctx->c.d_trace) return;
         std::vector<unsigned long long> t(512);
-        cuda_check(cudaMemcpy(t.data(), ctx->c.d_trace, 8 * 512, cudaMemcpyDeviceToHost), "trace");
+        ctx->c.copy(t.data(), ctx->c.d_trace, 8 * 512, cudaMemcpyDeviceToHost, "trace");
         const int n = (int)std::min<unsigned long long>(t[0], 255);
         for (int i = 0; i < n && 2 * i + 1 < cap; ++i) {
             out[2 * i] = t[1 + 2 * i];
@@ -712,7 +720,7 @@ lsb_status lsb_get_launch_count(const lsb_context* ctx, long long* launches) {
         check_ctx(ctx);
         const Context& c = ctx->c;
         long long dev = 0;
-        cuda_check(cudaMemcpy(&dev, c.d_launch_acc, sizeof(long long), cudaMemcpyDeviceToHost), "launch acc");
+        c.copy(&dev, c.d_launch_acc, sizeof(long long), cudaMemcpyDeviceToHost, "launch acc");
         *launches = c.launches + dev + c.batched_launches;
     });
 }

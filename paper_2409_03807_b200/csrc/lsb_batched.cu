@@ -708,9 +708,9 @@ struct BatchedEngine : BatchedBase {
             d_blk_aptr = alloc<int>(nblk + 1);
             d_blk_avert = alloc<int>(avert.size());
             d_tet_aloc = alloc<short>(aloc.size());
-            cuda_check(cudaMemcpy(d_blk_aptr, aptr.data(), 4 * aptr.size(), cudaMemcpyHostToDevice), "blk");
-            cuda_check(cudaMemcpy(d_blk_avert, avert.data(), 4 * avert.size(), cudaMemcpyHostToDevice), "blk");
-            cuda_check(cudaMemcpy(d_tet_aloc, aloc.data(), 2 * aloc.size(), cudaMemcpyHostToDevice), "blk");
+            c.copy(d_blk_aptr, aptr.data(), 4 * aptr.size(), cudaMemcpyHostToDevice, "blk");
+            c.copy(d_blk_avert, avert.data(), 4 * avert.size(), cudaMemcpyHostToDevice, "blk");
+            c.copy(d_tet_aloc, aloc.data(), 2 * aloc.size(), cudaMemcpyHostToDevice, "blk");
         }
         // vertex -> slots (ascending block order)
         std::vector<int> cnt(m.n_free + 1, 0);
@@ -724,17 +724,17 @@ struct BatchedEngine : BatchedBase {
         d_tet_loc = alloc<short>(4 * (size_t)m.E);
         d_vslot_ptr = alloc<int>(m.n_free + 1);
         d_vslot = alloc<int>(nslots);
-        cuda_check(cudaMemcpy(d_blk_tet0, tet0.data(), 4 * tet0.size(), cudaMemcpyHostToDevice), "blk");
-        cuda_check(cudaMemcpy(d_blk_vptr, vptr.data(), 4 * vptr.size(), cudaMemcpyHostToDevice), "blk");
-        cuda_check(cudaMemcpy(d_tet_loc, loc.data(), 2 * loc.size(), cudaMemcpyHostToDevice), "blk");
-        cuda_check(cudaMemcpy(d_vslot_ptr, sptr.data(), 4 * sptr.size(), cudaMemcpyHostToDevice), "blk");
-        cuda_check(cudaMemcpy(d_vslot, slots.data(), 4 * slots.size(), cudaMemcpyHostToDevice), "blk");
+        c.copy(d_blk_tet0, tet0.data(), 4 * tet0.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(d_blk_vptr, vptr.data(), 4 * vptr.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(d_tet_loc, loc.data(), 2 * loc.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(d_vslot_ptr, sptr.data(), 4 * sptr.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(d_vslot, slots.data(), 4 * slots.size(), cudaMemcpyHostToDevice, "blk");
         // --- decoder output layer (fp32, unpadded [n][h])
         const HostLayer& o = c.layers[c.nhid];
         std::vector<float> W(o.W.size());
         for (size_t i = 0; i < W.size(); ++i) W[i] = (float)o.W[i];
         d_W = alloc<float>(W.size());
-        cuda_check(cudaMemcpy(d_W, W.data(), 4 * W.size(), cudaMemcpyHostToDevice), "batched W");
+        c.copy(d_W, W.data(), 4 * W.size(), cudaMemcpyHostToDevice, "batched W");
         // --- chunk buffers
         const int n = c.n, h = c.h, V = m.V;
         int hmax = c.r;
@@ -767,7 +767,7 @@ struct BatchedEngine : BatchedBase {
                 const float d = (float)(c.pin_positions[3 * (size_t)v + k] - m.X[3 * (size_t)v + k]);
                 for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
             }
-        cuda_check(cudaMemcpy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice), "U pins");
+        c.copy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "U pins");
         const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
         if (c.precision == LSB_FP64)
             cuda_check(cudaFuncSetAttribute(elem_batched_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -886,7 +886,7 @@ struct BatchedEngine : BatchedBase {
         for (int l = 0; l < c.nhid; ++l)
             for (double v : c.layers[l].W) wf[off++] = (float)v;
         d_Whf = alloc<float>(std::max<size_t>(1, wtot));
-        if (wtot) cuda_check(cudaMemcpy(d_Whf, wf.data(), 4 * wtot, cudaMemcpyHostToDevice), "Whf");
+        if (wtot) c.copy(d_Whf, wf.data(), 4 * wtot, cudaMemcpyHostToDevice, "Whf");
         d_X[0] = alloc<float>((size_t)hmax * PH * hcols);
         d_X[1] = alloc<float>((size_t)hmax * PH * hcols);
         d_Q = alloc<float>((size_t)hmax * PH * hcols);
@@ -909,8 +909,8 @@ struct BatchedEngine : BatchedBase {
                 const float d = (float)(c.pin_positions[3 * (size_t)v + k] - c.mesh.X[3 * (size_t)v + k]);
                 for (int p = 0; p < PH; ++p) U0[((size_t)v * 3 + k) * PH + p] = d;
             }
-        cuda_check(cudaMemcpy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice), "Uh");
-        cuda_check(cudaMemset(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r), "Jv");
+        c.copy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "Uh");
+        cuda_check(cudaMemsetAsync(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r, c.stream), "Jv");
         const size_t gsmem = hess_smem(r);
         if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
@@ -996,7 +996,7 @@ struct BatchedEngine : BatchedBase {
                 rec[12 * (size_t)e + 11] = (float)c.lambda[e];
             }
             d_recf = alloc<float>(rec.size());
-            cuda_check(cudaMemcpy(d_recf, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice), "recf");
+            c.copy(d_recf, rec.data(), 4 * rec.size(), cudaMemcpyHostToDevice, "recf");
         }
         return d_recf;
     }

@@ -16,7 +16,7 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
     const int r = c.r;
     double* dZ = nullptr;
     cuda_check(cudaMalloc(&dZ, sizeof(double) * (size_t)K * r), "bench Z");
-    cuda_check(cudaMemcpy(dZ, Z, sizeof(double) * (size_t)K * r, cudaMemcpyHostToDevice), "bench Z");
+    c.copy(dZ, Z, sizeof(double) * (size_t)K * r, cudaMemcpyHostToDevice, "bench Z");
     void* flush = nullptr;
     if (flush_bytes) cuda_check(cudaMalloc(&flush, flush_bytes), "bench flush");
     cudaEvent_t ev[4];
@@ -34,7 +34,7 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
         cudaEventElapsedTime(&t1, ev[1], ev[2]);
         eval_ms[k] = t0;
         out_ms[k] = t1;
-        if (E) cuda_check(cudaMemcpy(&E[k], &c.d_state->f_eval, sizeof(double), cudaMemcpyDeviceToHost), "E");
+        if (E) c.copy(&E[k], &c.d_state->f_eval, sizeof(double), cudaMemcpyDeviceToHost, "E");
     }
     for (auto& e : ev) cudaEventDestroy(e);
     if (flush) cudaFree(flush);
@@ -60,7 +60,7 @@ void bench_steps(Context& c, int K, size_t flush_bytes, double* step_ms, lsb_exi
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (flush) cudaFree(flush);
-    if (reps) cuda_check(cudaMemcpy(reps, c.d_reports, sizeof(lsb_exit_report) * K, cudaMemcpyDeviceToHost), "reports");
+    if (reps) c.copy(reps, c.d_reports, sizeof(lsb_exit_report) * K, cudaMemcpyDeviceToHost, "reports");
 }
 
 }  // namespace lsb

@@ -200,7 +200,7 @@ struct Impl final : ImplBase {
     // persistent solve kernel (cooperative launch of thread-block clusters)
     typename SolveFn<TS>::type solve = nullptr;
     size_t solve_smem = 0;
-    int solve_spw = 1, solve_spw_ctrl = 1;
+    int solve_spw = 1, solve_spw_ctrl = 1, solve_tv_cap = 0, solve_tv_off = 0, solve_tv_off_ctrl = 0;
     int solve_grid = 0;
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
     SolveShared* d_sh = nullptr;
@@ -370,18 +370,25 @@ struct Impl final : ImplBase {
             return;
         }
         // self-issued rings: 9 warps x spw stages each, as many as fit (control CTAs: their
-        // control area follows the ring)
-        const size_t cap = 227 * 1024 - 256;
+        // control area follows the ring), then the tv / partials scratch
+        const size_t cap = 227 * 1024 - 512;
         const size_t ctrl_area = ((size_t)p.ctrl_smem_w + ctrl_fixed_words()) * sizeof(double);
         const int nw = kSolveThreads / 32;
+        {
+            const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
+            const int g_min = 96;  // clusters of 8/16 on 148 SMs give >= 112 CTAs
+            solve_tv_cap = std::max((ntiles + g_min - 1) / g_min * ks.tile_rows, c.hp);
+        }
+        const size_t tvb = ((size_t)solve_tv_cap * sizeof(double) + 127) & ~(size_t)127;
         solve_spw_ctrl = 0;
         for (int k = 1; k * nw <= kSolveMaxStages && k <= 3; ++k)
-            if (kSolveBarBytes + k * nw * ks.stage_bytes + ctrl_area <= cap) solve_spw_ctrl = k;
+            if (kSolveBarBytes + k * nw * ks.stage_bytes + ctrl_area + tvb <= cap) solve_spw_ctrl = k;
         solve_spw = std::max(solve_spw_ctrl, 1);
         for (int k = 1; k * nw <= kSolveMaxStages && k <= 2; ++k)
-            if (kSolveBarBytes + k * nw * ks.stage_bytes <= cap) solve_spw = std::max(solve_spw, k);
-        solve_smem = std::max(kSolveBarBytes + solve_spw_ctrl * nw * ks.stage_bytes + ctrl_area,
-                              kSolveBarBytes + solve_spw * nw * ks.stage_bytes);
+            if (kSolveBarBytes + k * nw * ks.stage_bytes + tvb <= cap) solve_spw = std::max(solve_spw, k);
+        solve_tv_off_ctrl = (int)(kSolveBarBytes + solve_spw_ctrl * nw * ks.stage_bytes + ctrl_area);
+        solve_tv_off = (int)(kSolveBarBytes + solve_spw * nw * ks.stage_bytes);
+        solve_smem = std::max((size_t)solve_tv_off_ctrl, (size_t)solve_tv_off) + tvb;
         if (solve_spw_ctrl == 0) solve_smem = cap + 1;
         if (solve_smem > 227 * 1024) {
             c.solve_reason = "shared memory " + std::to_string(solve_smem) + " B exceeds 227 KB";
@@ -412,6 +419,14 @@ struct Impl final : ImplBase {
             return;
         }
         solve_grid = nclusters * cs;
+        {
+            const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
+            if ((ntiles + solve_grid - 1) / solve_grid * ks.tile_rows > solve_tv_cap) {
+                c.solve_reason = "tv scratch too small for " + std::to_string(solve_grid) + " CTAs";
+                solve = nullptr;
+                return;
+            }
+        }
         ps = p;
         ps.e_part_out = static_cast<double*>(c.dmalloc(sizeof(double) * solve_grid));
         ps.e_part_elem = static_cast<double*>(c.dmalloc(sizeof(double) * solve_grid));
@@ -428,6 +443,9 @@ struct Impl final : ImplBase {
         sp.quasi = quasi;
         sp.spw = solve_spw;
         sp.spw_ctrl = solve_spw_ctrl;
+        sp.tv_off = solve_tv_off;
+        sp.tv_off_ctrl = solve_tv_off_ctrl;
+        sp.tv_cap = solve_tv_cap;
         if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);
         sp.want_grad = want_grad;
         sp.u_state = c.d_u_state;

@@ -114,6 +114,7 @@ struct Context {
 
     ~Context();
     void* dmalloc(size_t bytes);
+    void copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) const;
     void alloc_partials(int g_out, int g_elem, int g_vjp, int n_groups);
     void ensure_step_buffers(int steps);
     void upload_real(void* dst, const double* src, size_t count);  // converts to wsize

@@ -32,6 +32,9 @@ struct SolveParams {
     int want_grad;    // eval: gradient wanted
     int spw;          // ring stages per warp, non-control CTAs
     int spw_ctrl;     // ring stages per warp, control CTAs (their control area follows the ring)
+    int tv_off;       // byte offset of the tv/partials scratch (non-control CTAs)
+    int tv_off_ctrl;  // ditto, control CTAs (after their control area)
+    int tv_cap;       // its capacity in doubles (>= rows per CTA and >= hp)
     int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
     // dynamics
     const double* u_state;
@@ -208,35 +211,30 @@ __device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_
         const double* x = cs.xin[l & 1];
         double* xn = cs.xin[(l & 1) ^ 1];
         const double* Ws = cs.wsl + cs.woff[l];
-        double xr[kMaxHidden / 32];
-#pragma unroll
-        for (int k = 0; k < kMaxHidden / 32; ++k) xr[k] = lane + 32 * k < C ? x[lane + 32 * k] : 0.0;
-        for (int i = warp; i < nrow; i += 2 * nw) {
-            const int i2 = i + nw;
-            const bool two = i2 < nrow;
+        // rows per warp: the smallest power of two that covers nrow in one pass (<= 8),
+        // LPR = 32 / rpw lanes share one row (split-K) and reduce with log2(LPR) shuffles
+        int rpw = 1;
+        while (rpw < 8 && rpw * nw < nrow) rpw <<= 1;
+        const int LPR = 32 / rpw, sub = lane / LPR, sl = lane % LPR;
+        for (int i = warp * rpw + sub; i - sub < nrow; i += nw * rpw) {
+            const bool live = i < nrow;
             double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < kMaxHidden / 32; ++k) {
-                const int j = lane + 32 * k;
-                if (j < C) {
-                    s0 = fma(Ws[i * C + j], xr[k], s0);
-                    if (two) s1 = fma(Ws[i2 * C + j], xr[k], s1);
+            if (live) {
+                const double* wr = Ws + i * C;
+                int j = sl;
+                for (; j + LPR < C; j += 2 * LPR) {
+                    s0 = fma(wr[j], x[j], s0);
+                    s1 = fma(wr[j + LPR], x[j + LPR], s1);
                 }
+                if (j < C) s0 = fma(wr[j], x[j], s0);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            }
-            const double a0 = s0 + cs.bsl[l * 64 + i];
-            const double y0 = act_eval(p.hact[l], a0, 0);
-            if (lane < CS) cluster.map_shared_rank(xn, lane)[i0 + i] = y0;
-            if (lane == 0) cs.asl[l * 64 + i] = a0;
-            if (two) {
-                const double a1 = s1 + cs.bsl[l * 64 + i2];
-                const double y1 = act_eval(p.hact[l], a1, 0);
-                if (lane < CS) cluster.map_shared_rank(xn, lane)[i0 + i2] = y1;
-                if (lane == 0) cs.asl[l * 64 + i2] = a1;
+            double s = s0 + s1;
+            for (int o = LPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (live) {
+                const double a = s + cs.bsl[l * 64 + i];
+                const double y = act_eval(p.hact[l], a, 0);
+                for (int q = sl; q < CS; q += LPR) cluster.map_shared_rank(xn, q)[i0 + i] = y;
+                if (sl == 0) cs.asl[l * 64 + i] = a;
             }
         }
         stamp(120 + l);
@@ -278,6 +276,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     cs.asl = cs.bsl + kMaxLayers * 64;
     cs.sst = reinterpret_cast<DevState*>(cs.asl + kMaxLayers * 64);
     __shared__ double red[32];
+    __shared__ double s_energy[2];
     __shared__ int s_flag;
     ring_init(ring.full, NW * ring.spw);
     __syncthreads();
@@ -286,13 +285,22 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     const int t1 = (int)(((long long)ntiles * (cta + 1)) / G);
     const uint64_t pol_w = l2_policy(p.w_resident), pol_keep = l2_policy(1);
     auto issue_f = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep); };
-    auto issue_v = [&](int t, unsigned char* b, uint64_t* bar) {
-        issue_vjp_w<TS, HP>(p, t, b, bar, pol_w);
-        issue_vjp_tv<TS, HP>(p, t, b, bar, pol_keep);
-    };
+    double* tv_s = reinterpret_cast<double*>(smem + (is_ctrl ? sp.tv_off_ctrl : sp.tv_off));
     // the first forward tiles do not depend on z: prefetch now (a step rewrites the
     // qbar column of the row records first, so it prefetches after that)
     if (sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
+    // cold start (e.g. after an L2 flush): while the control cluster stages weights and runs
+    // the hidden forward, pull this CTA's share of W_out, the row records and the element
+    // arrays into L2 (only when W_out is L2-resident by policy)
+    if (p.w_resident && !(sp.exp & 8)) {
+        const size_t r1 = min((size_t)t1 * C::TR, (size_t)p.n), r0 = min((size_t)t0 * C::TR, r1);
+        prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
+        prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
+        const size_t e0 = (size_t)p.E * cta / G, e1 = (size_t)p.E * (cta + 1) / G;
+        prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
+        prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
+        prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
+    }
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     int tr = 0;
@@ -384,6 +392,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     if (!(sp.exp & 1)) eacc += fwd_tile<TS, HP>(p, b, t, y, has_inertia, inv_dt2, ident);
                 });
             }
+            // the ring streams the same W tiles (+ row records) for every pass: put the next
+            // pass's first tiles (VJP, or the next forward after a rejected step) in flight now
+            if (!(sp.exp & 2)) ring_prefetch(ring, t0, t1, issue_f);
             const double tot = block_sum(eacc, red);
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
@@ -413,79 +424,124 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         stamp(20);
         grid.sync();
         stamp(21);
-        // ================= energy + decision (every CTA, identical fixed-order sums)
-        int need = 0;
-        double E = 0.0;
+        // ================= gradient, speculatively: whether the line search accepts this
+        // point (Armijo) needs E, but the VJP is wanted in all other cases and nearly always
+        // here, so every CTA runs it when it may be needed and the control cluster alone
+        // sums the energy partials and decides (a rejected point's gradient is discarded).
+        int spec;
         {
-            double s = 0.0;
-            for (int b = tid; b < G; b += blockDim.x) s += __ldcg(p.e_part_elem + b);
-            const double e_el = block_sum(s, red);
-            s = 0.0;
-            for (int b = tid; b < G; b += blockDim.x) s += __ldcg(p.e_part_out + b);
-            const double e_in = block_sum(s, red);
-            E = e_el + (has_inertia ? e_in : 0.0);
             const int phase = __ldcg(&sh->phase), mode = __ldcg(&sh->mode);
-            if (phase == kPhaseFinalDecode || !isfinite(E)) need = 0;
-            else if (mode == kModeEval) need = __ldcg(&sh->want_grad);
-            else if (phase == kPhaseInit) need = 1;
-            else need = E <= __ldcg(&sh->f) + __ldcg(&sh->armijo_slope);
+            spec = phase == kPhaseFinalDecode ? 0 : (mode == kModeEval ? __ldcg(&sh->want_grad) : 1);
         }
-        if (need) {
-            // the VJP's W tiles do not depend on tv: put them in flight now
-            if (lane == 0) {
-                const int n = min(ring.spw, ring.count(t0, t1));
-                for (int j = 0; j < n; ++j) issue_vjp_w<TS, HP>(p, t0 + warp + NW * j, ring.buf(j), ring.bar(j), pol_w);
-            }
-            // ================= gather (4 lanes per vertex, contiguous CSR segments)
+        if (spec) {
+            // ================= vjp: tv for this CTA's rows (CSR gather, 2 lanes per vertex)
+            // while its first W tiles are in flight, then the self-issued TMA rings
             {
-                const bool ident = p.out_act == kIdentity;
-                const int nthr = G * blockDim.x;
-                for (int wb = (cta * blockDim.x + tid) & ~31; wb < 4 * p.n_free; wb += nthr)
-                    gather_vertex4(p, (wb + lane) >> 2, has_inertia, ident);
-            }
-            stamp(30);
-            fence_proxy_async();  // tv (generic writes) -> bulk copies below
-            grid.sync();
-            stamp(31);
-            // ================= vjp (self-issued TMA rings)
-            {
-                if (lane == 0) {
-                    const int n = min(ring.spw, ring.count(t0, t1));
-                    for (int j = 0; j < n; ++j) issue_vjp_tv<TS, HP>(p, t0 + warp + NW * j, ring.buf(j), ring.bar(j), pol_keep);
+                const int R0 = t0 * C::TR, R1 = min(t1 * C::TR, p.n);
+                // control CTAs: the energy partials' loads are issued now and summed after the
+                // VJP, off the critical path (G <= 160)
+                double pe[5], pi[5];
+                if (is_ctrl && warp == 0) {
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+                        const int b = lane + 32 * k;
+                        pe[k] = b < G ? __ldcg(p.e_part_elem + b) : 0.0;
+                        pi[k] = b < G ? __ldcg(p.e_part_out + b) : 0.0;
+                    }
                 }
+                if (!(sp.exp & 4)) gather_rows_smem(p, R0, R1, tv_s, has_inertia, p.out_act == kIdentity);
+                __syncthreads();
+                stamp(30);
+                if (sp.exp & 2) ring_prefetch(ring, t0, t1, issue_f);
                 double acc[C::NCH][C::V4];
 #pragma unroll
                 for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
                     for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
-                ring_run(ring, t0, t1, issue_v, [&](int t, const unsigned char* b) {
-                    if (!(sp.exp & 1)) vjp_tile<TS, HP>(p, b, t, acc);
+                ring_run(ring, t0, t1, issue_f, [&](int t, const unsigned char* b) {
+                    if (!(sp.exp & 1)) vjp_tile<TS, HP>(p, b, tv_s + (t * C::TR - R0), t, acc);
                 });
-                // per-warp partials -> this CTA's ybar partial (fixed warp order); the
-                // ring is idle now (every issued tile has been consumed)
-                double* wred = reinterpret_cast<double*>(ring.ring);  // NW x HP doubles <= ring bytes
+                // per-warp partials -> this CTA's ybar partial (fixed warp order) through the
+                // idle ring; then the ring is refilled and the cluster pre-reduces over DSMEM
+                // (rank order) so the control cluster sums G / CS cluster partials
                 __syncthreads();
+                double* wred = reinterpret_cast<double*>(ring.ring);  // NW x HP doubles <= ring bytes
 #pragma unroll
                 for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
                     for (int q = 0; q < C::V4; ++q) wred[warp * HP + (c * 32 + lane) * C::V4 + q] = acc[c][q];
                 __syncthreads();
+                double* cpart = tv_s;  // tv is consumed
                 for (int j = tid; j < HP; j += blockDim.x) {
                     double s = 0.0;
 #pragma unroll
                     for (int w = 0; w < NW; ++w) s += wred[w * HP + j];
-                    p.ybar_part[(size_t)cta * HP + j] = s;
+                    cpart[j] = s;
+                }
+                if (is_ctrl && warp == 0) {
+                    double s_el = 0.0, s_in = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+                        s_el += pe[k];
+                        s_in += pi[k];
+                    }
+                    s_el = warp_sum(s_el);
+                    s_in = warp_sum(s_in);
+                    if (lane == 0) {
+                        s_energy[0] = s_el;
+                        s_energy[1] = s_in;
+                    }
+                }
+                __syncthreads();
+                ring_prefetch(ring, t0, t1, issue_f);
+                cluster.sync();
+                {
+                    const int j0 = part_lo(HP, CS, crank), j1 = part_lo(HP, CS, crank + 1);
+                    for (int j = j0 + tid; j < j1; j += blockDim.x) {
+                        double v[CS];
+#pragma unroll
+                        for (int r = 0; r < CS; ++r) v[r] = cluster.map_shared_rank(cpart, r)[j];
+                        double s = 0.0;
+#pragma unroll
+                        for (int r = 0; r < CS; ++r) s += v[r];
+                        p.ybar_part[(size_t)(cta / CS) * HP + j] = s;
+                    }
                 }
             }
             stamp(40);
             grid.sync();
             stamp(41);
         }
-        // next forward's first tiles (drained at exit if there is no next forward)
-        ring_prefetch(ring, t0, t1, issue_f);
         // ================= control cluster: gradient, L-BFGS, next hidden forward
         if (is_ctrl) {
             DevState* s = cs.sst;
+            // energy (warp 0, fixed lane order; already summed during the VJP when it ran)
+            // and the real decision (every control CTA)
+            if (!spec && warp == 0) {
+                double s_el = 0.0, s_in = 0.0;
+#pragma unroll
+                for (int k = 0; k < 5; ++k) {
+                    const int b = lane + 32 * k;
+                    s_el += b < G ? __ldcg(p.e_part_elem + b) : 0.0;
+                    s_in += b < G ? __ldcg(p.e_part_out + b) : 0.0;
+                }
+                s_el = warp_sum(s_el);
+                s_in = warp_sum(s_in);
+                if (lane == 0) {
+                    s_energy[0] = s_el;
+                    s_energy[1] = s_in;
+                }
+            }
+            __syncthreads();
+            const double E = s_energy[0] + (has_inertia ? s_energy[1] : 0.0);
+            int need;
+            {
+                const int phase = __ldcg(&sh->phase), mode = __ldcg(&sh->mode);
+                if (phase == kPhaseFinalDecode || !isfinite(E)) need = 0;
+                else if (mode == kModeEval) need = __ldcg(&sh->want_grad);
+                else if (phase == kPhaseInit) need = 1;
+                else need = E <= __ldcg(&sh->f) + __ldcg(&sh->armijo_slope);
+            }
             if (crank == 0 && tid == 0) {
                 s->f_eval = E;
                 s->need_grad = need;
@@ -497,7 +553,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             }
             // pre-activations of the point just evaluated are in asl (own rows)
             cluster.sync();
-            if (need) ctrl_backward<TS, CS>(p, cs, cluster, crank, G, p.ybar_part, stamp);
+            if (need) ctrl_backward<TS, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
             if (crank == 0) {
                 if (warp == 0) {
                     int m = 0;

@@ -149,7 +149,7 @@ __device__ __forceinline__ void ring_init(uint64_t* full, int nst) {
 }
 
 // One warp computes every row of a forward tile: TR independent dot products,
-// interleaved butterfly reductions, lane j runs the epilogue of row j.
+// one multi-row reduction, lane (32 / TR) j runs the epilogue of row j.
 template <typename TS, int HP>
 __device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
                                            const double (&y)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4],
@@ -174,18 +174,31 @@ __device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsign
             }
         }
     }
+    // recursive-halving multi-row reduction: at offset o the lanes with bit o set keep
+    // the upper half of their rows and receive the partner's copy of it, so TR rows
+    // cost TR - 1 + log2(32 / TR) shuffles (not 5 TR).  Lane l ends up with the full
+    // sum of row l / (32 / TR).
+    static_assert(C::TR == 8 || C::TR == 16, "tile rows");
+    constexpr int LPR = 32 / C::TR;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+    for (int o = 16, n = C::TR; n > 1; o >>= 1) {
+        n >>= 1;
+        const bool up = (lane & o) != 0;
 #pragma unroll
-        for (int j = 0; j < C::TR; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-    double mine = 0.0;
+        for (int k = 0; k < n; ++k) {
+            const double give = up ? acc[k] : acc[k + n];
+            const double keep = up ? acc[k + n] : acc[k];
+            acc[k] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+        }
+    }
 #pragma unroll
-    for (int j = 0; j < C::TR; ++j)
-        if (lane == j) mine = acc[j];
+    for (int o = LPR / 2; o > 0; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+    const double mine = acc[0];
+    const int jr = lane / LPR;
     double e = 0.0;
-    if (lane < rows) {
-        const int row = t * C::TR + lane;
-        const double* e6 = ep + lane * 6;
+    if (lane % LPR == 0 && jr < rows) {
+        const int row = t * C::TR + jr;
+        const double* e6 = ep + jr * 6;
         const double a = mine + e6[0];
         double phi = a;
         if (!ident) {
@@ -205,13 +218,12 @@ __device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsign
 
 // One warp accumulates a VJP tile into its per-lane column accumulators.
 template <typename TS, int HP>
-__device__ __forceinline__ void vjp_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
+__device__ __forceinline__ void vjp_tile(const EvalParams<TS>& p, const unsigned char* st, const double* tv, int t,
                                          double (&acc)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4]) {
     using C = StreamCfg<TS, HP>;
     const int lane = threadIdx.x & 31;
     const int rows = min(C::TR, p.n - t * C::TR);
     const TS* tile = reinterpret_cast<const TS*>(st);
-    const double* tv = reinterpret_cast<const double*>(st + C::TILEB);
 #pragma unroll
     for (int j = 0; j < C::TR; ++j) {
         if (j < rows) {
@@ -271,17 +283,38 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
 template <typename TS>
 __device__ __forceinline__ void gather_vertex4(const EvalParams<TS>& p, int f, int has_inertia, bool ident) {
     const int lane = threadIdx.x & 31, q = lane & 3;
+    const bool valid = f < p.n_free;
+    const int row = 3 * f + (q < 3 ? q : 2);
+    // loads that do not depend on the segment bounds go first
+    double rin = 0.0, sc = 0.0;
+    int b = 0, e = 0;
+    if (valid) {
+        b = __ldg(p.csr_ptr + f);
+        e = __ldg(p.csr_ptr + f + 1);
+        if (has_inertia) rin = __ldcg(p.rin + row);
+        sc = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
+    }
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    if (f < p.n_free) {
-        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
-        const double2* F = reinterpret_cast<const double2*>(p.forces);
-#pragma unroll 4
-        for (int k = b + q; k < e; k += 4) {
-            const double2 a = __ldcg(F + 2 * (size_t)k);
-            const double2 c = __ldcg(F + 2 * (size_t)k + 1);
-            gx += a.x;
-            gy += a.y;
-            gz += c.x;
+    const double2* F = reinterpret_cast<const double2*>(p.forces);
+    // 6 entries per lane in one batch of loads (24 incident tets: one pass on Kuhn meshes)
+    for (int k0 = b + q; k0 < e; k0 += 24) {
+        double2 a[6], c[6];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+            const int k = k0 + 4 * u;
+            if (k < e) {
+                a[u] = __ldcg(F + 2 * (size_t)k);
+                c[u] = __ldcg(F + 2 * (size_t)k + 1);
+            } else {
+                a[u] = make_double2(0.0, 0.0);
+                c[u] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+            gx += a[u].x;
+            gy += a[u].y;
+            gz += c[u].x;
         }
     }
     // fixed-order combine: (q0 + q1) + (q2 + q3)
@@ -291,11 +324,56 @@ __device__ __forceinline__ void gather_vertex4(const EvalParams<TS>& p, int f, i
     gx += __shfl_xor_sync(0xffffffffu, gx, 2);
     gy += __shfl_xor_sync(0xffffffffu, gy, 2);
     gz += __shfl_xor_sync(0xffffffffu, gz, 2);
-    if (f < p.n_free && q < 3) {
-        const int row = 3 * f + q;
-        double g = q == 0 ? gx : (q == 1 ? gy : gz);
-        if (has_inertia) g += __ldcg(p.rin + row);
-        p.tv[row] = g * (ident ? p.eprow[6 * (size_t)row + 1] : __ldcg(p.dsout + row));
+    if (valid && q < 3) {
+        const double g = (q == 0 ? gx : (q == 1 ? gy : gz)) + rin;
+        p.tv[row] = g * sc;
+    }
+}
+
+// tv for the rows [R0, R1) of one CTA into shared memory, one thread per free
+// vertex: its CSR segment (ascending tet id) is summed in order from one batch of
+// up to 24 independent 256-bit loads (one request per 32-byte force entry).
+// Vertices straddling the range edge are computed by both neighbours, identically.
+__device__ __forceinline__ double4 ld_cg_d4(const double* p) {
+    double4 v;
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+template <typename TS>
+__device__ __forceinline__ void gather_rows_smem(const EvalParams<TS>& p, int R0, int R1, double* tv_s,
+                                                 int has_inertia, bool ident) {
+    const int f0 = R0 / 3, nf = R1 > R0 ? (R1 - 1) / 3 - f0 + 1 : 0;
+    for (int k = threadIdx.x; k < nf; k += blockDim.x) {
+        const int f = f0 + k;
+        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
+        double rin[3] = {0.0, 0.0, 0.0}, sc[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int row = 3 * f + c;
+            if (has_inertia) rin[c] = __ldcg(p.rin + row);
+            sc[c] = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
+        }
+        double gx = 0.0, gy = 0.0, gz = 0.0;
+        for (int k0 = b; k0 < e; k0 += 24) {
+            double4 v[24];
+#pragma unroll
+            for (int u = 0; u < 24; ++u)
+                v[u] = k0 + u < e ? ld_cg_d4(p.forces + 4 * (size_t)(k0 + u)) : make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 24; ++u) {
+                gx += v[u].x;
+                gy += v[u].y;
+                gz += v[u].z;
+            }
+        }
+        const double g[3] = {gx, gy, gz};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int row = 3 * f + c;
+            if (row >= R0 && row < R1) tv_s[row - R0] = (g[c] + rin[c]) * sc[c];
+        }
     }
 }
 
@@ -339,7 +417,9 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_tma_kernel(const EvalParam
     for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
         for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
-    ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) { vjp_tile<TS, HP>(p, b, t, acc); });
+    ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) {
+        vjp_tile<TS, HP>(p, b, reinterpret_cast<const double*>(b + C::TILEB), t, acc);
+    });
 #pragma unroll
     for (int c = 0; c < C::NCH; ++c)
 #pragma unroll

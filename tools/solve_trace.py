@@ -11,7 +11,7 @@ import paper_2409_03807_b200 as P  # noqa: E402
 from paper_2409_03807_b200 import configs  # noqa: E402
 
 names = {0: "enter", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
-         30: "gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid"}
+         30: "tv gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid"}
 for name in sys.argv[1:] or ["c2"]:
     pr = configs.build(name)
     sysm = pr.system()
