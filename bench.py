@@ -36,7 +36,11 @@ sys.path.insert(0, ROOT)
 FLUSH_BYTES = 512 << 20
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the reported kernel, from the
 # committed ncu --set full captures (profiles/); None until captured for that path.
-TRAFFIC = {}
+TRAFFIC = {
+    # profiles/r01_solve_c2_full.txt: one c2 fp64 E+grad eval (ncu flushes caches before the
+    # launch, like the bench's L2 flush): dram read 72.97 MB + write 4.86 MB
+    ("c2", True): 77.83e6,
+}
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
@@ -261,7 +265,7 @@ def main():
     solve = sysm.solve_kernel_info()
     if solve["in_use"]:
         # one persistent launch per evaluation: the kernel IS the evaluation
-        kname, alg, dur_s = "solve_kernel (persistent, cooperative clusters)", alg_total, float(of_ms.mean()) * 1e-3
+        kname, alg, dur_s = "solve_kernel (persistent cluster kernel, one launch per eval)", alg_total, float(of_ms.mean()) * 1e-3
     else:
         kname, alg, dur_s = "out_fwd_tma_kernel", alg_out, float(of_ms.mean()) * 1e-3
     achieved = alg / dur_s / 1e9

@@ -465,19 +465,19 @@ struct Impl final : ImplBase {
     void launch_solve(Context& c, int task, int quasi, int want_grad = 1) {
         SolveParams sp = solve_params(c, task, quasi, want_grad);
         cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[2];
+        // cluster launch only: the grid barrier is the kernel's own (grid_barrier), and
+        // the grid never exceeds the co-resident cluster count
+        cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = cs;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        at[1].id = cudaLaunchAttributeCooperative;
-        at[1].val.cooperative = 1;
         cfg.gridDim = dim3(solve_grid);
         cfg.blockDim = dim3(kSolveThreads);
         cfg.dynamicSmemBytes = solve_smem;
         cfg.stream = c.stream;
         cfg.attrs = at;
-        cfg.numAttrs = 2;
+        cfg.numAttrs = 1;
         cuda_check(cudaLaunchKernelEx(&cfg, solve, ps, sp), "solve kernel launch");
         c.launches += 1;
     }

@@ -24,7 +24,28 @@ struct SolveShared {
     int mode, phase, want_grad, done;
     double f, armijo_slope;  // f + 1e-4 alpha gtd threshold pieces
     int status;
+    unsigned grid_bar;       // grid barrier word (generation = top bit; never reset)
 };
+
+// Grid-wide barrier of the persistent kernel (all CTAs co-resident: the grid is
+// sized from cudaOccupancyMaxActiveClusters).  CTA 0 adds 2^31 - (G - 1), every
+// other CTA adds 1, so the top bit flips exactly when all G have arrived; waiters
+// spin until their generation bit changes.  gpu-scope fences on both sides order
+// every thread's prior writes (via bar.sync) before every later read.
+__device__ __forceinline__ void grid_barrier(unsigned* word, int cta, int G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned inc = cta == 0 ? (0x80000000u - (unsigned)(G - 1)) : 1u;
+        __threadfence();
+        unsigned old, cur;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(word), "r"(inc) : "memory");
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(word) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+        __threadfence();
+    }
+    __syncthreads();
+}
 
 struct SolveParams {
     int task;         // 0 = eval (ctrl start + one evaluation), 1 = minimize, 2 = step
@@ -252,7 +273,6 @@ template <typename TS, int HP, int CS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParams<TS> p, const SolveParams sp) {
     using C = StreamCfg<TS, HP>;
     extern __shared__ __align__(128) unsigned char smem[];
-    cg::grid_group grid = cg::this_grid();
     cg::cluster_group cluster = cg::this_cluster();
     const int G = gridDim.x, cta = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -371,7 +391,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     }
     stamp(2);
     fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
-    grid.sync();
+    grid_barrier(&sp.sh->grid_bar, cta, G);
     stamp(3);
     if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
 
@@ -399,7 +419,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
         stamp(10);
-        grid.sync();
+        grid_barrier(&sp.sh->grid_bar, cta, G);
         stamp(11);
         // ================= element pass
         {
@@ -422,7 +442,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_elem[cta] = tot;
         }
         stamp(20);
-        grid.sync();
+        grid_barrier(&sp.sh->grid_bar, cta, G);
         stamp(21);
         // ================= gradient, speculatively: whether the line search accepts this
         // point (Armijo) needs E, but the VJP is wanted in all other cases and nearly always
@@ -509,7 +529,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 }
             }
             stamp(40);
-            grid.sync();
+            grid_barrier(&sp.sh->grid_bar, cta, G);
             stamp(41);
         }
         // ================= control cluster: gradient, L-BFGS, next hidden forward
@@ -580,7 +600,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (more) ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
         }
         stamp(50);
-        grid.sync();
+        grid_barrier(&sp.sh->grid_bar, cta, G);
         stamp(51);
         if (__ldcg(&sh->done)) break;
     }
@@ -594,7 +614,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         for (int k = tid; k < nwords; k += blockDim.x) dst[k] = src[k];
     }
     if (sp.task == 2) {
-        grid.sync();
+        grid_barrier(&sp.sh->grid_bar, cta, G);
         const double dt = __ldcg(&st->dt);
         for (int v = cta * blockDim.x + tid; v < p.V; v += G * blockDim.x)
             for (int c = 0; c < 3; ++c) {
