@@ -420,6 +420,9 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             std::vector<double> Wh, bh;
             for (int l = 0; l < c.nhid; ++l) {
                 const HostLayer& hl = c.layers[l];
+                // even offsets: 16-byte aligned layer starts for the bulk-copy staging
+                if (Wh.size() & 1) Wh.push_back(0.0);
+                if (bh.size() & 1) bh.push_back(0.0);
                 c.hoff[l] = (int)Wh.size();
                 c.boff[l] = (int)bh.size();
                 c.hrows[l] = hl.rows;

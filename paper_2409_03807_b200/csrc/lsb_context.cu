@@ -200,6 +200,7 @@ struct Impl final : ImplBase {
     // persistent solve kernel (cooperative launch of thread-block clusters)
     typename SolveFn<TS>::type solve = nullptr;
     size_t solve_smem = 0;
+    unsigned launch_seq = 0;
     int solve_spw = 1, solve_spw_ctrl = 1, solve_tv_cap = 0, solve_tv_off = 0, solve_tv_off_ctrl = 0;
     int solve_grid = 0;
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
@@ -250,6 +251,7 @@ struct Impl final : ImplBase {
             cudaGraphDestroy(g);
         }
         cuda_check(cudaGraphLaunch(g_timed, c.stream), "graph launch (timed eval)");
+        c.launches += 6;  // ctrl, out_fwd, elem, gather, vjp, ctrl
     }
 
     void setup(Context& c) override {
@@ -447,6 +449,7 @@ struct Impl final : ImplBase {
         sp.tv_off_ctrl = solve_tv_off_ctrl;
         sp.tv_cap = solve_tv_cap;
         if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);
+        sp.seq = ++launch_seq;
         sp.want_grad = want_grad;
         sp.u_state = c.d_u_state;
         sp.v_state = c.d_v_state;

@@ -25,6 +25,7 @@ struct SolveShared {
     double f, armijo_slope;  // f + 1e-4 alpha gtd threshold pieces
     int status;
     unsigned grid_bar;       // grid barrier word (generation = top bit; never reset)
+    unsigned staged_seq;     // = SolveParams::seq once the control cluster's staging landed
 };
 
 // Grid-wide barrier of the persistent kernel (all CTAs co-resident: the grid is
@@ -56,6 +57,7 @@ struct SolveParams {
     int tv_off;       // byte offset of the tv/partials scratch (non-control CTAs)
     int tv_off_ctrl;  // ditto, control CTAs (after their control area)
     int tv_cap;       // its capacity in doubles (>= rows per CTA and >= hp)
+    unsigned seq;     // launch sequence number (host-incremented)
     int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
     // dynamics
     const double* u_state;
@@ -86,6 +88,7 @@ struct CtrlSmem {
     double* bsl;      // kMaxLayers * 64
     double* asl;      // kMaxLayers * 64
     DevState* sst;
+    uint64_t* wbar;  // kMaxLayers + 1 staging barriers (static smem)
     int woff[kMaxLayers];
 };
 constexpr size_t ctrl_fixed_words() {
@@ -101,23 +104,71 @@ __device__ __forceinline__ int part_owner(int j, int R) {
     return q;
 }
 
+// Stage this CTA's weight/bias row slices (+ the solver state on CTA 0): 16-byte
+// aligned pieces as 1-D bulk copies completing on one mbarrier per layer (wbar[l])
+// and one for the state (wbar[kMaxLayers]), so layer 0 can start while the rest
+// is in flight; misaligned pieces fall back to cp.async (waited here).  Users wait
+// with ctrl_wait_layer / ctrl_wait_state (parity 0: free once complete).
+__device__ __forceinline__ bool bulk_ok(const void* dst, const void* src, size_t bytes) {
+    return ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15u) == 0;
+}
 template <typename TS, int CS>
-__device__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state) {
+__device__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state, uint64_t* wbar) {
+    const int tid = threadIdx.x;
     int off = 0;
+    bool async_used = false;
+    if (tid == 0) {
+        for (int l = 0; l <= kMaxLayers; ++l) mbar_init(&wbar[l], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t keep = l2_policy(1);
     for (int l = 0; l < p.nhid; ++l) {
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
         cs.woff[l] = off;
-        stage_doubles(cs.wsl + off, p.Wh + p.hoff[l] + (size_t)i0 * C, (i1 - i0) * C);
-        stage_doubles(cs.bsl + l * 64, p.bh + p.boff[l] + i0, i1 - i0);
+        double* wd = cs.wsl + off;
+        const double* ws = p.Wh + p.hoff[l] + (size_t)i0 * C;
+        const size_t wb = (size_t)(i1 - i0) * C * 8;
+        double* bd = cs.bsl + l * 64;
+        const double* bs = p.bh + p.boff[l] + i0;
+        const size_t bb = (size_t)(i1 - i0) * 8;
+        const bool w_bulk = bulk_ok(wd, ws, wb), b_bulk = bulk_ok(bd, bs, bb);
+        if (!w_bulk) stage_doubles(wd, ws, (i1 - i0) * C);
+        if (!b_bulk) stage_doubles(bd, bs, i1 - i0);
+        async_used |= !w_bulk || !b_bulk;
+        if (tid == 0) {
+            unsigned tx = 0;
+            if (w_bulk && wb) {
+                tma_load_1d(wd, ws, (unsigned)wb, &wbar[l], keep);
+                tx += (unsigned)wb;
+            }
+            if (b_bulk && bb) {
+                tma_load_1d(bd, bs, (unsigned)bb, &wbar[l], keep);
+                tx += (unsigned)bb;
+            }
+            mbar_expect_tx(&wbar[l], tx);  // arrive + expect: completes when the bytes land
+        }
         off += ((i1 - i0) * C + 1) & ~1;
     }
-    if (with_state && c == 0)
-        stage_doubles(reinterpret_cast<double*>(cs.sst), reinterpret_cast<const double*>(p.st),
-                      (int)(sizeof(DevState) / sizeof(double)));
-    cp_async_wait_all();
-    __syncthreads();
+    if (with_state && c == 0) {
+        double* sd = reinterpret_cast<double*>(cs.sst);
+        const double* ss = reinterpret_cast<const double*>(p.st);
+        const bool s_bulk = bulk_ok(sd, ss, sizeof(DevState));
+        if (!s_bulk) stage_doubles(sd, ss, (int)(sizeof(DevState) / sizeof(double)));
+        async_used |= !s_bulk;
+        if (tid == 0) {
+            if (s_bulk) tma_load_1d(sd, ss, (unsigned)sizeof(DevState), &wbar[kMaxLayers], keep);
+            mbar_expect_tx(&wbar[kMaxLayers], s_bulk ? (unsigned)sizeof(DevState) : 0u);
+        }
+    }
+    if (async_used) {  // uniform across the CTA
+        cp_async_wait_all();
+        __syncthreads();
+    }
 }
+__device__ __forceinline__ void ctrl_wait_layer(uint64_t* wbar, int l) { mbar_wait(&wbar[l], 0); }
+__device__ __forceinline__ void ctrl_wait_state(uint64_t* wbar) { mbar_wait(&wbar[kMaxLayers], 0); }
 
 // Backward through the hidden layers.  ybar of the last hidden layer is the
 // fixed-order sum of the per-CTA partials (G x hp); each CTA reduces its own
@@ -179,6 +230,7 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
         }
         __syncthreads();
         const double* Ws = cs.wsl + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
         double* rb = cs.rbuf[l & 1];
         const int Rp = l > 0 ? p.hrows[l - 1] : C;
         for (int j = tid; j < C; j += nt) {
@@ -232,6 +284,7 @@ __device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_
         const double* x = cs.xin[l & 1];
         double* xn = cs.xin[(l & 1) ^ 1];
         const double* Ws = cs.wsl + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
         // rows per warp: the smallest power of two that covers nrow in one pass (<= 8),
         // LPR = 32 / rpw lanes share one row (split-K) and reduce with log2(LPR) shuffles
         int rpw = 1;
@@ -306,21 +359,6 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     const uint64_t pol_w = l2_policy(p.w_resident), pol_keep = l2_policy(1);
     auto issue_f = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep); };
     double* tv_s = reinterpret_cast<double*>(smem + (is_ctrl ? sp.tv_off_ctrl : sp.tv_off));
-    // the first forward tiles do not depend on z: prefetch now (a step rewrites the
-    // qbar column of the row records first, so it prefetches after that)
-    if (sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
-    // cold start (e.g. after an L2 flush): while the control cluster stages weights and runs
-    // the hidden forward, pull this CTA's share of W_out, the row records and the element
-    // arrays into L2 (only when W_out is L2-resident by policy)
-    if (p.w_resident && !(sp.exp & 8)) {
-        const size_t r1 = min((size_t)t1 * C::TR, (size_t)p.n), r0 = min((size_t)t0 * C::TR, r1);
-        prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
-        prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
-        const size_t e0 = (size_t)p.E * cta / G, e1 = (size_t)p.E * (cta + 1) / G;
-        prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
-        prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
-        prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
-    }
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     int tr = 0;
@@ -333,8 +371,42 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     };
     stamp(0);
 
-    // ---- control cluster: stage weights (+ state) once
-    if (is_ctrl) ctrl_stage<TS, CS>(p, cs, crank, true);
+    // ---- control cluster: stage weights (+ state) once.  Issued before any other bulk
+    // traffic: an SM's TMA engine serves requests in order.
+    __shared__ __align__(8) uint64_t s_wbar[kMaxLayers + 1];
+    cs.wbar = s_wbar;
+    if (is_ctrl) ctrl_stage<TS, CS>(p, cs, crank, true, s_wbar);
+    // the first forward tiles do not depend on z: prefetch now (a step rewrites the
+    // qbar column of the row records first, so it prefetches after that)
+    if (sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
+    // cold start (e.g. after an L2 flush): while the control cluster stages weights and runs
+    // the hidden forward, pull this CTA's share of W_out, the row records and the element
+    // arrays into L2 (only when W_out is L2-resident by policy)
+    if (p.w_resident && !is_ctrl && !(sp.exp & 8)) {
+        // the non-control CTAs cover every row / tet; they start once the control
+        // cluster's (latency-critical) staging has landed, so the bulk traffic overlaps
+        // the hidden forward instead of delaying it
+        if (lane == 0) {
+            unsigned s;
+            do {
+                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(s) : "l"(&sp.sh->staged_seq) : "memory");
+            } while (s != sp.seq);
+        }
+        __syncwarp();
+        const int q = cta - CS, Q = G - CS;
+        const size_t r0 = (size_t)p.n * q / Q, r1 = (size_t)p.n * (q + 1) / Q;
+        prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
+        prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
+        const size_t e0 = (size_t)p.E * q / Q, e1 = (size_t)p.E * (q + 1) / Q;
+        prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
+        prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
+        prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
+    }
+    if (is_ctrl && crank == 0) {
+        ctrl_wait_state(s_wbar);  // the state is written below
+        if (p.nhid > 0) ctrl_wait_layer(s_wbar, 0);
+        if (tid == 0) asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&sp.sh->staged_seq), "r"(sp.seq) : "memory");
+    }
     stamp(1);
 
     // ---- step prologue: qbar - X and warm start (all CTAs), reference reduced_step :249-256
@@ -425,18 +497,31 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         {
             double eacc = 0.0;
             const int stride = G * blockDim.x;
-            for (int e = cta * blockDim.x + tid; e < p.E; e += stride) {
-                const int4 t = __ldg(p.tets + e);
-                double rc[12];
-                load_rec<TS>(p.rec, (size_t)e, rc);
-                double u0[3], u1[3], u2[3], u3[3];
-                load_u(p.U, t.x, u0);
-                load_u(p.U, t.y, u1);
-                load_u(p.U, t.z, u2);
-                load_u(p.U, t.w, u3);
-                double f[12];
-                eacc += tet_energy_forces(u0, u1, u2, u3, rc, f);
-                store_forces_csr(p.forces, __ldg(p.fpos + e), f);
+            // two tets in flight per thread: both index loads, then all 8 vertex gathers
+            for (int e0 = cta * blockDim.x + tid; e0 < p.E; e0 += 2 * stride) {
+                const int e1 = e0 + stride;
+                const bool has1 = e1 < p.E;
+                const int4 ta = __ldg(p.tets + e0);
+                const int4 tb = has1 ? __ldg(p.tets + e1) : ta;
+                double u[2][4][3];
+                load_u(p.U, ta.x, u[0][0]);
+                load_u(p.U, ta.y, u[0][1]);
+                load_u(p.U, ta.z, u[0][2]);
+                load_u(p.U, ta.w, u[0][3]);
+                load_u(p.U, tb.x, u[1][0]);
+                load_u(p.U, tb.y, u[1][1]);
+                load_u(p.U, tb.z, u[1][2]);
+                load_u(p.U, tb.w, u[1][3]);
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (k == 1 && !has1) break;
+                    const int e = k ? e1 : e0;
+                    double rc[12];
+                    load_rec<TS>(p.rec, (size_t)e, rc);
+                    double f[12];
+                    eacc += tet_energy_forces(u[k][0], u[k][1], u[k][2], u[k][3], rc, f);
+                    store_forces_csr(p.forces, __ldg(p.fpos + e), f);
+                }
             }
             const double tot = block_sum(eacc, red);
             if (tid == 0) p.e_part_elem[cta] = tot;

@@ -12,12 +12,19 @@ from paper_2409_03807_b200 import configs  # noqa: E402
 
 names = {0: "enter", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
          30: "tv gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid"}
-for name in sys.argv[1:] or ["c2"]:
+flush = "--flush" in sys.argv
+if flush:
+    import torch
+    fbuf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["c2"]:
     pr = configs.build(name)
     sysm = pr.system()
     sysm.set_inertia(configs.timestep0_qbar(pr, sysm.mass), configs.DT)
     z = 0.5 * np.random.default_rng(0).standard_normal(pr.model.r)
     for rep in range(3):
+        if flush:
+            fbuf.zero_()
+            torch.cuda.synchronize()
         sysm.eval(z)
     buf = (C.c_ulonglong * 512)()
     cnt = C.c_int()
