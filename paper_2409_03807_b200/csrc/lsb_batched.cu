@@ -646,6 +646,7 @@ struct BatchedEngine : BatchedBase {
     int hcols = 0;
 
     ~BatchedEngine() override {
+        tc.release();
         for (void* p : allocs) cudaFree(p);
     }
     template <typename X>
@@ -775,7 +776,7 @@ struct BatchedEngine : BatchedBase {
         else
             cuda_check(cudaFuncSetAttribute(elem_batched_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)esmem), "elem smem");
-        tc.init(c, d_W, n, h, BC);
+        tc.init(c.stream, d_W, n, h, BC, c.num_sms);
     }
 
     // One chunk of N <= BC columns; Z (N x r, host) -> E (N), G (N x r or null).
@@ -825,7 +826,8 @@ struct BatchedEngine : BatchedBase {
                     d_blk_vptr, d_tet_loc, d_U, BC, d_part, d_eblk);
         }
         energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, nrow_tiles, d_epart, nblk, d_eblk, has_inertia, d_E);
-        c.batched_launches += 5 + c.nhid;
+        c.batched_launches += 5 + c.nhid + tc.launches;
+        tc.launches = 0;
         if (G) {
             combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, d_vslot_ptr, d_vslot, d_part, d_rin, has_inertia,
                                                          c.d_eprow, d_T);

@@ -1,16 +1,373 @@
-// tcgen05 (5th-gen tensor core) GEMMs of the batched path: W_out (n x h) times
-// a batch tile (forward) and W_out^T times the gathered gradients (VJP).
+// tcgen05 (5th-generation tensor core) GEMMs of the batched path (config 4 and the
+// config-5 tangent VJP): the output layer's forward C = W_out Y and its VJP
+// Ybar = W_out^T T over a batch of latent columns.
+//
+// Both are D(128 x N) = sum over 32-wide K slices of A_s (128 x 32) . B_s (N x 32)^T,
+// computed as 3xTF32 (hi.hi + hi.lo + lo.hi, fixed order) for ~fp32 accuracy:
+// tf32 keeps 10 mantissa bits, x = hi + lo with hi = rna_tf32(x) and lo = x - hi.
+//
+// Operand layout: every slice is pre-tiled into the canonical SWIZZLE_NONE
+// K-major UMMA layout (8-row x 16-byte core matrices; core (chunk c, row group g)
+// at ((c * R/8) + g) * 128 B, so SBO = 128 B between row groups and LBO = R * 16 B
+// between the two 16-byte K chunks one MMA consumes), hi block then lo block,
+// contiguous -- one 1-D bulk copy (TMA) per operand per slice.
+//
+// Kernel roles (192 threads): warps 0-3 epilogue (TMEM lane quarter = warp),
+// warp 4 lane 0 TMA producer, warp 5 lane 0 MMA issuer.  A 3-stage smem ring
+// (full/empty mbarriers; the MMA frees a stage with tcgen05.commit), and two TMEM
+// accumulators (acc_full/acc_empty) so the epilogue of job j overlaps the MMAs of j+1.
+//
+//   mode 0 (forward): job = 128-row tile of W_out, its S slices against the same
+//                     B slices (Y^T); rows written to C (row-major, ldc).
+//   mode 1 (VJP):     one 128-row A (W_out^T, h <= 128), job = contiguous slice range
+//                     (split-K); 128 x N partial per job, reduced in job order.
 #pragma once
 
-#include "lsb_context.hpp"
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lsb_common.cuh"
 
 namespace lsb {
+namespace tc {
 
+constexpr int kSliceK = 32;  // K elements (fp32 / tf32) per slice
+constexpr int kTileM = 128;
+constexpr int kStages = 3;
+constexpr int kThreads = 192;
+
+__host__ __device__ constexpr size_t slice_floats(int rows) { return 2 * (size_t)rows * kSliceK; }  // hi + lo
+
+// element (row, kk) of one hi-or-lo block with R rows (kk < 32)
+__host__ __device__ inline size_t core_off(int row, int kk, int R) {
+    const int c = kk >> 2, e = kk & 3, g = row >> 3, r = row & 7;
+    return (((size_t)c * (R >> 3) + g) * 8 + r) * 4 + e;
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    return __uint_as_float(u);
+}
+
+// Pack a strided fp32 matrix (element (row, k) = src[row * srs + k * sks], rows x K)
+// into tiles of R rows x S slices: block (tile t, slice s) at ((t * S) + s) * 2R*32.
+// Rows >= rows and k >= K are zero.
+__global__ void pack_kernel(const float* __restrict__ src, long long srs, long long sks, int rows, int K, int R,
+                            int tiles, int S, float* __restrict__ dst) {
+    const long long total = (long long)tiles * R * S * kSliceK;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        // i enumerates (tile, slice, row, kk): kk fastest when k is the contiguous source
+        // dimension (sks == 1), row fastest otherwise -- coalesced reads either way
+        int kk, row;
+        long long q;
+        if (sks == 1) {
+            kk = (int)(i % kSliceK);
+            q = i / kSliceK;
+            row = (int)(q % R);
+            q /= R;
+        } else {
+            row = (int)(i % R);
+            q = i / R;
+            kk = (int)(q % kSliceK);
+            q /= kSliceK;
+        }
+        const int s = (int)(q % S);
+        const int t = (int)(q / S);
+        const int grow = t * R + row, k = s * kSliceK + kk;
+        const float x = (grow < rows && k < K) ? src[(long long)grow * srs + (long long)k * sks] : 0.f;
+        const float hi = tf32_rna(x);
+        float* blk = dst + ((size_t)t * S + s) * slice_floats(R);
+        const size_t o = core_off(row, kk, R);
+        blk[o] = hi;
+        blk[(size_t)R * kSliceK + o] = x - hi;
+    }
+}
+
+// ---- PTX wrappers -------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+    // base_offset 0, lbo_mode 0, layout_type 0 = SWIZZLE_NONE
+    return d;
+}
+// kind::tf32, D f32, A/B tf32, both K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t make_idesc(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct GemmArgs {
+    const float* A;  // pre-tiled A slices (128 rows each)
+    const float* B;  // pre-tiled B slices (N rows each)
+    float* out;
+    int mode;        // 0 forward (jobs = A tiles), 1 split-K partials
+    int njobs;
+    int S;           // mode 0: slices per job; mode 1: total slices
+    int N;           // batch columns (multiple of 32, <= 256)
+    int ldc;         // mode 0: row stride of out
+    int m_valid;     // mode 0: valid rows of out
+    uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ void job_slices(const GemmArgs& g, int j, int& s0, int& s1) {
+    if (g.mode == 0) {
+        s0 = 0;
+        s1 = g.S;
+    } else {
+        s0 = (int)((long long)g.S * j / g.njobs);
+        s1 = (int)((long long)g.S * (j + 1) / g.njobs);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base_s;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = g.N;
+    const uint32_t a_bytes = (uint32_t)(slice_floats(kTileM) * 4), b_bytes = (uint32_t)(slice_floats(N) * 4);
+    const uint32_t stage_bytes = a_bytes + b_bytes;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&acc_full[a], 1);
+            mbar_init(&acc_empty[a], 128);
+        }
+        mbar_fence_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_s)),
+                     "r"(g.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+
+    if (warp == 4) {
+        // ---- TMA producer
+        if (lane == 0) {
+            const uint64_t pol_b = l2_policy(1);  // B slices: shared by every CTA
+            uint64_t pol_a;
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_a));
+            int it = 0;
+            for (int j = blockIdx.x; j < g.njobs; j += gridDim.x) {
+                int s0, s1;
+                job_slices(g, j, s0, s1);
+                for (int s = s0; s < s1; ++s, ++it) {
+                    const int st = it % kStages, u = it / kStages;
+                    if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
+                    unsigned char* sa = smem + (size_t)st * stage_bytes;
+                    const size_t a_slice = g.mode == 0 ? (size_t)j * g.S + s : (size_t)s;
+                    mbar_expect_tx(&full[st], stage_bytes);
+                    tma_load_1d(sa, g.A + a_slice * slice_floats(kTileM), a_bytes, &full[st], pol_a);
+                    tma_load_1d(sa + a_bytes, g.B + (size_t)s * slice_floats(N), b_bytes, &full[st], pol_b);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---- MMA issuer (single thread)
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(N);
+            int it = 0, jl = 0;
+            for (int j = blockIdx.x; j < g.njobs; j += gridDim.x, ++jl) {
+                const int acc = jl & 1, u = jl >> 1;
+                if (u > 0) mbar_wait(&acc_empty[acc], (u - 1) & 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * N);
+                int s0, s1;
+                job_slices(g, j, s0, s1);
+                for (int s = s0; s < s1; ++s, ++it) {
+                    const int st = it % kStages;
+                    mbar_wait(&full[st], (it / kStages) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + (size_t)st * stage_bytes);
+                    const uint32_t sb = sa + a_bytes;
+                    const uint32_t a_lo = (uint32_t)(kTileM * kSliceK * 4), b_lo = (uint32_t)(N * kSliceK * 4);
+#pragma unroll
+                    for (int ks = 0; ks < kSliceK / 8; ++ks) {
+                        // one MMA consumes K = 8 tf32 = two 16-byte chunks
+                        const uint32_t ao = (uint32_t)ks * 2 * (kTileM / 8) * 128, bo = (uint32_t)ks * 2 * (N / 8) * 128;
+                        const uint64_t ahi = make_desc(sa + ao, kTileM * 16, 128);
+                        const uint64_t alo = make_desc(sa + a_lo + ao, kTileM * 16, 128);
+                        const uint64_t bhi = make_desc(sb + bo, (uint32_t)N * 16, 128);
+                        const uint64_t blo = make_desc(sb + b_lo + bo, (uint32_t)N * 16, 128);
+                        mma_tf32(d, ahi, bhi, idesc, (s > s0 || ks > 0) ? 1u : 0u);
+                        mma_tf32(d, ahi, blo, idesc, 1u);
+                        mma_tf32(d, alo, bhi, idesc, 1u);
+                    }
+                    mma_commit(&empty[st]);  // stage reusable once these MMAs have read it
+                }
+                // (an empty job issues no MMA; its epilogue writes zeros)
+                mma_commit(&acc_full[acc]);
+            }
+        }
+    } else {
+        // ---- epilogue: warps 0-3, thread = accumulator row
+        const int row = warp * 32 + lane;
+        int jl = 0;
+        for (int j = blockIdx.x; j < g.njobs; j += gridDim.x, ++jl) {
+            const int acc = jl & 1, u = jl >> 1;
+            mbar_wait(&acc_full[acc], u & 1);
+            tc_fence_after();
+            int s0, s1;
+            job_slices(g, j, s0, s1);
+            const bool empty_job = s1 == s0;
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * N + c0), v);
+                if (empty_job) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                }
+                float* dst;
+                if (g.mode == 0) {
+                    const int grow = j * kTileM + row;
+                    if (grow >= g.m_valid) continue;
+                    dst = g.out + (size_t)grow * g.ldc + c0;
+                } else {
+                    dst = g.out + ((size_t)j * kTileM + row) * N + c0;
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols) : "memory");
+    }
+}
+
+// Ybar[m][b] = sum_j part[j][m][b] (job order), m < h
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int njobs, int h, int N, float* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h * N; i += gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int j = 0; j < njobs; ++j) s += __ldg(part + (size_t)j * kTileM * N + i);
+        out[i] = s;
+    }
+}
+
+}  // namespace tc
+
+// Host side: owns the pre-tiled W_out operands and the per-call B / partial buffers.
 struct TcGemm {
     bool enabled = false;
-    void init(Context&, const float*, int, int, int) {}
-    bool gemm_out(cudaStream_t, const float*, float*) { return false; }
-    bool gemm_vjp(cudaStream_t, const float*, float*) { return false; }
+    int n = 0, h = 0, N = 0, S1 = 0, S2 = 0, tiles1 = 0, jobs2 = 0, sms = 0;
+    float *A1 = nullptr, *A2 = nullptr, *B1 = nullptr, *B2 = nullptr, *part = nullptr;
+    size_t smem = 0;
+    uint32_t tmem_cols = 0;
+    long long launches = 0;
+
+    static void* dalloc(size_t bytes) {
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, bytes), "tc malloc");
+        return p;
+    }
+
+    // W: device fp32 n x h row-major.  N = batch columns per call.
+    void init(cudaStream_t s, const float* W, int n_, int h_, int N_, int num_sms) {
+        const char* env = getenv("LSB_TC");
+        if (env && env[0] == '0') return;
+        if (h_ > tc::kTileM || N_ % 32 != 0 || N_ > 256 || N_ < 32) return;
+        n = n_;
+        h = h_;
+        N = N_;
+        sms = num_sms;
+        S1 = (h + tc::kSliceK - 1) / tc::kSliceK;
+        S2 = (n + tc::kSliceK - 1) / tc::kSliceK;
+        tiles1 = (n + tc::kTileM - 1) / tc::kTileM;
+        jobs2 = std::min(S2, num_sms);
+        A1 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(tc::kTileM) * (size_t)tiles1 * S1));
+        A2 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(tc::kTileM) * (size_t)S2));
+        B1 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(N) * (size_t)S1));
+        B2 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(N) * (size_t)S2));
+        part = static_cast<float*>(dalloc(sizeof(float) * (size_t)jobs2 * tc::kTileM * N));
+        // A1: W rows x h (K); A2: W^T = h rows x n (K)
+        tc::pack_kernel<<<num_sms * 8, 256, 0, s>>>(W, h, 1, n, h, tc::kTileM, tiles1, S1, A1);
+        tc::pack_kernel<<<num_sms * 8, 256, 0, s>>>(W, 1, h, h, n, tc::kTileM, 1, S2, A2);
+        cuda_check(cudaGetLastError(), "tc pack W");
+        smem = (size_t)tc::kStages * (tc::slice_floats(tc::kTileM) + tc::slice_floats(N)) * 4;
+        if (smem > 227 * 1024) {
+            release();
+            return;
+        }
+        tmem_cols = 32;
+        while (tmem_cols < (uint32_t)(2 * N)) tmem_cols <<= 1;
+        cuda_check(cudaFuncSetAttribute(tc::gemm3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                   "tc smem");
+        cuda_check(cudaStreamSynchronize(s), "tc init");
+        enabled = true;
+    }
+    void release() {
+        for (float* p : {A1, A2, B1, B2, part})
+            if (p) cudaFree(p);
+        A1 = A2 = B1 = B2 = part = nullptr;
+        enabled = false;
+    }
+
+    // C (n x N, row-major, ldc = N) = W Y, Y: h x N (feature-major)
+    bool gemm_out(cudaStream_t s, const float* Y, float* C) {
+        if (!enabled) return false;
+        tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, N, N, h, N, 1, S1, B1);
+        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols};
+        tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
+        launches += 2;
+        return true;
+    }
+    // Ybar (h x N) = W^T T, T: n x N (row-major)
+    bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar) {
+        if (!enabled) return false;
+        tc::pack_kernel<<<sms * 8, 256, 0, s>>>(T, 1, N, N, n, N, 1, S2, B2);
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols};
+        tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
+        tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar);
+        launches += 3;
+        return true;
+    }
 };
 
 }  // namespace lsb

@@ -41,3 +41,22 @@ def test_batched_matches_single_instance(product):
     for b in range(0, 20, 5):
         e, g = sysm.eval(Z[b])
         assert rel_err(E[b], e) < 1e-5 and rel_err(G[b], g) < 1e-4
+
+
+def test_batched_tcgen05_matches_cuda_core_sgemm(product, monkeypatch):
+    """The tcgen05 3xTF32 GEMMs (default) against the CUDA-core SGEMM fallback (LSB_TC=0)
+    on the same batch: E and dE/dz agree to fp32 accuracy."""
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    Z = configs.latent_batch_c4(pr.model.r, 96)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("LSB_TC", flag)
+        sysm = pr.system("fp32")
+        sysm.set_inertia(configs.timestep0_qbar(pr, sysm.mass), configs.DT)
+        out[flag] = sysm.eval_batched(Z)
+        sysm.close()
+    E1, G1 = out["1"]
+    E0, G0 = out["0"]
+    assert rel_err(E1, E0) < 1e-6
+    assert rel_err(G1, G0) < 1e-5
