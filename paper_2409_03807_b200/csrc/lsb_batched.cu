@@ -169,11 +169,11 @@ __global__ void __launch_bounds__(256) sgemm_tn_splitk_kernel(int H, int N, int 
 }
 
 // Deterministic split-K reduction: Ybar[h][N] = sum_kc P[kc][h][N] (fp64 accumulate).
-__global__ void splitk_reduce_kernel(int HN, int nk, const float* P, float* out) {
+__global__ void splitk_reduce_kernel(int HN, int nk, const float* P, float* out, int N = 0, int ldo = 0) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HN; i += gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int k = 0; k < nk; ++k) s += P[(size_t)k * HN + i];
-        out[i] = (float)s;
+        out[ldo ? (size_t)(i / N) * ldo + i % N : (size_t)i] = (float)s;
     }
 }
 
@@ -250,6 +250,77 @@ __global__ void __launch_bounds__(kEcols) elem_batched_kernel(const int4* tets, 
     __syncthreads();
     if (col < N) {
         for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + threadIdx.x];
+        eblk[(size_t)blk * N + col] = esum;
+    }
+}
+
+// Element pass per (block of kTB tets, kEcols columns), thread = column:
+//  - the block's records (as fp32) and vertex slots are staged once in shared
+//    memory (no per-thread record loads or conversions);
+//  - displacements come through L1/L2 with the next tet's 12 values loaded while
+//    the current tet computes (register double buffer);
+//  - forces accumulate per (free vertex slot, column) in shared memory, tets in id
+//    order -> deterministic.
+template <typename TR>
+__global__ void __launch_bounds__(kEcols) elem_batched2_kernel(const TR* rec, const int* blk_tet0,
+                                                              const int* blk_vptr, const short* tet_loc,
+                                                              const int4* tets, const float* U, int N,
+                                                              float* partial, double* eblk) {
+    extern __shared__ float sm[];
+    const int blk = blockIdx.x, tid = threadIdx.x;
+    const int col = blockIdx.y * kEcols + tid;
+    const int e0 = blk_tet0[blk], ne = blk_tet0[blk + 1] - e0;
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    float* acc = sm;                    // [nv * 3][kEcols]
+    float* rs = acc + nv * 3 * kEcols;  // [kTB][12]
+    int* vs = reinterpret_cast<int*>(rs + kTB * 12);  // [kTB][4] row offsets v * 3 * N
+    short* ls = reinterpret_cast<short*>(vs + kTB * 4);  // [kTB][4] free slots
+    for (int i = tid; i < nv * 3 * kEcols; i += kEcols) acc[i] = 0.f;
+    for (int i = tid; i < ne * 12; i += kEcols) rs[i] = (float)rec[(size_t)e0 * 12 + i];
+    for (int i = tid; i < ne * 4; i += kEcols) {
+        const int4 t = __ldg(tets + e0 + (i >> 2));
+        const int k = i & 3;
+        vs[i] = (k == 0 ? t.x : k == 1 ? t.y : k == 2 ? t.z : t.w) * 3 * N;
+        ls[i] = tet_loc[(size_t)e0 * 4 + i];
+    }
+    __syncthreads();
+    double esum = 0.0;
+    if (col < N) {
+        const float* Uc = U + col;
+        float un[12];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) un[k * 3 + c] = __ldg(Uc + vs[k] + c * N);
+        for (int e = 0; e < ne; ++e) {
+            float u[4][3];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) u[k][c] = un[k * 3 + c];
+            if (e + 1 < ne) {
+                const int* vn = vs + (e + 1) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) un[k * 3 + c] = __ldg(Uc + vn[k] + c * N);
+            }
+            float rc[12];
+#pragma unroll
+            for (int q = 0; q < 12; ++q) rc[q] = rs[e * 12 + q];
+            float f[12];
+            esum += (double)tet_energy_forces_t<float>(u[0], u[1], u[2], u[3], rc, f);
+            const short* L = ls + e * 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int lv = L[k];
+                if (lv >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[(lv * 3 + c) * kEcols + tid] += f[k * 3 + c];
+                }
+            }
+        }
+        for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + tid];
         eblk[(size_t)blk * N + col] = esum;
     }
 }
@@ -627,9 +698,14 @@ struct BatchedEngine : BatchedBase {
     int *d_blk_aptr = nullptr, *d_blk_avert = nullptr;
     short* d_tet_aloc = nullptr;
     int max_nva = 0;
+    size_t esmem2 = 0;
     // buffers
     float *d_W = nullptr;  // W_out fp32 [n][h] (unpadded)
     float *d_Z = nullptr, *d_Y[kMaxLayers + 1] = {}, *d_A[kMaxLayers] = {};
+    // group buffers: the hidden layers run once over a group of up to kGroup columns
+    static constexpr int kGroup = 4096;
+    float *d_Zg = nullptr, *d_Yg[kMaxLayers + 1] = {}, *d_Ag[kMaxLayers] = {}, *d_Ybg = nullptr, *d_Gbg[2] = {};
+    double* d_Eg = nullptr;
     float *d_C = nullptr, *d_U = nullptr, *d_rin = nullptr, *d_T = nullptr, *d_part = nullptr, *d_P = nullptr;
     float *d_Ybar = nullptr, *d_Gb[2] = {};
     double *d_epart = nullptr, *d_eblk = nullptr, *d_E = nullptr;
@@ -740,6 +816,16 @@ struct BatchedEngine : BatchedBase {
         const int n = c.n, h = c.h, V = m.V;
         int hmax = c.r;
         for (int l = 0; l < c.nhid; ++l) hmax = std::max(hmax, c.hrows[l]);
+        d_Zg = alloc<float>((size_t)c.r * kGroup);
+        for (int l = 0; l < c.nhid; ++l) {
+            d_Yg[l + 1] = alloc<float>((size_t)c.hrows[l] * kGroup);
+            d_Ag[l] = alloc<float>((size_t)c.hrows[l] * kGroup);
+        }
+        d_Yg[0] = d_Zg;
+        d_Ybg = alloc<float>((size_t)h * kGroup);
+        d_Gbg[0] = alloc<float>((size_t)hmax * kGroup);
+        d_Gbg[1] = alloc<float>((size_t)hmax * kGroup);
+        d_Eg = alloc<double>(kGroup);
         d_Z = alloc<float>((size_t)c.r * BC);
         for (int l = 0; l < c.nhid; ++l) {
             d_Y[l + 1] = alloc<float>((size_t)c.hrows[l] * BC);
@@ -769,6 +855,12 @@ struct BatchedEngine : BatchedBase {
                 for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
             }
         c.copy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "U pins");
+        esmem2 = (size_t)max_nv * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
+                 kTB * 4 * sizeof(short);
+        cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)esmem2), "elem2 smem");
+        cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)esmem2), "elem2 smem");
         const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
         if (c.precision == LSB_FP64)
             cuda_check(cudaFuncSetAttribute(elem_batched_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -779,98 +871,101 @@ struct BatchedEngine : BatchedBase {
         tc.init(c.stream, d_W, n, h, BC, c.num_sms);
     }
 
-    // One chunk of N <= BC columns; Z (N x r, host) -> E (N), G (N x r or null).
-    void run_chunk(Context& c, int N, const double* Z, double* E, double* G) {
+    // One group of N <= kGroup columns; Z (N x r, host) -> E (N), G (N x r or null).
+    // Hidden layers (forward and backward) run once over the whole group; the output
+    // layer, element pass and VJP run per chunk of BC columns.
+    void run_group(Context& c, int N, const double* Z, double* E, double* G) {
         cudaStream_t s = c.stream;
-        const int n = c.n, h = c.h, r = c.r, V = c.mesh.V;
-        (void)V;
-        // objective parameters from the single-instance state (host mirror)
+        const int n = c.n, h = c.h, r = c.r;
+        const int Np = (N + BC - 1) / BC * BC;  // padded to whole chunks (zero columns)
         DevState* hs = c.h_state;
         cuda_check(cudaMemcpyAsync(hs, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s), "state");
         cuda_check(cudaStreamSynchronize(s), "sync");
         const int has_inertia = hs->has_inertia;
         const double inv_dt2 = hs->inv_dt2;
-        // Z^T -> [r][BC] (columns beyond N are zero)
-        std::vector<float> zt((size_t)r * BC, 0.f);
+        // Z^T -> [r][Np]
+        std::vector<float> zt((size_t)r * Np, 0.f);
         for (int b = 0; b < N; ++b)
-            for (int k = 0; k < r; ++k) zt[(size_t)k * BC + b] = (float)Z[(size_t)b * r + k];
-        cuda_check(cudaMemcpyAsync(d_Z, zt.data(), 4 * zt.size(), cudaMemcpyHostToDevice, s), "Z");
-        // hidden forward
+            for (int k = 0; k < r; ++k) zt[(size_t)k * Np + b] = (float)Z[(size_t)b * r + k];
+        cuda_check(cudaMemcpyAsync(d_Zg, zt.data(), 4 * zt.size(), cudaMemcpyHostToDevice, s), "Z");
+        // hidden forward over the group
         for (int l = 0; l < c.nhid; ++l) {
             const int M = c.hrows[l], K = c.hcols[l];
-            dim3 grid((BC + 31) / 32, (M + 31) / 32);
-            small_gemm_kernel<<<grid, 256, 0, s>>>(M, BC, K, c.d_Wh + c.hoff[l], 0, d_Y[l], c.d_bh + c.boff[l],
-                                                   d_Y[l + 1], d_A[l], c.hact[l], nullptr, 0);
+            dim3 grid((Np + 31) / 32, (M + 31) / 32);
+            small_gemm_kernel<<<grid, 256, 0, s>>>(M, Np, K, c.d_Wh + c.hoff[l], 0, d_Yg[l], c.d_bh + c.boff[l],
+                                                   d_Yg[l + 1], d_Ag[l], c.hact[l], nullptr, 0);
         }
-        // output layer: C = W_out Y_L (tcgen05 when available, else SGEMM)
-        if (!tc.gemm_out(s, d_Y[c.nhid], d_C)) {
-            dim3 g1((BC + 127) / 128, (n + 127) / 128);
-            sgemm_nn_kernel<<<g1, 256, 0, s>>>(n, BC, h, d_W, h, d_Y[c.nhid], BC, d_C, BC);
-        }
-        {
-            dim3 g((n + 63) / 64, (BC + 63) / 64);
-            out_epilogue_kernel<<<g, 256, 0, s>>>(n, BC, d_C, c.d_eprow, c.d_ut, has_inertia, inv_dt2, d_U, d_rin,
-                                                  d_epart);
-        }
-        // element pass
-        {
-            dim3 g(nblk, (BC + kEcols - 1) / kEcols);
-            const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
-            if (c.precision == LSB_FP64)
-                elem_batched_kernel<double><<<g, kEcols, esmem, s>>>(
-                    reinterpret_cast<const int4*>(c.d_tets), static_cast<const double*>(c.d_rec), d_blk_tet0,
-                    d_blk_vptr, d_tet_loc, d_U, BC, d_part, d_eblk);
-            else
-                elem_batched_kernel<float><<<g, kEcols, esmem, s>>>(
-                    reinterpret_cast<const int4*>(c.d_tets), static_cast<const float*>(c.d_rec), d_blk_tet0,
-                    d_blk_vptr, d_tet_loc, d_U, BC, d_part, d_eblk);
-        }
-        energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, nrow_tiles, d_epart, nblk, d_eblk, has_inertia, d_E);
-        c.batched_launches += 5 + c.nhid + tc.launches;
-        tc.launches = 0;
-        if (G) {
-            combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, d_vslot_ptr, d_vslot, d_part, d_rin, has_inertia,
-                                                         c.d_eprow, d_T);
-            // Ybar = W_out^T T
-            if (!tc.gemm_vjp(s, d_T, d_Ybar)) {
-                dim3 g2((BC + 127) / 128, (h + 127) / 128, nk);
-                sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, BC, n, kchunk, d_W, h, d_T, BC, d_P);
-                splitk_reduce_kernel<<<c.num_sms, 256, 0, s>>>(h * BC, nk, d_P, d_Ybar);
+        c.batched_launches += c.nhid;
+        for (int c0 = 0; c0 < Np; c0 += BC) {
+            const float* Yc = d_Yg[c.nhid] + c0;  // h x BC slice, row stride Np
+            // output layer: C = W_out Y_L (tcgen05 when available, else SGEMM)
+            if (!tc.gemm_out(s, Yc, Np, d_C)) {
+                dim3 g1((BC + 127) / 128, (n + 127) / 128);
+                sgemm_nn_kernel<<<g1, 256, 0, s>>>(n, BC, h, d_W, h, Yc, Np, d_C, BC);
+                c.batched_launches += 1;
             }
-            // hidden backward: g_{l-1} = W_l^T (g_l * phi'(A_l))
-            const float* gin = d_Ybar;
+            {
+                dim3 g((n + 63) / 64, (BC + 63) / 64);
+                out_epilogue_kernel<<<g, 256, 0, s>>>(n, BC, d_C, c.d_eprow, c.d_ut, has_inertia, inv_dt2, d_U,
+                                                      d_rin, d_epart);
+            }
+            {
+                dim3 g(nblk, (BC + kEcols - 1) / kEcols);
+                if (c.precision == LSB_FP64)
+                    elem_batched2_kernel<double><<<g, kEcols, esmem2, s>>>(
+                        static_cast<const double*>(c.d_rec), d_blk_tet0, d_blk_vptr, d_tet_loc,
+                        reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
+                else
+                    elem_batched2_kernel<float><<<g, kEcols, esmem2, s>>>(
+                        static_cast<const float*>(c.d_rec), d_blk_tet0, d_blk_vptr, d_tet_loc,
+                        reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
+            }
+            energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, nrow_tiles, d_epart, nblk, d_eblk, has_inertia, d_Eg + c0);
+            c.batched_launches += 3;
+            if (G) {
+                combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, d_vslot_ptr, d_vslot, d_part, d_rin, has_inertia,
+                                                             c.d_eprow, d_T);
+                c.batched_launches += 1;
+                // Ybar[:, c0:c0+BC] = W_out^T T
+                if (!tc.gemm_vjp(s, d_T, d_Ybg + c0, Np)) {
+                    dim3 g2((BC + 127) / 128, (h + 127) / 128, nk);
+                    sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, BC, n, kchunk, d_W, h, d_T, BC, d_P);
+                    splitk_reduce_kernel<<<c.num_sms, 256, 0, s>>>(h * BC, nk, d_P, d_Ybg + c0, BC, Np);
+                    c.batched_launches += 2;
+                }
+            }
+            c.batched_launches += tc.launches;
+            tc.launches = 0;
+        }
+        std::vector<double> e(Np);
+        if (G) {
+            // hidden backward over the group: g_{l-1} = W_l^T (g_l * phi'(A_l))
+            const float* gin = d_Ybg;
             int buf = 0;
             for (int l = c.nhid - 1; l >= 0; --l) {
                 const int R = c.hrows[l], C = c.hcols[l];
-                // out[C][BC] = W_l^T [C x R] * (gin * phi'(A_l)) ; gating applied on the input side:
-                // precompute gated input in place via small_gemm with identity W? simpler: gate kernel
-                dim3 grid((BC + 31) / 32, (C + 31) / 32);
-                gate_mul(s, R, gin, d_A[l], c.hact[l], d_Gb[buf]);
-                small_gemm_kernel<<<grid, 256, 0, s>>>(C, BC, R, c.d_Wh + c.hoff[l], 1, d_Gb[buf], nullptr,
-                                                       d_Gb[buf ^ 1], nullptr, -1, nullptr, 0);
-                gin = d_Gb[buf ^ 1];
+                dim3 grid((Np + 31) / 32, (C + 31) / 32);
+                gate_mul(s, R * Np, gin, d_Ag[l], c.hact[l], d_Gbg[buf]);
+                small_gemm_kernel<<<grid, 256, 0, s>>>(C, Np, R, c.d_Wh + c.hoff[l], 1, d_Gbg[buf], nullptr,
+                                                       d_Gbg[buf ^ 1], nullptr, -1, nullptr, 0);
+                gin = d_Gbg[buf ^ 1];
                 buf ^= 1;
                 c.batched_launches += 2;
             }
-            c.batched_launches += 3;
-            std::vector<float> gz((size_t)r * BC);
+            std::vector<float> gz((size_t)r * Np);
             cuda_check(cudaMemcpyAsync(gz.data(), gin, 4 * gz.size(), cudaMemcpyDeviceToHost, s), "G");
-            std::vector<double> e(BC);
-            cuda_check(cudaMemcpyAsync(e.data(), d_E, 8 * BC, cudaMemcpyDeviceToHost, s), "E");
+            cuda_check(cudaMemcpyAsync(e.data(), d_Eg, 8 * Np, cudaMemcpyDeviceToHost, s), "E");
             cuda_check(cudaStreamSynchronize(s), "sync");
-            for (int b = 0; b < N; ++b) {
-                E[b] = e[b];
-                for (int k = 0; k < r; ++k) G[(size_t)b * r + k] = gz[(size_t)k * BC + b];
-            }
+            for (int b = 0; b < N; ++b)
+                for (int k = 0; k < r; ++k) G[(size_t)b * r + k] = gz[(size_t)k * Np + b];
         } else {
-            std::vector<double> e(BC);
-            cuda_check(cudaMemcpyAsync(e.data(), d_E, 8 * BC, cudaMemcpyDeviceToHost, s), "E");
+            cuda_check(cudaMemcpyAsync(e.data(), d_Eg, 8 * Np, cudaMemcpyDeviceToHost, s), "E");
             cuda_check(cudaStreamSynchronize(s), "sync");
-            for (int b = 0; b < N; ++b) E[b] = e[b];
         }
+        for (int b = 0; b < N; ++b) E[b] = e[b];
     }
 
-    static void gate_mul(cudaStream_t s, int R, const float* g, const float* A, int act, float* out);
+    static void gate_mul(cudaStream_t s, int total, const float* g, const float* A, int act, float* out);
 
     void init_hessian(Context& c) {
         const int r = c.r, h = c.h, n = c.n;
@@ -1011,8 +1106,7 @@ __global__ void gate_kernel(int total, const float* g, const float* A, int act, 
 }
 }  // namespace
 
-void BatchedEngine::gate_mul(cudaStream_t s, int R, const float* g, const float* A, int act, float* out) {
-    const int total = R * kBC;
+void BatchedEngine::gate_mul(cudaStream_t s, int total, const float* g, const float* A, int act, float* out) {
     gate_kernel<<<(total + 255) / 256, 256, 0, s>>>(total, g, A, act, out);
 }
 
@@ -1027,9 +1121,9 @@ static BatchedEngine& engine(Context& c) {
 
 void batched_eval(Context& c, int B, const double* Z, double* E, double* G) {
     BatchedEngine& eng = engine(c);
-    for (int b0 = 0; b0 < B; b0 += eng.BC) {
-        const int N = std::min(eng.BC, B - b0);
-        eng.run_chunk(c, N, Z + (size_t)b0 * c.r, E + b0, G ? G + (size_t)b0 * c.r : nullptr);
+    for (int b0 = 0; b0 < B; b0 += BatchedEngine::kGroup) {
+        const int N = std::min(BatchedEngine::kGroup, B - b0);
+        eng.run_group(c, N, Z + (size_t)b0 * c.r, E + b0, G ? G + (size_t)b0 * c.r : nullptr);
     }
 }
 

@@ -283,11 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
 }
 
 // Ybar[m][b] = sum_j part[j][m][b] (job order), m < h
-__global__ void reduce_parts_kernel(const float* __restrict__ part, int njobs, int h, int N, float* __restrict__ out) {
+__global__ void reduce_parts_kernel(const float* __restrict__ part, int njobs, int h, int N, float* __restrict__ out,
+                                    int ldo) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h * N; i += gridDim.x * blockDim.x) {
         float s = 0.f;
         for (int j = 0; j < njobs; ++j) s += __ldg(part + (size_t)j * kTileM * N + i);
-        out[i] = s;
+        out[(size_t)(i / N) * ldo + i % N] = s;
     }
 }
 
@@ -349,22 +350,22 @@ struct TcGemm {
         enabled = false;
     }
 
-    // C (n x N, row-major, ldc = N) = W Y, Y: h x N (feature-major)
-    bool gemm_out(cudaStream_t s, const float* Y, float* C) {
+    // C (n x N, row-major, ldc = N) = W Y, Y: h x N (feature-major, row stride ldy)
+    bool gemm_out(cudaStream_t s, const float* Y, int ldy, float* C) {
         if (!enabled) return false;
-        tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, N, N, h, N, 1, S1, B1);
+        tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
         tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
     }
-    // Ybar (h x N) = W^T T, T: n x N (row-major)
-    bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar) {
+    // Ybar (h x N, row stride ldo) = W^T T, T: n x N (row-major)
+    bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar, int ldo) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 8, 256, 0, s>>>(T, 1, N, N, n, N, 1, S2, B2);
         tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
-        tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar);
+        tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
         launches += 3;
         return true;
     }
