@@ -644,6 +644,279 @@ __global__ void __launch_bounds__(128, 3) elem_hess_kernel(const int4* tets, con
     }
 }
 
+// Element Hessian contraction, v2.  CTA = (block of kTB tets, GP = 128/R points);
+// per tet: thread (point pl, direction b) forms dF_b, alpha_b, beta_b and
+// M_b = 2 psi_I dF_b + psi_J dcof[dF_b] into smem (double-buffered, one barrier per
+// tet); threads b < 12 add one force component each to the point's vertex
+// accumulators (same summation order as v1).  The contraction
+//   C_ab += vol (dF_a : M_b) + vol psi_II alpha_a alpha_b + vol lambda beta_a beta_b
+// is register-blocked: each thread owns 4 x 4 (a, b) entries of one point's full
+// R x R matrix and reads 4 dF_a and 4 M_b rows as float4 (24 vector loads for 16
+// entries); the a <= b entries are written out (pair order of v1).
+template <int R>
+__global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const float* rec, const int* blk_tet0,
+                                                        const int* blk_vptr, const short* tet_loc,
+                                                        const int* blk_aptr, const int* blk_avert,
+                                                        const short* tet_aloc, const float* U, const float* Jv,
+                                                        int P, float* Cpart, float* gpart) {
+    constexpr int GP = 128 / R;               // points per CTA
+    constexpr int NB = R / 4;                 // 4-wide blocks per side
+    constexpr int NBLK = GP * NB * NB;        // 4x4 blocks per CTA
+    constexpr int BPT = (NBLK + 127) / 128;   // blocks per thread
+    constexpr int NPAIR = R * (R + 1) / 2;
+    __shared__ __align__(16) float sh_dF[2][GP][R][12];
+    __shared__ __align__(16) float sh_M[2][GP][R][12];
+    __shared__ __align__(16) float sh_ab[2][GP][R][2];
+    __shared__ __align__(16) float sh_sc[2][GP][4];
+    __shared__ __align__(16) float sh_rec[kTB][12];   // the block's records
+    __shared__ short sh_loc[kTB][8];                  // free slots (4), touched slots (4)
+    extern __shared__ __align__(16) float dyn[];
+    const int tid = threadIdx.x;
+    const int pl = tid / R, b = tid % R;
+    const int p0 = blockIdx.y * GP;
+    const int blk = blockIdx.x;
+    const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    const int a0 = blk_aptr[blk], nva = blk_aptr[blk + 1] - a0;
+    float* Us = dyn;                            // [nva][3][GP]
+    float* accg = Us + (size_t)nva * 3 * GP;    // [nv][3][GP]
+    static_assert(GP % 4 == 0, "16-byte staging of U");
+    for (int i = tid; i < nva * 3 * (GP / 4); i += 128) {
+        const int vcl = i / (GP / 4), k4 = i % (GP / 4);
+        const int va = __ldg(blk_avert + a0 + vcl / 3), c = vcl % 3;
+        cp_async16(Us + (size_t)vcl * GP + 4 * k4, U + ((size_t)va * 3 + c) * P + p0 + 4 * k4);
+    }
+    for (int i = tid; i < nv * 3 * GP; i += 128) accg[i] = 0.f;
+    for (int i = tid; i < (e1 - e0) * 12; i += 128) sh_rec[i / 12][i % 12] = rec[(size_t)e0 * 12 + i];
+    for (int i = tid; i < (e1 - e0) * 4; i += 128) {
+        sh_loc[i >> 2][i & 3] = tet_loc[(size_t)e0 * 4 + i];
+        sh_loc[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i];
+    }
+    int cpl[BPT], cbi[BPT], cbj[BPT];
+    float cacc[BPT][16];
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        const int id = tid + 128 * k;
+        cpl[k] = id < NBLK ? id / (NB * NB) : -1;
+        cbi[k] = (id % (NB * NB)) / NB;
+        cbj[k] = id % NB;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) cacc[k][q] = 0.f;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const bool live = p0 + pl < P;
+    // this thread's Jacobian column (point pl, direction b) of the current tet's 12 dofs,
+    // read from L2 one tet ahead (coalesced over the CTA's points x directions)
+    const float* Jp = Jv + ((size_t)(p0 + pl)) * R + b;
+    const size_t jstride = (size_t)P * R;  // per (vertex, component) row
+    float dun[12];
+    if (live && e0 < e1) {
+        const int4 t = __ldg(tets + e0);
+        const int vv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
+    }
+    for (int e = e0; e < e1; ++e) {
+        const int buf = (e - e0) & 1;
+        float rc[12];
+#pragma unroll
+        for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
+        if (live) {
+            int la[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) la[k] = sh_loc[e - e0][4 + k];
+            float duc[12];
+#pragma unroll
+            for (int q = 0; q < 12; ++q) duc[q] = dun[q];
+            if (e + 1 < e1) {
+                const int4 t = __ldg(tets + e + 1);
+                const int vv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
+            }
+            float A[9], dA[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                float du[4], uu[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uu[k] = Us[(la[k] * 3 + a) * GP + pl];
+                    du[k] = duc[k * 3 + a];
+                }
+#pragma unroll
+                for (int c2 = 0; c2 < 3; ++c2) {
+                    A[a * 3 + c2] = (uu[1] - uu[0]) * rc[c2] + (uu[2] - uu[0]) * rc[3 + c2] + (uu[3] - uu[0]) * rc[6 + c2];
+                    dA[a * 3 + c2] = (du[1] - du[0]) * rc[c2] + (du[2] - du[0]) * rc[3 + c2] + (du[3] - du[0]) * rc[6 + c2];
+                }
+            }
+            float F[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
+            float cof[9];
+            cof[0] = F[4] * F[8] - F[7] * F[5];
+            cof[3] = F[7] * F[2] - F[1] * F[8];
+            cof[6] = F[1] * F[5] - F[4] * F[2];
+            cof[1] = F[5] * F[6] - F[8] * F[3];
+            cof[4] = F[8] * F[0] - F[2] * F[6];
+            cof[7] = F[2] * F[3] - F[5] * F[0];
+            cof[2] = F[3] * F[7] - F[6] * F[4];
+            cof[5] = F[6] * F[1] - F[0] * F[7];
+            cof[8] = F[0] * F[4] - F[3] * F[1];
+            const float vol = rc[9], mu = rc[10], lam = rc[11];
+            const float trA = A[0] + A[4] + A[8];
+            float q = 0.f;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) q += A[k] * A[k];
+            const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+            const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
+                               A[6] * (A[1] * A[5] - A[4] * A[2]);
+            const float jm1 = trA + m2 + detA;
+            const float uI = 4.f + 2.f * trA + q;  // I + 1
+            const float psiI = 0.5f * mu * (1.f - 1.f / uI);
+            const float psiII = 0.5f * mu / (uI * uI);
+            const float psiJ = lam * jm1 - 0.75f * mu;
+            float alpha = 0.f, beta = 0.f;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                alpha += 2.f * F[k] * dA[k];
+                beta += cof[k] * dA[k];
+            }
+            float dc[9];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int ci = (c + 1) % 3, cj = (c + 2) % 3;
+                const float a1[3] = {F[ci], F[3 + ci], F[6 + ci]}, a2[3] = {F[cj], F[3 + cj], F[6 + cj]};
+                const float d1[3] = {dA[ci], dA[3 + ci], dA[6 + ci]}, d2[3] = {dA[cj], dA[3 + cj], dA[6 + cj]};
+                dc[0 * 3 + c] = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
+                dc[1 * 3 + c] = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
+                dc[2 * 3 + c] = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
+            }
+            float* dFo = sh_dF[buf][pl][b];
+            float* Mo = sh_M[buf][pl][b];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                dFo[k] = dA[k];
+                Mo[k] = 2.f * psiI * dA[k] + psiJ * dc[k];
+            }
+            dFo[9] = dFo[10] = dFo[11] = 0.f;
+            Mo[9] = Mo[10] = Mo[11] = 0.f;
+            sh_ab[buf][pl][b][0] = alpha;
+            sh_ab[buf][pl][b][1] = beta;
+            if (b == 12 % R) {
+                sh_sc[buf][pl][0] = vol * psiII;
+                sh_sc[buf][pl][1] = vol * lam;
+                sh_sc[buf][pl][2] = vol;
+            }
+            // elastic forces: threads b < 12 own one (vertex, component) each (row of P
+            // selected with compile-time indices only: no local-memory arrays)
+            if (b < 12 || R < 12) {
+                float cA[9];
+                cA[0] = A[4] * A[8] - A[7] * A[5];
+                cA[3] = A[7] * A[2] - A[1] * A[8];
+                cA[6] = A[1] * A[5] - A[4] * A[2];
+                cA[1] = A[5] * A[6] - A[8] * A[3];
+                cA[4] = A[8] * A[0] - A[2] * A[6];
+                cA[7] = A[2] * A[3] - A[5] * A[0];
+                cA[2] = A[3] * A[7] - A[6] * A[4];
+                cA[5] = A[6] * A[1] - A[0] * A[7];
+                cA[8] = A[0] * A[4] - A[3] * A[1];
+                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
+                for (int fk = b; fk < 12; fk += R) {
+                    const int kk = fk / 3, a = fk % 3;
+                    float Pa[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int aa = 0; aa < 3; ++aa)
+                        if (aa == a) {
+#pragma unroll
+                            for (int bb = 0; bb < 3; ++bb) {
+                                const float id = aa == bb ? 1.f : 0.f;
+                                Pa[bb] = c1 * (A[aa * 3 + bb] + A[bb * 3 + aa] - trA * id - cA[aa * 3 + bb]) +
+                                         c2 * F[aa * 3 + bb] + c3 * cof[aa * 3 + bb];
+                            }
+                        }
+                    float hc[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        hc[c] = vol * (Pa[0] * rc[c * 3 + 0] + Pa[1] * rc[c * 3 + 1] + Pa[2] * rc[c * 3 + 2]);
+                    float hv;
+                    if (kk == 0) {
+                        float s0 = 0.f;
+                        s0 += hc[0];
+                        s0 += hc[1];
+                        s0 += hc[2];
+                        hv = -s0;
+                    } else {
+                        hv = kk == 1 ? hc[0] : (kk == 2 ? hc[1] : hc[2]);
+                    }
+                    const int lv = sh_loc[e - e0][kk];
+                    if (lv >= 0) accg[(lv * 3 + a) * GP + pl] += hv;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < BPT; ++k) {
+            const int pc = cpl[k];
+            if (pc >= 0 && p0 + pc < P) {
+                float dFr[4][12], Mr[4][12];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float4* s1 = reinterpret_cast<const float4*>(sh_dF[buf][pc][4 * cbi[k] + i]);
+                    const float4* s2 = reinterpret_cast<const float4*>(sh_M[buf][pc][4 * cbj[k] + i]);
+#pragma unroll
+                    for (int v = 0; v < 3; ++v) {
+                        const float4 x = s1[v], y = s2[v];
+                        dFr[i][4 * v] = x.x; dFr[i][4 * v + 1] = x.y; dFr[i][4 * v + 2] = x.z; dFr[i][4 * v + 3] = x.w;
+                        Mr[i][4 * v] = y.x; Mr[i][4 * v + 1] = y.y; Mr[i][4 * v + 2] = y.z; Mr[i][4 * v + 3] = y.w;
+                    }
+                }
+                const float4 abA0 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbi[k]])[0];
+                const float4 abA1 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbi[k]])[1];
+                const float4 abB0 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbj[k]])[0];
+                const float4 abB1 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbj[k]])[1];
+                const float al_a[4] = {abA0.x, abA0.z, abA1.x, abA1.z}, be_a[4] = {abA0.y, abA0.w, abA1.y, abA1.w};
+                const float al_b[4] = {abB0.x, abB0.z, abB1.x, abB1.z}, be_b[4] = {abB0.y, abB0.w, abB1.y, abB1.w};
+                const float4 sc = reinterpret_cast<const float4*>(sh_sc[buf][pc])[0];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        float s = 0.f;
+#pragma unroll
+                        for (int k9 = 0; k9 < 9; ++k9) s += dFr[i][k9] * Mr[j][k9];
+                        cacc[k][i * 4 + j] += sc.z * s + sc.x * al_a[i] * al_b[j] + sc.y * be_a[i] * be_b[j];
+                    }
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BPT; ++k) {
+        const int pc = cpl[k];
+        if (pc >= 0 && p0 + pc < P) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int a = 4 * cbi[k] + i, bb = 4 * cbj[k] + j;
+                    if (a <= bb) {
+                        const int pr = a * R - a * (a - 1) / 2 + (bb - a);
+                        Cpart[((size_t)blk * P + p0 + pc) * NPAIR + pr] = cacc[k][i * 4 + j];
+                    }
+                }
+        }
+    }
+    for (int i = tid; i < nv * 3 * GP; i += 128) {
+        const int pp = i % GP;
+        if (p0 + pp < P) gpart[((size_t)(v0 * 3) + i / GP) * P + p0 + pp] = accg[i];
+    }
+}
+
 // C[p][pair] = sum over blocks (fixed order, fp64): CTA per 32 (p, pair) entries,
 // 8 warps stride the blocks, fixed combine order.
 __global__ void __launch_bounds__(256) hess_reduce_kernel(int nblk, int P, int npair, const float* Cpart, double* C) {
@@ -1009,15 +1282,15 @@ struct BatchedEngine : BatchedBase {
         c.copy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "Uh");
         cuda_check(cudaMemsetAsync(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r, c.stream), "Jv");
         const size_t gsmem = hess_smem(r);
-        if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
-        if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
-        if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         hess_ready = true;
     }
 
     size_t hess_smem(int r) const {
         const int gp = 128 / r;
-        return ((size_t)max_nva * 3 * gp * r + (size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;
+        return ((size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;  // Us + accg (elem_hess2)
     }
 
     // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
@@ -1054,13 +1327,13 @@ struct BatchedEngine : BatchedBase {
             const float* recf = static_cast<const float*>(rec_f32(c));
             const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
             if (r == 8)
-                elem_hess_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                elem_hess2_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                          d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
             else if (r == 16)
-                elem_hess_kernel<16><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                elem_hess2_kernel<16><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                           d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
             else
-                elem_hess_kernel<32><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                elem_hess2_kernel<32><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                           d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
         }
         hess_reduce_kernel<<<(P * npair + 31) / 32, 256, 0, s>>>(nblk, P, npair, d_Cpart, d_Ch);
