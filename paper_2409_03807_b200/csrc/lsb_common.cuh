@@ -184,6 +184,21 @@ __device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes) {
     }
 }
 
+// DSMEM: address of the same shared variable in cluster CTA `rank`, remote store/load
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void dsmem_st_f64(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double dsmem_ld_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 // Order this thread's generic-proxy global writes before later async-proxy
 // (cp.async.bulk) reads of them; used before the barrier that publishes them.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }

@@ -336,6 +336,8 @@ struct Impl final : ImplBase {
         };
         cs = 8;
         if (slice_words(8) * 8 + fixed > 200 * 1024 || (maxrows + 7) / 8 > 64) cs = 16;
+        if (const char* e = getenv("LSB_CTRL_CLUSTER"))  // developer override (8 or 16)
+            if (atoi(e) == 16) cs = 16;
         if (slice_words(cs) * 8 + fixed > 220 * 1024 || (maxrows + cs - 1) / cs > 64)
             throw LsbError(LSB_EINVAL, "decoder: hidden layers too large for the control cluster");
         p.cs = cs;

@@ -82,14 +82,19 @@ struct SolveParams {
 constexpr int kCtrlRecv = 1024;  // CS x (rows per CTA) receive slots (<= 16 x 64)
 struct CtrlSmem {
     double* wsl;      // staged W row slices
-    double* xin[2];   // layer inputs (kMaxHidden each), double-buffered across layers
-    double* rbuf[2];  // backward receive buffers [src CTA][own row] (kCtrlRecv each)
+    double* xin0;     // layer inputs (kMaxHidden each), double-buffered across layers
+    double* xin1;
+    double* rbuf0;    // backward receive buffers [src CTA][own row] (kCtrlRecv each)
+    double* rbuf1;
+    // selects instead of runtime-indexed member arrays: keeps the struct in registers
+    __device__ __forceinline__ double* xin(int k) const { return k ? xin1 : xin0; }
+    __device__ __forceinline__ double* rbuf(int k) const { return k ? rbuf1 : rbuf0; }
     double* tmp;      // ybar reduction scratch (kSolveThreads)
     double* bsl;      // kMaxLayers * 64
     double* asl;      // kMaxLayers * 64
     DevState* sst;
     uint64_t* wbar;  // kMaxLayers + 1 staging barriers (static smem)
-    int woff[kMaxLayers];
+    int* woff;       // kMaxLayers weight-slice offsets (static smem)
 };
 constexpr size_t ctrl_fixed_words() {
     return 2 * kMaxHidden + 2 * kCtrlRecv + kSolveThreads + 2 * kMaxLayers * 64 + sizeof(DevState) / sizeof(double) + 8;
@@ -113,7 +118,7 @@ __device__ __forceinline__ bool bulk_ok(const void* dst, const void* src, size_t
     return ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15u) == 0;
 }
 template <typename TS, int CS>
-__device__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state, uint64_t* wbar) {
+__device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state, uint64_t* wbar) {
     const int tid = threadIdx.x;
     int off = 0;
     bool async_used = false;
@@ -176,7 +181,7 @@ __device__ __forceinline__ void ctrl_wait_state(uint64_t* wbar) { mbar_wait(&wba
 // of j (layer l-1 rows; CTA 0 for l = 0), which sums the CS partials in CTA order.
 // Result -> sst->gz (CTA 0).  Ends with __syncthreads.
 template <typename TS, int CS, typename Stamp>
-__device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
+__device__ __forceinline__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
                               const double* ypart, Stamp& stamp) {
     const int tid = threadIdx.x, nt = blockDim.x;
     if (p.nhid == 0) {
@@ -219,7 +224,6 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
         }
         __syncthreads();  // tmp is reused below
     }
-    stamp(90);
     for (int l = p.nhid - 1; l >= 0; --l) {
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
@@ -231,7 +235,7 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
         __syncthreads();
         const double* Ws = cs.wsl + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
-        double* rb = cs.rbuf[l & 1];
+        double* rb = cs.rbuf(l & 1);
         const int Rp = l > 0 ? p.hrows[l - 1] : C;
         for (int j = tid; j < C; j += nt) {
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -246,11 +250,9 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
             const double s = (s0 + s1) + (s2 + s3);
             const int o = l > 0 ? part_owner<CS>(j, Rp) : 0;
             const int jl = l > 0 ? j - part_lo(Rp, CS, o) : j;
-            cluster.map_shared_rank(rb, o)[c * 64 + jl] = s;
+            dsmem_st_f64(dsmem_addr(rb + c * 64 + jl, o), s);
         }
-        stamp(130 + l);
         cluster.sync();
-        stamp(140 + l);
         // own rows of layer l-1 (or z for l = 0 on CTA 0): fixed CTA-order sum
         const int nown = l > 0 ? part_lo(Rp, CS, c + 1) - part_lo(Rp, CS, c) : (c == 0 ? C : 0);
         for (int k = 0; k < 2; ++k) {
@@ -270,19 +272,19 @@ __device__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster
 // Forward through the hidden layers at sst->zt (CTA 0); the owner of each output
 // row pushes it into every CTA's next-layer input buffer.  y_last -> p.y_last.
 template <typename TS, int CS, typename Stamp>
-__device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, Stamp& stamp) {
+__device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, Stamp& stamp) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nw = blockDim.x >> 5;
     {
         const double* zsrc = cluster.map_shared_rank(cs.sst->zt, 0);
-        for (int j = tid; j < p.r; j += blockDim.x) cs.xin[0][j] = zsrc[j];
+        for (int j = tid; j < p.r; j += blockDim.x) cs.xin(0)[j] = zsrc[j];
     }
     __syncthreads();
     for (int l = 0; l < p.nhid; ++l) {
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
-        const double* x = cs.xin[l & 1];
-        double* xn = cs.xin[(l & 1) ^ 1];
+        const double* x = cs.xin(l & 1);
+        double* xn = cs.xin((l & 1) ^ 1);
         const double* Ws = cs.wsl + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
         // rows per warp: the smallest power of two that covers nrow in one pass (<= 8),
@@ -307,15 +309,14 @@ __device__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_
             if (live) {
                 const double a = s + cs.bsl[l * 64 + i];
                 const double y = act_eval(p.hact[l], a, 0);
-                for (int q = sl; q < CS; q += LPR) cluster.map_shared_rank(xn, q)[i0 + i] = y;
+                for (int q = sl; q < CS; q += LPR) dsmem_st_f64(dsmem_addr(xn + i0 + i, q), y);
                 if (sl == 0) cs.asl[l * 64 + i] = a;
             }
         }
-        stamp(120 + l);
         cluster.sync();
     }
     if (c == 0) {
-        const double* x = cs.xin[p.nhid & 1];
+        const double* x = cs.xin(p.nhid & 1);
         const int R = p.nhid > 0 ? p.hrows[p.nhid - 1] : p.r;
         for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < R ? x[j] : 0.0;
     }
@@ -340,11 +341,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     double* cbase = reinterpret_cast<double*>(smem + kSolveBarBytes + (size_t)NW * sp.spw_ctrl * C::STAGEB);
     CtrlSmem cs;
     cs.wsl = cbase;
-    cs.xin[0] = cbase + p.ctrl_smem_w;
-    cs.xin[1] = cs.xin[0] + kMaxHidden;
-    cs.rbuf[0] = cs.xin[1] + kMaxHidden;
-    cs.rbuf[1] = cs.rbuf[0] + kCtrlRecv;
-    cs.tmp = cs.rbuf[1] + kCtrlRecv;
+    cs.xin0 = cbase + p.ctrl_smem_w;
+    cs.xin1 = cs.xin0 + kMaxHidden;
+    cs.rbuf0 = cs.xin1 + kMaxHidden;
+    cs.rbuf1 = cs.rbuf0 + kCtrlRecv;
+    cs.tmp = cs.rbuf1 + kCtrlRecv;
     cs.bsl = cs.tmp + kSolveThreads;
     cs.asl = cs.bsl + kMaxLayers * 64;
     cs.sst = reinterpret_cast<DevState*>(cs.asl + kMaxLayers * 64);
@@ -374,7 +375,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     // ---- control cluster: stage weights (+ state) once.  Issued before any other bulk
     // traffic: an SM's TMA engine serves requests in order.
     __shared__ __align__(8) uint64_t s_wbar[kMaxLayers + 1];
+    __shared__ int s_woff[kMaxLayers];
     cs.wbar = s_wbar;
+    cs.woff = s_woff;
     if (is_ctrl) ctrl_stage<TS, CS>(p, cs, crank, true, s_wbar);
     // the first forward tiles do not depend on z: prefetch now (a step rewrites the
     // qbar column of the row records first, so it prefetches after that)
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     for (int j = j0 + tid; j < j1; j += blockDim.x) {
                         double v[CS];
 #pragma unroll
-                        for (int r = 0; r < CS; ++r) v[r] = cluster.map_shared_rank(cpart, r)[j];
+                        for (int r = 0; r < CS; ++r) v[r] = dsmem_ld_f64(dsmem_addr(cpart + j, r));
                         double s = 0.0;
 #pragma unroll
                         for (int r = 0; r < CS; ++r) s += v[r];
