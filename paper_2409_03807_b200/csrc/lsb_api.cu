@@ -420,9 +420,10 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             std::vector<double> Wh, bh;
             for (int l = 0; l < c.nhid; ++l) {
                 const HostLayer& hl = c.layers[l];
-                // even offsets: 16-byte aligned layer starts for the bulk-copy staging
-                if (Wh.size() & 1) Wh.push_back(0.0);
-                if (bh.size() & 1) bh.push_back(0.0);
+                // offsets multiple of 4 elements: 16-byte aligned layer starts for the bulk-copy
+                // staging in both fp64 and fp32 copies
+                while (Wh.size() & 3) Wh.push_back(0.0);
+                while (bh.size() & 3) bh.push_back(0.0);
                 c.hoff[l] = (int)Wh.size();
                 c.boff[l] = (int)bh.size();
                 c.hrows[l] = hl.rows;
@@ -433,6 +434,11 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
             }
             c.d_Wh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, Wh.size())));
             c.d_bh = static_cast<double*>(c.dmalloc(8 * std::max<size_t>(1, bh.size())));
+            {  // storage-precision copy for the solve kernel's control cluster (fp32 mode)
+                std::vector<float> wf(Wh.begin(), Wh.end());
+                c.d_Wh_f = static_cast<float*>(c.dmalloc(4 * std::max<size_t>(1, wf.size())));
+                if (!wf.empty()) c.copy(c.d_Wh_f, wf.data(), 4 * wf.size(), cudaMemcpyHostToDevice, "Wh f32");
+            }
             if (!Wh.empty()) {
                 c.copy(c.d_Wh, Wh.data(), 8 * Wh.size(), cudaMemcpyHostToDevice, "Wh");
                 c.copy(c.d_bh, bh.data(), 8 * bh.size(), cudaMemcpyHostToDevice, "bh");

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -104,6 +105,8 @@ __global__ void count_loop_kernel(const DevState* st, long long* acc) {
 }
 
 // ------------------------------------------------------------------ Impl<TS>
+constexpr int kSolveDefaultMaxRows = 262144;
+
 template <typename TS>
 struct KernelSet {
     void (*out_fwd)(const EvalParams<TS>);
@@ -202,6 +205,7 @@ struct Impl final : ImplBase {
     size_t solve_smem = 0;
     unsigned launch_seq = 0;
     int solve_spw = 1, solve_spw_ctrl = 1, solve_tv_cap = 0, solve_tv_off = 0, solve_tv_off_ctrl = 0;
+    int solve_wsl_words = 0, solve_tv_global = 0;
     int solve_grid = 0;
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
     SolveShared* d_sh = nullptr;
@@ -284,6 +288,8 @@ struct Impl final : ImplBase {
         p.csr_ent = c.d_csr_ent;
         p.fpos = reinterpret_cast<const int4*>(c.d_fpos);
         p.Wh = c.d_Wh;
+        p.Wh_s = std::is_same<TS, double>::value ? reinterpret_cast<const TS*>(c.d_Wh)
+                                                  : reinterpret_cast<const TS*>(c.d_Wh_f);
         p.bh = c.d_bh;
         for (int l = 0; l < c.nhid; ++l) {
             p.hoff[l] = c.hoff[l];
@@ -373,35 +379,51 @@ struct Impl final : ImplBase {
             c.solve_reason = "no solve kernel instantiated for this width";
             return;
         }
-        // self-issued rings: 9 warps x spw stages each, as many as fit (control CTAs: their
-        // control area follows the ring), then the tv / partials scratch
-        const size_t cap = 227 * 1024 - 512;
-        const size_t ctrl_area = ((size_t)p.ctrl_smem_w + ctrl_fixed_words()) * sizeof(double);
-        const int nw = kSolveThreads / 32;
+        // control-area weights in storage precision: per-layer row slices, 16-byte aligned
         {
-            const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
-            const int g_min = 96;  // clusters of 8/16 on 148 SMs give >= 112 CTAs
-            solve_tv_cap = std::max((ntiles + g_min - 1) / g_min * ks.tile_rows, c.hp);
+            size_t w = 0;
+            for (int l = 0; l < c.nhid; ++l)
+                w += ((size_t)((c.hrows[l] + cs - 1) / cs) * c.hcols[l] + 3) & ~(size_t)3;
+            solve_wsl_words = (int)((w * sizeof(TS) + 7) / 8);
         }
-        const size_t tvb = ((size_t)solve_tv_cap * sizeof(double) + 127) & ~(size_t)127;
-        solve_spw_ctrl = 0;
-        for (int k = 1; k * nw <= kSolveMaxStages && k <= 3; ++k)
-            if (kSolveBarBytes + k * nw * ks.stage_bytes + ctrl_area + tvb <= cap) solve_spw_ctrl = k;
-        solve_spw = std::max(solve_spw_ctrl, 1);
-        for (int k = 1; k * nw <= kSolveMaxStages && k <= 2; ++k)
-            if (kSolveBarBytes + k * nw * ks.stage_bytes + tvb <= cap) solve_spw = std::max(solve_spw, k);
-        solve_tv_off_ctrl = (int)(kSolveBarBytes + solve_spw_ctrl * nw * ks.stage_bytes + ctrl_area);
-        solve_tv_off = (int)(kSolveBarBytes + solve_spw * nw * ks.stage_bytes);
-        solve_smem = std::max((size_t)solve_tv_off_ctrl, (size_t)solve_tv_off) + tvb;
-        if (solve_spw_ctrl == 0) solve_smem = cap + 1;
-        if (solve_smem > 227 * 1024) {
-            c.solve_reason = "shared memory " + std::to_string(solve_smem) + " B exceeds 227 KB";
+        // self-issued rings: 9 warps x spw stages each, as many as fit (control CTAs: their
+        // control area follows the ring), then the tv / partials scratch -- or, when that does
+        // not fit, tv in global memory streamed with the VJP tiles
+        const size_t cap = 227 * 1024 - 2048;  // static smem of the kernel (barriers, flags) + margin
+        const size_t ctrl_area = ((size_t)solve_wsl_words + ctrl_fixed_words()) * sizeof(double);
+        const int nw = kSolveThreads / 32;
+        const char* tvenv = getenv("LSB_SOLVE_TV_GLOBAL");  // developer / test override
+        for (int tvg = (tvenv && tvenv[0] == '1') ? 1 : 0; tvg < 2; ++tvg) {
+            solve_tv_global = tvg;
+            if (tvg == 0) {
+                const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
+                const int g_min = 96;  // clusters of 8/16 on 148 SMs give >= 112 CTAs
+                solve_tv_cap = std::max((ntiles + g_min - 1) / g_min * ks.tile_rows, c.hp);
+            } else {
+                solve_tv_cap = c.hp;  // partials only
+            }
+            const size_t tvb = ((size_t)solve_tv_cap * sizeof(double) + 127) & ~(size_t)127;
+            solve_spw_ctrl = 0;
+            for (int k = 1; k * nw <= kSolveMaxStages && k <= 3; ++k)
+                if (kSolveBarBytes + k * nw * ks.stage_bytes + ctrl_area + tvb <= cap) solve_spw_ctrl = k;
+            solve_spw = std::max(solve_spw_ctrl, 1);
+            for (int k = 1; k * nw <= kSolveMaxStages && k <= 2; ++k)
+                if (kSolveBarBytes + k * nw * ks.stage_bytes + tvb <= cap) solve_spw = std::max(solve_spw, k);
+            solve_tv_off_ctrl = (int)(kSolveBarBytes + solve_spw_ctrl * nw * ks.stage_bytes + ctrl_area);
+            solve_tv_off = (int)(kSolveBarBytes + solve_spw * nw * ks.stage_bytes);
+            solve_smem = std::max((size_t)solve_tv_off_ctrl, (size_t)solve_tv_off) + tvb;
+            if (solve_spw_ctrl == 0) solve_smem = SIZE_MAX;  // no ring stage fits beside the control area
+            if (solve_smem <= cap) break;
+        }
+        if (solve_smem > cap || solve_spw_ctrl < 1 || solve_spw < 1) {
+            c.solve_reason = "shared memory: no ring fits beside the control area within 227 KB";
             solve = nullptr;
             return;
         }
         if (cudaFuncSetAttribute(solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem) != cudaSuccess ||
             (cs == 16 && cudaFuncSetAttribute(solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
-            c.solve_reason = std::string("attribute: ") + cudaGetErrorString(cudaGetLastError());
+            c.solve_reason = std::string("attribute: ") + cudaGetErrorString(cudaGetLastError()) + " (smem " +
+                             std::to_string(solve_smem) + " B)";
             solve = nullptr;
             return;
         }
@@ -423,7 +445,7 @@ struct Impl final : ImplBase {
             return;
         }
         solve_grid = nclusters * cs;
-        {
+        if (!solve_tv_global) {
             const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
             if ((ntiles + solve_grid - 1) / solve_grid * ks.tile_rows > solve_tv_cap) {
                 c.solve_reason = "tv scratch too small for " + std::to_string(solve_grid) + " CTAs";
@@ -437,8 +459,14 @@ struct Impl final : ImplBase {
         ps.ybar_part = static_cast<double*>(c.dmalloc(sizeof(double) * (size_t)solve_grid * c.hp));
         d_sh = static_cast<SolveShared*>(c.dmalloc(sizeof(SolveShared)));
         c.solve_grid = solve_grid;
+        // Default path: the persistent kernel wins where an evaluation is latency-bound (configs
+        // 1-2); for very large n (config 3) the multi-kernel path, which streams on all SMs with
+        // several CTAs each, is faster (measured 275 vs 337 us per c3 evaluation), so it stays
+        // the default there.  lsb_set_solve_kernel(ctx, 1) selects the persistent kernel anyway.
+        if (c.n > kSolveDefaultMaxRows) c.use_solve = false;
         c.solve_reason = "ring stages/warp " + std::to_string(solve_spw) + " (control CTAs " +
-                         std::to_string(solve_spw_ctrl) + "), smem " + std::to_string(solve_smem) + " B";
+                         std::to_string(solve_spw_ctrl) + "), smem " + std::to_string(solve_smem) + " B, cluster " +
+                         std::to_string(cs) + (solve_tv_global ? ", tv in global memory" : "");
     }
 
     SolveParams solve_params(Context& c, int task, int quasi, int want_grad = 1) {
@@ -450,6 +478,8 @@ struct Impl final : ImplBase {
         sp.tv_off = solve_tv_off;
         sp.tv_off_ctrl = solve_tv_off_ctrl;
         sp.tv_cap = solve_tv_cap;
+        sp.tv_global = solve_tv_global;
+        sp.wsl_words = solve_wsl_words;
         if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);
         sp.seq = ++launch_seq;
         sp.want_grad = want_grad;

@@ -85,6 +85,7 @@ struct Context {
     int *d_csr_ptr = nullptr, *d_csr_ent = nullptr;
     int* d_fpos = nullptr;  // E x 4 CSR positions of tet-slot forces
     double *d_Wh = nullptr, *d_bh = nullptr;
+    float* d_Wh_f = nullptr;  // hidden weights in fp32 (solve kernel, fp32 mode)
     double* d_a_hid = nullptr;
     double* d_y_last = nullptr;
     size_t l2_bytes = 126u << 20;

@@ -101,6 +101,7 @@ struct EvalParams {
     const int4* fpos;    // E: CSR position of each tet slot's force (-1 = pinned vertex)
     // hidden layers (fp64)
     const double* Wh;    // row-major, concatenated
+    const TS* Wh_s;      // the same in storage precision (solve kernel control cluster)
     const double* bh;
     int hoff[kMaxLayers], boff[kMaxLayers], hrows[kMaxLayers], hcols[kMaxLayers], hact[kMaxLayers];
     double* a_hid;       // nhid x kMaxHidden pre-activations at zt

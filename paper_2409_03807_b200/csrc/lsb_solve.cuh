@@ -57,6 +57,8 @@ struct SolveParams {
     int tv_off;       // byte offset of the tv/partials scratch (non-control CTAs)
     int tv_off_ctrl;  // ditto, control CTAs (after their control area)
     int tv_cap;       // its capacity in doubles (>= rows per CTA and >= hp)
+    int tv_global;    // 1: tv lives in global memory and streams with the VJP tiles (large n)
+    int wsl_words;    // control-area weight slices, in 8-byte words (stored as TS)
     unsigned seq;     // launch sequence number (host-incremented)
     int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
     // dynamics
@@ -128,18 +130,20 @@ __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs
     }
     __syncthreads();
     const uint64_t keep = l2_policy(1);
+    TS* wsl = reinterpret_cast<TS*>(cs.wsl);
     for (int l = 0; l < p.nhid; ++l) {
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
         cs.woff[l] = off;
-        double* wd = cs.wsl + off;
-        const double* ws = p.Wh + p.hoff[l] + (size_t)i0 * C;
-        const size_t wb = (size_t)(i1 - i0) * C * 8;
+        TS* wd = wsl + off;
+        const TS* ws = p.Wh_s + p.hoff[l] + (size_t)i0 * C;
+        const size_t wb = (size_t)(i1 - i0) * C * sizeof(TS);
         double* bd = cs.bsl + l * 64;
         const double* bs = p.bh + p.boff[l] + i0;
         const size_t bb = (size_t)(i1 - i0) * 8;
         const bool w_bulk = bulk_ok(wd, ws, wb), b_bulk = bulk_ok(bd, bs, bb);
-        if (!w_bulk) stage_doubles(wd, ws, (i1 - i0) * C);
+        if (!w_bulk)
+            for (int k = tid; k < (i1 - i0) * C; k += blockDim.x) wd[k] = ws[k];
         if (!b_bulk) stage_doubles(bd, bs, i1 - i0);
         async_used |= !w_bulk || !b_bulk;
         if (tid == 0) {
@@ -154,7 +158,7 @@ __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs
             }
             mbar_expect_tx(&wbar[l], tx);  // arrive + expect: completes when the bytes land
         }
-        off += ((i1 - i0) * C + 1) & ~1;
+        off += ((i1 - i0) * C + 3) & ~3;
     }
     if (with_state && c == 0) {
         double* sd = reinterpret_cast<double*>(cs.sst);
@@ -233,7 +237,7 @@ __device__ __forceinline__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem&
             if (i < nrow) gys[i] = gy[k] * act_eval(p.hact[l], cs.asl[l * 64 + i], 1);
         }
         __syncthreads();
-        const double* Ws = cs.wsl + cs.woff[l];
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
         double* rb = cs.rbuf(l & 1);
         const int Rp = l > 0 ? p.hrows[l - 1] : C;
@@ -241,12 +245,12 @@ __device__ __forceinline__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem&
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int i = 0;
             for (; i + 4 <= nrow; i += 4) {
-                s0 = fma(Ws[i * C + j], gys[i], s0);
-                s1 = fma(Ws[(i + 1) * C + j], gys[i + 1], s1);
-                s2 = fma(Ws[(i + 2) * C + j], gys[i + 2], s2);
-                s3 = fma(Ws[(i + 3) * C + j], gys[i + 3], s3);
+                s0 = fma((double)Ws[i * C + j], gys[i], s0);
+                s1 = fma((double)Ws[(i + 1) * C + j], gys[i + 1], s1);
+                s2 = fma((double)Ws[(i + 2) * C + j], gys[i + 2], s2);
+                s3 = fma((double)Ws[(i + 3) * C + j], gys[i + 3], s3);
             }
-            for (; i < nrow; ++i) s0 = fma(Ws[i * C + j], gys[i], s0);
+            for (; i < nrow; ++i) s0 = fma((double)Ws[i * C + j], gys[i], s0);
             const double s = (s0 + s1) + (s2 + s3);
             const int o = l > 0 ? part_owner<CS>(j, Rp) : 0;
             const int jl = l > 0 ? j - part_lo(Rp, CS, o) : j;
@@ -285,7 +289,7 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
         const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
         const double* x = cs.xin(l & 1);
         double* xn = cs.xin((l & 1) ^ 1);
-        const double* Ws = cs.wsl + cs.woff[l];
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
         // rows per warp: the smallest power of two that covers nrow in one pass (<= 8),
         // LPR = 32 / rpw lanes share one row (split-K) and reduce with log2(LPR) shuffles
@@ -296,13 +300,13 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
             const bool live = i < nrow;
             double s0 = 0.0, s1 = 0.0;
             if (live) {
-                const double* wr = Ws + i * C;
+                const TS* wr = Ws + i * C;
                 int j = sl;
                 for (; j + LPR < C; j += 2 * LPR) {
-                    s0 = fma(wr[j], x[j], s0);
-                    s1 = fma(wr[j + LPR], x[j + LPR], s1);
+                    s0 = fma((double)wr[j], x[j], s0);
+                    s1 = fma((double)wr[j + LPR], x[j + LPR], s1);
                 }
-                if (j < C) s0 = fma(wr[j], x[j], s0);
+                if (j < C) s0 = fma((double)wr[j], x[j], s0);
             }
             double s = s0 + s1;
             for (int o = LPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     double* cbase = reinterpret_cast<double*>(smem + kSolveBarBytes + (size_t)NW * sp.spw_ctrl * C::STAGEB);
     CtrlSmem cs;
     cs.wsl = cbase;
-    cs.xin0 = cbase + p.ctrl_smem_w;
+    cs.xin0 = cbase + sp.wsl_words;
     cs.xin1 = cs.xin0 + kMaxHidden;
     cs.rbuf0 = cs.xin1 + kMaxHidden;
     cs.rbuf1 = cs.rbuf0 + kCtrlRecv;
@@ -360,6 +364,15 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     const uint64_t pol_w = l2_policy(p.w_resident), pol_keep = l2_policy(1);
     auto issue_f = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep); };
     double* tv_s = reinterpret_cast<double*>(smem + (is_ctrl ? sp.tv_off_ctrl : sp.tv_off));
+    auto issue_vw = [&](int t, unsigned char* b, uint64_t* bar) { issue_vjp_w<TS, HP>(p, t, b, bar, pol_w); };
+    auto issue_vjp = [&](int t, unsigned char* b, uint64_t* bar) {
+        if (sp.tv_global) {
+            issue_vjp_w<TS, HP>(p, t, b, bar, pol_w);
+            issue_vjp_tv<TS, HP>(p, t, b, bar, pol_keep);
+        } else {
+            issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep);
+        }
+    };
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     int tr = 0;
@@ -473,6 +486,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     double inv_dt2 = __ldcg(&st->inv_dt2);
     int has_inertia = __ldcg(&st->has_inertia);
     for (;;) {
+        // whether this point's gradient may be needed (known from the solver phase alone; see
+        // the speculative VJP below)
+        int spec;
+        {
+            const int phase = __ldcg(&sh->phase), mode = __ldcg(&sh->mode);
+            spec = phase == kPhaseFinalDecode ? 0 : (mode == kModeEval ? __ldcg(&sh->want_grad) : 1);
+        }
         // ================= out_fwd (self-issued TMA rings; first tiles already in flight)
         {
             double eacc = 0.0;
@@ -487,9 +507,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     if (!(sp.exp & 1)) eacc += fwd_tile<TS, HP>(p, b, t, y, has_inertia, inv_dt2, ident);
                 });
             }
-            // the ring streams the same W tiles (+ row records) for every pass: put the next
-            // pass's first tiles (VJP, or the next forward after a rejected step) in flight now
-            if (!(sp.exp & 2)) ring_prefetch(ring, t0, t1, issue_f);
+            // the ring streams the same W tiles for every pass: put the next pass's first tiles in
+            // flight now (with tv in global memory the VJP's tiles carry tv instead of the row
+            // records: their W part goes now, the tv part after the gather)
+            if (sp.tv_global && spec) ring_prefetch(ring, t0, t1, issue_vw);
+            else if (!(sp.exp & 2)) ring_prefetch(ring, t0, t1, issue_f);
             const double tot = block_sum(eacc, red);
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
@@ -536,11 +558,6 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         // point (Armijo) needs E, but the VJP is wanted in all other cases and nearly always
         // here, so every CTA runs it when it may be needed and the control cluster alone
         // sums the energy partials and decides (a rejected point's gradient is discarded).
-        int spec;
-        {
-            const int phase = __ldcg(&sh->phase), mode = __ldcg(&sh->mode);
-            spec = phase == kPhaseFinalDecode ? 0 : (mode == kModeEval ? __ldcg(&sh->want_grad) : 1);
-        }
         if (spec) {
             // ================= vjp: tv for this CTA's rows (CSR gather, 2 lanes per vertex)
             // while its first W tiles are in flight, then the self-issued TMA rings
@@ -557,17 +574,26 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                         pi[k] = b < G ? __ldcg(p.e_part_out + b) : 0.0;
                     }
                 }
-                if (!(sp.exp & 4)) gather_rows_smem(p, R0, R1, tv_s, has_inertia, p.out_act == kIdentity);
+                if (!(sp.exp & 4))
+                    gather_rows_smem(p, R0, R1, sp.tv_global ? p.tv + R0 : tv_s, has_inertia, p.out_act == kIdentity);
+                if (sp.tv_global) fence_proxy_async();  // generic tv writes -> this CTA's bulk copies
                 __syncthreads();
                 stamp(30);
                 if (sp.exp & 2) ring_prefetch(ring, t0, t1, issue_f);
+                if (sp.tv_global && lane == 0) {  // the tv parts of the tiles already in flight
+                    const int n = min(ring.spw, ring.count(t0, t1));
+                    for (int j = 0; j < n; ++j)
+                        issue_vjp_tv<TS, HP>(p, t0 + warp + NW * j, ring.buf(j), ring.bar(j), pol_keep);
+                }
                 double acc[C::NCH][C::V4];
 #pragma unroll
                 for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
                     for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
-                ring_run(ring, t0, t1, issue_f, [&](int t, const unsigned char* b) {
-                    if (!(sp.exp & 1)) vjp_tile<TS, HP>(p, b, tv_s + (t * C::TR - R0), t, acc);
+                ring_run(ring, t0, t1, issue_vjp, [&](int t, const unsigned char* b) {
+                    const double* tvp = sp.tv_global ? reinterpret_cast<const double*>(b + C::TILEB)
+                                                     : tv_s + (t * C::TR - R0);
+                    if (!(sp.exp & 1)) vjp_tile<TS, HP>(p, b, tvp, t, acc);
                 });
                 // per-warp partials -> this CTA's ybar partial (fixed warp order) through the
                 // idle ring; then the ring is refilled and the cluster pre-reduces over DSMEM

@@ -273,67 +273,14 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
     if (threadIdx.x == 0) p.e_part_out[blockIdx.x] = 0.5 * inv_dt2 * tot;
 }
 
-// ---------------------------------------------------------------- K3b: vertex gather (+ inertia)
-// tv_i = s_i phi'(a_i) (sum of the per-tet forces on DOF i in ascending tet id
-// + inertia residual) -- the full-space gradient times the output scaling.
-// One free vertex, 4 cooperating lanes: lane q sums segment entries k = b + q,
-// b + q + 4, ... of the vertex's CSR force vectors (ascending tet id), the four
-// partials are combined in fixed lane order; + inertia, times s -> tv (3 rows).
-// Must be called by all lanes of the warp (lanes 4v..4v+3 share vertex v).
-template <typename TS>
-__device__ __forceinline__ void gather_vertex4(const EvalParams<TS>& p, int f, int has_inertia, bool ident) {
-    const int lane = threadIdx.x & 31, q = lane & 3;
-    const bool valid = f < p.n_free;
-    const int row = 3 * f + (q < 3 ? q : 2);
-    // loads that do not depend on the segment bounds go first
-    double rin = 0.0, sc = 0.0;
-    int b = 0, e = 0;
-    if (valid) {
-        b = __ldg(p.csr_ptr + f);
-        e = __ldg(p.csr_ptr + f + 1);
-        if (has_inertia) rin = __ldcg(p.rin + row);
-        sc = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
-    }
-    double gx = 0.0, gy = 0.0, gz = 0.0;
-    const double2* F = reinterpret_cast<const double2*>(p.forces);
-    // 6 entries per lane in one batch of loads (24 incident tets: one pass on Kuhn meshes)
-    for (int k0 = b + q; k0 < e; k0 += 24) {
-        double2 a[6], c[6];
-#pragma unroll
-        for (int u = 0; u < 6; ++u) {
-            const int k = k0 + 4 * u;
-            if (k < e) {
-                a[u] = __ldcg(F + 2 * (size_t)k);
-                c[u] = __ldcg(F + 2 * (size_t)k + 1);
-            } else {
-                a[u] = make_double2(0.0, 0.0);
-                c[u] = make_double2(0.0, 0.0);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 6; ++u) {
-            gx += a[u].x;
-            gy += a[u].y;
-            gz += c[u].x;
-        }
-    }
-    // fixed-order combine: (q0 + q1) + (q2 + q3)
-    gx += __shfl_xor_sync(0xffffffffu, gx, 1);
-    gy += __shfl_xor_sync(0xffffffffu, gy, 1);
-    gz += __shfl_xor_sync(0xffffffffu, gz, 1);
-    gx += __shfl_xor_sync(0xffffffffu, gx, 2);
-    gy += __shfl_xor_sync(0xffffffffu, gy, 2);
-    gz += __shfl_xor_sync(0xffffffffu, gz, 2);
-    if (valid && q < 3) {
-        const double g = (q == 0 ? gx : (q == 1 ? gy : gz)) + rin;
-        p.tv[row] = g * sc;
-    }
-}
 
 // tv for the rows [R0, R1) of one CTA into shared memory, one thread per free
 // vertex: its CSR segment (ascending tet id) is summed in order from one batch of
 // up to 24 independent 256-bit loads (one request per 32-byte force entry).
 // Vertices straddling the range edge are computed by both neighbours, identically.
+// ---------------------------------------------------------------- K3b: vertex gather (+ inertia)
+// tv_i = s_i phi'(a_i) (sum of the per-tet forces on DOF i in ascending tet id + inertia
+// residual) -- the full-space gradient times the output scaling.
 __device__ __forceinline__ double4 ld_cg_d4(const double* p) {
     double4 v;
     asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
@@ -341,40 +288,48 @@ __device__ __forceinline__ double4 ld_cg_d4(const double* p) {
                  : "l"(p));
     return v;
 }
+// One free vertex f: its CSR segment (ascending tet id) summed in order from one batch
+// of up to 24 independent 256-bit loads; rows 3f..3f+2 inside [R0, R1) are written to
+// dst[row - R0] as tv = s (g + inertia residual).
+template <typename TS>
+__device__ __forceinline__ void gather_vertex1(const EvalParams<TS>& p, int f, int R0, int R1, double* dst,
+                                               int has_inertia, bool ident) {
+    const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
+    double rin[3] = {0.0, 0.0, 0.0}, sc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int row = 3 * f + c;
+        if (has_inertia) rin[c] = __ldcg(p.rin + row);
+        sc[c] = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
+    }
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    for (int k0 = b; k0 < e; k0 += 24) {
+        double4 v[24];
+#pragma unroll
+        for (int u = 0; u < 24; ++u)
+            v[u] = k0 + u < e ? ld_cg_d4(p.forces + 4 * (size_t)(k0 + u)) : make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 24; ++u) {
+            gx += v[u].x;
+            gy += v[u].y;
+            gz += v[u].z;
+        }
+    }
+    const double g[3] = {gx, gy, gz};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int row = 3 * f + c;
+        if (row >= R0 && row < R1) dst[row - R0] = (g[c] + rin[c]) * sc[c];
+    }
+}
+
+// tv for the rows [R0, R1) of one CTA (all threads call it); vertices straddling the
+// range edge are computed by both neighbours, identically.
 template <typename TS>
 __device__ __forceinline__ void gather_rows_smem(const EvalParams<TS>& p, int R0, int R1, double* tv_s,
                                                  int has_inertia, bool ident) {
     const int f0 = R0 / 3, nf = R1 > R0 ? (R1 - 1) / 3 - f0 + 1 : 0;
-    for (int k = threadIdx.x; k < nf; k += blockDim.x) {
-        const int f = f0 + k;
-        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
-        double rin[3] = {0.0, 0.0, 0.0}, sc[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int row = 3 * f + c;
-            if (has_inertia) rin[c] = __ldcg(p.rin + row);
-            sc[c] = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
-        }
-        double gx = 0.0, gy = 0.0, gz = 0.0;
-        for (int k0 = b; k0 < e; k0 += 24) {
-            double4 v[24];
-#pragma unroll
-            for (int u = 0; u < 24; ++u)
-                v[u] = k0 + u < e ? ld_cg_d4(p.forces + 4 * (size_t)(k0 + u)) : make_double4(0.0, 0.0, 0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < 24; ++u) {
-                gx += v[u].x;
-                gy += v[u].y;
-                gz += v[u].z;
-            }
-        }
-        const double g[3] = {gx, gy, gz};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int row = 3 * f + c;
-            if (row >= R0 && row < R1) tv_s[row - R0] = (g[c] + rin[c]) * sc[c];
-        }
-    }
+    for (int k = threadIdx.x; k < nf; k += blockDim.x) gather_vertex1(p, f0 + k, R0, R1, tv_s, has_inertia, ident);
 }
 
 template <typename TS>
@@ -383,10 +338,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams<TS> p) {
     if (!st->need_grad) return;
     const bool ident = p.out_act == kIdentity;
     const int has_inertia = st->has_inertia;
-    const int nthr = gridDim.x * blockDim.x;
-    // warp-uniform trip count: gather_vertex4 shuffles across the whole warp
-    for (int wb = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; wb < 4 * p.n_free; wb += nthr)
-        gather_vertex4(p, (wb + (threadIdx.x & 31)) >> 2, has_inertia, ident);
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < p.n_free; f += gridDim.x * blockDim.x)
+        gather_vertex1(p, f, 0, p.n, p.tv, has_inertia, ident);
 }
 
 // ---------------------------------------------------------------- K4 (TMA): VJP partials

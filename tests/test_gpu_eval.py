@@ -127,3 +127,28 @@ def test_nonfinite_energy_raises(product):
     sysm = P.ReducedSystem(mesh, 1.0, 1.0, 1.0, model, "fp64")
     with pytest.raises(P.LsbError, match="non-finite"):
         sysm.eval(np.ones(2))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_eval_solve_kernel_tv_in_global_memory(precision, oracle, product, monkeypatch):
+    """The persistent kernel's large-n VJP variant (tv in global memory, streamed with the
+    W_out tiles; chosen automatically for config 3) forced on config 2."""
+    from paper_2409_03807_b200 import configs
+    monkeypatch.setenv("LSB_SOLVE_TV_GLOBAL", "1")
+    pr, sysm, ob = _pair("c2", precision, oracle, product)
+    info = sysm.solve_kernel_info()
+    assert info["in_use"] and "tv in global memory" in info["reason"], info
+    qbar = configs.timestep0_qbar(pr, ob.mass)
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    rng = np.random.default_rng(8)
+    for trial in range(3):
+        z = 0.5 * rng.standard_normal(pr.model.r)
+        g = np.zeros(pr.model.r)
+        E = obj.eval(z, g)
+        Eo, go = ob.eval(z, qbar=qbar, dt=configs.DT)
+        assert rel_err(E, Eo) < TOL[precision]
+        assert rel_err(g, go) < TOL[precision]
+    # a device L-BFGS solve through the same path
+    z = np.zeros(pr.model.r)
+    rep = product.lbfgs_minimize(obj, z, configs.solver_config())
+    assert rep.code == 1
