@@ -107,6 +107,10 @@ __device__ __forceinline__ D4 ld_stream(const D4* p) {
 }
 
 // ---- asynchronous global -> shared staging (LDGSTS): issue everything, wait once ----------
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));

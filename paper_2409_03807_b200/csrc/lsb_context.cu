@@ -335,10 +335,10 @@ struct Impl final : ImplBase {
             maxrows = std::max(maxrows, c.hrows[l]);
         }
         const size_t fixed = (3 * kMaxHidden + 128 + 2 * kMaxLayers * 64) * sizeof(double) + sizeof(DevState) + 64;
-        auto slice_words = [&](int k) {
-            size_t w = 0;
-            for (int l = 0; l < c.nhid; ++l) w += (((size_t)((c.hrows[l] + k - 1) / k) * c.hcols[l] + 1) & ~(size_t)1);
-            return w;
+        auto slice_words = [&](int k) {  // 8-byte words of the staged slices (stored as TS)
+            size_t e = 0;
+            for (int l = 0; l < c.nhid; ++l) e += (((size_t)((c.hrows[l] + k - 1) / k) * c.hcols[l] + 3) & ~(size_t)3);
+            return (e * sizeof(TS) + 7) / 8;
         };
         cs = 8;
         if (slice_words(8) * 8 + fixed > 200 * 1024 || (maxrows + 7) / 8 > 64) cs = 16;

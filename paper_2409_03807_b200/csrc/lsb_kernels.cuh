@@ -683,6 +683,26 @@ __global__ void __launch_bounds__(256) vjp_kernel(const EvalParams<TS> p) {
     if (threadIdx.x == 0) p.grp_cnt[grp] = 0;
 }
 
+// cp.async staging of count elements of TS (doubles: stage_doubles; floats: 16-byte granules
+// when both ends are 16-byte aligned, else 4-byte granules)
+template <typename TS>
+__device__ __forceinline__ void stage_ts(TS* dst, const TS* src, int count);
+template <>
+__device__ __forceinline__ void stage_ts<double>(double* dst, const double* src, int count) {
+    stage_doubles(dst, src, count);
+}
+template <>
+__device__ __forceinline__ void stage_ts<float>(float* dst, const float* src, int count) {
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(dst);
+    if (((sa | da) & 15u) == 0) {
+        const int body = count / 4;
+        for (int k = threadIdx.x; k < body; k += blockDim.x) cp_async16(dst + 4 * k, src + 4 * k);
+        for (int k = 4 * body + threadIdx.x; k < count; k += blockDim.x) cp_async4(dst + k, src + k);
+    } else {
+        for (int k = threadIdx.x; k < count; k += blockDim.x) cp_async4(dst + k, src + k);
+    }
+}
+
 // ---------------------------------------------------------------- K5/K6: cluster control
 // Row partition of a layer with R rows over CS CTAs.
 __device__ __forceinline__ int part_lo(int R, int cs, int c) { return (int)(((long long)R * c) / cs); }
@@ -698,10 +718,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
     const int c = (int)cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nw = blockDim.x >> 5;
-    double* wsl = csm;                                  // staged weight slices
+    TS* wsl = reinterpret_cast<TS*>(csm);               // staged weight slices (storage precision)
     double* ybuf = csm + p.ctrl_smem_w;                 // kMaxHidden
-    double* slice[2] = {ybuf + kMaxHidden, ybuf + kMaxHidden + 64};
-    double* part[2] = {ybuf + kMaxHidden + 128, ybuf + 2 * kMaxHidden + 128};
+    // pointer selects rather than runtime-indexed pointer arrays: no local memory (every
+    // cluster barrier invalidates L1)
+    double* const slice0 = ybuf + kMaxHidden;
+    double* const part0 = ybuf + kMaxHidden + 128;
+    double* const part1 = ybuf + 2 * kMaxHidden + 128;
     double* bsl = ybuf + 3 * kMaxHidden + 128;          // bias slices (kMaxLayers * 64)
     double* asl = bsl + kMaxLayers * 64;                // pre-activation slices (kMaxLayers * 64)
     DevState* sst = reinterpret_cast<DevState*>(asl + kMaxLayers * 64);
@@ -710,17 +733,17 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
 
     // 0. stage own row slices of every hidden layer, biases, pre-activations and
     //    (CTA 0) the solver state into shared memory: all copies in flight at once
-    int woff[kMaxLayers];
+    __shared__ int woff[kMaxLayers];
     {
         int off = 0;
         for (int l = 0; l < p.nhid; ++l) {
             const int R = p.hrows[l], C = p.hcols[l];
             const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-            woff[l] = off;
-            stage_doubles(wsl + off, p.Wh + p.hoff[l] + (size_t)i0 * C, (i1 - i0) * C);
+            if (tid == 0) woff[l] = off;
+            stage_ts(wsl + off, p.Wh_s + p.hoff[l] + (size_t)i0 * C, (i1 - i0) * C);
             stage_doubles(bsl + l * 64, p.bh + p.boff[l] + i0, i1 - i0);
             if (need) stage_doubles(asl + l * 64, p.a_hid + l * kMaxHidden + i0, i1 - i0);
-            off += ((i1 - i0) * C + 1) & ~1;
+            off += ((i1 - i0) * C + 3) & ~3;
         }
     }
     if (c == 0) stage_doubles(reinterpret_cast<double*>(sst), reinterpret_cast<const double*>(p.st),
@@ -738,22 +761,30 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
                 double s = 0.0;
 #pragma unroll 8
                 for (int b = 0; b < p.n_groups; ++b) s += __ldcg(p.ybar_grp + (size_t)b * p.hp + j);
-                slice[0][j - j0] = s;
+                slice0[j - j0] = s;
             }
             __syncthreads();
             // ---- backward through hidden layers (transpose of decode_jacobian, net.cpp:159-190)
             for (int l = p.nhid - 1; l >= 0; --l) {
                 const int R = p.hrows[l], C = p.hcols[l];
                 const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-                double* pt = part[l & 1];
-                for (int i = tid; i < i1 - i0; i += blockDim.x) slice[0][i] *= act_eval(p.hact[l], asl[l * 64 + i], 1);
+                double* pt = (l & 1) ? part1 : part0;
+                for (int i = tid; i < i1 - i0; i += blockDim.x) slice0[i] *= act_eval(p.hact[l], asl[l * 64 + i], 1);
                 __syncthreads();
-                // partial W^T abar over own rows, all C columns
-                const double* Ws = wsl + woff[l];
+                // partial W^T abar over own rows, all C columns (4 independent chains)
+                const TS* Ws = wsl + woff[l];
+                const int nr = i1 - i0;
                 for (int j = tid; j < C; j += blockDim.x) {
-                    double s = 0.0;
-                    for (int i = 0; i < i1 - i0; ++i) s = fma(Ws[i * C + j], slice[0][i], s);
-                    pt[j] = s;
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                    int i = 0;
+                    for (; i + 4 <= nr; i += 4) {
+                        s0 = fma((double)Ws[i * C + j], slice0[i], s0);
+                        s1 = fma((double)Ws[(i + 1) * C + j], slice0[i + 1], s1);
+                        s2 = fma((double)Ws[(i + 2) * C + j], slice0[i + 2], s2);
+                        s3 = fma((double)Ws[(i + 3) * C + j], slice0[i + 3], s3);
+                    }
+                    for (; i < nr; ++i) s0 = fma((double)Ws[i * C + j], slice0[i], s0);
+                    pt[j] = (s0 + s1) + (s2 + s3);
                 }
                 cluster.sync();
                 // own slice of the previous layer's ybar: sum the CS partials in rank order
@@ -763,7 +794,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
                     for (int j = k0 + tid; j < k1; j += blockDim.x) {
                         double s = 0.0;
                         for (int q = 0; q < CS; ++q) s += cluster.map_shared_rank(pt, q)[j];
-                        slice[0][j - k0] = s;
+                        slice0[j - k0] = s;
                     }
                 } else if (c == 0) {
                     for (int j = tid; j < C; j += blockDim.x) {
@@ -828,38 +859,33 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
     cluster.sync();
     more = *cluster.map_shared_rank(&more_s, 0);
     if (more) {
-        // ---- hidden forward at zt (reference mlp_forward, net.cpp:134-142)
+        // ---- hidden forward at zt (reference mlp_forward, net.cpp:134-142); the owner of each
+        // output row pushes it into every CTA's next input buffer (part0/part1), one cluster
+        // barrier per layer
         const double* zsrc = cluster.map_shared_rank(sst->zt, 0);
-        for (int j = tid; j < p.r; j += blockDim.x) ybuf[j] = zsrc[j];
+        for (int j = tid; j < p.r; j += blockDim.x) part0[j] = zsrc[j];
         __syncthreads();
         for (int l = 0; l < p.nhid; ++l) {
             const int R = p.hrows[l], C = p.hcols[l];
             const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-            double* out = slice[l & 1];
-            const double* Ws = wsl + woff[l];
+            const double* x = (l & 1) ? part1 : part0;
+            double* xn = (l & 1) ? part0 : part1;
+            const TS* Ws = wsl + woff[l];
             for (int i = warp; i < i1 - i0; i += nw) {
                 double s = 0.0;
-                for (int j = lane; j < C; j += 32) s = fma(Ws[i * C + j], ybuf[j], s);
+                for (int j = lane; j < C; j += 32) s = fma((double)Ws[i * C + j], x[j], s);
                 s = warp_sum(s);
-                if (lane == 0) {
-                    const double a = s + bsl[l * 64 + i];
-                    p.a_hid[l * kMaxHidden + i0 + i] = a;
-                    out[i] = act_eval(p.hact[l], a, 0);
-                }
+                const double a = s + bsl[l * 64 + i];
+                const double y = act_eval(p.hact[l], a, 0);
+                if (lane < CS) cluster.map_shared_rank(xn, lane)[i0 + i] = y;
+                if (lane == 0) p.a_hid[l * kMaxHidden + i0 + i] = a;
             }
             cluster.sync();
-            // gather the full layer output from every CTA's slice
-            for (int j = tid; j < R; j += blockDim.x) {
-                int q = (int)(((long long)j * CS) / R);
-                while (q + 1 < CS && part_lo(R, CS, q + 1) <= j) ++q;
-                while (part_lo(R, CS, q) > j) --q;
-                ybuf[j] = cluster.map_shared_rank(out, q)[j - part_lo(R, CS, q)];
-            }
-            __syncthreads();
         }
+        const double* ylast = (p.nhid & 1) ? part1 : part0;
         if (c == 0) {
             const int h = p.nhid > 0 ? p.hrows[p.nhid - 1] : p.r;
-            for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < h ? ybuf[j] : 0.0;
+            for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < h ? ylast[j] : 0.0;
         }
     }
     // CTA 0 publishes the solver state and sets the WHILE condition
