@@ -290,7 +290,9 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
         const double* x = cs.xin(l & 1);
         double* xn = cs.xin((l & 1) ^ 1);
         const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
+        stamp(-(300 + l * 10 + 0));
         ctrl_wait_layer(cs.wbar, l);
+        stamp(-(300 + l * 10 + 1));
         // rows per warp: the smallest power of two that covers nrow in one pass (<= 8),
         // LPR = 32 / rpw lanes share one row (split-K) and reduce with log2(LPR) shuffles
         int rpw = 1;
@@ -309,15 +311,20 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
                 if (j < C) s0 = fma((double)wr[j], x[j], s0);
             }
             double s = s0 + s1;
+            stamp(-(300 + l * 10 + 2));
             for (int o = LPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            stamp(-(300 + l * 10 + 3));
             if (live) {
                 const double a = s + cs.bsl[l * 64 + i];
                 const double y = act_eval(p.hact[l], a, 0);
+                stamp(-(300 + l * 10 + 4 + (y == 12345.0)));
                 for (int q = sl; q < CS; q += LPR) dsmem_st_f64(dsmem_addr(xn + i0 + i, q), y);
                 if (sl == 0) cs.asl[l * 64 + i] = a;
             }
+            stamp(-(300 + l * 10 + 6));
         }
         cluster.sync();
+        stamp(-(300 + l * 10 + 7));
     }
     if (c == 0) {
         const double* x = cs.xin(p.nhid & 1);
@@ -377,9 +384,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     SolveShared* sh = sp.sh;
     int tr = 0;
     auto stamp = [&](int tag) {
-        if (sp.trace && cta == 0 && tid == 0 && tr < 255) {
-            sp.trace[1 + 2 * tr] = (unsigned long long)tag;
-            sp.trace[2 + 2 * tr] = globaltimer();
+        // tag < 0: fine-grained cycle stamp (clock64), recorded only with LSB_SOLVE_EXP & 32
+        if (sp.trace && cta == 0 && tid == 0 && tr < 255 && (tag >= 0 || (sp.exp & 32))) {
+            sp.trace[1 + 2 * tr] = (unsigned long long)(tag >= 0 ? tag : -tag);
+            sp.trace[2 + 2 * tr] = tag >= 0 ? globaltimer() : (unsigned long long)clock64();
             sp.trace[0] = (unsigned long long)(++tr);
         }
     };
