@@ -28,7 +28,8 @@ namespace {
 
 constexpr int kBC = 128;       // batch columns per chunk
 constexpr int kEcols = 64;     // columns per element CTA
-constexpr int kTB = 48;        // tets per element block
+constexpr int kTB = 48;        // tets per element block (Hessian path; also the staging capacity)
+constexpr int kTBE = 24;       // tets per element block of the batched evaluation (more CTAs resident)
 
 __device__ __forceinline__ float act_f(int a, float x, int order) {
     return (float)act_eval(a, (double)x, order);
@@ -322,6 +323,164 @@ __global__ void __launch_bounds__(kEcols) elem_batched2_kernel(const TR* rec, co
         }
         for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + tid];
         eblk[(size_t)blk * N + col] = esum;
+    }
+}
+
+// ---- packed fp32x2 element math (sm_100 FFMA2/FMUL2/FADD2): two latent columns per thread
+struct f2 {
+    float2 v;
+};
+__device__ __forceinline__ f2 F2(float a) { return {make_float2(a, a)}; }
+__device__ __forceinline__ f2 F2(float a, float b) { return {make_float2(a, b)}; }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return {__fadd2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return {__fmul2_rn(a.v, b.v)}; }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
+// a*b - c*d
+__device__ __forceinline__ f2 dmd2(f2 a, f2 b, f2 c, f2 d) { return fma2(a, b, mul2(F2(-1.f), mul2(c, d))); }
+
+// SNH energy density and P for two columns (same algebra as snh_psi_P; A row-major)
+__device__ __forceinline__ f2 snh_psi_P2(const f2* A, float mu, float lambda, f2* P) {
+    const f2 trA = add2(add2(A[0], A[4]), A[8]);
+    f2 q = mul2(A[0], A[0]);
+#pragma unroll
+    for (int k = 1; k < 9; ++k) q = fma2(A[k], A[k], q);
+    f2 m2 = dmd2(A[0], A[4], A[1], A[3]);
+    m2 = add2(m2, dmd2(A[0], A[8], A[2], A[6]));
+    m2 = add2(m2, dmd2(A[4], A[8], A[5], A[7]));
+    f2 cA[9];
+    cA[0 * 3 + 0] = dmd2(A[1 * 3 + 1], A[2 * 3 + 2], A[2 * 3 + 1], A[1 * 3 + 2]);
+    cA[1 * 3 + 0] = dmd2(A[2 * 3 + 1], A[0 * 3 + 2], A[0 * 3 + 1], A[2 * 3 + 2]);
+    cA[2 * 3 + 0] = dmd2(A[0 * 3 + 1], A[1 * 3 + 2], A[1 * 3 + 1], A[0 * 3 + 2]);
+    cA[0 * 3 + 1] = dmd2(A[1 * 3 + 2], A[2 * 3 + 0], A[2 * 3 + 2], A[1 * 3 + 0]);
+    cA[1 * 3 + 1] = dmd2(A[2 * 3 + 2], A[0 * 3 + 0], A[0 * 3 + 2], A[2 * 3 + 0]);
+    cA[2 * 3 + 1] = dmd2(A[0 * 3 + 2], A[1 * 3 + 0], A[1 * 3 + 2], A[0 * 3 + 0]);
+    cA[0 * 3 + 2] = dmd2(A[1 * 3 + 0], A[2 * 3 + 1], A[2 * 3 + 0], A[1 * 3 + 1]);
+    cA[1 * 3 + 2] = dmd2(A[2 * 3 + 0], A[0 * 3 + 1], A[0 * 3 + 0], A[2 * 3 + 1]);
+    cA[2 * 3 + 2] = dmd2(A[0 * 3 + 0], A[1 * 3 + 1], A[1 * 3 + 0], A[0 * 3 + 1]);
+    const f2 detA = fma2(A[6], cA[6], fma2(A[3], cA[3], mul2(A[0], cA[0])));
+    const f2 jm1 = add2(add2(trA, m2), detA);
+    const f2 i_minus = fma2(F2(2.f), trA, q);
+    const f2 x = mul2(i_minus, F2(0.25f));
+    const f2 L = F2(log1p_minus_x(x.v.x), log1p_minus_x(x.v.y));
+    // psi = 3/8 mu q - 3/4 mu (m2 + detA) - 1/2 mu L + 1/2 lambda jm1^2
+    f2 psi = mul2(F2(0.375f * mu), q);
+    psi = fma2(F2(-0.75f * mu), add2(m2, detA), psi);
+    psi = fma2(F2(-0.5f * mu), L, psi);
+    psi = fma2(F2(0.5f * lambda), mul2(jm1, jm1), psi);
+    const f2 c1 = F2(0.75f * mu);
+    const f2 c2 = F2(mu * i_minus.v.x / (4.f * (4.f + i_minus.v.x)), mu * i_minus.v.y / (4.f * (4.f + i_minus.v.y)));
+    const f2 c3 = mul2(F2(lambda), jm1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+            const f2 Aab = A[a * 3 + bb], Aba = A[bb * 3 + a];
+            f2 t1 = sub2(add2(Aab, Aba), cA[a * 3 + bb]);
+            f2 cofF = sub2(cA[a * 3 + bb], Aba);
+            f2 F = Aab;
+            if (a == bb) {
+                t1 = sub2(t1, trA);
+                cofF = add2(add2(cofF, F2(1.f)), trA);
+                F = add2(F, F2(1.f));
+            }
+            P[a * 3 + bb] = fma2(c3, cofF, fma2(c2, F, mul2(c1, t1)));
+        }
+    return psi;
+}
+
+// Two-column element kernel: thread = columns (2 t, 2 t + 1) of a 2 kEcols-column tile.
+template <typename TR>
+__global__ void __launch_bounds__(kEcols) elem_batched_f2_kernel(const TR* rec, const int* blk_tet0,
+                                                                const int* blk_vptr, const short* tet_loc,
+                                                                const int4* tets, const float* U, int N,
+                                                                float* partial, double* eblk) {
+    extern __shared__ float sm[];
+    constexpr int NC = 2 * kEcols;  // columns per CTA
+    const int blk = blockIdx.x, tid = threadIdx.x;
+    const int col = blockIdx.y * NC + 2 * tid;  // first of the two columns (N is even)
+    const int e0 = blk_tet0[blk], ne = blk_tet0[blk + 1] - e0;
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    float2* acc = reinterpret_cast<float2*>(sm);          // [nv * 3][kEcols] float2
+    float* rs = reinterpret_cast<float*>(acc + nv * 3 * kEcols);  // [kTB][12]
+    int* vs = reinterpret_cast<int*>(rs + kTB * 12);      // [kTB][4] row offsets v * 3 * N
+    short* ls = reinterpret_cast<short*>(vs + kTB * 4);   // [kTB][4] free slots
+    for (int i = tid; i < nv * 3 * kEcols; i += kEcols) acc[i] = make_float2(0.f, 0.f);
+    for (int i = tid; i < ne * 12; i += kEcols) rs[i] = (float)rec[(size_t)e0 * 12 + i];
+    for (int i = tid; i < ne * 4; i += kEcols) {
+        const int4 t = __ldg(tets + e0 + (i >> 2));
+        const int k = i & 3;
+        vs[i] = (k == 0 ? t.x : k == 1 ? t.y : k == 2 ? t.z : t.w) * 3 * N;
+        ls[i] = tet_loc[(size_t)e0 * 4 + i];
+    }
+    __syncthreads();
+    double esum0 = 0.0, esum1 = 0.0;
+    if (col < N) {
+        const float* Uc = U + col;
+        float2 un[12];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) un[k * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc + vs[k] + c * N));
+        for (int e = 0; e < ne; ++e) {
+            f2 u[12];
+#pragma unroll
+            for (int q = 0; q < 12; ++q) u[q].v = un[q];
+            if (e + 1 < ne) {
+                const int* vn = vs + (e + 1) * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        un[k * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc + vn[k] + c * N));
+            }
+            const float* rc = rs + e * 12;
+            // D = [u1 - u0, u2 - u0, u3 - u0] (row a = component), A = D Dm^-1
+            f2 D[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                D[a * 3 + 0] = sub2(u[1 * 3 + a], u[0 * 3 + a]);
+                D[a * 3 + 1] = sub2(u[2 * 3 + a], u[0 * 3 + a]);
+                D[a * 3 + 2] = sub2(u[3 * 3 + a], u[0 * 3 + a]);
+            }
+            f2 A[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int bb = 0; bb < 3; ++bb)
+                    A[a * 3 + bb] = fma2(D[a * 3 + 2], F2(rc[2 * 3 + bb]),
+                                         fma2(D[a * 3 + 1], F2(rc[1 * 3 + bb]), mul2(D[a * 3 + 0], F2(rc[0 * 3 + bb]))));
+            f2 P[9];
+            const f2 psi = snh_psi_P2(A, rc[10], rc[11], P);
+            const float vol = rc[9];
+            esum0 += (double)(vol * psi.v.x);
+            esum1 += (double)(vol * psi.v.y);
+            const short* L = ls + e * 4;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                f2 s0 = F2(0.f);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const f2 hv = mul2(F2(vol), fma2(P[a * 3 + 2], F2(rc[c * 3 + 2]),
+                                                     fma2(P[a * 3 + 1], F2(rc[c * 3 + 1]), mul2(P[a * 3 + 0], F2(rc[c * 3 + 0])))));
+                    s0 = add2(s0, hv);
+                    const int lv = L[c + 1];
+                    if (lv >= 0) {
+                        float2& d = acc[(lv * 3 + a) * kEcols + tid];
+                        d = __fadd2_rn(d, hv.v);
+                    }
+                }
+                const int lv0 = L[0];
+                if (lv0 >= 0) {
+                    float2& d = acc[(lv0 * 3 + a) * kEcols + tid];
+                    d = __fadd2_rn(d, make_float2(-s0.v.x, -s0.v.y));
+                }
+            }
+        }
+        for (int i = 0; i < nv * 3; ++i)
+            *reinterpret_cast<float2*>(partial + ((size_t)(v0 * 3) + i) * N + col) = acc[i * kEcols + tid];
+        eblk[(size_t)blk * N + col] = esum0;
+        eblk[(size_t)blk * N + col + 1] = esum1;
     }
 }
 
@@ -971,7 +1130,8 @@ struct BatchedEngine : BatchedBase {
     int *d_blk_aptr = nullptr, *d_blk_avert = nullptr;
     short* d_tet_aloc = nullptr;
     int max_nva = 0;
-    size_t esmem2 = 0;
+    size_t esmem2 = 0, esmem_f2 = 0;
+    bool use_f2 = true;
     // buffers
     float *d_W = nullptr;  // W_out fp32 [n][h] (unpadded)
     float *d_Z = nullptr, *d_Y[kMaxLayers + 1] = {}, *d_A[kMaxLayers] = {};
@@ -1005,6 +1165,64 @@ struct BatchedEngine : BatchedBase {
         allocs.push_back(p);
         return static_cast<X*>(p);
     }
+
+    // Blocks of tb consecutive tets with their touched free vertices (slots), local slot of
+    // every tet corner, and per free vertex its slots in ascending block order.
+    struct FreeBlocks {
+        int nblk = 0, nslots = 0, max_nv = 0;
+        int *tet0 = nullptr, *vptr = nullptr, *vslot_ptr = nullptr, *vslot = nullptr;
+        short* loc = nullptr;
+    };
+    FreeBlocks build_free_blocks(Context& c, int tb) {
+        const HostMesh& m = c.mesh;
+        FreeBlocks fb;
+        fb.nblk = (m.E + tb - 1) / tb;
+        std::vector<int> tet0(fb.nblk + 1), vptr(fb.nblk + 1, 0);
+        std::vector<short> loc(4 * (size_t)m.E, -1);
+        std::vector<int> slot_vertex;
+        for (int bk = 0; bk < fb.nblk; ++bk) {
+            tet0[bk] = bk * tb;
+            const int e1 = std::min(m.E, (bk + 1) * tb);
+            std::vector<int> verts;
+            for (int e = bk * tb; e < e1; ++e)
+                for (int k = 0; k < 4; ++k) {
+                    const int f = m.free_index[m.T[4 * (size_t)e + k]];
+                    if (f >= 0) verts.push_back(f);
+                }
+            std::sort(verts.begin(), verts.end());
+            verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+            for (int e = bk * tb; e < e1; ++e)
+                for (int k = 0; k < 4; ++k) {
+                    const int f = m.free_index[m.T[4 * (size_t)e + k]];
+                    if (f >= 0)
+                        loc[4 * (size_t)e + k] =
+                            (short)(std::lower_bound(verts.begin(), verts.end(), f) - verts.begin());
+                }
+            vptr[bk + 1] = vptr[bk] + (int)verts.size();
+            fb.max_nv = std::max(fb.max_nv, (int)verts.size());
+            slot_vertex.insert(slot_vertex.end(), verts.begin(), verts.end());
+        }
+        tet0[fb.nblk] = m.E;
+        fb.nslots = vptr[fb.nblk];
+        std::vector<int> cnt(m.n_free + 1, 0);
+        for (int s = 0; s < fb.nslots; ++s) cnt[slot_vertex[s] + 1]++;
+        std::vector<int> sptr(m.n_free + 1, 0);
+        for (int f = 0; f < m.n_free; ++f) sptr[f + 1] = sptr[f] + cnt[f + 1];
+        std::vector<int> slots(fb.nslots), fill(sptr.begin(), sptr.end() - 1);
+        for (int s = 0; s < fb.nslots; ++s) slots[fill[slot_vertex[s]]++] = s;
+        fb.tet0 = alloc<int>(fb.nblk + 1);
+        fb.vptr = alloc<int>(fb.nblk + 1);
+        fb.loc = alloc<short>(4 * (size_t)m.E);
+        fb.vslot_ptr = alloc<int>(m.n_free + 1);
+        fb.vslot = alloc<int>(fb.nslots);
+        c.copy(fb.tet0, tet0.data(), 4 * tet0.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(fb.vptr, vptr.data(), 4 * vptr.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(fb.loc, loc.data(), 2 * loc.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(fb.vslot_ptr, sptr.data(), 4 * sptr.size(), cudaMemcpyHostToDevice, "blk");
+        c.copy(fb.vslot, slots.data(), 4 * slots.size(), cudaMemcpyHostToDevice, "blk");
+        return fb;
+    }
+    FreeBlocks eb;  // the batched evaluation's (smaller) element blocks
 
     void init(Context& c) {
         const HostMesh& m = c.mesh;
@@ -1109,7 +1327,8 @@ struct BatchedEngine : BatchedBase {
         d_U = alloc<float>((size_t)V * 3 * BC);
         d_rin = alloc<float>((size_t)n * BC);
         d_T = alloc<float>((size_t)n * BC);
-        d_part = alloc<float>((size_t)nslots * 3 * BC);
+        eb = build_free_blocks(c, kTBE);
+        d_part = alloc<float>((size_t)std::max(nslots, eb.nslots) * 3 * BC);
         kchunk = 256;
         nk = (n + kchunk - 1) / kchunk;
         d_P = alloc<float>((size_t)nk * h * BC);
@@ -1118,7 +1337,7 @@ struct BatchedEngine : BatchedBase {
         d_Gb[1] = alloc<float>((size_t)hmax * BC);
         nrow_tiles = (n + 63) / 64;
         d_epart = alloc<double>((size_t)nrow_tiles * BC);
-        d_eblk = alloc<double>((size_t)nblk * BC);
+        d_eblk = alloc<double>((size_t)std::max(nblk, eb.nblk) * BC);
         d_E = alloc<double>(BC);
         // pinned rows of U: pin displacement, constant across columns
         std::vector<float> U0((size_t)V * 3 * BC, 0.f);
@@ -1128,8 +1347,18 @@ struct BatchedEngine : BatchedBase {
                 for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
             }
         c.copy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "U pins");
-        esmem2 = (size_t)max_nv * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
+        esmem2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
                  kTB * 4 * sizeof(short);
+        esmem_f2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float2) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
+                   kTB * 4 * sizeof(short);
+        cuda_check(cudaFuncSetAttribute(elem_batched_f2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)esmem_f2), "elem f2 smem");
+        {
+            const char* e = getenv("LSB_ELEM_F2");
+            // measured slower than the scalar kernel (half the threads per column tile lowers
+            // occupancy more than FFMA2 saves issue slots): opt-in
+            use_f2 = (e && e[0] == '1') && BC % (2 * kEcols) == 0;
+        }
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem2), "elem2 smem");
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1171,32 +1400,40 @@ struct BatchedEngine : BatchedBase {
         c.batched_launches += c.nhid;
         for (int c0 = 0; c0 < Np; c0 += BC) {
             const float* Yc = d_Yg[c.nhid] + c0;  // h x BC slice, row stride Np
-            // output layer: C = W_out Y_L (tcgen05 when available, else SGEMM)
-            if (!tc.gemm_out(s, Yc, Np, d_C)) {
+            // output layer u = s (W_out Y_L + b) + shift - X: tcgen05 GEMM with the epilogue fused
+            // (U, inertia residual, energy partials per 128-row tile); else SGEMM + epilogue kernel
+            int e_tiles = nrow_tiles;
+            if (tc.gemm_out_fused(s, Yc, Np, c.d_eprow, d_U, d_rin, d_epart, has_inertia, inv_dt2)) {
+                e_tiles = tc.tiles1;
+            } else {
                 dim3 g1((BC + 127) / 128, (n + 127) / 128);
                 sgemm_nn_kernel<<<g1, 256, 0, s>>>(n, BC, h, d_W, h, Yc, Np, d_C, BC);
-                c.batched_launches += 1;
-            }
-            {
                 dim3 g((n + 63) / 64, (BC + 63) / 64);
                 out_epilogue_kernel<<<g, 256, 0, s>>>(n, BC, d_C, c.d_eprow, c.d_ut, has_inertia, inv_dt2, d_U,
                                                       d_rin, d_epart);
+                c.batched_launches += 2;
             }
-            {
-                dim3 g(nblk, (BC + kEcols - 1) / kEcols);
+            if (use_f2 && c.precision != LSB_FP64) {
+                // packed fp32x2: thread = two adjacent columns, 2 kEcols columns per CTA
+                dim3 g(eb.nblk, (BC + 2 * kEcols - 1) / (2 * kEcols));
+                elem_batched_f2_kernel<float><<<g, kEcols, esmem_f2, s>>>(
+                    static_cast<const float*>(c.d_rec), eb.tet0, eb.vptr, eb.loc,
+                    reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
+            } else {
+                dim3 g(eb.nblk, (BC + kEcols - 1) / kEcols);
                 if (c.precision == LSB_FP64)
                     elem_batched2_kernel<double><<<g, kEcols, esmem2, s>>>(
-                        static_cast<const double*>(c.d_rec), d_blk_tet0, d_blk_vptr, d_tet_loc,
+                        static_cast<const double*>(c.d_rec), eb.tet0, eb.vptr, eb.loc,
                         reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
                 else
                     elem_batched2_kernel<float><<<g, kEcols, esmem2, s>>>(
-                        static_cast<const float*>(c.d_rec), d_blk_tet0, d_blk_vptr, d_tet_loc,
+                        static_cast<const float*>(c.d_rec), eb.tet0, eb.vptr, eb.loc,
                         reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
             }
-            energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, nrow_tiles, d_epart, nblk, d_eblk, has_inertia, d_Eg + c0);
-            c.batched_launches += 3;
+            energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, e_tiles, d_epart, eb.nblk, d_eblk, has_inertia, d_Eg + c0);
+            c.batched_launches += 2;
             if (G) {
-                combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, d_vslot_ptr, d_vslot, d_part, d_rin, has_inertia,
+                combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, eb.vslot_ptr, eb.vslot, d_part, d_rin, has_inertia,
                                                              c.d_eprow, d_T);
                 c.batched_launches += 1;
                 // Ybar[:, c0:c0+BC] = W_out^T T

@@ -142,10 +142,19 @@ struct GemmArgs {
     int ldc;         // mode 0: row stride of out
     int m_valid;     // mode 0: valid rows of out
     uint32_t tmem_cols;
+    // mode 2 (forward with the output-layer epilogue fused): u = s (C + b) + shift - X ->
+    // U[slot][col]; inertia residual rin[row][col]; per-column energy partial per 128-row tile
+    const double* eprow;  // n x 6 {b, s, shift - X, m, U slot, qbar - X}
+    const double* ut;     // q-bar - X (unused: taken from eprow col 5)
+    float* U;
+    float* rin;
+    double* epart;        // [tiles][N]
+    int has_inertia;
+    double inv_dt2;
 };
 
 __device__ __forceinline__ void job_slices(const GemmArgs& g, int j, int& s0, int& s1) {
-    if (g.mode == 0) {
+    if (g.mode != 1) {
         s0 = 0;
         s1 = g.S;
     } else {
@@ -158,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
     __shared__ uint32_t tmem_base_s;
+    __shared__ double esum_s[4][256];  // mode 2: per-warp column energy partials
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = g.N;
     const uint32_t a_bytes = (uint32_t)(slice_floats(kTileM) * 4), b_bytes = (uint32_t)(slice_floats(N) * 4);
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                     const int st = it % kStages, u = it / kStages;
                     if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
                     unsigned char* sa = smem + (size_t)st * stage_bytes;
-                    const size_t a_slice = g.mode == 0 ? (size_t)j * g.S + s : (size_t)s;
+                    const size_t a_slice = g.mode != 1 ? (size_t)j * g.S + s : (size_t)s;
                     mbar_expect_tx(&full[st], stage_bytes);
                     tma_load_1d(sa, g.A + a_slice * slice_floats(kTileM), a_bytes, &full[st], pol_a);
                     tma_load_1d(sa + a_bytes, g.B + (size_t)s * slice_floats(N), b_bytes, &full[st], pol_b);
@@ -260,6 +270,54 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0.f;
                 }
+                if (g.mode == 2) {
+                    // fused output-layer epilogue for row grow, columns c0..c0+31
+                    const int grow = j * kTileM + row;
+                    double e[32];
+                    if (grow < g.m_valid) {
+                        const double* e6 = g.eprow + (size_t)grow * 6;
+                        const double b = e6[0], s = e6[1], sh = e6[2], m = e6[3], qb = e6[5];
+                        const int slot = (int)e6[4];
+                        float* Ur = g.U + ((size_t)(slot >> 2) * 3 + (slot & 3)) * N + c0;
+                        float* Rr = g.rin + (size_t)grow * N + c0;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            float4 uo, ro;
+                            float* up = &uo.x;
+                            float* rp = &ro.x;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const double u = s * ((double)v[i + q] + b) + sh;
+                                up[q] = (float)u;
+                                const double d = u - qb;
+                                rp[q] = (float)(g.inv_dt2 * m * d);
+                                e[i + q] = g.has_inertia ? m * d * d : 0.0;
+                            }
+                            *reinterpret_cast<float4*>(Ur + i) = uo;
+                            if (g.has_inertia) *reinterpret_cast<float4*>(Rr + i) = ro;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) e[i] = 0.0;
+                    }
+                    // per-column sums over the warp's 32 rows: recursive halving, lane c ends with
+                    // column c0 + c (fixed order)
+#pragma unroll
+                    for (int o = 16, nn = 32; o > 0; o >>= 1) {
+                        nn >>= 1;
+                        const bool up = (lane & o) != 0;
+#pragma unroll
+                        for (int k = 0; k < nn; ++k) {
+                            const double give = up ? e[k] : e[k + nn];
+                            const double keep = up ? e[k + nn] : e[k];
+                            e[k] = keep + __shfl_xor_sync(0xffffffffu, give, o);
+                        }
+                    }
+                    // lane l holds column c0 + bitrev-free index: lanes with bit o set kept the upper
+                    // half at each step -> column = lane
+                    esum_s[warp][c0 + lane] = e[0];
+                    continue;
+                }
                 float* dst;
                 if (g.mode == 0) {
                     const int grow = j * kTileM + row;
@@ -273,6 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
             }
             tc_fence_before();
             mbar_arrive(&acc_empty[acc]);
+            if (g.mode == 2) {
+                named_bar_sync(1, 128);  // the 4 epilogue warps' column partials are in esum_s
+                for (int c = threadIdx.x; c < N; c += 128)
+                    g.epart[(size_t)j * N + c] =
+                        0.5 * g.inv_dt2 * ((esum_s[0][c] + esum_s[1][c]) + (esum_s[2][c] + esum_s[3][c]));
+                named_bar_sync(1, 128);  // esum_s reusable for the next job
+            }
         }
     }
     __syncthreads();
@@ -354,16 +419,30 @@ struct TcGemm {
     bool gemm_out(cudaStream_t s, const float* Y, int ldy, float* C) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
-        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols};
+        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
     }
+    // Forward with the output-layer epilogue fused (mode 2): U, rin and per-128-row-tile
+    // energy partials epart[tiles1][N] straight from TMEM.
+    bool gemm_out_fused(cudaStream_t s, const float* Y, int ldy, const double* eprow, float* U, float* rin,
+                        double* epart, int has_inertia, double inv_dt2) {
+        if (!enabled) return false;
+        tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
+        tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, eprow, nullptr, U, rin, epart,
+                       has_inertia, inv_dt2};
+        tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
+        launches += 2;
+        return true;
+    }
+
     // Ybar (h x N, row stride ldo) = W^T T, T: n x N (row-major)
     bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar, int ldo) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 8, 256, 0, s>>>(T, 1, N, N, n, N, 1, S2, B2);
-        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols};
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                       0.0};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
         tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
         launches += 3;
