@@ -23,6 +23,8 @@
  *   lsb_simulate          <- the cmd_simulate step loop               (proj/tools/lipsub_cli.cpp:280-297)
  *   lsb_eval_batched      <- a loop of ReducedObjective::eval over z  (no reference batched API)
  *   lsb_hessian_batched   <- reduced_potential_hessian                (proj/include/lipsub/losses.hpp:131-133; proj/src/losses.cpp:301-316)
+ *   lsb_objective_hessian <- ReducedObjective::hessian                (proj/include/lipsub/reduced_solver.hpp:71; proj/src/reduced_solver.cpp:204-229)
+ *   lsb_projective_newton <- projective_newton_minimize(obj, hessian) (proj/include/lipsub/reduced_solver.hpp:56-57; proj/src/reduced_solver.cpp:133-182)
  *   lsb_lipschitz_loss    <- lipschitz_loss(model, pairs, 2, pot)     (proj/include/lipsub/losses.hpp:120-122; proj/src/losses.cpp:237-244)
  *   lsb_make_bar_mesh     <- make_bar_3d (6-tet variant)              (proj/include/lipsub/mesh.hpp:76-77; proj/src/mesh.cpp:357-397)
  *   lsb_make_bar_decoder  <- make_mlp_model (Xavier-normal variant)   (proj/include/lipsub/net.hpp:39-41; proj/src/net.cpp:90-123)
@@ -160,6 +162,13 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
 lsb_status lsb_eval_batched(lsb_context* ctx, int B, const double* Z, double* E, double* G /* nullable */);
 /* Reduced elastic-potential Hessians d2P/dz2 (B*r*r) — reduced_potential_hessian. */
 lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double* H);
+/* Objective Hessians d2E/dz2 (B*r*r) — ReducedObjective::hessian: the elastic part plus,
+ * when lsb_set_inertia set qbar, the M/h^2 block and the inertia residual's decoder curvature. */
+lsb_status lsb_objective_hessian(lsb_context* ctx, int B, const double* Z, double* H);
+/* Projective-Newton minimisation of the current objective from z (in/out):
+ * projective_newton_minimize with the SPD-projected objective Hessian and the
+ * Armijo line search; exit codes as lsb_lbfgs (lbfgs_history unused). */
+lsb_status lsb_projective_newton(lsb_context* ctx, double* z, const lsb_solver_config* cfg, lsb_exit_report* report);
 /* Second-order Lipschitz loss mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2. */
 lsb_status lsb_lipschitz_loss(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss);
 

@@ -9,6 +9,8 @@
 //   ReducedObjective::eval / as_objective     proj/include/lipsub/reduced_solver.hpp:59-72
 //   SimState, FrameInput, reduced_step        proj/include/lipsub/reduced_solver.hpp:43-48, 75-84
 //   reduced_potential_hessian, lipschitz_loss proj/include/lipsub/losses.hpp:111-133
+//   HessianFn, projective_newton_minimize     proj/include/lipsub/reduced_solver.hpp:53-57
+//   ReducedObjective::hessian                 proj/include/lipsub/reduced_solver.hpp:71
 // Eigen::VectorXd is replaced by std::vector<double> (Eigen is not a dependency).
 // Errors: LSB_EINVAL -> std::invalid_argument, everything else ->
 // std::runtime_error (the reference's exception types); solver outcomes are
@@ -208,6 +210,13 @@ class ReducedSystem {
         check(lsb_eval(ctx_, z.data(), &v, grad ? grad->data() : nullptr));
         return v;
     }
+    // ReducedObjective::hessian (reduced_solver.cpp:204-229) for a batch of points.
+    std::vector<double> objective_hessians(const std::vector<double>& Z) {
+        const int B = (int)(Z.size() / r_);
+        std::vector<double> H((size_t)B * r_ * r_);
+        check(lsb_objective_hessian(ctx_, B, Z.data(), H.data()));
+        return H;
+    }
     // reduced_potential_hessian (losses.cpp:301-316) for a batch of points (B x r row-major).
     std::vector<double> hessians(const std::vector<double>& Z) {
         const int B = (int)(Z.size() / r_);
@@ -237,7 +246,24 @@ struct ReducedObjective {
         ReducedSystem* s = system;
         return [s](const VectorXd& z, VectorXd* g) { return s->eval(z, g); };
     }
+    // d2E/dz2 (row-major r x r), reduced_solver.cpp:204-229
+    std::vector<double> hessian(const VectorXd& z) const {
+        bind();
+        return system->objective_hessians(z);
+    }
 };
+
+using HessianFn = std::function<std::vector<double>(const VectorXd&)>;  // row-major n x n
+
+// Device overload: evaluations and objective Hessians on the GPU (lsb_projective_newton).
+inline ExitReport projective_newton_minimize(const ReducedObjective& obj, VectorXd& z, const SolverConfig& cfg) {
+    cfg.validate();
+    obj.bind();
+    lsb_exit_report rep{};
+    const lsb_solver_config c = cfg.c();
+    check(lsb_projective_newton(obj.system->handle(), z.data(), &c, &rep));
+    return ExitReport::from(rep);
+}
 
 // Device-resident overload: the whole L-BFGS loop runs in one CUDA graph.
 inline ExitReport lbfgs_minimize(const ReducedObjective& obj, VectorXd& z, const SolverConfig& cfg) {

@@ -688,6 +688,152 @@ ExitReport lbfgs_minimize(const Objective& objective, std::vector<double>& x, co
     return finish(report);
 }
 
+// ---- project_spd (energy.cpp:370-380) and projective Newton (reduced_solver.cpp:133-182) ----
+namespace {
+// cyclic Jacobi: A (n x n, symmetric, row-major) -> eigenvalues w, eigenvectors V (columns)
+void jacobi_eigh(std::vector<double> A, int n, std::vector<double>& w, std::vector<double>& V) {
+    V.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += A[(size_t)p * n + q] * A[(size_t)p * n + q];
+        if (off < 1e-30) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const double apq = A[(size_t)p * n + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                const double app = A[(size_t)p * n + p], aqq = A[(size_t)q * n + q];
+                const double theta = (aqq - app) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < n; ++k) {  // A <- A G (columns p, q)
+                    const double akp = A[(size_t)k * n + p], akq = A[(size_t)k * n + q];
+                    A[(size_t)k * n + p] = cs * akp - sn * akq;
+                    A[(size_t)k * n + q] = sn * akp + cs * akq;
+                }
+                for (int k = 0; k < n; ++k) {  // A <- G^T A (rows p, q)
+                    const double apk = A[(size_t)p * n + k], aqk = A[(size_t)q * n + k];
+                    A[(size_t)p * n + k] = cs * apk - sn * aqk;
+                    A[(size_t)q * n + k] = sn * apk + cs * aqk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
+                    V[(size_t)k * n + p] = cs * vkp - sn * vkq;
+                    V[(size_t)k * n + q] = sn * vkp + cs * vkq;
+                }
+            }
+    }
+    w.resize(n);
+    for (int i = 0; i < n; ++i) w[i] = A[(size_t)i * n + i];
+}
+
+// LDL^T (no pivoting: the input is SPD after projection) solve of H d = rhs; false on a
+// non-positive pivot
+bool ldlt_solve(const std::vector<double>& H, int n, const std::vector<double>& rhs, std::vector<double>& x) {
+    std::vector<double> L((size_t)n * n, 0.0), D(n);
+    for (int j = 0; j < n; ++j) {
+        double dj = H[(size_t)j * n + j];
+        for (int k = 0; k < j; ++k) dj -= L[(size_t)j * n + k] * L[(size_t)j * n + k] * D[k];
+        if (!(dj > 0.0)) return false;
+        D[j] = dj;
+        L[(size_t)j * n + j] = 1.0;
+        for (int i = j + 1; i < n; ++i) {
+            double s = H[(size_t)i * n + j];
+            for (int k = 0; k < j; ++k) s -= L[(size_t)i * n + k] * L[(size_t)j * n + k] * D[k];
+            L[(size_t)i * n + j] = s / dj;
+        }
+    }
+    x = rhs;
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < i; ++k) x[i] -= L[(size_t)i * n + k] * x[k];
+    for (int i = 0; i < n; ++i) x[i] /= D[i];
+    for (int i = n - 1; i >= 0; --i)
+        for (int k = i + 1; k < n; ++k) x[i] -= L[(size_t)k * n + i] * x[k];
+    return true;
+}
+}  // namespace
+
+std::vector<double> project_spd(const std::vector<double>& H, int n) {
+    std::vector<double> w, V;
+    jacobi_eigh(H, n, w, V);
+    double wmin = w[0], wmax = w[0];
+    for (double v : w) {
+        wmin = std::min(wmin, v);
+        wmax = std::max(wmax, v);
+    }
+    if (wmin >= 0.0) return H;  // energy.cpp:375
+    const double floor = 1e-10 * std::max(wmax, 0.0);
+    for (double& v : w)
+        if (v < 0.0) v = floor;
+    std::vector<double> P((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < n; ++k) s += V[(size_t)i * n + k] * w[k] * V[(size_t)j * n + k];
+            P[(size_t)i * n + j] = s;
+        }
+    return P;
+}
+
+ExitReport projective_newton_minimize(const Objective& objective, const HessianFn& hessian, std::vector<double>& x,
+                                      const SolverConfig& cfg) {
+    validate(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto finish = [&](ExitReport r) {
+        r.wall_time_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return r;
+    };
+    const int n = (int)x.size();
+    std::vector<double> g(n);
+    double f = objective(x, &g);
+    ExitReport report;
+    report.evals++;
+    for (int iter = 0; iter < cfg.max_iters; ++iter) {
+        report.iterations = iter;
+        report.final_grad_inf_norm = inf_norm(g);
+        if (report.final_grad_inf_norm < cfg.epsilon) {
+            report.code = 1;
+            return finish(report);
+        }
+        const std::vector<double> H = project_spd(hessian(x), n);
+        std::vector<double> mg(n), d;
+        for (int k = 0; k < n; ++k) mg[k] = -g[k];
+        if (!ldlt_solve(H, n, mg, d)) throw std::runtime_error("projective newton: factorization failed");
+        for (double v : d)
+            if (!std::isfinite(v)) throw std::runtime_error("projective newton: singular system");
+        const double gtd = dot(g, d);
+        if (!(gtd < 0.0)) {
+            report.code = 2;
+            return finish(report);
+        }
+        std::vector<double> trial(n);
+        bool ok = false;
+        double a = 1.0;
+        for (int ls = 0; ls < cfg.max_linesearch; ++ls) {
+            for (int k = 0; k < n; ++k) trial[k] = x[k] + a * d[k];
+            const double ft = objective(trial, nullptr);
+            report.value_evals++;
+            if (std::isfinite(ft) && ft <= f + kArmijoC * a * gtd) {
+                ok = true;
+                break;
+            }
+            a *= 0.5;
+        }
+        if (!ok) {
+            report.code = 3;
+            return finish(report);
+        }
+        x = trial;
+        f = objective(x, &g);
+        report.evals++;
+    }
+    report.iterations = cfg.max_iters;
+    report.final_grad_inf_norm = inf_norm(g);
+    report.code = report.final_grad_inf_norm < cfg.epsilon ? 1 : 4;
+    return finish(report);
+}
+
 double ReducedObjective::eval(const std::vector<double>& z, std::vector<double>* grad) const {
     // reduced_solver.cpp:184-202: the gradient goes through a materialised J (:200).
     const std::vector<double> q = decode(*model, z);

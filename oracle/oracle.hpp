@@ -153,6 +153,17 @@ using Objective = std::function<double(const std::vector<double>&, std::vector<d
 
 ExitReport lbfgs_minimize(const Objective& obj, std::vector<double>& x, const SolverConfig& cfg);
 
+// project_spd (energy.cpp:370-380): symmetric eigendecomposition (here cyclic Jacobi, the
+// reference uses Eigen::SelfAdjointEigenSolver); returned unchanged when the smallest
+// eigenvalue is >= 0, else negative eigenvalues clamp to 1e-10 * max(lambda_max, 0).
+// H is n x n row-major.
+std::vector<double> project_spd(const std::vector<double>& H, int n);
+using HessianFn = std::function<std::vector<double>(const std::vector<double>&)>;  // reduced_solver.hpp:53
+// projective_newton_minimize (reduced_solver.cpp:133-182): Newton direction from the
+// SPD-projected Hessian (LDL^T solve), Armijo line search (:43-54).
+ExitReport projective_newton_minimize(const Objective& obj, const HessianFn& hess, std::vector<double>& x,
+                                      const SolverConfig& cfg);
+
 struct ReducedObjective {  // reduced_solver.hpp:59-72
     const Model* model = nullptr;
     const Mesh* mesh = nullptr;

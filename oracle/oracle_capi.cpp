@@ -374,6 +374,84 @@ int orc_lbfgs_minimize(orc_objective_cb cb, void* user, int n, double* x, double
     }
 }
 
+
+// ---- project_spd / projective Newton (energy.cpp:370-380, reduced_solver.cpp:133-182) ----------
+int orc_project_spd(const double* H, int n, double* out) {
+    try {
+        const auto P = project_spd(std::vector<double>(H, H + (size_t)n * n), n);
+        std::memcpy(out, P.data(), P.size() * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+typedef void (*orc_hessian_cb)(const double* x, double* H, int n, void* user);
+int orc_projective_newton(orc_objective_cb cb, orc_hessian_cb hcb, void* user, int n, double* x, double epsilon,
+                          int max_iters, int max_ls, int* code, int* iterations, double* gnorm) {
+    try {
+        SolverConfig cfg;
+        cfg.epsilon = epsilon;
+        cfg.max_iters = max_iters;
+        cfg.max_linesearch = max_ls;
+        std::vector<double> xx(x, x + n);
+        const ExitReport r = projective_newton_minimize(
+            [&](const std::vector<double>& v, std::vector<double>* g) {
+                if (g) g->resize(n);
+                return cb(v.data(), g ? g->data() : nullptr, n, user);
+            },
+            [&](const std::vector<double>& v) {
+                std::vector<double> H((size_t)n * n);
+                hcb(v.data(), H.data(), n, user);
+                return H;
+            },
+            xx, cfg);
+        std::memcpy(x, xx.data(), n * 8);
+        *code = r.code;
+        *iterations = r.iterations;
+        *gnorm = r.final_grad_inf_norm;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+// Projective Newton on the problem's reduced objective (qbar nullable = quasi-static).
+int orc_objective_projective_newton(void* p, const double* qbar, double dt, double* z, double epsilon,
+                                    int max_iters, int max_ls, int* code, int* iterations, double* gnorm,
+                                    int* evals, int* value_evals) {
+    try {
+        auto* c = static_cast<Ctx*>(p);
+        ReducedObjective obj;
+        obj.model = &c->model;
+        obj.mesh = &c->mesh;
+        obj.mat = &c->mat;
+        obj.pin_positions = c->pins;
+        obj.mass = c->mass;
+        obj.dt = dt;
+        if (qbar) {
+            obj.has_qbar = true;
+            obj.qbar.assign(qbar, qbar + c->model.n);
+        }
+        SolverConfig cfg;
+        cfg.epsilon = epsilon;
+        cfg.max_iters = max_iters;
+        cfg.max_linesearch = max_ls;
+        const int r = c->model.r;
+        std::vector<double> zz(z, z + r);
+        const ExitReport rep = projective_newton_minimize(
+            [&](const std::vector<double>& v, std::vector<double>* g) { return obj.eval(v, g); },
+            [&](const std::vector<double>& v) { return obj.hessian(v); }, zz, cfg);
+        std::memcpy(z, zz.data(), r * 8);
+        *code = rep.code;
+        *iterations = rep.iterations;
+        *gnorm = rep.final_grad_inf_norm;
+        if (evals) *evals = rep.evals;
+        if (value_evals) *value_evals = rep.value_evals;
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // ---- dynamics ---------------------------------------------------------------------------------
 // Runs `steps` implicit-Euler reduced steps from (positions, velocities, z),
 // gravity force f = m g, static pins at rest.  State arrays are in/out.

@@ -21,6 +21,7 @@ _I = C.POINTER(C.c_int)
 _lib = None
 
 OBJECTIVE_CB = C.CFUNCTYPE(C.c_double, _D, _D, C.c_int, C.c_void_p)
+HESSIAN_CB = C.CFUNCTYPE(None, _D, _D, C.c_int, C.c_void_p)
 
 
 def build():
@@ -61,6 +62,11 @@ def lib():
             "orc_decode_second_directional": (C.c_int, [C.c_void_p, _D, _D, _D, _D]),
             "orc_objective_eval": (C.c_int, [C.c_void_p, _D, C.c_double, _D, _D, _D]),
             "orc_objective_hessian": (C.c_int, [C.c_void_p, _D, C.c_double, _D, _D]),
+            "orc_project_spd": (C.c_int, [_D, C.c_int, _D]),
+            "orc_projective_newton": (C.c_int, [OBJECTIVE_CB, HESSIAN_CB, C.c_void_p, C.c_int, _D, C.c_double,
+                                                C.c_int, C.c_int, _I, _I, _D]),
+            "orc_objective_projective_newton": (C.c_int, [C.c_void_p, _D, C.c_double, _D, C.c_double, C.c_int,
+                                                          C.c_int, _I, _I, _D, _I, _I]),
             "orc_objective_eval_batch": (C.c_int, [C.c_void_p, _D, C.c_double, C.c_int, _D, _D, _D, C.c_int]),
             "orc_lbfgs_minimize": (C.c_int, [OBJECTIVE_CB, C.c_void_p, C.c_int, _D, C.c_double, C.c_int, C.c_int,
                                              C.c_int, _I, _I, _D]),
@@ -255,6 +261,17 @@ class Oracle:
         _chk(lib().orc_objective_hessian(self.h, _d(qb), dt, _d(np.ascontiguousarray(z, np.float64)), _d(H)))
         return H
 
+    def projective_newton(self, z0, qbar=None, dt=0.05, epsilon=1e-5, max_iters=1024, max_ls=128):
+        """projective_newton_minimize on this problem's ReducedObjective (reduced_solver.cpp:133-182)."""
+        z = np.ascontiguousarray(z0, np.float64).copy()
+        qb = None if qbar is None else np.ascontiguousarray(qbar, np.float64)
+        code, it, gn, ev, vev = C.c_int(), C.c_int(), C.c_double(), C.c_int(), C.c_int()
+        _chk(lib().orc_objective_projective_newton(self.h, _d(qb), dt, _d(z), epsilon, max_iters, max_ls,
+                                                   C.byref(code), C.byref(it), C.byref(gn), C.byref(ev),
+                                                   C.byref(vev)))
+        return {"z": z, "code": code.value, "iterations": it.value, "gnorm": gn.value, "evals": ev.value,
+                "value_evals": vev.value}
+
     def eval_batch(self, Z, qbar=None, dt=0.05, want_grad=True, threads=1):
         Z = np.ascontiguousarray(Z, np.float64)
         B = Z.shape[0]
@@ -294,6 +311,39 @@ class Oracle:
         out = C.c_double()
         _chk(lib().orc_lipschitz_loss2(self.h, Z1.shape[0], _d(Z1), _d(Z2), threads, C.byref(out)))
         return out.value
+
+
+def project_spd(H):
+    """project_spd (energy.cpp:370-380)."""
+    H = np.ascontiguousarray(H, np.float64)
+    out = np.zeros_like(H)
+    _chk(lib().orc_project_spd(_d(H), H.shape[0], _d(out)))
+    return out
+
+
+def projective_newton_minimize(fn, hess, x, epsilon=1e-5, max_iters=1024, max_ls=128):
+    """Oracle projective Newton on Python callbacks fn(x, grad_or_None) and hess(x) -> H."""
+    n = x.shape[0]
+
+    def cb(xp, gp, nn, user):
+        xv = np.ctypeslib.as_array(xp, shape=(nn,)).copy()
+        if gp:
+            g = np.zeros(nn)
+            v = fn(xv, g)
+            np.ctypeslib.as_array(gp, shape=(nn,))[:] = g
+            return v
+        return fn(xv, None)
+
+    def hcb(xp, hp, nn, user):
+        xv = np.ctypeslib.as_array(xp, shape=(nn,)).copy()
+        np.ctypeslib.as_array(hp, shape=(nn * nn,))[:] = np.asarray(hess(xv), np.float64).reshape(-1)
+
+    cbf, hcf = OBJECTIVE_CB(cb), HESSIAN_CB(hcb)
+    xx = np.ascontiguousarray(x, np.float64).copy()
+    code, it, gn = C.c_int(), C.c_int(), C.c_double()
+    _chk(lib().orc_projective_newton(cbf, hcf, None, n, _d(xx), epsilon, max_iters, max_ls, C.byref(code),
+                                     C.byref(it), C.byref(gn)))
+    return xx, {"code": code.value, "iterations": it.value, "gnorm": gn.value}
 
 
 def lbfgs_minimize(fn, x, epsilon=1e-5, max_iters=1024, max_ls=128, history=8):

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -12,6 +13,7 @@
 #include "../../include/lipsub_b200.h"
 #include "lsb_batched.hpp"
 #include "lsb_context.hpp"
+#include "lsb_newton.hpp"
 
 namespace lsb {
 void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms, double* E);
@@ -787,6 +789,105 @@ lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double*
         require(B >= 0 && (B == 0 || (Z && H)), "hessian_batched: bad arguments");
         if (B == 0) return;
         batched_hessian(ctx->c, B, Z, H);
+    });
+}
+
+lsb_status lsb_objective_hessian(lsb_context* ctx, int B, const double* Z, double* H) {
+    return run([&] {
+        check_ctx(ctx);
+        require(B >= 0 && (B == 0 || (Z && H)), "objective_hessian: bad arguments");
+        if (B == 0) return;
+        batched_objective_hessian(ctx->c, B, Z, H);
+    });
+}
+
+// projective_newton_minimize(objective, hessian, z, cfg) (reduced_solver.cpp:133-182) on this
+// context's objective: device E / grad E and device objective Hessians, host d x d algebra.
+lsb_status lsb_projective_newton(lsb_context* ctx, double* z, const lsb_solver_config* cfg, lsb_exit_report* report) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z != nullptr && cfg != nullptr, "projective newton: null argument");
+        require(cfg->epsilon > 0 && cfg->max_iters > 0 && cfg->max_linesearch > 0, "solver config: invalid");
+        Context& c = ctx->c;
+        const auto t0 = std::chrono::steady_clock::now();
+        const int r = c.r;
+        int value_evals = 0, grad_evals = 0;
+        auto objective = [&](const std::vector<double>& x, std::vector<double>* g) {
+            put_zt(c, x.data());
+            c.impl->eval(c, g != nullptr);
+            get_state(c);
+            const DevState* s = c.h_state;
+            if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+            if (g) {
+                g->assign(s->gz, s->gz + r);
+                ++grad_evals;
+            } else {
+                ++value_evals;
+            }
+            return s->f_eval;
+        };
+        auto inf_norm = [](const std::vector<double>& v) {
+            double m = 0.0;
+            for (double x : v) m = std::max(m, std::fabs(x));
+            return m;
+        };
+        std::vector<double> x(z, z + r), g(r), H((size_t)r * r);
+        double f = objective(x, &g);
+        lsb_exit_report rep{};
+        rep.code = 4;
+        bool done = false;
+        for (int iter = 0; iter < cfg->max_iters && !done; ++iter) {
+            rep.iterations = iter;
+            rep.final_grad_inf_norm = inf_norm(g);
+            if (rep.final_grad_inf_norm < cfg->epsilon) {
+                rep.code = 1;
+                done = true;
+                break;
+            }
+            batched_objective_hessian(c, 1, x.data(), H.data());
+            const std::vector<double> Hp = newton::project_spd(H, r);
+            std::vector<double> mg(r), d;
+            for (int k = 0; k < r; ++k) mg[k] = -g[k];
+            if (!newton::ldlt_solve(Hp, r, mg, d)) throw LsbError(LSB_ENONFINITE, "projective newton: factorization failed");
+            for (double v : d)
+                if (!std::isfinite(v)) throw LsbError(LSB_ENONFINITE, "projective newton: singular system");
+            double gtd = 0.0;
+            for (int k = 0; k < r; ++k) gtd += g[k] * d[k];
+            if (!(gtd < 0.0)) {
+                rep.code = 2;
+                done = true;
+                break;
+            }
+            std::vector<double> trial(r);
+            bool ok = false;
+            double a = 1.0;
+            for (int ls = 0; ls < cfg->max_linesearch; ++ls) {  // armijo (reduced_solver.cpp:43-54)
+                for (int k = 0; k < r; ++k) trial[k] = x[k] + a * d[k];
+                const double ft = objective(trial, nullptr);
+                if (std::isfinite(ft) && ft <= f + 1e-4 * a * gtd) {
+                    ok = true;
+                    break;
+                }
+                a *= 0.5;
+            }
+            if (!ok) {
+                rep.code = 3;
+                done = true;
+                break;
+            }
+            x = trial;
+            f = objective(x, &g);
+        }
+        if (!done) {
+            rep.iterations = cfg->max_iters;
+            rep.final_grad_inf_norm = inf_norm(g);
+            rep.code = rep.final_grad_inf_norm < cfg->epsilon ? 1 : 4;
+        }
+        std::memcpy(z, x.data(), sizeof(double) * r);
+        rep.wall_time_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        rep.value_evals = value_evals;
+        rep.grad_evals = grad_evals;
+        if (report) *report = rep;
     });
 }
 

@@ -568,7 +568,10 @@ __global__ void tangent_pack_kernel(int h, int P, int r, int cols, const float* 
 }
 
 // u -> U[v][3][P]; J_ia = s_i C_ia -> Jv[v][3][P][r] (pinned rows: pin displacement, zero J).
-__global__ void tangent_out_kernel(int n, int P, int r, const float* C, const double* eprow, float* U, float* Jv) {
+// With inertia (objective Hessian): rin[row][p] = m (u - (qbar - X)) / h^2, the inertia part
+// of the full-space residual whose contraction with the decoder curvature enters H.
+__global__ void tangent_out_kernel(int n, int P, int r, const float* C, const double* eprow, float* U, float* Jv,
+                                   int inertia, double inv_dt2, float* rin) {
     const int w = 1 + r;
     const int total = n * P;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
@@ -577,9 +580,53 @@ __global__ void tangent_out_kernel(int n, int P, int r, const float* C, const do
         const float* c = C + (size_t)row * P * w + (size_t)p * w;
         const int slot = (int)e6[4];
         const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
-        U[vc * P + p] = (float)(e6[1] * ((double)c[0] + e6[0]) + e6[2]);
+        const double u = e6[1] * ((double)c[0] + e6[0]) + e6[2];
+        U[vc * P + p] = (float)u;
+        if (inertia) rin[(size_t)row * P + p] = (float)(inv_dt2 * e6[3] * (u - e6[5]));
         for (int a = 0; a < r; ++a) Jv[(vc * P + p) * r + a] = (float)(e6[1] * c[1 + a]);
     }
+}
+
+// Inertia block of the objective Hessian (reduced_solver.cpp:218-221):
+//   C[p][ab] += sum_rows (m / h^2) J_a J_b,  a <= b.
+// CTA per point, thread per pair; rows streamed through shared-memory tiles of J (row
+// order fixed -> deterministic).
+__global__ void __launch_bounds__(256) inertia_hess_kernel(int n, int P, int r, const double* eprow, const float* Jv,
+                                                           double inv_dt2, double* C) {
+    constexpr int TRW = 64;
+    __shared__ float Js[TRW][33];
+    __shared__ float ms[TRW];
+    const int p = blockIdx.x, tid = threadIdx.x;
+    const int npair = r * (r + 1) / 2;
+    int a = 0, bb = 0;
+    if (tid < npair) {
+        int rem = tid;
+        while (rem >= r - a) {
+            rem -= r - a;
+            ++a;
+        }
+        bb = a + rem;
+    }
+    double acc = 0.0;
+    for (int r0 = 0; r0 < n; r0 += TRW) {
+        const int nr = min(TRW, n - r0);
+        __syncthreads();
+        for (int i = tid; i < nr * r; i += blockDim.x) {
+            const int rr = i / r, k = i % r;
+            const int row = r0 + rr;
+            const int slot = (int)eprow[(size_t)row * 6 + 4];
+            const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
+            Js[rr][k] = Jv[(vc * P + p) * r + k];
+            if (k == 0) ms[rr] = (float)eprow[(size_t)row * 6 + 3];
+        }
+        __syncthreads();
+        if (tid < npair) {
+            float s = 0.f;
+            for (int rr = 0; rr < nr; ++rr) s = fmaf(ms[rr] * Js[rr][a], Js[rr][bb], s);
+            acc += (double)s;
+        }
+    }
+    if (tid < npair) C[(size_t)p * npair + tid] += inv_dt2 * acc;
 }
 
 // Per-tet elastic Hessian contraction.  CTA = (tet block, group of GP points),
@@ -1152,6 +1199,7 @@ struct BatchedEngine : BatchedBase {
     float *d_X[2] = {}, *d_Q = nullptr, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
     float *d_Cpart = nullptr, *d_gpart = nullptr, *d_Th = nullptr, *d_Yh = nullptr, *d_Ph = nullptr, *d_Zh = nullptr;
     double *d_Ch = nullptr, *d_H = nullptr;
+    float* d_rinh = nullptr;  // inertia residual of the objective Hessian (n x PH)
     int hcols = 0;
 
     ~BatchedEngine() override {
@@ -1502,6 +1550,7 @@ struct BatchedEngine : BatchedBase {
         d_Uh = alloc<float>((size_t)c.mesh.V * 3 * PH);
         d_Jv = alloc<float>((size_t)c.mesh.V * 3 * PH * r);
         d_Cpart = alloc<float>((size_t)nblk * PH * npair);
+        d_rinh = alloc<float>((size_t)c.n * PH);
         d_gpart = alloc<float>((size_t)nslots * 3 * PH);
         d_Th = alloc<float>((size_t)n * PH);
         d_Yh = alloc<float>((size_t)h * PH);
@@ -1531,9 +1580,18 @@ struct BatchedEngine : BatchedBase {
     }
 
     // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
-    void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout) {
+    void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout, bool with_inertia = false) {
         if (!hess_ready) init_hessian(c);
         cudaStream_t s = c.stream;
+        int inertia = 0;
+        double inv_dt2 = 0.0;
+        if (with_inertia) {
+            DevState* hs = c.h_state;
+            cuda_check(cudaMemcpyAsync(hs, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s), "state");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+            inertia = hs->has_inertia;
+            inv_dt2 = hs->inv_dt2;
+        }
         const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols, npair = r * (r + 1) / 2;
         std::vector<float> zt((size_t)r * P, 0.f);
         for (int p = 0; p < N; ++p)
@@ -1556,7 +1614,8 @@ struct BatchedEngine : BatchedBase {
             dim3 g((P * (1 + r) + 127) / 128, (n + 127) / 128);
             sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (1 + r), h, d_W, h, d_Bt, P * (1 + r), d_Ct, P * (1 + r));
         }
-        tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv);
+        tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv, inertia, inv_dt2,
+                                                         d_rinh);
         {
             const int gp = 128 / r;
             dim3 g(nblk, (P + gp - 1) / gp);
@@ -1574,8 +1633,10 @@ struct BatchedEngine : BatchedBase {
                                                           d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
         }
         hess_reduce_kernel<<<(P * npair + 31) / 32, 256, 0, s>>>(nblk, P, npair, d_Cpart, d_Ch);
-        // gradient of the elastic potential (no inertia), times s
-        combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, d_vslot_ptr, d_vslot, d_gpart, nullptr, 0, c.d_eprow, d_Th);
+        if (inertia) inertia_hess_kernel<<<P, 256, 0, s>>>(n, P, r, c.d_eprow, d_Jv, inv_dt2, d_Ch);
+        // full-space residual (elastic gradient [+ inertia]), times s
+        combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, d_vslot_ptr, d_vslot, d_gpart, d_rinh, inertia, c.d_eprow,
+                                                     d_Th);
         {
             dim3 g2((P + 127) / 128, (h + 127) / 128, nk);
             sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, P, n, kchunk, d_W, h, d_Th, P, d_Ph);
@@ -1634,6 +1695,17 @@ void batched_eval(Context& c, int B, const double* Z, double* E, double* G) {
     for (int b0 = 0; b0 < B; b0 += BatchedEngine::kGroup) {
         const int N = std::min(BatchedEngine::kGroup, B - b0);
         eng.run_group(c, N, Z + (size_t)b0 * c.r, E + b0, G ? G + (size_t)b0 * c.r : nullptr);
+    }
+}
+
+// ReducedObjective::hessian (reduced_solver.cpp:204-229) at B points: the elastic Hessian plus,
+// when the context has inertia set, the M / h^2 block and the inertia residual's curvature.
+void batched_objective_hessian(Context& c, int B, const double* Z, double* H) {
+    BatchedEngine& eng = engine(c);
+    const int r = c.r;
+    for (int b0 = 0; b0 < B; b0 += BatchedEngine::PH) {
+        const int N = std::min(BatchedEngine::PH, B - b0);
+        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, H + (size_t)b0 * r * r, true);
     }
 }
 

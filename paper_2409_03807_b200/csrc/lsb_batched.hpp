@@ -8,6 +8,7 @@ namespace lsb {
 
 void batched_eval(Context& c, int B, const double* Z, double* E, double* G);
 void batched_hessian(Context& c, int B, const double* Z, double* H);
+void batched_objective_hessian(Context& c, int B, const double* Z, double* H);
 double lipschitz_loss(Context& c, int P, const double* Z1, const double* Z2);
 
 }  // namespace lsb

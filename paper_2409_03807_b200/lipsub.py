@@ -348,6 +348,15 @@ class ReducedSystem:
         check(lib().lsb_lbfgs(self._h, dptr(z), C.byref(c), C.byref(rep)))
         return z, ExitReport._from(rep)
 
+    def projective_newton(self, z: np.ndarray, cfg: SolverConfig) -> Tuple[np.ndarray, ExitReport]:
+        """Device objective + device objective Hessians, host d x d projection / LDL^T."""
+        cfg.validate()
+        z = np.array(z, dtype=np.float64, copy=True)
+        rep = _capi.lsb_exit_report()
+        c = cfg._c()
+        check(lib().lsb_projective_newton(self._h, dptr(z), C.byref(c), C.byref(rep)))
+        return z, ExitReport._from(rep)
+
     # --- dynamics
     def set_state(self, state: SimState):
         check(lib().lsb_set_state(self._h, dptr(np.ascontiguousarray(state.positions, np.float64)),
@@ -395,6 +404,13 @@ class ReducedSystem:
         Z = np.ascontiguousarray(Z, np.float64).reshape(-1, self.r)
         H = np.zeros((Z.shape[0], self.r, self.r))
         check(lib().lsb_hessian_batched(self._h, Z.shape[0], dptr(Z), dptr(H)))
+        return H
+
+    def objective_hessian_batched(self, Z: np.ndarray) -> np.ndarray:
+        """ReducedObjective::hessian at each row of Z (inertia included when set)."""
+        Z = np.ascontiguousarray(Z, np.float64).reshape(-1, self.r)
+        H = np.zeros((Z.shape[0], self.r, self.r))
+        check(lib().lsb_objective_hessian(self._h, Z.shape[0], dptr(Z), dptr(H)))
         return H
 
     def lipschitz_loss(self, Z1: np.ndarray, Z2: np.ndarray) -> float:
@@ -450,6 +466,11 @@ class ReducedObjective:
         v, g = self.system.eval(z, want_grad=True)
         grad[:] = g
         return v
+
+    def hessian(self, z: np.ndarray) -> np.ndarray:
+        """reference ReducedObjective::hessian (reduced_solver.cpp:204-229)."""
+        self._bind()
+        return self.system.objective_hessian_batched(np.asarray(z, np.float64).reshape(1, -1))[0]
 
     def as_objective(self) -> Callable:
         return lambda z, g=None: self.eval(z, g)
@@ -532,6 +553,76 @@ def _host_lbfgs(objective, x, cfg):
                 hist.pop(0)
         x[:] = trial
         f, g = f_new, g_new
+    rep.iterations = cfg.max_iters
+    rep.final_grad_inf_norm = float(np.max(np.abs(g)))
+    rep.code = ExitCode.Converged if rep.final_grad_inf_norm < cfg.epsilon else ExitCode.IterationCap
+    return finish(rep)
+
+
+def project_spd(H: np.ndarray) -> np.ndarray:
+    """reference project_spd (energy.cpp:370-380): unchanged when PSD, else negative
+    eigenvalues clamp to 1e-10 * max(lambda_max, 0)."""
+    H = np.asarray(H, np.float64)
+    w, V = np.linalg.eigh(H)
+    if w.min() >= 0.0:
+        return H
+    w = np.where(w < 0.0, 1e-10 * max(w.max(), 0.0), w)
+    return (V * w) @ V.T
+
+
+def projective_newton_minimize(objective, hessian, x: np.ndarray, cfg: SolverConfig) -> ExitReport:
+    """reference projective_newton_minimize (reduced_solver.cpp:133-182); x is updated in place.
+
+    For a ReducedObjective (hessian None or its own .hessian) the evaluations and the
+    objective Hessians run on the device (lsb_projective_newton); for other callables
+    objective(x, grad_or_None) / hessian(x) the same algorithm runs on the host."""
+    cfg.validate()
+    if isinstance(objective, ReducedObjective) and (hessian is None or getattr(hessian, "__self__", None) is objective):
+        objective._bind()
+        z, rep = objective.system.projective_newton(x, cfg)
+        x[:] = z
+        return rep
+    import time
+    t0 = time.perf_counter()
+    rep = ExitReport()
+    n = x.shape[0]
+    g = np.zeros(n)
+    f = objective(x, g)
+    rep.grad_evals += 1
+
+    def finish(r):
+        r.wall_time_ms = (time.perf_counter() - t0) * 1e3
+        return r
+
+    for it in range(cfg.max_iters):
+        rep.iterations = it
+        rep.final_grad_inf_norm = float(np.max(np.abs(g))) if n else 0.0
+        if rep.final_grad_inf_norm < cfg.epsilon:
+            rep.code = ExitCode.Converged
+            return finish(rep)
+        H = project_spd(hessian(x))
+        d = np.linalg.solve(H, -g)
+        if not np.all(np.isfinite(d)):
+            raise RuntimeError("projective newton: singular system")
+        gtd = g.dot(d)
+        if not (gtd < 0.0):
+            rep.code = ExitCode.Saddle
+            return finish(rep)
+        a, ok = 1.0, False
+        for _ in range(cfg.max_linesearch):
+            trial = x + a * d
+            ft = objective(trial, None)
+            rep.value_evals += 1
+            if math.isfinite(ft) and ft <= f + 1e-4 * a * gtd:
+                ok = True
+                break
+            a *= 0.5
+        if not ok:
+            rep.code = ExitCode.LinesearchCap
+            return finish(rep)
+        x[:] = trial
+        f = objective(x, g)
+        rep.grad_evals += 1
     rep.iterations = cfg.max_iters
     rep.final_grad_inf_norm = float(np.max(np.abs(g)))
     rep.code = ExitCode.Converged if rep.final_grad_inf_norm < cfg.epsilon else ExitCode.IterationCap

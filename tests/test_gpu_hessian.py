@@ -65,3 +65,45 @@ def test_hessian_general_decoder(oracle, product):
     H = sysm.hessian_batched(Z)
     for k in range(5):
         assert rel_err(H[k], o.reduced_potential_hessian(Z[k])) < 1e-4
+
+
+@pytest.mark.parametrize("inertia", [True, False])
+def test_objective_hessian_matches_oracle(inertia, oracle, product):
+    """lsb_objective_hessian == ReducedObjective::hessian (reduced_solver.cpp:204-229), with the
+    M/h^2 block and the inertia residual's curvature when qbar is set (1e-4, fp32 path)."""
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system("fp32")
+    ob = oracle.problem("c1")
+    qbar = configs.timestep0_qbar(pr, ob.mass) if inertia else None
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    rng = np.random.default_rng(21)
+    Z = 0.5 * rng.standard_normal((5, pr.model.r))
+    for z in Z:
+        Hg = obj.hessian(z)
+        Ho = ob.hessian(z, qbar=qbar, dt=configs.DT)
+        assert rel_err(Hg, Ho) < 1e-4, rel_err(Hg, Ho)
+        assert np.abs(Hg - Hg.T).max() == 0.0
+
+
+@pytest.mark.parametrize("inertia", [True, False])
+def test_projective_newton_matches_oracle(inertia, oracle, product):
+    """Device projective Newton (projective_newton_minimize, reduced_solver.cpp:133-182) against
+    the oracle's on config 1: same exit code, the same minimiser."""
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    ob = oracle.problem("c1")
+    qbar = configs.timestep0_qbar(pr, ob.mass) if inertia else None
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    cfg = configs.solver_config()
+    cfg.epsilon = 1e-8
+    z = np.zeros(pr.model.r)
+    rep = product.projective_newton_minimize(obj, obj.hessian, z, cfg)
+    res = ob.projective_newton(np.zeros(pr.model.r), qbar=qbar, dt=configs.DT, epsilon=1e-8)
+    assert rep.code == res["code"] == 1, (rep.code, res["code"])
+    assert abs(rep.iterations - res["iterations"]) <= 1, (rep.iterations, res["iterations"])
+    assert np.abs(z - res["z"]).max() < 1e-7 * max(1.0, np.abs(res["z"]).max())
+    g = np.zeros(pr.model.r)
+    obj.eval(z, g)
+    assert np.abs(g).max() < 1e-8

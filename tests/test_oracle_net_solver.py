@@ -213,3 +213,57 @@ def test_lipschitz_constant_decoder_and_coincident(oracle):
     z = rng.standard_normal((1, 3))
     with pytest.raises(ValueError, match="coincident"):
         o.lipschitz_loss2(z, z.copy())
+
+
+# ---- project_spd (test_energy.cpp:344-370) and projective Newton (test_solvers.cpp:94-113) ----
+def test_project_spd_reference_cases(oracle):
+    A = np.array([[2.0, 1.0], [1.0, 2.0]])
+    assert np.array_equal(oracle.project_spd(A), A)  # PSD input returned unchanged
+    P = oracle.project_spd(np.diag([1.0, -1.0]))
+    assert abs(P[0, 0] - 1.0) < 1e-12 and abs(P[1, 1] - 1e-10) < 1e-20
+    rng = np.random.default_rng(41)
+    for _ in range(12):
+        A = rng.standard_normal((5, 5))
+        A = 0.5 * (A + A.T)
+        P = oracle.project_spd(A)
+        assert np.linalg.eigvalsh(P).min() >= -1e-12
+        assert np.abs(P - P.T).max() <= 1e-12 * np.abs(P).max()
+
+
+def test_projective_newton_quadratic_one_step(oracle):
+    A = np.array([[4.0, 1.0, 0.0], [1.0, 3.0, 0.5], [0.0, 0.5, 2.0]])
+    b = np.array([1.0, 0.0, -1.0])
+
+    def fn(x, g):
+        if g is not None:
+            g[:] = A @ x - b
+        return 0.5 * x @ A @ x - b @ x
+
+    x, rep = oracle.projective_newton_minimize(fn, lambda x: A, np.zeros(3), epsilon=1e-10)
+    assert rep["code"] == 1 and rep["iterations"] == 1
+    assert np.abs(x - np.linalg.solve(A, b)).max() < 1e-10
+
+
+def test_projective_newton_reduced_objective_matches_lbfgs_minimizer(oracle):
+    from paper_2409_03807_b200 import configs
+    ob = oracle.problem("c1")
+    # timestep-0 objective: qbar = X_free + h^2 g
+    X = ob.mesh_arrays()[0]
+    free = np.nonzero(ob.mesh_arrays()[4] >= 0)[0]
+    qbar = X[free].reshape(-1) + configs.DT ** 2 * np.tile(configs.GRAVITY, free.size)
+    res = ob.projective_newton(np.zeros(ob.r), qbar=qbar, dt=configs.DT, epsilon=1e-8)
+    assert res["code"] == 1 and res["iterations"] < 20
+    E, g = ob.eval(res["z"], qbar=qbar, dt=configs.DT)
+    assert np.abs(g).max() < 1e-8
+    xl, code, _, _ = oracle.lbfgs_minimize(lambda z, gg: _obj(ob, z, gg, qbar), np.zeros(ob.r), epsilon=1e-8)
+    assert code == 1
+    assert np.abs(xl - res["z"]).max() < 1e-6
+
+
+def _obj(ob, z, g, qbar):
+    from paper_2409_03807_b200 import configs
+    if g is None:
+        return ob.eval(z, qbar=qbar, dt=configs.DT, want_grad=False)
+    E, gg = ob.eval(z, qbar=qbar, dt=configs.DT)
+    g[:] = gg
+    return E
