@@ -23,6 +23,8 @@
  *   lsb_simulate          <- the cmd_simulate step loop               (proj/tools/lipsub_cli.cpp:280-297)
  *   lsb_eval_batched      <- a loop of ReducedObjective::eval over z  (no reference batched API)
  *   lsb_hessian_batched   <- reduced_potential_hessian                (proj/include/lipsub/losses.hpp:131-133; proj/src/losses.cpp:301-316)
+ *   lsb_set_cubature      <- SolverConfig::runtime_cubature / ReducedObjective::runtime_cubature
+ *                            (proj/include/lipsub/reduced_solver.hpp:23,67; ElementSubset energy.hpp:25-36)
  *   lsb_objective_hessian <- ReducedObjective::hessian                (proj/include/lipsub/reduced_solver.hpp:71; proj/src/reduced_solver.cpp:204-229)
  *   lsb_projective_newton <- projective_newton_minimize(obj, hessian) (proj/include/lipsub/reduced_solver.hpp:56-57; proj/src/reduced_solver.cpp:133-182)
  *   lsb_lipschitz_loss    <- lipschitz_loss(model, pairs, 2, pot)     (proj/include/lipsub/losses.hpp:120-122; proj/src/losses.cpp:237-244)
@@ -162,6 +164,10 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
 lsb_status lsb_eval_batched(lsb_context* ctx, int B, const double* Z, double* E, double* G /* nullable */);
 /* Reduced elastic-potential Hessians d2P/dz2 (B*r*r) — reduced_potential_hessian. */
 lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double* H);
+/* Runtime cubature: the elastic term becomes sum_k weights[k] * E_{ids[k]} (ElementSubset).
+ * count == 0 or ids == NULL restores the full element set.  Applies to every evaluation,
+ * solve, step, batched and Hessian call of the context; the mass matrix is unchanged. */
+lsb_status lsb_set_cubature(lsb_context* ctx, int count, const int* ids, const double* weights);
 /* Objective Hessians d2E/dz2 (B*r*r) — ReducedObjective::hessian: the elastic part plus,
  * when lsb_set_inertia set qbar, the M/h^2 block and the inertia residual's decoder curvature. */
 lsb_status lsb_objective_hessian(lsb_context* ctx, int B, const double* Z, double* H);

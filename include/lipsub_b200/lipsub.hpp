@@ -210,6 +210,12 @@ class ReducedSystem {
         check(lsb_eval(ctx_, z.data(), &v, grad ? grad->data() : nullptr));
         return v;
     }
+    // Runtime cubature (ElementSubset, energy.hpp:25-36); empty ids restore the full set.
+    void set_cubature(const std::vector<int>& ids, const std::vector<double>& weights) {
+        if (ids.size() != weights.size()) throw std::invalid_argument("cubature: ids and weights differ in length");
+        check(lsb_set_cubature(ctx_, (int)ids.size(), ids.empty() ? nullptr : ids.data(),
+                               weights.empty() ? nullptr : weights.data()));
+    }
     // ReducedObjective::hessian (reduced_solver.cpp:204-229) for a batch of points.
     std::vector<double> objective_hessians(const std::vector<double>& Z) {
         const int B = (int)(Z.size() / r_);

@@ -351,12 +351,18 @@ Assembled assemble(const Mesh& m, const Material& mat, const std::vector<double>
 }
 
 void elastic_hessian_apply(const Mesh& m, const Material& mat, const std::vector<double>& positions,
-                           const std::vector<double>& in, int k, std::vector<double>& out) {
-    // energy.cpp:481-493 (full unit-weight subset).
+                           const std::vector<double>& in, int k, std::vector<double>& out,
+                           const std::vector<int>* ids, const std::vector<double>* w) {
+    // energy.cpp:481-493 over an ElementSubset (ids, weights; null = full unit-weight set).
     ElementDerivatives ed;
     std::vector<double> loc_in(12 * static_cast<size_t>(k)), loc_out(12 * static_cast<size_t>(k));
-    for (int e = 0; e < m.E; ++e) {
+    const int count = ids ? static_cast<int>(ids->size()) : m.E;
+    for (int kk = 0; kk < count; ++kk) {
+        const int e = ids ? (*ids)[kk] : kk;
+        const double we = ids ? (*w)[kk] : 1.0;
         element_snh(m, mat.mu[e], mat.lambda[e], e, positions.data(), true, ed);
+        if (ids)
+            for (double& v : ed.hess) v *= we;
         int map[12];
         for (int v = 0; v < 4; ++v) {
             const int f = m.free_index[m.T[4 * e + v]];
@@ -865,11 +871,11 @@ std::vector<double> ReducedObjective::hessian(const std::vector<double>& z) cons
     // reduced_solver.cpp:204-229
     const int r = model->r, n = model->n;
     const std::vector<double> q = decode(*model, z);
-    const Assembled ap = assemble(*mesh, *mat, q, pin_positions);
+    const Assembled ap = assemble(*mesh, *mat, q, pin_positions, cub_ids, cub_w);
     const std::vector<double> J = decode_jacobian(*model, z);
     std::vector<double> residual = ap.gradient;
     std::vector<double> HJ(static_cast<size_t>(n) * r, 0.0);
-    elastic_hessian_apply(*mesh, *mat, dof_unpack(*mesh, q, pin_positions), J, r, HJ);
+    elastic_hessian_apply(*mesh, *mat, dof_unpack(*mesh, q, pin_positions), J, r, HJ, cub_ids, cub_w);
     if (has_qbar) {
         const double inv_dt2 = 1.0 / (dt * dt);
         for (int i = 0; i < n; ++i) {

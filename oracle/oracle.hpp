@@ -101,7 +101,8 @@ Assembled assemble(const Mesh& m, const Material& mat, const std::vector<double>
 
 // elastic_hessian_apply (energy.cpp:481-493): out(n x k, row-major) += sum_e H_e in_e.
 void elastic_hessian_apply(const Mesh& m, const Material& mat, const std::vector<double>& positions,
-                           const std::vector<double>& in, int k, std::vector<double>& out);
+                           const std::vector<double>& in, int k, std::vector<double>& out,
+                           const std::vector<int>* ids = nullptr, const std::vector<double>* w = nullptr);
 
 // ---- net: proj/src/net.cpp ----------------------------------------------------
 enum Act { Identity = 0, Silu = 1, Tanh = 2, Elu = 3 };  // net.hpp:13 + [EXT] Elu

@@ -26,7 +26,22 @@ struct Ctx {  // one problem instance: mesh + material + decoder + mass
     std::vector<double> mass;
     double total_mass = 0.0;
     std::vector<double> pins;  // V*3 pin positions (rest)
+    bool has_cub = false;      // runtime cubature (ElementSubset) for the objective calls
+    std::vector<int> cub_ids;
+    std::vector<double> cub_w;
 };
+// ReducedObjective over the context (+ its runtime cubature when set)
+void bind_objective(ReducedObjective& obj, Ctx* c) {
+    obj.model = &c->model;
+    obj.mesh = &c->mesh;
+    obj.mat = &c->mat;
+    obj.pin_positions = c->pins;
+    obj.mass = c->mass;
+    if (c->has_cub) {
+        obj.cub_ids = &c->cub_ids;
+        obj.cub_w = &c->cub_w;
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -268,11 +283,7 @@ int orc_objective_eval(void* p, const double* qbar, double dt, const double* z, 
     try {
         auto* c = static_cast<Ctx*>(p);
         ReducedObjective obj;
-        obj.model = &c->model;
-        obj.mesh = &c->mesh;
-        obj.mat = &c->mat;
-        obj.pin_positions = c->pins;
-        obj.mass = c->mass;
+        bind_objective(obj, c);
         obj.dt = dt;
         if (qbar) {
             obj.has_qbar = true;
@@ -290,11 +301,7 @@ int orc_objective_hessian(void* p, const double* qbar, double dt, const double* 
     try {
         auto* c = static_cast<Ctx*>(p);
         ReducedObjective obj;
-        obj.model = &c->model;
-        obj.mesh = &c->mesh;
-        obj.mat = &c->mat;
-        obj.pin_positions = c->pins;
-        obj.mass = c->mass;
+        bind_objective(obj, c);
         obj.dt = dt;
         if (qbar) {
             obj.has_qbar = true;
@@ -314,11 +321,7 @@ int orc_objective_eval_batch(void* p, const double* qbar, double dt, int B, cons
         auto* c = static_cast<Ctx*>(p);
         const int r = c->model.r;
         ReducedObjective obj;
-        obj.model = &c->model;
-        obj.mesh = &c->mesh;
-        obj.mat = &c->mat;
-        obj.pin_positions = c->pins;
-        obj.mass = c->mass;
+        bind_objective(obj, c);
         obj.dt = dt;
         if (qbar) {
             obj.has_qbar = true;
@@ -375,6 +378,19 @@ int orc_lbfgs_minimize(orc_objective_cb cb, void* user, int n, double* x, double
 }
 
 
+// Runtime cubature for the objective calls of this context (count 0 = full set).
+int orc_set_cubature(void* p, int count, const int* ids, const double* w) {
+    try {
+        auto* c = static_cast<Ctx*>(p);
+        c->has_cub = count > 0 && ids;
+        c->cub_ids.assign(ids, ids + (c->has_cub ? count : 0));
+        c->cub_w.assign(w, w + (c->has_cub ? count : 0));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // ---- project_spd / projective Newton (energy.cpp:370-380, reduced_solver.cpp:133-182) ----------
 int orc_project_spd(const double* H, int n, double* out) {
     try {
@@ -421,11 +437,7 @@ int orc_objective_projective_newton(void* p, const double* qbar, double dt, doub
     try {
         auto* c = static_cast<Ctx*>(p);
         ReducedObjective obj;
-        obj.model = &c->model;
-        obj.mesh = &c->mesh;
-        obj.mat = &c->mat;
-        obj.pin_positions = c->pins;
-        obj.mass = c->mass;
+        bind_objective(obj, c);
         obj.dt = dt;
         if (qbar) {
             obj.has_qbar = true;

@@ -63,6 +63,7 @@ def lib():
             "orc_objective_eval": (C.c_int, [C.c_void_p, _D, C.c_double, _D, _D, _D]),
             "orc_objective_hessian": (C.c_int, [C.c_void_p, _D, C.c_double, _D, _D]),
             "orc_project_spd": (C.c_int, [_D, C.c_int, _D]),
+            "orc_set_cubature": (C.c_int, [C.c_void_p, C.c_int, _I, _D]),
             "orc_projective_newton": (C.c_int, [OBJECTIVE_CB, HESSIAN_CB, C.c_void_p, C.c_int, _D, C.c_double,
                                                 C.c_int, C.c_int, _I, _I, _D]),
             "orc_objective_projective_newton": (C.c_int, [C.c_void_p, _D, C.c_double, _D, C.c_double, C.c_int,
@@ -260,6 +261,14 @@ class Oracle:
         qb = None if qbar is None else np.ascontiguousarray(qbar, np.float64)
         _chk(lib().orc_objective_hessian(self.h, _d(qb), dt, _d(np.ascontiguousarray(z, np.float64)), _d(H)))
         return H
+
+    def set_cubature(self, ids=None, weights=None):
+        if ids is None:
+            _chk(lib().orc_set_cubature(self.h, 0, None, None))
+            return
+        ids = np.ascontiguousarray(ids, np.int32)
+        w = np.ascontiguousarray(weights, np.float64)
+        _chk(lib().orc_set_cubature(self.h, int(ids.size), ids.ctypes.data_as(_I), _d(w)))
 
     def projective_newton(self, z0, qbar=None, dt=0.05, epsilon=1e-5, max_iters=1024, max_ls=128):
         """projective_newton_minimize on this problem's ReducedObjective (reduced_solver.cpp:133-182)."""

@@ -44,6 +44,16 @@ void* Context::dmalloc(size_t bytes) {
 // Every host<->device copy of a context goes through its (non-blocking) stream and
 // waits for it: copies are then ordered after the allocation memsets and kernels
 // queued on that stream (a legacy-stream cudaMemcpy is not).
+void Context::dfree(void* p) {
+    if (!p) return;
+    for (size_t i = 0; i < allocations.size(); ++i)
+        if (allocations[i] == p) {
+            cudaFree(p);
+            allocations.erase(allocations.begin() + (long)i);
+            return;
+        }
+}
+
 void Context::copy(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) const {
     cuda_check(cudaMemcpyAsync(dst, src, bytes, kind, stream), what);
     cuda_check(cudaStreamSynchronize(stream), what);
@@ -252,6 +262,42 @@ lsb_status lsb_gaussian_stream(uint64_t seed, uint64_t tag, int count, double st
     });
 }
 
+// Element-set device arrays (tets, records {Dm^-1, vol, mu, lambda}, CSR-ordered force
+// slots, fpos, CSR) from c.mesh / c.mu / c.lambda; previous buffers are released.
+static void upload_elements(Context& c) {
+    const HostMesh& m = c.mesh;
+    const size_t w = c.wsize;
+    for (void* q : {(void*)c.d_tets, c.d_rec, (void*)c.d_forces, (void*)c.d_fpos, (void*)c.d_csr_ptr, (void*)c.d_csr_ent})
+        c.dfree(q);
+    c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * std::max<size_t>(1, (size_t)m.E)));
+    if (m.E) c.copy(c.d_tets, m.T.data(), sizeof(int) * 4 * (size_t)m.E, cudaMemcpyHostToDevice, "tets");
+    {
+        std::vector<double> rec(12 * std::max<size_t>(1, (size_t)m.E), 0.0);
+        for (int e = 0; e < m.E; ++e) {
+            double* o = &rec[12 * (size_t)e];
+            std::copy(&m.Dminv[9 * (size_t)e], &m.Dminv[9 * (size_t)e] + 9, o);
+            o[9] = m.vol[e];
+            o[10] = c.mu[e];
+            o[11] = c.lambda[e];
+        }
+        c.d_rec = c.dmalloc(rec.size() * w);
+        c.upload_real(c.d_rec, rec.data(), rec.size());
+    }
+    c.d_forces = static_cast<double*>(c.dmalloc(4 * std::max<size_t>(1, m.csr_ent.size()) * 8));
+    {  // CSR position of each (tet, slot) force; -1 for pinned vertices
+        std::vector<int> fpos(4 * std::max<size_t>(1, (size_t)m.E), -1);
+        for (int f = 0; f < m.n_free; ++f)
+            for (int k = m.csr_ptr[f]; k < m.csr_ptr[f + 1]; ++k) fpos[m.csr_ent[k]] = k;
+        c.d_fpos = static_cast<int*>(c.dmalloc(fpos.size() * 4));
+        c.copy(c.d_fpos, fpos.data(), fpos.size() * 4, cudaMemcpyHostToDevice, "fpos");
+    }
+    c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
+    c.copy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice, "csr");
+    c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
+    if (!m.csr_ent.empty())
+        c.copy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice, "csr");
+}
+
 lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, int precision, int device,
                       lsb_context** out) {
     return run([&] {
@@ -391,33 +437,8 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         }
         c.d_vfree = static_cast<int*>(c.dmalloc(sizeof(int) * m.n_free));
         c.copy(c.d_vfree, m.free_vertex.data(), sizeof(int) * m.n_free, cudaMemcpyHostToDevice, "vfree");
-        c.d_tets = static_cast<int*>(c.dmalloc(sizeof(int) * 4 * (size_t)m.E));
-        c.copy(c.d_tets, m.T.data(), sizeof(int) * 4 * (size_t)m.E, cudaMemcpyHostToDevice, "tets");
-        {
-            std::vector<double> rec(12 * (size_t)m.E);
-            for (int e = 0; e < m.E; ++e) {
-                double* o = &rec[12 * (size_t)e];
-                std::copy(&m.Dminv[9 * (size_t)e], &m.Dminv[9 * (size_t)e] + 9, o);
-                o[9] = m.vol[e];
-                o[10] = c.mu[e];
-                o[11] = c.lambda[e];
-            }
-            c.d_rec = c.dmalloc(rec.size() * w);
-            c.upload_real(c.d_rec, rec.data(), rec.size());
-        }
+        upload_elements(c);
         c.d_U = static_cast<double*>(c.dmalloc(4 * (size_t)m.V * 8));
-        c.d_forces = static_cast<double*>(c.dmalloc(4 * std::max<size_t>(1, m.csr_ent.size()) * 8));
-        {  // CSR position of each (tet, slot) force; -1 for pinned vertices
-            std::vector<int> fpos(4 * (size_t)m.E, -1);
-            for (int f = 0; f < m.n_free; ++f)
-                for (int k = m.csr_ptr[f]; k < m.csr_ptr[f + 1]; ++k) fpos[m.csr_ent[k]] = k;
-            c.d_fpos = static_cast<int*>(c.dmalloc(fpos.size() * 4));
-            c.copy(c.d_fpos, fpos.data(), fpos.size() * 4, cudaMemcpyHostToDevice, "fpos");
-        }
-        c.d_csr_ptr = static_cast<int*>(c.dmalloc(sizeof(int) * (m.n_free + 1)));
-        c.copy(c.d_csr_ptr, m.csr_ptr.data(), sizeof(int) * (m.n_free + 1), cudaMemcpyHostToDevice, "csr");
-        c.d_csr_ent = static_cast<int*>(c.dmalloc(sizeof(int) * std::max<size_t>(1, m.csr_ent.size())));
-        c.copy(c.d_csr_ent, m.csr_ent.data(), sizeof(int) * m.csr_ent.size(), cudaMemcpyHostToDevice, "csr");
         {  // hidden layers, fp64, row-major and transposed
             std::vector<double> Wh, bh;
             for (int l = 0; l < c.nhid; ++l) {
@@ -789,6 +810,68 @@ lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double*
         require(B >= 0 && (B == 0 || (Z && H)), "hessian_batched: bad arguments");
         if (B == 0) return;
         batched_hessian(ctx->c, B, Z, H);
+    });
+}
+
+// Runtime cubature (SolverConfig::runtime_cubature / ReducedObjective::runtime_cubature,
+// reduced_solver.hpp:23,67; assemble over an ElementSubset, energy.cpp:418-432): the elastic
+// term sums w_k E_{ids[k]}.  Linear in the element volume, so the active element set is the
+// subset with vol * w; count == 0 (or ids NULL) restores the full set.
+lsb_status lsb_set_cubature(lsb_context* ctx, int count, const int* ids, const double* weights) {
+    return run([&] {
+        check_ctx(ctx);
+        Context& c = ctx->c;
+        if (!c.has_full) {
+            c.mesh_full = c.mesh;
+            c.mu_full = c.mu;
+            c.lambda_full = c.lambda;
+            c.has_full = true;
+        }
+        const HostMesh& F = c.mesh_full;
+        HostMesh m = F;
+        std::vector<double> mu = c.mu_full, lam = c.lambda_full;
+        if (count > 0 && ids) {
+            require(weights != nullptr, "cubature: weights required with ids");
+            m.E = count;
+            m.T.assign(4 * (size_t)count, 0);
+            m.Dminv.assign(9 * (size_t)count, 0.0);
+            m.vol.assign(count, 0.0);
+            mu.assign(count, 0.0);
+            lam.assign(count, 0.0);
+            for (int k = 0; k < count; ++k) {
+                const int e = ids[k];
+                require(e >= 0 && e < F.E, "cubature: element id out of range");
+                require(std::isfinite(weights[k]), "cubature: non-finite weight");
+                std::copy(&F.T[4 * (size_t)e], &F.T[4 * (size_t)e] + 4, &m.T[4 * (size_t)k]);
+                std::copy(&F.Dminv[9 * (size_t)e], &F.Dminv[9 * (size_t)e] + 9, &m.Dminv[9 * (size_t)k]);
+                m.vol[k] = F.vol[e] * weights[k];
+                mu[k] = c.mu_full[e];
+                lam[k] = c.lambda_full[e];
+            }
+            // vertex (free slot) -> incident (element k * 4 + corner), ascending k
+            std::vector<int> cnt(m.n_free + 1, 0);
+            for (int k = 0; k < count; ++k)
+                for (int s = 0; s < 4; ++s) {
+                    const int f = m.free_index[m.T[4 * (size_t)k + s]];
+                    if (f >= 0) cnt[f + 1]++;
+                }
+            m.csr_ptr.assign(m.n_free + 1, 0);
+            for (int f = 0; f < m.n_free; ++f) m.csr_ptr[f + 1] = m.csr_ptr[f] + cnt[f + 1];
+            m.csr_ent.assign(m.csr_ptr[m.n_free], 0);
+            std::vector<int> fill(m.csr_ptr.begin(), m.csr_ptr.end() - 1);
+            for (int k = 0; k < count; ++k)
+                for (int s = 0; s < 4; ++s) {
+                    const int f = m.free_index[m.T[4 * (size_t)k + s]];
+                    if (f >= 0) m.csr_ent[fill[f]++] = 4 * k + s;
+                }
+        }
+        sync(c);
+        c.mesh = std::move(m);
+        c.mu = std::move(mu);
+        c.lambda = std::move(lam);
+        upload_elements(c);
+        c.impl->rebind_elements(c);
+        c.batched.reset();  // rebuilt lazily over the new element set
     });
 }
 

@@ -319,7 +319,8 @@ struct Impl final : ImplBase {
         const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
         p.grid_out = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<TS>, 256, 0), "occupancy elem");
-        p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.num_sms * std::max(1, occ)));
+        c.grid_elem_cap = c.num_sms * std::max(1, occ);
+        p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.grid_elem_cap));
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, kStreamThreads, vjp_smem),
                    "occupancy vjp");
         p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
@@ -700,6 +701,22 @@ struct Impl final : ImplBase {
         }
         cuda_check(cudaGraphLaunch(g_step, c.stream), "graph launch (step)");
         c.launches += 4;  // prep, start, finalize, count (bodies via device accumulator)
+    }
+
+    void rebind_elements(Context& c) override {
+        for (EvalParams<TS>* q : {&p, &ps}) {
+            q->E = c.mesh.E;
+            q->tets = reinterpret_cast<const int4*>(c.d_tets);
+            q->rec = static_cast<const TS*>(c.d_rec);
+            q->forces = c.d_forces;
+            q->csr_ptr = c.d_csr_ptr;
+            q->csr_ent = c.d_csr_ent;
+            q->fpos = reinterpret_cast<const int4*>(c.d_fpos);
+        }
+        p.grid_elem = std::max(1, std::min((c.mesh.E + 255) / 256, c.grid_elem_cap));
+        c.grid_elem = p.grid_elem;
+        ps.grid_elem = p.grid_elem;
+        invalidate_graphs();
     }
 
     void invalidate_graphs() override {

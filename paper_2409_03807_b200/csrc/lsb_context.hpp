@@ -34,6 +34,8 @@ struct ImplBase {
     virtual void step(Context& c) = 0;
     virtual void profile(Context& c, int reps, float* ms) = 0;
     virtual void invalidate_graphs() = 0;
+    // the element set changed (runtime cubature): re-point the element arrays, regrid
+    virtual void rebind_elements(Context& c) = 0;
     // One evaluation at st->zt as a graph with event-record nodes:
     // ev[0] | ctrl(start) | ev[1] | out_fwd | ev[2] | elem, vjp, ctrl | ev[3]
     virtual void eval_timed(Context& c, cudaEvent_t* ev) = 0;
@@ -112,6 +114,13 @@ struct Context {
     std::unique_ptr<BatchedBase> batched;
     long long batched_launches = 0;
     std::vector<void*> allocations;
+    void dfree(void* p);
+    // runtime cubature (SolverConfig::runtime_cubature, reduced_solver.hpp:23): the full mesh and
+    // material are kept here while `mesh`, `mu`, `lambda` hold the active (weighted) subset
+    bool has_full = false;
+    HostMesh mesh_full;
+    std::vector<double> mu_full, lambda_full;
+    int grid_elem_cap = 1;
 
     ~Context();
     void* dmalloc(size_t bytes);

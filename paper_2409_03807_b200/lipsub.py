@@ -406,6 +406,18 @@ class ReducedSystem:
         check(lib().lsb_hessian_batched(self._h, Z.shape[0], dptr(Z), dptr(H)))
         return H
 
+    def set_cubature(self, ids: Optional[np.ndarray] = None, weights: Optional[np.ndarray] = None):
+        """Runtime cubature (ElementSubset: elastic term = sum_k w_k E_{ids_k}); None restores
+        the full element set."""
+        if ids is None:
+            check(lib().lsb_set_cubature(self._h, 0, None, None))
+            return
+        ids = np.ascontiguousarray(ids, np.int32)
+        w = np.ascontiguousarray(weights, np.float64)
+        if ids.shape != w.shape:
+            raise ValueError("cubature: ids and weights differ in length")
+        check(lib().lsb_set_cubature(self._h, int(ids.size), ids.ctypes.data_as(C.POINTER(C.c_int)), dptr(w)))
+
     def objective_hessian_batched(self, Z: np.ndarray) -> np.ndarray:
         """ReducedObjective::hessian at each row of Z (inertia included when set)."""
         Z = np.ascontiguousarray(Z, np.float64).reshape(-1, self.r)

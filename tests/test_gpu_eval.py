@@ -152,3 +152,52 @@ def test_eval_solve_kernel_tv_in_global_memory(precision, oracle, product, monke
     z = np.zeros(pr.model.r)
     rep = product.lbfgs_minimize(obj, z, configs.solver_config())
     assert rep.code == 1
+
+
+@pytest.mark.parametrize("path", ["solve", "graph"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_runtime_cubature_matches_oracle(precision, path, oracle, product):
+    """lsb_set_cubature (ElementSubset runtime cubature): a random 30% weighted subset on config 1,
+    E / grad E, the objective Hessian and a device L-BFGS solve against the oracle; restoring the
+    full set gives the original objective."""
+    from paper_2409_03807_b200 import configs
+    pr, sysm, ob = _pair("c1", precision, oracle, product)
+    sysm.use_solve_kernel(path == "solve")
+    rng = np.random.default_rng(31)
+    E_all = pr.mesh.num_elements()
+    ids = np.sort(rng.choice(E_all, size=E_all * 3 // 10, replace=False)).astype(np.int32)
+    w = 0.5 + 3.0 * rng.random(ids.size)
+    qbar = configs.timestep0_qbar(pr, ob.mass)
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    z0 = 0.4 * rng.standard_normal(pr.model.r)
+    E_full = obj.eval(z0)
+    sysm.set_cubature(ids, w)
+    ob.set_cubature(ids, w)
+    for trial in range(3):
+        z = 0.4 * rng.standard_normal(pr.model.r)
+        g = np.zeros(pr.model.r)
+        E = obj.eval(z, g)
+        Eo, go = ob.eval(z, qbar=qbar, dt=configs.DT)
+        assert rel_err(E, Eo) < TOL[precision] and rel_err(g, go) < TOL[precision]
+    Hg = obj.hessian(z0)
+    Ho = ob.hessian(z0, qbar=qbar, dt=configs.DT)
+    assert rel_err(Hg, Ho) < 1e-4
+    cfg = configs.solver_config()
+    z = np.zeros(pr.model.r)
+    rep = product.lbfgs_minimize(obj, z, cfg)
+
+    def fo(zz, gg):
+        if gg is None:
+            return ob.eval(zz, qbar=qbar, dt=configs.DT, want_grad=False)
+        e, gq = ob.eval(zz, qbar=qbar, dt=configs.DT)
+        gg[:] = gq
+        return e
+
+    zo, code, iters, _ = oracle.lbfgs_minimize(fo, np.zeros(pr.model.r), epsilon=cfg.epsilon,
+                                               history=cfg.lbfgs_history)
+    assert rep.code == code == 1
+    if precision == "fp64":
+        assert rep.iterations == iters
+    assert np.abs(z - zo).max() < 1e-5
+    sysm.set_cubature(None)
+    assert rel_err(obj.eval(z0), E_full) < 1e-15

@@ -134,3 +134,20 @@ def test_lumped_mass_conserves(oracle):
     _, _, Dm, vol, _ = o.mesh_arrays()
     assert abs(vol.sum() - 0.0625) < 1e-12
     assert np.all(vol > 0)
+
+
+def test_runtime_cubature_full_unit_set_is_plain_assembly(oracle):
+    """ElementSubset::full with unit weights shares the plain-assembly code path (energy.hpp:22-24):
+    bit-identical; all weights 2 doubles the elastic energy exactly."""
+    ob = oracle.problem("c1")
+    z = 0.3 * np.random.default_rng(3).standard_normal(ob.r)
+    E0, g0 = ob.eval(z)
+    ids = np.arange(ob.E, dtype=np.int32)
+    ob.set_cubature(ids, np.ones(ob.E))
+    E1, g1 = ob.eval(z)
+    assert E1 == E0 and np.array_equal(g1, g0)
+    ob.set_cubature(ids, 2.0 * np.ones(ob.E))
+    E2, g2 = ob.eval(z)
+    assert E2 == 2.0 * E0 and np.array_equal(g2, 2.0 * g0)
+    ob.set_cubature(None)
+    assert ob.eval(z)[0] == E0
