@@ -10,3 +10,4 @@ from .lipsub import (Activation, ExitCode, ExitReport, FrameInput, Layer, Mesh, 
                      gravity_force, lame_from_young, lbfgs_minimize, lipschitz_loss, make_bar_decoder,
                      make_bar_mesh, reduced_step, rest_state)
 from ._capi import LibraryMissing, LsbError, lib  # noqa: F401
+from .checkpoint import load_checkpoint, save_checkpoint  # noqa: F401
