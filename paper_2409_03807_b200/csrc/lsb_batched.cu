@@ -207,54 +207,6 @@ __global__ void __launch_bounds__(256) out_epilogue_kernel(int n, int N, const f
                                                                 red[2][threadIdx.x] + red[3][threadIdx.x]);
 }
 
-// ---------------------------------------------------------------- batched element pass
-// One CTA per (tet block, 64-column tile); thread = column.
-template <typename TR>
-__global__ void __launch_bounds__(kEcols) elem_batched_kernel(const int4* tets, const TR* rec, const int* blk_tet0,
-                                                             const int* blk_vptr, const short* tet_loc,
-                                                             const float* U, int N, float* partial,
-                                                             double* eblk) {
-    extern __shared__ float acc[];  // [nv][3][kEcols]
-    const int blk = blockIdx.x;
-    const int col = blockIdx.y * kEcols + threadIdx.x;
-    const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
-    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
-    for (int i = threadIdx.x; i < nv * 3 * kEcols; i += blockDim.x) acc[i] = 0.f;
-    __syncthreads();
-    double esum = 0.0;
-    if (col < N) {
-        for (int e = e0; e < e1; ++e) {
-            const int4 t = __ldg(tets + e);
-            double rd[12];
-            load_rec<TR>(rec, (size_t)e, rd);
-            float rc[12];
-#pragma unroll
-            for (int q = 0; q < 12; ++q) rc[q] = (float)rd[q];
-            const int vv[4] = {t.x, t.y, t.z, t.w};
-            float u[4][3];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) u[k][c] = __ldg(U + ((size_t)vv[k] * 3 + c) * N + col);
-            float f[12];
-            esum += (double)tet_energy_forces_t<float>(u[0], u[1], u[2], u[3], rc, f);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int lv = tet_loc[(size_t)e * 4 + k];
-                if (lv >= 0) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[(lv * 3 + c) * kEcols + threadIdx.x] += f[k * 3 + c];
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (col < N) {
-        for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + threadIdx.x];
-        eblk[(size_t)blk * N + col] = esum;
-    }
-}
-
 // Element pass per (block of kTB tets, kEcols columns), thread = column:
 //  - the block's records (as fp32) and vertex slots are staged once in shared
 //    memory (no per-thread record loads or conversions);
@@ -627,227 +579,6 @@ __global__ void __launch_bounds__(256) inertia_hess_kernel(int n, int P, int r, 
         }
     }
     if (tid < npair) C[(size_t)p * npair + tid] += inv_dt2 * acc;
-}
-
-// Per-tet elastic Hessian contraction.  CTA = (tet block, group of GP points),
-// thread = (point, direction b).  The block's vertex displacements and
-// Jacobian rows for the CTA's points are staged in shared memory once
-// (cp.async, all in flight).  Per tet each thread forms dF_b, the stress
-// differential M_b = 2 psi_I dF_b + psi_J (dcof F)[dF_b] and the scalars
-// alpha_b = 2F : dF_b, beta_b = cof F : dF_b, publishes them (double-buffered,
-// one barrier per tet) and accumulates its share of the pairs (a <= b):
-//   C_ab += vol (dF_a : M_b + psi_II alpha_a alpha_b + lambda beta_a beta_b)
-// (= J^T hess(P) J restricted to the tet).  Thread (point, 0) also accumulates
-// the block's elastic forces (gradient of P) for the decoder-curvature term.
-template <int R>
-__global__ void __launch_bounds__(128, 3) elem_hess_kernel(const int4* tets, const float* rec, const int* blk_tet0,
-                                                           const int* blk_vptr, const short* tet_loc,
-                                                           const int* blk_aptr, const int* blk_avert,
-                                                           const short* tet_aloc, const float* U, const float* Jv,
-                                                           int P, float* Cpart, float* gpart) {
-    constexpr int GP = 128 / R;                  // points per CTA
-    constexpr int NPAIR = R * (R + 1) / 2;
-    constexpr int PPT = (NPAIR * GP + 127) / 128;  // pairs per thread
-    __shared__ float sh_dF[2][GP][R][9];
-    __shared__ float sh_M[2][GP][R][9];
-    __shared__ float sh_ab[2][GP][R][2];
-    __shared__ float sh_sc[2][GP][3];
-    extern __shared__ __align__(16) float dyn[];
-    const int tid = threadIdx.x;
-    const int pl = tid / R, b = tid % R;
-    const int p0 = blockIdx.y * GP;
-    const int blk = blockIdx.x;
-    const int e0 = blk_tet0[blk], e1 = blk_tet0[blk + 1];
-    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
-    const int a0 = blk_aptr[blk], nva = blk_aptr[blk + 1] - a0;
-    float* Js = dyn;                                 // [nva][3][GP][R]
-    float* Us = Js + (size_t)nva * 3 * GP * R;       // [nva][3][GP]
-    float* accg = Us + (size_t)nva * 3 * GP;         // [nv][3][GP]
-    // ---- stage (all copies in flight, one wait)
-    for (int i = tid; i < nva * 3; i += 128) {
-        const int va = __ldg(blk_avert + a0 + i / 3), c = i % 3;
-        const size_t vc = (size_t)va * 3 + c;
-        const float* src = Jv + (vc * P + p0) * R;
-        float* dst = Js + (size_t)i * GP * R;
-        for (int k = 0; k < GP * R; k += 4) cp_async16(dst + k, src + k);
-    }
-    static_assert(GP % 4 == 0, "16-byte staging of U");
-    for (int i = tid; i < nva * 3 * (GP / 4); i += 128) {
-        const int vcl = i / (GP / 4), k4 = i % (GP / 4);
-        const int va = __ldg(blk_avert + a0 + vcl / 3), c = vcl % 3;
-        cp_async16(Us + (size_t)vcl * GP + 4 * k4, U + ((size_t)va * 3 + c) * P + p0 + 4 * k4);
-    }
-    for (int i = tid; i < nv * 3 * GP; i += 128) accg[i] = 0.f;
-    float cacc[PPT];
-    int pa[PPT], pb[PPT], ppt[PPT];
-#pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-        cacc[k] = 0.f;
-        const int slot = tid + 128 * k;
-        ppt[k] = -1;
-        pa[k] = pb[k] = 0;
-        if (slot < NPAIR * GP && p0 + slot / NPAIR < P) {
-            int a = 0, rem = slot % NPAIR;
-            while (rem >= R - a) {
-                rem -= R - a;
-                ++a;
-            }
-            ppt[k] = slot / NPAIR;
-            pa[k] = a;
-            pb[k] = a + rem;
-        }
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    const bool live = p0 + pl < P;
-    for (int e = e0; e < e1; ++e) {
-        const int buf = (e - e0) & 1;
-        const int4 t = __ldg(tets + e);
-        float rc[12];
-        {
-            const float4* r4 = reinterpret_cast<const float4*>(rec + (size_t)e * 12);
-            const float4 x0 = __ldg(r4), x1 = __ldg(r4 + 1), x2 = __ldg(r4 + 2);
-            rc[0] = x0.x; rc[1] = x0.y; rc[2] = x0.z; rc[3] = x0.w;
-            rc[4] = x1.x; rc[5] = x1.y; rc[6] = x1.z; rc[7] = x1.w;
-            rc[8] = x2.x; rc[9] = x2.y; rc[10] = x2.z; rc[11] = x2.w;
-        }
-        if (live) {
-            int la[4];
-            la[0] = tet_aloc[(size_t)e * 4 + 0];
-            la[1] = tet_aloc[(size_t)e * 4 + 1];
-            la[2] = tet_aloc[(size_t)e * 4 + 2];
-            la[3] = tet_aloc[(size_t)e * 4 + 3];
-            float A[9], dA[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                float du[4], uu[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uu[k] = Us[(la[k] * 3 + a) * GP + pl];
-                    du[k] = Js[((size_t)(la[k] * 3 + a) * GP + pl) * R + b];
-                }
-#pragma unroll
-                for (int c2 = 0; c2 < 3; ++c2) {
-                    A[a * 3 + c2] = (uu[1] - uu[0]) * rc[c2] + (uu[2] - uu[0]) * rc[3 + c2] + (uu[3] - uu[0]) * rc[6 + c2];
-                    dA[a * 3 + c2] = (du[1] - du[0]) * rc[c2] + (du[2] - du[0]) * rc[3 + c2] + (du[3] - du[0]) * rc[6 + c2];
-                }
-            }
-            float F[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
-            float cof[9];
-            cof[0] = F[4] * F[8] - F[7] * F[5];
-            cof[3] = F[7] * F[2] - F[1] * F[8];
-            cof[6] = F[1] * F[5] - F[4] * F[2];
-            cof[1] = F[5] * F[6] - F[8] * F[3];
-            cof[4] = F[8] * F[0] - F[2] * F[6];
-            cof[7] = F[2] * F[3] - F[5] * F[0];
-            cof[2] = F[3] * F[7] - F[6] * F[4];
-            cof[5] = F[6] * F[1] - F[0] * F[7];
-            cof[8] = F[0] * F[4] - F[3] * F[1];
-            const float vol = rc[9], mu = rc[10], lam = rc[11];
-            const float trA = A[0] + A[4] + A[8];
-            float q = 0.f;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) q += A[k] * A[k];
-            const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
-            const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
-                               A[6] * (A[1] * A[5] - A[4] * A[2]);
-            const float jm1 = trA + m2 + detA;
-            const float uI = 4.f + 2.f * trA + q;  // I + 1
-            const float psiI = 0.5f * mu * (1.f - 1.f / uI);
-            const float psiII = 0.5f * mu / (uI * uI);
-            const float psiJ = lam * jm1 - 0.75f * mu;
-            float alpha = 0.f, beta = 0.f;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                alpha += 2.f * F[k] * dA[k];
-                beta += cof[k] * dA[k];
-            }
-            // (dcof F)[dF]: column c of cof is f_i x f_j, (i, j) = (1,2), (2,0), (0,1)
-            float dc[9];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int ci = (c + 1) % 3, cj = (c + 2) % 3;
-                const float a1[3] = {F[ci], F[3 + ci], F[6 + ci]}, a2[3] = {F[cj], F[3 + cj], F[6 + cj]};
-                const float d1[3] = {dA[ci], dA[3 + ci], dA[6 + ci]}, d2[3] = {dA[cj], dA[3 + cj], dA[6 + cj]};
-                dc[0 * 3 + c] = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
-                dc[1 * 3 + c] = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
-                dc[2 * 3 + c] = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
-            }
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                sh_dF[buf][pl][b][k] = dA[k];
-                sh_M[buf][pl][b][k] = 2.f * psiI * dA[k] + psiJ * dc[k];
-            }
-            sh_ab[buf][pl][b][0] = alpha;
-            sh_ab[buf][pl][b][1] = beta;
-            if (b == 0) {
-                sh_sc[buf][pl][0] = vol * psiII;
-                sh_sc[buf][pl][1] = vol * lam;
-                sh_sc[buf][pl][2] = vol;
-                // elastic forces of this tet at this point (cancellation-free P)
-                float cA[9];
-                cA[0] = A[4] * A[8] - A[7] * A[5];
-                cA[3] = A[7] * A[2] - A[1] * A[8];
-                cA[6] = A[1] * A[5] - A[4] * A[2];
-                cA[1] = A[5] * A[6] - A[8] * A[3];
-                cA[4] = A[8] * A[0] - A[2] * A[6];
-                cA[7] = A[2] * A[3] - A[5] * A[0];
-                cA[2] = A[3] * A[7] - A[6] * A[4];
-                cA[5] = A[6] * A[1] - A[0] * A[7];
-                cA[8] = A[0] * A[4] - A[3] * A[1];
-                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
-                float Pst[9];
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int bb = 0; bb < 3; ++bb) {
-                        const float id = a == bb ? 1.f : 0.f;
-                        Pst[a * 3 + bb] = c1 * (A[a * 3 + bb] + A[bb * 3 + a] - trA * id - cA[a * 3 + bb]) +
-                                          c2 * F[a * 3 + bb] + c3 * cof[a * 3 + bb];
-                    }
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    float s0 = 0.f;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float hv = vol * (Pst[a * 3 + 0] * rc[c * 3 + 0] + Pst[a * 3 + 1] * rc[c * 3 + 1] +
-                                                Pst[a * 3 + 2] * rc[c * 3 + 2]);
-                        const int lv = tet_loc[(size_t)e * 4 + c + 1];
-                        if (lv >= 0) accg[(lv * 3 + a) * GP + pl] += hv;
-                        s0 += hv;
-                    }
-                    const int lv0 = tet_loc[(size_t)e * 4];
-                    if (lv0 >= 0) accg[(lv0 * 3 + a) * GP + pl] -= s0;
-                }
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-            const int pp = ppt[k];
-            if (pp >= 0) {
-                const int a = pa[k], bb = pb[k];
-                float s = 0.f;
-#pragma unroll
-                for (int k9 = 0; k9 < 9; ++k9) s += sh_dF[buf][pp][a][k9] * sh_M[buf][pp][bb][k9];
-                cacc[k] += sh_sc[buf][pp][2] * s + sh_sc[buf][pp][0] * sh_ab[buf][pp][a][0] * sh_ab[buf][pp][bb][0] +
-                           sh_sc[buf][pp][1] * sh_ab[buf][pp][a][1] * sh_ab[buf][pp][bb][1];
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < PPT; ++k)
-        if (ppt[k] >= 0) {
-            const int pr = (tid + 128 * k) % NPAIR;
-            Cpart[((size_t)blk * P + p0 + ppt[k]) * NPAIR + pr] = cacc[k];
-        }
-    for (int i = tid; i < nv * 3 * GP; i += 128) {
-        const int pp = i % GP;
-        if (p0 + pp < P) gpart[((size_t)(v0 * 3) + i / GP) * P + p0 + pp] = accg[i];
-    }
 }
 
 // Element Hessian contraction, v2.  CTA = (block of kTB tets, GP = 128/R points);
@@ -1411,13 +1142,6 @@ struct BatchedEngine : BatchedBase {
                                         (int)esmem2), "elem2 smem");
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem2), "elem2 smem");
-        const size_t esmem = (size_t)max_nv * 3 * kEcols * sizeof(float);
-        if (c.precision == LSB_FP64)
-            cuda_check(cudaFuncSetAttribute(elem_batched_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)esmem), "elem smem");
-        else
-            cuda_check(cudaFuncSetAttribute(elem_batched_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)esmem), "elem smem");
         tc.init(c.stream, d_W, n, h, BC, c.num_sms);
     }
 

@@ -322,100 +322,6 @@ static __device__ int lbfgs_control(DevState* st, int r) {
     return 1;
 }
 
-// ---------------------------------------------------------------- K2: output layer forward
-// LPR lanes per row (32-byte vectors), RPW rows per warp step, UNR steps per
-// iteration; lane k < UNR*RPW runs the epilogue of row row0 + k with its
-// per-row vectors prefetched together with W.
-template <typename TS, int HP>
-__global__ void __launch_bounds__(256) out_fwd_kernel(const EvalParams<TS> p) {
-    using V = typename VecT<TS>::type;
-    constexpr int VEC = VecT<TS>::N;
-    constexpr int NVR = HP / VEC;
-    constexpr int LPR = NVR < 32 ? NVR : 32;
-    constexpr int NVL = NVR / LPR;
-    constexpr int RPW = 32 / LPR;
-    constexpr int UNR = NVL >= 2 ? 2 : (RPW >= 4 ? 2 : 4);
-    constexpr int RPI = UNR * RPW;  // rows per warp iteration (<= 32)
-    static_assert(RPI <= 32, "rows per iteration");
-    __shared__ double red[32];
-    const int lane = threadIdx.x & 31;
-    const int sub = lane / LPR, l = lane % LPR;
-    double yv[NVL][VEC];
-#pragma unroll
-    for (int k = 0; k < NVL; ++k)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) yv[k][q] = p.y_last[(l + k * LPR) * VEC + q];
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int tw = (gridDim.x * blockDim.x) >> 5;
-    const V* W = reinterpret_cast<const V*>(p.Wout);
-    const int resident = p.w_resident;
-    const int has_inertia = p.st->has_inertia;
-    const double inv_dt2 = p.st->inv_dt2;
-    const bool ident = p.out_act == kIdentity;
-    double eacc = 0.0;
-    for (int row0 = gw * RPI; row0 < p.n; row0 += tw * RPI) {
-        V w[UNR][NVL];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const int row = row0 + u * RPW + sub;
-            if (row < p.n) {
-#pragma unroll
-                for (int k = 0; k < NVL; ++k) w[u][k] = ld_w(W + (size_t)row * NVR + l + k * LPR, resident);
-            }
-        }
-        // epilogue operands of row row0 + lane
-        const int erow = row0 + lane;
-        const bool eact = lane < RPI && erow < p.n;
-        double eb = 0, es = 0, ec = 0, eut = 0, em = 0;
-        int ev = 0;
-        if (eact) {
-            eb = __ldg(p.bout + erow);
-            es = __ldg(p.sout + erow);
-            ec = __ldg(p.cout + erow);
-            ev = __ldg(p.vfree + erow / 3);
-            if (has_inertia) {
-                eut = p.ut[erow];
-                em = __ldg(p.mass + erow);
-            }
-        }
-        double mine = 0.0;
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            double acc = 0.0;
-            const int row = row0 + u * RPW + sub;
-            if (row < p.n) {
-#pragma unroll
-                for (int k = 0; k < NVL; ++k)
-#pragma unroll
-                    for (int q = 0; q < VEC; ++q) acc = fma((double)w[u][k].v[q], yv[k][q], acc);
-            }
-#pragma unroll
-            for (int o = LPR >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            // row (u, s) lives in lanes s*LPR..; lane k = u*RPW + s takes it
-            const double v = __shfl_sync(0xffffffffu, acc, (lane % RPW) * LPR);
-            if (lane / RPW == u) mine = v;
-        }
-        if (eact) {
-            const double a = mine + eb;
-            double phi = a;
-            if (!ident) {
-                phi = act_eval(p.out_act, a, 0);
-                p.dsout[erow] = es * act_eval(p.out_act, a, 1);
-            }
-            const double uval = es * phi + ec;
-            const int c = erow - 3 * (erow / 3);
-            p.U[(size_t)ev * 4 + c] = uval;
-            if (has_inertia) {
-                const double diff = uval - eut;
-                p.rin[erow] = inv_dt2 * (em * diff);
-                eacc += em * diff * diff;
-            }
-        }
-    }
-    const double tot = block_sum(eacc, red);
-    if (threadIdx.x == 0) p.e_part_out[blockIdx.x] = 0.5 * inv_dt2 * tot;
-}
-
 // ---------------------------------------------------------------- K3: element pass
 template <typename TS>
 __device__ __forceinline__ void load_rec(const TS* rec, size_t e, double* out12);
@@ -570,117 +476,6 @@ __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
         st->need_grad = need;
         if (need) st->grad_evals++;
     }
-}
-
-// ---------------------------------------------------------------- K4: gather + VJP partials
-template <typename TS, int HP>
-__global__ void __launch_bounds__(256) vjp_kernel(const EvalParams<TS> p) {
-    using V = typename VecT<TS>::type;
-    constexpr int VEC = VecT<TS>::N;
-    constexpr int NVR = HP / VEC;
-    constexpr int LPR = NVR < 32 ? NVR : 32;
-    constexpr int NVL = NVR / LPR;
-    constexpr int RPW = 32 / LPR;
-    constexpr int NWARP = 8;
-    extern __shared__ double dsm[];
-    double* wred = dsm;                 // NWARP * HP
-    double* tv = dsm + NWARP * HP;      // 3 * vpb
-    __shared__ int am_grp_last;
-    DevState* st = p.st;
-    if (!st->need_grad) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane / LPR, l = lane % LPR;
-    double acc[NVL][VEC];
-#pragma unroll
-    for (int k = 0; k < NVL; ++k)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[k][q] = 0;
-    const V* W = reinterpret_cast<const V*>(p.Wout);
-    const int resident = p.w_resident;
-    const int nslab = (p.n_free + p.vpb - 1) / p.vpb;
-    const bool ident = p.out_act == kIdentity;
-    const int has_inertia = st->has_inertia;
-    for (int slab = blockIdx.x; slab < nslab; slab += gridDim.x) {
-        const int f0 = slab * p.vpb;
-        const int f1 = min(f0 + p.vpb, p.n_free);
-        const int R = 3 * (f1 - f0);
-        // phase 1: g = sum of incident tet forces (ascending tet id) + inertia, times s
-        for (int t = threadIdx.x; t < R; t += blockDim.x) {
-            const int f = f0 + t / 3, c = t % 3;
-            const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
-            double g = 0;
-#pragma unroll 8
-            for (int k = b; k < e; ++k) g += __ldcg(p.forces + (size_t)__ldg(p.csr_ent + k) * 3 + c);
-            const int row = 3 * f + c;
-            if (has_inertia) g += p.rin[row];
-            tv[t] = g * (ident ? __ldg(p.sout + row) : p.dsout[row]);
-        }
-        __syncthreads();
-        // phase 2: ybar += W_out[rows]^T tv, UNR rows of loads in flight per lane
-        constexpr int UNR = NVL >= 2 ? 2 : 4;
-        for (int rr0 = warp * RPW + sub; rr0 < R; rr0 += NWARP * RPW * UNR) {
-            V w[UNR][NVL];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int rr = rr0 + u * NWARP * RPW;
-                if (rr < R) {
-#pragma unroll
-                    for (int k = 0; k < NVL; ++k) w[u][k] = ld_w(W + ((size_t)3 * f0 + rr) * NVR + l + k * LPR, resident);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int rr = rr0 + u * NWARP * RPW;
-                if (rr < R) {
-                    const double tval = tv[rr];
-#pragma unroll
-                    for (int k = 0; k < NVL; ++k)
-#pragma unroll
-                        for (int q = 0; q < VEC; ++q) acc[k][q] = fma((double)w[u][k].v[q], tval, acc[k][q]);
-                }
-            }
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int k = 0; k < NVL; ++k)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-            double v = acc[k][q];
-            for (int o = LPR; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            acc[k][q] = v;
-        }
-    if (sub == 0) {
-#pragma unroll
-        for (int k = 0; k < NVL; ++k)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) wred[warp * HP + (l + k * LPR) * VEC + q] = acc[k][q];
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < HP; j += blockDim.x) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < NWARP; ++w) s += wred[w * HP + j];
-        p.ybar_part[(size_t)blockIdx.x * HP + j] = s;
-    }
-    // group-last block sums its group's partials in block order
-    __threadfence();
-    __syncthreads();
-    const int grp = blockIdx.x / p.group;
-    const int g0 = grp * p.group, g1 = min(g0 + p.group, (int)gridDim.x);
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(p.grp_cnt + grp, 1u);
-        am_grp_last = (prev == (unsigned)(g1 - g0 - 1));
-    }
-    __syncthreads();
-    if (!am_grp_last) return;
-    __threadfence();
-    for (int j = threadIdx.x; j < HP; j += blockDim.x) {
-        double s = 0.0;
-        for (int b = g0; b < g1; ++b) s += p.ybar_part[(size_t)b * HP + j];
-        p.ybar_grp[(size_t)grp * HP + j] = s;
-    }
-    if (threadIdx.x == 0) p.grp_cnt[grp] = 0;
 }
 
 // cp.async staging of count elements of TS (doubles: stage_doubles; floats: 16-byte granules
