@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <chrono>
+#include <cstddef>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -573,7 +574,19 @@ lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
 }
 
 static void put_zt(Context& c, const double* z) {
-    cuda_check(cudaMemcpyAsync(c.d_state->zt, z, sizeof(double) * c.r, cudaMemcpyHostToDevice, c.stream), "z upload");
+    // staged through the pinned host mirror: a truly asynchronous DMA (pageable sources are
+    // copied synchronously by the driver)
+    if (z != c.h_state->zt) std::memcpy(c.h_state->zt, z, sizeof(double) * c.r);
+    cuda_check(cudaMemcpyAsync(c.d_state->zt, c.h_state->zt, sizeof(double) * c.r, cudaMemcpyHostToDevice, c.stream),
+               "z upload");
+}
+
+// The evaluation result only (configuration + current-evaluation block of DevState:
+// f_eval, status, zt, gz; ~1 KB of the ~20 KB state).
+static void get_eval_result(Context& c) {
+    cuda_check(cudaMemcpyAsync(c.h_state, c.d_state, offsetof(DevState, phase), cudaMemcpyDeviceToHost, c.stream),
+               "eval result");
+    sync(c);
 }
 
 lsb_status lsb_eval(lsb_context* ctx, const double* z, double* value, double* grad) {
@@ -583,7 +596,7 @@ lsb_status lsb_eval(lsb_context* ctx, const double* z, double* value, double* gr
         Context& c = ctx->c;
         put_zt(c, z);
         c.impl->eval(c, grad != nullptr);
-        get_state(c);
+        get_eval_result(c);
         const DevState* s = c.h_state;
         if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
         *value = s->f_eval;
@@ -898,7 +911,7 @@ lsb_status lsb_projective_newton(lsb_context* ctx, double* z, const lsb_solver_c
         auto objective = [&](const std::vector<double>& x, std::vector<double>* g) {
             put_zt(c, x.data());
             c.impl->eval(c, g != nullptr);
-            get_state(c);
+            get_eval_result(c);
             const DevState* s = c.h_state;
             if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
             if (g) {
