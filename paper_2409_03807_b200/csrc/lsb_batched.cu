@@ -450,6 +450,26 @@ __global__ void combine_kernel(int n, int N, const int* vslot_ptr, const int* vs
     }
 }
 
+// combine_kernel with its output written straight into the tcgen05 VJP B operand: T[row][col]
+// as a tf32 hi/lo pair in the K-major core-matrix tiles (B row = col, K = row; lsb_tc.cuh).
+__global__ void combine_pack_kernel(int n, int N, const int* vslot_ptr, const int* vslot, const float* partial,
+                                    const float* rin, int has_inertia, const double* eprow, float* B2) {
+    const size_t total = (size_t)n * N;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int row = (int)(idx / N), col = (int)(idx % N);
+        const int f = row / 3, c = row - 3 * f;
+        double g = 0.0;
+        for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) g += partial[((size_t)vslot[k] * 3 + c) * N + col];
+        if (has_inertia) g += rin[idx];
+        const float x = (float)(g * eprow[(size_t)row * 6 + 1]);
+        const float hi = tc::tf32_rna(x);
+        float* blk = B2 + (size_t)(row / tc::kSliceK) * tc::slice_floats(N);
+        const size_t o = tc::core_off(col, row % tc::kSliceK, N);
+        blk[o] = hi;
+        blk[(size_t)N * tc::kSliceK + o] = x - hi;
+    }
+}
+
 // E[b] = sum of inertia partials + element block partials (fixed order, fp64):
 // block = column; 256 threads stride the partial rows, fixed-tree block sum.
 __global__ void __launch_bounds__(256) energy_reduce_kernel(int N, int nrow_tiles, const double* epart, int nblk,
@@ -1205,11 +1225,16 @@ struct BatchedEngine : BatchedBase {
             energy_reduce_kernel<<<BC, 256, 0, s>>>(BC, e_tiles, d_epart, eb.nblk, d_eblk, has_inertia, d_Eg + c0);
             c.batched_launches += 2;
             if (G) {
-                combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, eb.vslot_ptr, eb.vslot, d_part, d_rin, has_inertia,
-                                                             c.d_eprow, d_T);
-                c.batched_launches += 1;
-                // Ybar[:, c0:c0+BC] = W_out^T T
-                if (!tc.gemm_vjp(s, d_T, d_Ybg + c0, Np)) {
+                // Ybar[:, c0:c0+BC] = W_out^T T: tcgen05 with T packed by the combine, else SGEMM
+                if (tc.enabled) {
+                    combine_pack_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, eb.vslot_ptr, eb.vslot, d_part, d_rin,
+                                                                      has_inertia, c.d_eprow, tc.B2);
+                    tc.gemm_vjp_prepacked(s, d_Ybg + c0, Np);
+                    c.batched_launches += 1;
+                } else {
+                    combine_kernel<<<c.num_sms * 8, 256, 0, s>>>(n, BC, eb.vslot_ptr, eb.vslot, d_part, d_rin,
+                                                                 has_inertia, c.d_eprow, d_T);
+                    c.batched_launches += 1;
                     dim3 g2((BC + 127) / 128, (h + 127) / 128, nk);
                     sgemm_tn_splitk_kernel<<<g2, 256, 0, s>>>(h, BC, n, kchunk, d_W, h, d_T, BC, d_P);
                     splitk_reduce_kernel<<<c.num_sms, 256, 0, s>>>(h * BC, nk, d_P, d_Ybg + c0, BC, Np);

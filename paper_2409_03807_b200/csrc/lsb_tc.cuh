@@ -391,6 +391,7 @@ struct TcGemm {
         A2 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(tc::kTileM) * (size_t)S2));
         B1 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(N) * (size_t)S1));
         B2 = static_cast<float*>(dalloc(sizeof(float) * tc::slice_floats(N) * (size_t)S2));
+        cuda_check(cudaMemsetAsync(B2, 0, sizeof(float) * tc::slice_floats(N) * (size_t)S2, s), "tc B2");  // K padding
         part = static_cast<float*>(dalloc(sizeof(float) * (size_t)jobs2 * tc::kTileM * N));
         // A1: W rows x h (K); A2: W^T = h rows x n (K)
         tc::pack_kernel<<<num_sms * 8, 256, 0, s>>>(W, h, 1, n, h, tc::kTileM, tiles1, S1, A1);
@@ -433,6 +434,17 @@ struct TcGemm {
         tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, eprow, nullptr, U, rin, epart,
                        has_inertia, inv_dt2};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
+        launches += 2;
+        return true;
+    }
+
+    // VJP with B already packed into B2 by the caller (combine_pack_kernel)
+    bool gemm_vjp_prepacked(cudaStream_t s, float* Ybar, int ldo) {
+        if (!enabled) return false;
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                       0.0};
+        tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
+        tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
         launches += 2;
         return true;
     }
