@@ -26,7 +26,7 @@ namespace lsb {
 
 namespace {
 
-constexpr int kBC = 128;       // batch columns per chunk
+constexpr int kBC = 256;       // batch columns per chunk (tcgen05 N)
 constexpr int kEcols = 64;     // columns per element CTA
 constexpr int kTB = 48;        // tets per element block (Hessian path; also the staging capacity)
 constexpr int kTBE = 24;       // tets per element block of the batched evaluation (more CTAs resident)

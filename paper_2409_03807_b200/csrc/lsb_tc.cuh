@@ -34,7 +34,7 @@ namespace tc {
 
 constexpr int kSliceK = 32;  // K elements (fp32 / tf32) per slice
 constexpr int kTileM = 128;
-constexpr int kStages = 3;
+constexpr int kStages = 3;  // maximum ring depth (N = 256 tiles fit 2)
 constexpr int kThreads = 192;
 
 __host__ __device__ constexpr size_t slice_floats(int rows) { return 2 * (size_t)rows * kSliceK; }  // hi + lo
@@ -142,6 +142,7 @@ struct GemmArgs {
     int ldc;         // mode 0: row stride of out
     int m_valid;     // mode 0: valid rows of out
     uint32_t tmem_cols;
+    int stages;  // ring depth (<= kStages, by shared memory)
     // mode 2 (forward with the output-layer epilogue fused): u = s (C + b) + shift - X ->
     // U[slot][col]; inertia residual rin[row][col]; per-column energy partial per 128-row tile
     const double* eprow;  // n x 6 {b, s, shift - X, m, U slot, qbar - X}
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
     const uint32_t a_bytes = (uint32_t)(slice_floats(kTileM) * 4), b_bytes = (uint32_t)(slice_floats(N) * 4);
     const uint32_t stage_bytes = a_bytes + b_bytes;
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < g.stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                 int s0, s1;
                 job_slices(g, j, s0, s1);
                 for (int s = s0; s < s1; ++s, ++it) {
-                    const int st = it % kStages, u = it / kStages;
+                    const int st = it % g.stages, u = it / g.stages;
                     if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
                     unsigned char* sa = smem + (size_t)st * stage_bytes;
                     const size_t a_slice = g.mode != 1 ? (size_t)j * g.S + s : (size_t)s;
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                 int s0, s1;
                 job_slices(g, j, s0, s1);
                 for (int s = s0; s < s1; ++s, ++it) {
-                    const int st = it % kStages;
-                    mbar_wait(&full[st], (it / kStages) & 1);
+                    const int st = it % g.stages;
+                    mbar_wait(&full[st], (it / g.stages) & 1);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)st * stage_bytes);
                     const uint32_t sb = sa + a_bytes;
@@ -366,6 +367,7 @@ struct TcGemm {
     float *A1 = nullptr, *A2 = nullptr, *B1 = nullptr, *B2 = nullptr, *part = nullptr;
     size_t smem = 0;
     uint32_t tmem_cols = 0;
+    int stages = tc::kStages;
     long long launches = 0;
 
     static void* dalloc(size_t bytes) {
@@ -397,8 +399,11 @@ struct TcGemm {
         tc::pack_kernel<<<num_sms * 8, 256, 0, s>>>(W, h, 1, n, h, tc::kTileM, tiles1, S1, A1);
         tc::pack_kernel<<<num_sms * 8, 256, 0, s>>>(W, 1, h, h, n, tc::kTileM, 1, S2, A2);
         cuda_check(cudaGetLastError(), "tc pack W");
-        smem = (size_t)tc::kStages * (tc::slice_floats(tc::kTileM) + tc::slice_floats(N)) * 4;
-        if (smem > 227 * 1024) {
+        stages = tc::kStages;
+        while (stages > 1 && (size_t)stages * (tc::slice_floats(tc::kTileM) + tc::slice_floats(N)) * 4 > 220 * 1024)
+            --stages;
+        smem = (size_t)stages * (tc::slice_floats(tc::kTileM) + tc::slice_floats(N)) * 4;
+        if (stages < 2) {
             release();
             return;
         }
@@ -420,7 +425,7 @@ struct TcGemm {
     bool gemm_out(cudaStream_t s, const float* Y, int ldy, float* C) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
-        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
+        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
@@ -431,8 +436,8 @@ struct TcGemm {
                         double* epart, int has_inertia, double inv_dt2) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
-        tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, eprow, nullptr, U, rin, epart,
-                       has_inertia, inv_dt2};
+        tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, stages, eprow, nullptr, U, rin,
+                       epart, has_inertia, inv_dt2};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
@@ -441,7 +446,7 @@ struct TcGemm {
     // VJP with B already packed into B2 by the caller (combine_pack_kernel)
     bool gemm_vjp_prepacked(cudaStream_t s, float* Ybar, int ldo) {
         if (!enabled) return false;
-        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
                        0.0};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
         tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
@@ -453,7 +458,7 @@ struct TcGemm {
     bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar, int ldo) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 8, 256, 0, s>>>(T, 1, N, N, n, N, 1, S2, B2);
-        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
                        0.0};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
         tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
