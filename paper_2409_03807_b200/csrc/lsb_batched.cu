@@ -454,19 +454,33 @@ __global__ void combine_kernel(int n, int N, const int* vslot_ptr, const int* vs
 // as a tf32 hi/lo pair in the K-major core-matrix tiles (B row = col, K = row; lsb_tc.cuh).
 __global__ void combine_pack_kernel(int n, int N, const int* vslot_ptr, const int* vslot, const float* partial,
                                     const float* rin, int has_inertia, const double* eprow, float* B2) {
-    const size_t total = (size_t)n * N;
+    // thread = (4 consecutive rows = one 16-byte core-matrix chunk, column): the hi and lo
+    // chunks are float4 stores, contiguous across adjacent columns; partial reads stay
+    // coalesced over columns
+    const int nq = (n + 3) / 4;
+    const size_t total = (size_t)nq * N;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const int row = (int)(idx / N), col = (int)(idx % N);
-        const int f = row / 3, c = row - 3 * f;
-        double g = 0.0;
-        for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) g += partial[((size_t)vslot[k] * 3 + c) * N + col];
-        if (has_inertia) g += rin[idx];
-        const float x = (float)(g * eprow[(size_t)row * 6 + 1]);
-        const float hi = tc::tf32_rna(x);
-        float* blk = B2 + (size_t)(row / tc::kSliceK) * tc::slice_floats(N);
-        const size_t o = tc::core_off(col, row % tc::kSliceK, N);
-        blk[o] = hi;
-        blk[(size_t)N * tc::kSliceK + o] = x - hi;
+        const int q4 = (int)(idx / N), col = (int)(idx % N);
+        float hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int row = 4 * q4 + e;
+            float x = 0.f;
+            if (row < n) {
+                const int f = row / 3, c = row - 3 * f;
+                double g = 0.0;
+                for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) g += partial[((size_t)vslot[k] * 3 + c) * N + col];
+                if (has_inertia) g += rin[(size_t)row * N + col];
+                x = (float)(g * eprow[(size_t)row * 6 + 1]);
+            }
+            hi[e] = tc::tf32_rna(x);
+            lo[e] = x - hi[e];
+        }
+        const int row0 = 4 * q4;
+        float* blk = B2 + (size_t)(row0 / tc::kSliceK) * tc::slice_floats(N);
+        const size_t o = tc::core_off(col, row0 % tc::kSliceK, N);  // 16-byte aligned chunk of 4 rows
+        *reinterpret_cast<float4*>(blk + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(blk + (size_t)N * tc::kSliceK + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
     }
 }
 
