@@ -966,6 +966,11 @@ struct BatchedEngine : BatchedBase {
     double *d_Ch = nullptr, *d_H = nullptr;
     float* d_rinh = nullptr;  // inertia residual of the objective Hessian (n x PH)
     int hcols = 0;
+    struct PackedLayer {
+        float* A = nullptr;
+        int tiles = 0, S = 0;
+    };
+    std::vector<PackedLayer> hA;  // hidden weights as tcgen05 A tiles (tangent GEMMs)
 
     ~BatchedEngine() override {
         tc.release();
@@ -1305,6 +1310,17 @@ struct BatchedEngine : BatchedBase {
             for (double v : c.layers[l].W) wf[off++] = (float)v;
         d_Whf = alloc<float>(std::max<size_t>(1, wtot));
         if (wtot) c.copy(d_Whf, wf.data(), 4 * wtot, cudaMemcpyHostToDevice, "Whf");
+        if (tc.enabled) {
+            size_t wo = 0;
+            hA.resize(c.nhid);
+            for (int l = 0; l < c.nhid; ++l) {
+                const int R = c.hrows[l], K = c.hcols[l];
+                hA[l].A = alloc<float>(TcGemm::packed_a_floats(R, K));
+                tc.pack_a(c.stream, d_Whf + wo, R, K, hA[l].A, hA[l].tiles, hA[l].S);
+                wo += (size_t)R * K;
+            }
+            cuda_check(cudaGetLastError(), "pack hidden");
+        }
         d_X[0] = alloc<float>((size_t)hmax * PH * hcols);
         d_X[1] = alloc<float>((size_t)hmax * PH * hcols);
         d_Q = alloc<float>((size_t)hmax * PH * hcols);
@@ -1365,15 +1381,19 @@ struct BatchedEngine : BatchedBase {
         size_t woff = 0;
         for (int l = 0; l < c.nhid; ++l) {
             const int R = c.hrows[l], K = c.hcols[l];
-            dim3 g((P * cols + 127) / 128, (R + 127) / 128);
-            sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_X[cur], P * cols, d_Q, P * cols);
+            if (!tc.enabled ||
+                !tc.gemm_general(s, hA[l].A, hA[l].tiles, hA[l].S, R, d_X[cur], P * cols, K, P * cols, d_Q, P * cols)) {
+                dim3 g((P * cols + 127) / 128, (R + 127) / 128);
+                sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_X[cur], P * cols, d_Q, P * cols);
+            }
             tangent_act_kernel<<<c.num_sms * 8, 256, 0, s>>>(R, P, r, cols, d_Q, c.d_bh + c.boff[l], c.hact[l], d_X[cur ^ 1]);
             woff += (size_t)R * K;
             cur ^= 1;
         }
         const float* XL = d_X[cur];
         tangent_pack_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, XL, d_Bt);
-        {
+        if (!tc.enabled ||
+            !tc.gemm_general(s, tc.A1, tc.tiles1, tc.S1, n, d_Bt, P * (1 + r), h, P * (1 + r), d_Ct, P * (1 + r))) {
             dim3 g((P * (1 + r) + 127) / 128, (n + 127) / 128);
             sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (1 + r), h, d_W, h, d_Bt, P * (1 + r), d_Ct, P * (1 + r));
         }

@@ -143,6 +143,8 @@ struct GemmArgs {
     int m_valid;     // mode 0: valid rows of out
     uint32_t tmem_cols;
     int stages;  // ring depth (<= kStages, by shared memory)
+    int ntn;     // mode 3: N tiles per M tile (job j -> M tile j / ntn, N tile j % ntn)
+    int ncols;   // mode 3: valid output columns
     // mode 2 (forward with the output-layer epilogue fused): u = s (C + b) + shift - X ->
     // U[slot][col]; inertia residual rin[row][col]; per-column energy partial per 128-row tile
     const double* eprow;  // n x 6 {b, s, shift - X, m, U slot, qbar - X}
@@ -209,10 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                     const int st = it % g.stages, u = it / g.stages;
                     if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
                     unsigned char* sa = smem + (size_t)st * stage_bytes;
-                    const size_t a_slice = g.mode != 1 ? (size_t)j * g.S + s : (size_t)s;
+                    const size_t a_slice = g.mode == 3 ? (size_t)(j / g.ntn) * g.S + s
+                                           : (g.mode != 1 ? (size_t)j * g.S + s : (size_t)s);
+                    const size_t b_slice = g.mode == 3 ? (size_t)(j % g.ntn) * g.S + s : (size_t)s;
                     mbar_expect_tx(&full[st], stage_bytes);
                     tma_load_1d(sa, g.A + a_slice * slice_floats(kTileM), a_bytes, &full[st], pol_a);
-                    tma_load_1d(sa + a_bytes, g.B + (size_t)s * slice_floats(N), b_bytes, &full[st], pol_b);
+                    tma_load_1d(sa + a_bytes, g.B + b_slice * slice_floats(N), b_bytes, &full[st], pol_b);
                 }
             }
         }
@@ -319,6 +323,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                     esum_s[warp][c0 + lane] = e[0];
                     continue;
                 }
+                if (g.mode == 3) {  // general tile grid, masked columns
+                    const int grow = (j / g.ntn) * kTileM + row;
+                    const int col0 = (j % g.ntn) * N + c0;
+                    if (grow < g.m_valid) {
+                        float* d3 = g.out + (size_t)grow * g.ldc + col0;
+                        if (col0 + 32 <= g.ncols && (g.ldc & 3) == 0) {
+#pragma unroll
+                            for (int i = 0; i < 32; i += 4)
+                                *reinterpret_cast<float4*>(d3 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        } else {
+                            for (int i = 0; i < 32 && col0 + i < g.ncols; ++i) d3[i] = v[i];
+                        }
+                    }
+                    continue;
+                }
                 float* dst;
                 if (g.mode == 0) {
                     const int grow = j * kTileM + row;
@@ -415,6 +434,9 @@ struct TcGemm {
         enabled = true;
     }
     void release() {
+        if (Bg) cudaFree(Bg);
+        Bg = nullptr;
+        Bg_floats = 0;
         for (float* p : {A1, A2, B1, B2, part})
             if (p) cudaFree(p);
         A1 = A2 = B1 = B2 = part = nullptr;
@@ -425,7 +447,7 @@ struct TcGemm {
     bool gemm_out(cudaStream_t s, const float* Y, int ldy, float* C) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
-        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
+        tc::GemmArgs a{A1, B1, C, 0, tiles1, S1, N, N, n, tmem_cols, stages, 1, N, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
@@ -436,18 +458,51 @@ struct TcGemm {
                         double* epart, int has_inertia, double inv_dt2) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 2, 256, 0, s>>>(Y, 1, ldy, N, h, N, 1, S1, B1);
-        tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, stages, eprow, nullptr, U, rin,
-                       epart, has_inertia, inv_dt2};
+        tc::GemmArgs a{A1, B1, nullptr, 2, tiles1, S1, N, N, n, tmem_cols, stages, 1, N, eprow, nullptr, U,
+                       rin, epart, has_inertia, inv_dt2};
         tc::gemm3_kernel<<<std::min(tiles1, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
     }
 
+    // General C (M x ncols, row stride ldc) = A B on a tile grid: A pre-tiled (tiles_m x S slices,
+    // pack_rows), B feature-major (K x ncols, row stride ldb) packed here into 256-column tiles.
+    float* Bg = nullptr;
+    size_t Bg_floats = 0;
+    bool gemm_general(cudaStream_t s, const float* Apacked, int tiles_m, int S, int m_valid, const float* B, int ldb,
+                      int K, int ncols, float* C, int ldc) {
+        if (!enabled || N != 256) return false;
+        const int ntn = (ncols + N - 1) / N;
+        const size_t need = (size_t)ntn * S * tc::slice_floats(N);
+        if (need > Bg_floats) {
+            if (Bg) cudaFree(Bg);
+            Bg = static_cast<float*>(dalloc(sizeof(float) * need));
+            Bg_floats = need;
+        }
+        tc::pack_kernel<<<sms * 8, 256, 0, s>>>(B, 1, ldb, ncols, K, N, ntn, S, Bg);
+        tc::GemmArgs a{Apacked, Bg, C, 3, tiles_m * ntn, S, N, ldc, m_valid, tmem_cols, stages, ntn, ncols,
+                       nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
+        tc::gemm3_kernel<<<std::min(tiles_m * ntn, sms), tc::kThreads, smem, s>>>(a);
+        launches += 2;
+        return true;
+    }
+    // Pack a row-major fp32 matrix (rows x K) as A tiles (128-row tiles, S = ceil(K / 32)
+    // slices) into dst, which holds packed_a_floats(rows, K) floats.
+    static size_t packed_a_floats(int rows, int K) {
+        return tc::slice_floats(tc::kTileM) * (size_t)((rows + tc::kTileM - 1) / tc::kTileM) *
+               ((K + tc::kSliceK - 1) / tc::kSliceK);
+    }
+    void pack_a(cudaStream_t s, const float* W, int rows, int K, float* dst, int& tiles_m, int& S) const {
+        tiles_m = (rows + tc::kTileM - 1) / tc::kTileM;
+        S = (K + tc::kSliceK - 1) / tc::kSliceK;
+        tc::pack_kernel<<<sms * 4, 256, 0, s>>>(W, K, 1, rows, K, tc::kTileM, tiles_m, S, dst);
+    }
+
     // VJP with B already packed into B2 by the caller (combine_pack_kernel)
     bool gemm_vjp_prepacked(cudaStream_t s, float* Ybar, int ldo) {
         if (!enabled) return false;
-        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-                       0.0};
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, 1, N, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       0, 0.0};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
         tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
         launches += 2;
@@ -458,8 +513,8 @@ struct TcGemm {
     bool gemm_vjp(cudaStream_t s, const float* T, float* Ybar, int ldo) {
         if (!enabled) return false;
         tc::pack_kernel<<<sms * 8, 256, 0, s>>>(T, 1, N, N, n, N, 1, S2, B2);
-        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-                       0.0};
+        tc::GemmArgs a{A2, B2, part, 1, jobs2, S2, N, 0, 0, tmem_cols, stages, 1, N, nullptr, nullptr, nullptr, nullptr, nullptr,
+                       0, 0.0};
         tc::gemm3_kernel<<<jobs2, tc::kThreads, smem, s>>>(a);
         tc::reduce_parts_kernel<<<sms * 2, 256, 0, s>>>(part, jobs2, h, N, Ybar, ldo);
         launches += 3;
