@@ -998,4 +998,428 @@ double lipschitz_loss2(const Model& model, const Mesh& mesh, const Material& mat
     return total / static_cast<double>(P);
 }
 
+
+// ---------------------------------------------------------------- third derivatives (energy.cpp)
+namespace {
+
+// kj_det3 (energy.cpp:55-65) for a matrix given by its columns x[0..2]: the 9 x 9 block
+// matrix of skew(column) blocks (vec index a + 3 b).
+void kj_det3_cols(const double x[3][3], double* KJ) {
+    for (int i = 0; i < 81; ++i) KJ[i] = 0.0;
+    skew(x[2], -1.0, KJ, 9, 0, 3);
+    skew(x[1], 1.0, KJ, 9, 0, 6);
+    skew(x[2], 1.0, KJ, 9, 3, 0);
+    skew(x[0], -1.0, KJ, 9, 3, 6);
+    skew(x[1], -1.0, KJ, 9, 6, 0);
+    skew(x[0], 1.0, KJ, 9, 6, 3);
+}
+
+// The element quantities of element_snh (energy.cpp:280-298) plus psiIII (snh_core :216).
+struct SnhFrame {
+    double gI[9], gJ[9], KJ[81], B[108];
+    double psiI, psiII, psiIII, psiJ, psiJJ, vol;
+};
+
+void snh_frame(const Mesh& m, double mu, double lambda, int e, const double* positions, SnhFrame& o) {
+    const int* t = &m.T[4 * e];
+    const double* dminv = &m.Dminv[9 * static_cast<size_t>(e)];
+    double ds[9], dd[9];
+    for (int c = 0; c < 3; ++c)
+        for (int a = 0; a < 3; ++a) {
+            const double xs = positions[3 * t[c + 1] + a] - positions[3 * t[0] + a];
+            const double xr = m.X[3 * t[c + 1] + a] - m.X[3 * t[0] + a];
+            ds[a * 3 + c] = xs;
+            dd[a * 3 + c] = xs - xr;
+        }
+    double F[9], A[9];
+    matmul3(dd, dminv, A);
+    matmul3(ds, dminv, F);
+    const double de = 3.0, acoef = de / (de + 1.0);
+    const double trA = A[0] + A[4] + A[8];
+    double sqA = 0.0;
+    for (int i = 0; i < 9; ++i) sqA += A[i] * A[i];
+    const double i_minus = 2.0 * trA + sqA;
+    const double m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+    const double jm1 = trA + m2 + det3(A);
+    const double u = de + i_minus + 1.0;
+    o.psiI = 0.5 * mu * (1.0 - 1.0 / u);
+    o.psiII = 0.5 * mu / (u * u);
+    o.psiIII = -mu / (u * u * u);
+    o.psiJ = lambda * jm1 - acoef * mu;
+    o.psiJJ = lambda;
+    double f[3][3];
+    for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+            f[b][a] = F[a * 3 + b];
+            o.gI[a + 3 * b] = 2.0 * F[a * 3 + b];
+        }
+    auto cross = [](const double* x, const double* y, double* out) {
+        out[0] = x[1] * y[2] - x[2] * y[1];
+        out[1] = x[2] * y[0] - x[0] * y[2];
+        out[2] = x[0] * y[1] - x[1] * y[0];
+    };
+    cross(f[1], f[2], &o.gJ[0]);
+    cross(f[2], f[0], &o.gJ[3]);
+    cross(f[0], f[1], &o.gJ[6]);
+    kj_det3_cols(f, o.KJ);
+    for (int i = 0; i < 108; ++i) o.B[i] = 0.0;
+    for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+            const int fidx = a + 3 * b;
+            for (int c = 0; c < 3; ++c) {
+                o.B[fidx * 12 + (c + 1) * 3 + a] += dminv[c * 3 + b];
+                o.B[fidx * 12 + a] -= dminv[c * 3 + b];
+            }
+        }
+    o.vol = m.vol[e];
+}
+
+}  // namespace
+
+void element_third_contraction(const Mesh& m, double mu, double lambda, int e, const double* positions,
+                               const double* M_local, double* out12) {
+    // snh_third_contraction (energy.cpp:303-320): grad_x <H_e(x), M>, M symmetric 12 x 12.
+    SnhFrame c;
+    snh_frame(m, mu, lambda, e, positions, c);
+    double BM[9 * 12], MF[81];  // MF = B M B^T
+    for (int i = 0; i < 9; ++i)
+        for (int j = 0; j < 12; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 12; ++k) s += c.B[i * 12 + k] * M_local[k * 12 + j];
+            BM[i * 12 + j] = s;
+        }
+    for (int i = 0; i < 9; ++i)
+        for (int j = 0; j < 9; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 12; ++k) s += BM[i * 12 + k] * c.B[j * 12 + k];
+            MF[i * 9 + j] = s;
+        }
+    double trM = 0.0, qII = 0.0, kJM = 0.0, MgI[9], MgJ[9];
+    for (int i = 0; i < 9; ++i) {
+        trM += MF[i * 9 + i];
+        double s1 = 0.0, s2 = 0.0;
+        for (int j = 0; j < 9; ++j) {
+            s1 += MF[i * 9 + j] * c.gI[j];
+            s2 += MF[i * 9 + j] * c.gJ[j];
+            kJM += c.KJ[i * 9 + j] * MF[i * 9 + j];
+        }
+        MgI[i] = s1;
+        MgJ[i] = s2;
+    }
+    for (int i = 0; i < 9; ++i) qII += c.gI[i] * MgI[i];
+    // j_third (energy.cpp:120-131), 3D: g[i + 3 j] = <kj_det3(E_ij), MF>
+    double j3[9];
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) {
+            double basis[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+            basis[j][i] = 1.0;  // column j, row i
+            double K[81];
+            kj_det3_cols(basis, K);
+            double s = 0.0;
+            for (int k = 0; k < 81; ++k) s += K[k] * MF[k];
+            j3[i + 3 * j] = s;
+        }
+    double v[9];
+    for (int i = 0; i < 9; ++i) {
+        double kjmgj = 0.0;
+        for (int j = 0; j < 9; ++j) kjmgj += c.KJ[i * 9 + j] * MgJ[j];
+        v[i] = c.psiIII * qII * c.gI[i] + 4.0 * c.psiII * MgI[i] + 2.0 * c.psiJJ * kjmgj +
+               2.0 * trM * c.psiII * c.gI[i] + c.psiJJ * kJM * c.gJ[i] + c.psiJ * j3[i];
+    }
+    for (int j = 0; j < 12; ++j) {
+        double s = 0.0;
+        for (int i = 0; i < 9; ++i) s += c.B[i * 12 + j] * v[i];
+        out12[j] = c.vol * s;
+    }
+}
+
+void elastic_third_contraction(const Mesh& m, const Material& mat, const std::vector<double>& positions,
+                               const std::vector<double>& A, const std::vector<double>& B, int k,
+                               std::vector<double>& qbar, const std::vector<int>* ids,
+                               const std::vector<double>* w) {
+    // energy.cpp:495-510: M_e = (A_e B_e^T + B_e A_e^T) / 2, qbar += w_e local.
+    const int count = ids ? static_cast<int>(ids->size()) : m.E;
+    std::vector<double> Ae(12 * static_cast<size_t>(k)), Be(12 * static_cast<size_t>(k));
+    double M[144], local[12];
+    for (int kk = 0; kk < count; ++kk) {
+        const int e = ids ? (*ids)[kk] : kk;
+        const double we = ids ? (*w)[kk] : 1.0;
+        int map[12];
+        for (int v = 0; v < 4; ++v) {
+            const int f = m.free_index[m.T[4 * e + v]];
+            for (int c = 0; c < 3; ++c) map[3 * v + c] = f < 0 ? -1 : 3 * f + c;
+        }
+        for (int i = 0; i < 12; ++i)
+            for (int j = 0; j < k; ++j) {
+                Ae[i * k + j] = map[i] >= 0 ? A[static_cast<size_t>(map[i]) * k + j] : 0.0;
+                Be[i * k + j] = map[i] >= 0 ? B[static_cast<size_t>(map[i]) * k + j] : 0.0;
+            }
+        for (int i = 0; i < 12; ++i)
+            for (int j = 0; j < 12; ++j) {
+                double s = 0.0;
+                for (int l = 0; l < k; ++l) s += Ae[i * k + l] * Be[j * k + l] + Be[i * k + l] * Ae[j * k + l];
+                M[i * 12 + j] = 0.5 * s;
+            }
+        element_third_contraction(m, mat.mu[e], mat.lambda[e], e, positions.data(), M, local);
+        for (int i = 0; i < 12; ++i)
+            if (map[i] >= 0) qbar[map[i]] += we * local[i];
+    }
+}
+
+// ---------------------------------------------------------------- theta gradient (losses.cpp, tape.cpp)
+namespace {
+
+// One point's forward trace: tape_decode with want_jacobian (losses.cpp:56-85) and every
+// tape_second_directional (losses.cpp:105-118) for the pairs c <= d.
+struct PointTrace {
+    std::vector<std::vector<double>> y;     // y[l + 1] = layer l output; y[0] = z
+    std::vector<std::vector<double>> a;     // pre-activations
+    std::vector<std::vector<double>> G;     // G[l + 1] (rows x r); G[0] = I
+    std::vector<std::vector<double>> ahat;  // W_l G[l]
+    std::vector<std::vector<std::vector<double>>> S;  // S[l + 1][pair]; S[0] = 0
+    std::vector<std::vector<double>> Ws;    // W_l S[l][pair] (per layer, pair-major rows x npair)
+    std::vector<double> q, J;               // n, n x r
+};
+
+void trace_point(const Model& model, const std::vector<double>& z, PointTrace& t) {
+    const int r = model.r, L = static_cast<int>(model.dec.size()), np = r * (r + 1) / 2;
+    t.y.assign(1, z);
+    t.G.assign(1, std::vector<double>(static_cast<size_t>(r) * r, 0.0));
+    for (int i = 0; i < r; ++i) t.G[0][static_cast<size_t>(i) * r + i] = 1.0;
+    t.S.assign(1, std::vector<std::vector<double>>(np, std::vector<double>(r, 0.0)));
+    t.a.clear();
+    t.ahat.clear();
+    t.Ws.clear();
+    for (int l = 0; l < L; ++l) {
+        const Layer& ly = model.dec[l];
+        const int R = ly.rows, K = ly.cols;
+        std::vector<double> a = matvec(ly, t.y[l]), y(R), ah(static_cast<size_t>(R) * r, 0.0),
+            G(static_cast<size_t>(R) * r), Ws(static_cast<size_t>(R) * np, 0.0);
+        for (int i = 0; i < R; ++i) {
+            a[i] += ly.b[i];
+            y[i] = activation_eval(ly.act, a[i], 0);
+            for (int k = 0; k < K; ++k) {
+                const double w = ly.W[static_cast<size_t>(i) * K + k];
+                for (int c = 0; c < r; ++c) ah[static_cast<size_t>(i) * r + c] += w * t.G[l][static_cast<size_t>(k) * r + c];
+                for (int s = 0; s < np; ++s) Ws[static_cast<size_t>(i) * np + s] += w * t.S[l][s][k];
+            }
+            const double d1 = activation_eval(ly.act, a[i], 1);
+            for (int c = 0; c < r; ++c) G[static_cast<size_t>(i) * r + c] = ah[static_cast<size_t>(i) * r + c] * d1;
+        }
+        std::vector<std::vector<double>> S(np, std::vector<double>(R));
+        for (int i = 0; i < R; ++i) {
+            const double d1 = activation_eval(ly.act, a[i], 1), d2 = activation_eval(ly.act, a[i], 2);
+            int s = 0;
+            for (int c = 0; c < r; ++c)
+                for (int d = c; d < r; ++d, ++s)
+                    S[s][i] = d2 * (ah[static_cast<size_t>(i) * r + c] * ah[static_cast<size_t>(i) * r + d]) +
+                              d1 * Ws[static_cast<size_t>(i) * np + s];
+        }
+        t.a.push_back(std::move(a));
+        t.y.push_back(std::move(y));
+        t.ahat.push_back(std::move(ah));
+        t.G.push_back(std::move(G));
+        t.Ws.push_back(std::move(Ws));
+        t.S.push_back(std::move(S));
+    }
+    const int n = model.n;
+    t.q.resize(n);
+    t.J.resize(static_cast<size_t>(n) * r);
+    for (int i = 0; i < n; ++i) {
+        t.q[i] = t.y[L][i] * model.scale[i] + model.shift[i];
+        for (int c = 0; c < r; ++c) t.J[static_cast<size_t>(i) * r + c] = t.G[L][static_cast<size_t>(i) * r + c] * model.scale[i];
+    }
+}
+
+// Per point: H (tape_reduced_derivative order 2, losses.cpp:136-146) and the state its
+// backward needs.
+struct PointState {
+    PointTrace tr;
+    std::vector<double> X, g, HJ, H;  // positions, grad P, K J, H (r x r)
+};
+
+void point_forward(const Model& model, const Mesh& mesh, const Material& mat, const std::vector<double>& pins,
+                   const std::vector<double>& z, PointState& st) {
+    const int r = model.r, n = model.n, L = static_cast<int>(model.dec.size());
+    trace_point(model, z, st.tr);
+    st.X = dof_unpack(mesh, st.tr.q, pins);
+    st.g = assemble(mesh, mat, st.tr.q, pins).gradient;        // potential_gradient (tape.cpp:245-260)
+    st.HJ.assign(static_cast<size_t>(n) * r, 0.0);            // potential_hessian_apply (tape.cpp:262-279)
+    elastic_hessian_apply(mesh, mat, st.X, st.tr.J, r, st.HJ);
+    st.H.assign(static_cast<size_t>(r) * r, 0.0);
+    for (int i = 0; i < n; ++i)                               // matmul_tn(J, hj)
+        for (int a = 0; a < r; ++a)
+            for (int b = 0; b < r; ++b)
+                st.H[a * r + b] += st.tr.J[static_cast<size_t>(i) * r + a] * st.HJ[static_cast<size_t>(i) * r + b];
+    int s = 0;
+    for (int a = 0; a < r; ++a)
+        for (int b = a; b < r; ++b, ++s) {  // dot(g, s_ab), symmetric_from_entries
+            double v = 0.0;
+            for (int i = 0; i < n; ++i) v += st.g[i] * st.tr.S[L][s][i] * model.scale[i];
+            st.H[a * r + b] += v;
+            if (a != b) st.H[b * r + a] += v;
+        }
+}
+
+// Reverse sweep of one point's H with adjoint Hbar (r x r), accumulating dL/dtheta.
+void point_backward(const Model& model, const Mesh& mesh, const Material& mat, const PointState& st,
+                    const std::vector<double>& Hbar, std::vector<std::vector<double>>& gW,
+                    std::vector<std::vector<double>>& gb) {
+    const int r = model.r, n = model.n, L = static_cast<int>(model.dec.size()), np = r * (r + 1) / 2;
+    const PointTrace& tr = st.tr;
+    // symmetric_from_entries backward (tape.cpp:212-222)
+    std::vector<double> ebar(np);
+    {
+        int s = 0;
+        for (int a = 0; a < r; ++a)
+            for (int b = a; b < r; ++b, ++s) ebar[s] = Hbar[a * r + b] + (a != b ? Hbar[b * r + a] : 0.0);
+    }
+    // matmul_tn(J, hj) backward (tape.cpp:162-167): Jbar = hj Hbar^T, hjbar = J Hbar
+    std::vector<double> Jbar(static_cast<size_t>(n) * r, 0.0), hjbar(static_cast<size_t>(n) * r, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int a = 0; a < r; ++a) {
+            double s1 = 0.0, s2 = 0.0;
+            for (int b = 0; b < r; ++b) {
+                s1 += st.HJ[static_cast<size_t>(i) * r + b] * Hbar[a * r + b];
+                s2 += tr.J[static_cast<size_t>(i) * r + b] * Hbar[b * r + a];
+            }
+            Jbar[static_cast<size_t>(i) * r + a] = s1;
+            hjbar[static_cast<size_t>(i) * r + a] = s2;
+        }
+    // potential_hessian_apply backward (tape.cpp:271-277): Ybar += H hjbar; qbar += third(J, hjbar)
+    elastic_hessian_apply(mesh, mat, st.X, hjbar, r, Jbar);
+    std::vector<double> qbar(n, 0.0);
+    elastic_third_contraction(mesh, mat, st.X, tr.J, hjbar, r, qbar);
+    // dot(g, s_ab) backward: gbar = sum ebar s_ab; sbar_ab = ebar g
+    std::vector<double> gbar(n, 0.0);
+    for (int s = 0; s < np; ++s)
+        for (int i = 0; i < n; ++i) gbar[i] += ebar[s] * tr.S[L][s][i] * model.scale[i];
+    // potential_gradient backward (tape.cpp:254-259): qbar += H gbar
+    elastic_hessian_apply(mesh, mat, st.X, gbar, 1, qbar);
+    // decoder: q = y_L * scale + shift, J = G_L * scale, s_ab = S_L * scale
+    std::vector<double> ybar(n), Gbar(static_cast<size_t>(n) * r);
+    std::vector<std::vector<double>> Sbar(np, std::vector<double>(n));
+    for (int i = 0; i < n; ++i) {
+        ybar[i] = qbar[i] * model.scale[i];
+        for (int c = 0; c < r; ++c) Gbar[static_cast<size_t>(i) * r + c] = Jbar[static_cast<size_t>(i) * r + c] * model.scale[i];
+        for (int s = 0; s < np; ++s) Sbar[s][i] = ebar[s] * st.g[i] * model.scale[i];
+    }
+    for (int l = L - 1; l >= 0; --l) {
+        const Layer& ly = model.dec[l];
+        const int R = ly.rows, K = ly.cols;
+        std::vector<double>& W = gW[l];
+        std::vector<double>& bv = gb[l];
+        std::vector<double> abar(R, 0.0), ahbar(static_cast<size_t>(R) * r, 0.0);
+        std::vector<std::vector<double>> Sprev(np, std::vector<double>(K, 0.0));
+        for (int i = 0; i < R; ++i) {
+            const double ai = tr.a[l][i];
+            const double d1 = activation_eval(ly.act, ai, 1), d2 = activation_eval(ly.act, ai, 2),
+                         d3 = activation_eval(ly.act, ai, 3);
+            // second directional recurrence (losses.cpp:111-116) backward, every pair
+            int s = 0;
+            for (int c = 0; c < r; ++c)
+                for (int d = c; d < r; ++d, ++s) {
+                    const double tb = Sbar[s][i];
+                    if (tb == 0.0) continue;
+                    const double pc = tr.ahat[l][static_cast<size_t>(i) * r + c], pd = tr.ahat[l][static_cast<size_t>(i) * r + d];
+                    abar[i] += tb * pc * pd * d3 + tb * tr.Ws[l][static_cast<size_t>(i) * np + s] * d2;
+                    ahbar[static_cast<size_t>(i) * r + c] += tb * d2 * pd;
+                    ahbar[static_cast<size_t>(i) * r + d] += tb * d2 * pc;
+                    const double u = tb * d1;  // carried = d1 * (W s_prev)
+                    for (int k = 0; k < K; ++k) {
+                        W[static_cast<size_t>(i) * K + k] += u * tr.S[l][s][k];
+                        Sprev[s][k] += ly.W[static_cast<size_t>(i) * K + k] * u;
+                    }
+                }
+            // G = ahat * d1 (losses.cpp:75-78)
+            double gsum = 0.0;
+            for (int c = 0; c < r; ++c) {
+                const double gb_ = Gbar[static_cast<size_t>(i) * r + c];
+                ahbar[static_cast<size_t>(i) * r + c] += gb_ * d1;
+                gsum += gb_ * tr.ahat[l][static_cast<size_t>(i) * r + c];
+            }
+            abar[i] += gsum * d2 + ybar[i] * d1;  // d1 = act'(a); y = act(a)
+        }
+        // ahat = W G_prev; a = W y_prev + b
+        std::vector<double> Gprev(static_cast<size_t>(K) * r, 0.0), yprev(K, 0.0);
+        for (int i = 0; i < R; ++i) {
+            bv[i] += abar[i];
+            for (int k = 0; k < K; ++k) {
+                double s = abar[i] * tr.y[l][k];
+                for (int c = 0; c < r; ++c) s += ahbar[static_cast<size_t>(i) * r + c] * tr.G[l][static_cast<size_t>(k) * r + c];
+                W[static_cast<size_t>(i) * K + k] += s;
+                const double w = ly.W[static_cast<size_t>(i) * K + k];
+                yprev[k] += w * abar[i];
+                for (int c = 0; c < r; ++c) Gprev[static_cast<size_t>(k) * r + c] += w * ahbar[static_cast<size_t>(i) * r + c];
+            }
+        }
+        ybar = std::move(yprev);
+        Gbar = std::move(Gprev);
+        Sbar = std::move(Sprev);
+    }
+}
+
+}  // namespace
+
+double lipschitz_loss2_grad(const Model& model, const Mesh& mesh, const Material& mat,
+                            const std::vector<double>& pin_positions, int P, const double* Z1, const double* Z2,
+                            std::vector<std::vector<double>>& gW, std::vector<std::vector<double>>& gb,
+                            int nthreads) {
+    // build_lipschitz_loss (losses.cpp:196-213) order 2 + Tape::backward (tape.cpp:46-59).
+    if (P <= 0) throw std::invalid_argument("lipschitz loss: no pairs");
+    const int r = model.r, L = static_cast<int>(model.dec.size());
+    for (int p = 0; p < P; ++p) {
+        double dz2 = 0.0;
+        for (int c = 0; c < r; ++c) dz2 += (Z1[p * r + c] - Z2[p * r + c]) * (Z1[p * r + c] - Z2[p * r + c]);
+        if (dz2 <= 0.0) throw std::invalid_argument("lipschitz loss: coincident pair");
+    }
+    nthreads = std::max(1, std::min(nthreads, P));
+    std::vector<double> terms(P, 0.0);
+    std::vector<std::vector<std::vector<double>>> tW(nthreads), tb(nthreads);
+    for (int k = 0; k < nthreads; ++k)
+        for (int l = 0; l < L; ++l) {
+            tW[k].emplace_back(model.dec[l].W.size(), 0.0);
+            tb[k].emplace_back(model.dec[l].b.size(), 0.0);
+        }
+    auto work = [&](int k, int p0, int p1) {
+        PointState s1, s2;
+        std::vector<double> Hbar(static_cast<size_t>(r) * r);
+        for (int p = p0; p < p1; ++p) {
+            const std::vector<double> z1(Z1 + p * r, Z1 + (p + 1) * r), z2(Z2 + p * r, Z2 + (p + 1) * r);
+            point_forward(model, mesh, mat, pin_positions, z1, s1);
+            point_forward(model, mesh, mat, pin_positions, z2, s2);
+            double d2 = 0.0, dz2 = 0.0;
+            for (size_t i = 0; i < s1.H.size(); ++i) d2 += (s1.H[i] - s2.H[i]) * (s1.H[i] - s2.H[i]);
+            for (int c = 0; c < r; ++c) dz2 += (z1[c] - z2[c]) * (z1[c] - z2[c]);
+            terms[p] = d2 / dz2;
+            // scale(sum, 1/P) . scale(dot(diff, diff), 1/dz2) . sub(d1, d2) backward
+            const double f = 2.0 / (dz2 * static_cast<double>(P));
+            for (size_t i = 0; i < Hbar.size(); ++i) Hbar[i] = f * (s1.H[i] - s2.H[i]);
+            point_backward(model, mesh, mat, s1, Hbar, tW[k], tb[k]);
+            for (double& v : Hbar) v = -v;
+            point_backward(model, mesh, mat, s2, Hbar, tW[k], tb[k]);
+        }
+    };
+    if (nthreads == 1) {
+        work(0, 0, P);
+    } else {
+        std::vector<std::thread> th;
+        for (int k = 0; k < nthreads; ++k) th.emplace_back(work, k, (P * k) / nthreads, (P * (k + 1)) / nthreads);
+        for (auto& t : th) t.join();
+    }
+    gW.assign(L, {});
+    gb.assign(L, {});
+    for (int l = 0; l < L; ++l) {
+        gW[l].assign(model.dec[l].W.size(), 0.0);
+        gb[l].assign(model.dec[l].b.size(), 0.0);
+        for (int k = 0; k < nthreads; ++k) {
+            for (size_t i = 0; i < gW[l].size(); ++i) gW[l][i] += tW[k][l][i];
+            for (size_t i = 0; i < gb[l].size(); ++i) gb[l][i] += tb[k][l][i];
+        }
+    }
+    double total = 0.0;
+    for (int p = 0; p < P; ++p) total += terms[p];
+    return total / static_cast<double>(P);
+}
+
 }  // namespace orc

@@ -209,4 +209,23 @@ double lipschitz_loss2(const Model& model, const Mesh& mesh, const Material& mat
                        const std::vector<double>& pin_positions, int P, const double* Z1,
                        const double* Z2, int nthreads);
 
+// snh_third_contraction (energy.cpp:303-320): out12 = grad_x <H_e(x), M_local> for one
+// tet, M_local symmetric 12 x 12 row-major (local dofs corner-major).
+void element_third_contraction(const Mesh& m, double mu, double lambda, int e, const double* positions,
+                               const double* M_local, double* out12);
+// elastic_third_contraction (energy.cpp:495-510): qbar (n) += sum_e w_e
+// grad <H_e, (A_e B_e^T + B_e A_e^T) / 2>, A and B n x k row-major.
+void elastic_third_contraction(const Mesh& m, const Material& mat, const std::vector<double>& positions,
+                               const std::vector<double>& A, const std::vector<double>& B, int k,
+                               std::vector<double>& qbar, const std::vector<int>* ids = nullptr,
+                               const std::vector<double>* w = nullptr);
+// Order-2 Lipschitz loss and its parameter gradient: build_lipschitz_loss (losses.cpp:196-213)
+// followed by Tape::backward (tape.cpp:46-59) through tape_decode (losses.cpp:56-85),
+// tape_second_directional (:105-118), tape_reduced_derivative (:136-146) and the potential
+// couplings' backward (tape.cpp:245-279).  gW[l] is row-major like Layer::W.
+double lipschitz_loss2_grad(const Model& model, const Mesh& mesh, const Material& mat,
+                            const std::vector<double>& pin_positions, int P, const double* Z1, const double* Z2,
+                            std::vector<std::vector<double>>& gW, std::vector<std::vector<double>>& gb,
+                            int nthreads);
+
 }  // namespace orc

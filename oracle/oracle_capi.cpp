@@ -528,6 +528,38 @@ int orc_lipschitz_loss2(void* p, int P, const double* Z1, const double* Z2, int 
         return fail(e);
     }
 }
+int orc_elastic_third_contraction(void* p, const double* q, int k, const double* A, const double* B, double* qbar) {
+    try {
+        auto* c = static_cast<Ctx*>(p);
+        const int n = c->mesh.num_dofs();
+        std::vector<double> qq(q, q + n), va(A, A + static_cast<size_t>(n) * k), vb(B, B + static_cast<size_t>(n) * k),
+            out(n, 0.0);
+        elastic_third_contraction(c->mesh, c->mat, dof_unpack(c->mesh, qq, c->pins), va, vb, k, out);
+        std::memcpy(qbar, out.data(), out.size() * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+// grad: per decoder layer, W (row-major) then b.
+int orc_lipschitz_loss2_grad(void* p, int P, const double* Z1, const double* Z2, int nthreads, double* loss,
+                             double* grad) {
+    try {
+        auto* c = static_cast<Ctx*>(p);
+        std::vector<std::vector<double>> gW, gb;
+        *loss = lipschitz_loss2_grad(c->model, c->mesh, c->mat, c->pins, P, Z1, Z2, gW, gb, nthreads);
+        size_t o = 0;
+        for (size_t l = 0; l < gW.size(); ++l) {
+            std::memcpy(grad + o, gW[l].data(), gW[l].size() * 8);
+            o += gW[l].size();
+            std::memcpy(grad + o, gb[l].data(), gb[l].size() * 8);
+            o += gb[l].size();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
 
 int orc_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
 

@@ -75,6 +75,8 @@ def lib():
                                        C.c_int, _D, _D, _D, _I, _I, _D, _D, _I, _I, _D]),
             "orc_reduced_potential_hessian": (C.c_int, [C.c_void_p, _D, _D]),
             "orc_lipschitz_loss2": (C.c_int, [C.c_void_p, C.c_int, _D, _D, C.c_int, _D]),
+            "orc_elastic_third_contraction": (C.c_int, [C.c_void_p, _D, C.c_int, _D, _D, _D]),
+            "orc_lipschitz_loss2_grad": (C.c_int, [C.c_void_p, C.c_int, _D, _D, C.c_int, _D, _D]),
             "orc_hardware_threads": (C.c_int, []),
         }
         for name, (res, args) in sigs.items():
@@ -320,6 +322,31 @@ class Oracle:
         out = C.c_double()
         _chk(lib().orc_lipschitz_loss2(self.h, Z1.shape[0], _d(Z1), _d(Z2), threads, C.byref(out)))
         return out.value
+
+    def third_contraction(self, q, A, B):
+        """elastic_third_contraction (energy.cpp:495-510) at configuration q."""
+        q = np.ascontiguousarray(q, np.float64)
+        A = np.ascontiguousarray(A, np.float64)
+        B = np.ascontiguousarray(B, np.float64)
+        out = np.zeros(self.n)
+        _chk(lib().orc_elastic_third_contraction(self.h, _d(q), A.shape[1], _d(A), _d(B), _d(out)))
+        return out
+
+    def lipschitz_loss2_grad(self, Z1, Z2, threads=1):
+        """(loss, [(dW, db) per decoder layer]) of the order-2 Lipschitz loss."""
+        Z1 = np.ascontiguousarray(Z1, np.float64)
+        Z2 = np.ascontiguousarray(Z2, np.float64)
+        layers = self.decoder_layers()[0]
+        flat = np.zeros(sum(W.size + b.size for W, b, _ in layers))
+        out = C.c_double()
+        _chk(lib().orc_lipschitz_loss2_grad(self.h, Z1.shape[0], _d(Z1), _d(Z2), threads, C.byref(out), _d(flat)))
+        grads, o = [], 0
+        for W, b, _ in layers:
+            gW = flat[o:o + W.size].reshape(W.shape)
+            o += W.size
+            grads.append((gW, flat[o:o + b.size].copy()))
+            o += b.size
+        return out.value, grads
 
 
 def project_spd(H):
