@@ -177,6 +177,15 @@ lsb_status lsb_objective_hessian(lsb_context* ctx, int B, const double* Z, doubl
 lsb_status lsb_projective_newton(lsb_context* ctx, double* z, const lsb_solver_config* cfg, lsb_exit_report* report);
 /* Second-order Lipschitz loss mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2. */
 lsb_status lsb_lipschitz_loss(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss);
+/* The same loss and its gradient with respect to every decoder parameter: the
+ * training-side backward of build_lipschitz_loss(..., order 2, pot) followed by
+ * Tape::backward / param_gradient (proj/src/losses.cpp:196-213, proj/src/tape.cpp:46-79,
+ * 245-279).  grad holds, per decoder layer in order (hidden layers, then the output
+ * layer), W (rows x cols, row-major) then b (rows): sum over layers of rows*(cols+1)
+ * doubles.  Requires an identity output layer and r in {8, 16, 32} (as the Hessian path);
+ * fp32 device arithmetic, fp64 accumulation; LSB_EINVAL on a coincident pair. */
+lsb_status lsb_lipschitz_loss_grad(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss,
+                                   double* grad);
 
 /* Persistent solve kernel (one cooperative launch of thread-block clusters per
  * evaluation / solve / step).  lsb_get_solve_info reports its grid (0 = not

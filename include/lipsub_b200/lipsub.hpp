@@ -322,4 +322,19 @@ inline double lipschitz_loss(ReducedSystem& system, const std::vector<std::pair<
     return loss;
 }
 
+// The same loss and dL/dtheta, flattened per decoder layer as W (row-major) then b
+// (build_lipschitz_loss + Tape::backward, losses.cpp:196-213, tape.cpp:46-79).
+inline double lipschitz_loss_grad(ReducedSystem& system, const std::vector<std::pair<VectorXd, VectorXd>>& pairs,
+                                  std::vector<double>& grad) {
+    if (pairs.empty()) throw std::invalid_argument("lipschitz loss: no pairs");
+    std::vector<double> Z1, Z2;
+    for (const auto& [a, b] : pairs) {
+        Z1.insert(Z1.end(), a.begin(), a.end());
+        Z2.insert(Z2.end(), b.begin(), b.end());
+    }
+    double loss = 0.0;
+    check(lsb_lipschitz_loss_grad(system.handle(), (int)pairs.size(), Z1.data(), Z2.data(), &loss, grad.data()));
+    return loss;
+}
+
 }  // namespace lipsub_b200

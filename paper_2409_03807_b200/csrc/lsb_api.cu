@@ -1002,4 +1002,20 @@ lsb_status lsb_lipschitz_loss(lsb_context* ctx, int P, const double* Z1, const d
     });
 }
 
+lsb_status lsb_lipschitz_loss_grad(lsb_context* ctx, int P, const double* Z1, const double* Z2, double* loss,
+                                   double* grad) {
+    return run([&] {
+        check_ctx(ctx);
+        require(P > 0, "lipschitz loss: no pairs");  // losses.cpp:199
+        require(Z1 && Z2 && loss && grad, "lipschitz loss: null argument");
+        const int r = ctx->c.r;
+        for (int p = 0; p < P; ++p) {  // losses.cpp:202-204
+            double dz2 = 0.0;
+            for (int k = 0; k < r; ++k) dz2 += (Z1[p * r + k] - Z2[p * r + k]) * (Z1[p * r + k] - Z2[p * r + k]);
+            require(dz2 > 0.0, "lipschitz loss: coincident pair");
+        }
+        *loss = lipschitz_loss_grad(ctx->c, P, Z1, Z2, grad);
+    });
+}
+
 }  // extern "C"

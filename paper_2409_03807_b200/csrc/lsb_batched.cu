@@ -21,6 +21,7 @@
 
 #include "lsb_batched.hpp"
 #include "lsb_tc.cuh"
+#include "lsb_theta.cuh"
 
 namespace lsb {
 
@@ -961,7 +962,7 @@ struct BatchedEngine : BatchedBase {
     static constexpr int PH = 64;  // points per Hessian chunk
     bool hess_ready = false;
     float *d_Whf = nullptr;  // hidden weights fp32 (concatenated, row-major)
-    float *d_X[2] = {}, *d_Q = nullptr, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
+    float *d_Xl[kMaxLayers + 1] = {}, *d_Ql[kMaxLayers] = {}, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
     float *d_Cpart = nullptr, *d_gpart = nullptr, *d_Th = nullptr, *d_Yh = nullptr, *d_Ph = nullptr, *d_Zh = nullptr;
     double *d_Ch = nullptr, *d_H = nullptr;
     float* d_rinh = nullptr;  // inertia residual of the objective Hessian (n x PH)
@@ -1321,9 +1322,8 @@ struct BatchedEngine : BatchedBase {
             }
             cuda_check(cudaGetLastError(), "pack hidden");
         }
-        d_X[0] = alloc<float>((size_t)hmax * PH * hcols);
-        d_X[1] = alloc<float>((size_t)hmax * PH * hcols);
-        d_Q = alloc<float>((size_t)hmax * PH * hcols);
+        for (int l = 0; l <= c.nhid; ++l) d_Xl[l] = alloc<float>((size_t)hmax * PH * hcols);
+        for (int l = 0; l < c.nhid; ++l) d_Ql[l] = alloc<float>((size_t)hmax * PH * hcols);
         d_Bt = alloc<float>((size_t)h * PH * (1 + r));
         d_Ct = alloc<float>((size_t)n * PH * (1 + r));
         d_Uh = alloc<float>((size_t)c.mesh.V * 3 * PH);
@@ -1353,6 +1353,186 @@ struct BatchedEngine : BatchedBase {
         hess_ready = true;
     }
 
+    // ---------------------------------------------------------------- theta-gradient (lsb_theta.cuh)
+    bool theta_ready = false;
+    float *d_Hbf = nullptr, *d_ebf = nullptr, *d_Bt2 = nullptr, *d_Bfwd = nullptr, *d_Ct2 = nullptr;
+    float *d_Wv = nullptr, *d_gbar = nullptr, *d_partJ = nullptr, *d_partq = nullptr, *d_Abar = nullptr;
+    float *d_XbL = nullptr, *d_Xbar[2] = {}, *d_Abl = nullptr, *d_spart = nullptr;
+    double *d_gW = nullptr, *d_gb = nullptr;
+    size_t gw_total = 0, gb_total = 0, spart_floats = 0, tsmem = 0;
+    std::vector<size_t> gw_off, gb_off, hw_off;  // per layer (hidden..., output); fp32 hidden weight offsets
+
+    static constexpr int kSplitOut = 64;  // split-K of W_out^T Abar (K = n)
+    static constexpr int kSplitHid = 32;  // split-K of Abar_l X_l^T (K = PH * cols)
+
+    void init_theta(Context& c) {
+        if (!hess_ready) init_hessian(c);
+        const int r = c.r, h = c.h, n = c.n, P = PH, npair = r * (r + 1) / 2, V = c.mesh.V;
+        int hmax = r;
+        for (int l = 0; l < c.nhid; ++l) hmax = std::max(hmax, c.hrows[l]);
+        d_Hbf = alloc<float>((size_t)P * r * r);
+        d_ebf = alloc<float>((size_t)P * npair);
+        d_Bt2 = alloc<float>((size_t)h * P * (r + 1));
+        d_Bfwd = alloc<float>((size_t)P * (r + 2) * h);
+        d_Ct2 = alloc<float>((size_t)n * P * (r + 1));
+        d_Wv = alloc<float>((size_t)V * 3 * P * r);
+        d_gbar = alloc<float>((size_t)V * 3 * P);
+        cuda_check(cudaMemsetAsync(d_Wv, 0, 4 * (size_t)V * 3 * P * r, c.stream), "Wv");
+        cuda_check(cudaMemsetAsync(d_gbar, 0, 4 * (size_t)V * 3 * P, c.stream), "Gb");
+        d_partJ = alloc<float>((size_t)nslots * 3 * P * r);
+        d_partq = alloc<float>((size_t)nslots * 3 * P);
+        d_Abar = alloc<float>((size_t)n * P * (r + 2));
+        d_XbL = alloc<float>((size_t)h * P * (r + 2));
+        d_Xbar[0] = alloc<float>((size_t)hmax * P * hcols);
+        d_Xbar[1] = alloc<float>((size_t)hmax * P * hcols);
+        d_Abl = alloc<float>((size_t)hmax * P * hcols);
+        gw_off.assign(c.nhid + 1, 0);
+        gb_off.assign(c.nhid + 1, 0);
+        hw_off.assign(c.nhid, 0);
+        size_t hw = 0;
+        spart_floats = std::max((size_t)n * h, (size_t)h * P * (r + 2) * kSplitOut);
+        for (int l = 0; l <= c.nhid; ++l) {
+            const size_t rows = l < c.nhid ? c.hrows[l] : n, cols = l < c.nhid ? c.hcols[l] : h;
+            gw_off[l] = gw_total;
+            gb_off[l] = gb_total;
+            gw_total += rows * cols;
+            gb_total += rows;
+            if (l < c.nhid) {
+                hw_off[l] = hw;
+                hw += rows * cols;
+                spart_floats = std::max(spart_floats, rows * cols * kSplitHid);
+                spart_floats = std::max(spart_floats, cols * P * hcols);
+            }
+        }
+        d_spart = alloc<float>(spart_floats);
+        d_gW = alloc<double>(gw_total);
+        d_gb = alloc<double>(gb_total);
+        const int gp = 128 / r;
+        tsmem = ((size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp * r + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;
+        if (tsmem > 227 * 1024 - 4096)
+            throw LsbError(LSB_EINVAL, "lipschitz grad: element blocks too large for shared memory");
+        if (r == 8) cuda_check(cudaFuncSetAttribute(theta::elem_theta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem), "smem");
+        if (r == 16) cuda_check(cudaFuncSetAttribute(theta::elem_theta_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem), "smem");
+        if (r == 32) cuda_check(cudaFuncSetAttribute(theta::elem_theta_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem), "smem");
+        cuda_check(cudaStreamSynchronize(c.stream), "theta init");
+        theta_ready = true;
+    }
+
+    // C[M][N] (fp32 store and/or fp64 accumulate) = sum_k A[m*sam + k*sak] B[k*sbk + n*sbn]
+    void gemm_strided(cudaStream_t s, int M, int N, int K, int nz, const float* A, long long sam, long long sak,
+                      const float* B, long long sbk, long long sbn, float* out32, double* acc64, int sms) {
+        int kchunk = (K + nz - 1) / nz;
+        kchunk = (kchunk + 15) / 16 * 16;
+        nz = (K + kchunk - 1) / kchunk;
+        dim3 g((N + 127) / 128, (M + 127) / 128, nz);
+        theta::sgemm_strided_kernel<<<g, 256, 0, s>>>(M, N, K, kchunk, A, sam, sak, B, sbk, sbn, d_spart);
+        theta::splitk_out_kernel<<<sms * 4, 256, 0, s>>>((long long)M * N, nz, d_spart, out32, acc64);
+    }
+
+    template <int R>
+    void launch_theta_elem(Context& c, int P) {
+        constexpr int GP = 128 / R;
+        dim3 g(nblk, (P + GP - 1) / GP);
+        const float* recf = static_cast<const float*>(rec_f32(c));
+        const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
+        theta::elem_theta_kernel<R><<<g, 128, tsmem, c.stream>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                                                                 d_blk_avert, d_tet_aloc, d_Uh, d_Jv, d_Wv, d_gbar, P,
+                                                                 d_partJ, d_partq);
+    }
+    template <int R>
+    void launch_theta_small(Context& c, int which, int rows, int l, int cur) {
+        const int P = PH, cols = hcols;
+        cudaStream_t s = c.stream;
+        if (which == 0)
+            theta::theta_prep_kernel<R><<<c.num_sms * 4, 256, 0, s>>>(c.h, P, cols, d_Xl[c.nhid], d_Hbf, d_ebf, d_Bt2,
+                                                                      d_Bfwd);
+        else if (which == 1)
+            theta::theta_top_kernel<R><<<c.num_sms * 8, 256, 0, s>>>(c.h, P, cols, d_XbL, d_ebf, d_Xbar[0]);
+        else
+            theta::tangent_act_bwd_kernel<R><<<(rows * P + 127) / 128, 128, 0, s>>>(
+                rows, P, cols, d_Ql[l], c.d_bh + c.boff[l], c.hact[l], d_Xbar[cur], d_Abl);
+    }
+    void theta_small(Context& c, int which, int rows = 0, int l = 0, int cur = 0) {
+        if (c.r == 8) launch_theta_small<8>(c, which, rows, l, cur);
+        else if (c.r == 16) launch_theta_small<16>(c, which, rows, l, cur);
+        else launch_theta_small<32>(c, which, rows, l, cur);
+    }
+
+    // One chunk of N <= PH points (pairs interleaved z1, z2): H via run_hessian_chunk, the
+    // loss terms and dL/dH on the host (fp64), then the device reverse sweep accumulating
+    // dL/dtheta into d_gW / d_gb.  inv_P = 1 / (number of pairs in the whole loss).
+    void run_theta_chunk(Context& c, int N, const double* Z, double inv_P, double& loss_sum) {
+        if (!theta_ready) init_theta(c);
+        const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols, npair = r * (r + 1) / 2;
+        std::vector<double> H((size_t)N * r * r);
+        run_hessian_chunk(c, N, Z, H.data());
+        cudaStream_t s = c.stream;
+        // scale(sum, 1/P) . scale(dot(diff, diff), 1/dz2) . sub(H1, H2) backward; then the
+        // symmetric_from_entries backward (tape.cpp:212-222) for ebar
+        std::vector<float> hb((size_t)P * r * r, 0.f), eb((size_t)P * npair, 0.f);
+        std::vector<double> Hb((size_t)r * r);
+        for (int q = 0; q + 1 < N; q += 2) {
+            const double* H1 = &H[(size_t)q * r * r];
+            const double* H2 = &H[(size_t)(q + 1) * r * r];
+            const double* z1 = Z + (size_t)q * r;
+            const double* z2 = Z + (size_t)(q + 1) * r;
+            double d2 = 0.0, dz2 = 0.0;
+            for (int k = 0; k < r * r; ++k) d2 += (H1[k] - H2[k]) * (H1[k] - H2[k]);
+            for (int k = 0; k < r; ++k) dz2 += (z1[k] - z2[k]) * (z1[k] - z2[k]);
+            loss_sum += d2 / dz2;
+            const double f = 2.0 * inv_P / dz2;
+            for (int k = 0; k < r * r; ++k) Hb[k] = f * (H1[k] - H2[k]);
+            for (int side = 0; side < 2; ++side) {
+                const double sg = side == 0 ? 1.0 : -1.0;
+                const int pt = q + side;
+                for (int k = 0; k < r * r; ++k) hb[(size_t)pt * r * r + k] = (float)(sg * Hb[k]);
+                int sidx = 0;
+                for (int a = 0; a < r; ++a)
+                    for (int b = a; b < r; ++b, ++sidx)
+                        eb[(size_t)pt * npair + sidx] = (float)(sg * (Hb[a * r + b] + (a != b ? Hb[b * r + a] : 0.0)));
+            }
+        }
+        c.copy(d_Hbf, hb.data(), 4 * hb.size(), cudaMemcpyHostToDevice, "Hbar");
+        c.copy(d_ebf, eb.data(), 4 * eb.size(), cudaMemcpyHostToDevice, "ebar");
+        // h-level operands, output GEMM -> W = J Hbar and gbar in the vertex layout
+        theta_small(c, 0);
+        if (!tc.enabled ||
+            !tc.gemm_general(s, tc.A1, tc.tiles1, tc.S1, n, d_Bt2, P * (r + 1), h, P * (r + 1), d_Ct2, P * (r + 1))) {
+            dim3 g((P * (r + 1) + 127) / 128, (n + 127) / 128);
+            sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (r + 1), h, d_W, h, d_Bt2, P * (r + 1), d_Ct2, P * (r + 1));
+        }
+        theta::theta_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct2, c.d_eprow, d_Wv, d_gbar);
+        // element pass: Jbar = 2 K W, qbar = T[J, W] + K gbar (block partials), then per row
+        if (r == 8) launch_theta_elem<8>(c, P);
+        else if (r == 16) launch_theta_elem<16>(c, P);
+        else launch_theta_elem<32>(c, P);
+        theta::theta_combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_vslot_ptr, d_vslot, d_partJ, d_partq,
+                                                                   c.d_eprow, d_Th, d_Abar);
+        const int w2 = P * (r + 2);
+        // output layer: dW_out += Abar Bfwd, db_out += sum_p s qbar
+        gemm_strided(s, n, h, w2, 1, d_Abar, w2, 1, d_Bfwd, h, 1, nullptr, d_gW + gw_off[c.nhid], c.num_sms);
+        theta::rowsum_acc_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, P, w2, r + 2, d_Abar, d_gb + gb_off[c.nhid]);
+        // adjoint of the top hidden block: W_out^T Abar, then S-bar = ebar rho
+        gemm_strided(s, h, w2, n, kSplitOut, d_W, 1, h, d_Abar, w2, 1, d_XbL, nullptr, c.num_sms);
+        theta_small(c, 1);
+        int cur = 0;
+        for (int l = c.nhid - 1; l >= 0; --l) {
+            const int R = c.hrows[l], K = c.hcols[l];
+            theta_small(c, 2, R, l, cur);
+            gemm_strided(s, R, K, P * cols, kSplitHid, d_Abl, (long long)P * cols, 1, d_Xl[l], 1, (long long)P * cols,
+                         nullptr, d_gW + gw_off[l], c.num_sms);
+            theta::rowsum_acc_kernel<<<(R + 127) / 128, 128, 0, s>>>(R, P, (long long)P * cols, cols, d_Abl,
+                                                                     d_gb + gb_off[l]);
+            if (l > 0) {
+                gemm_strided(s, K, P * cols, R, 1, d_Whf + hw_off[l], 1, K, d_Abl, (long long)P * cols, 1,
+                             d_Xbar[cur ^ 1], nullptr, c.num_sms);
+                cur ^= 1;
+            }
+        }
+        cuda_check(cudaGetLastError(), "theta chunk");
+        c.batched_launches += 12 + 5 * c.nhid;
+    }
+
     size_t hess_smem(int r) const {
         const int gp = 128 / r;
         return ((size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;  // Us + accg (elem_hess2)
@@ -1376,21 +1556,20 @@ struct BatchedEngine : BatchedBase {
         for (int p = 0; p < N; ++p)
             for (int k = 0; k < r; ++k) zt[(size_t)k * P + p] = (float)Z[(size_t)p * r + k];
         cuda_check(cudaMemcpyAsync(d_Zh, zt.data(), 4 * zt.size(), cudaMemcpyHostToDevice, s), "Zh");
-        tangent_init_kernel<<<c.num_sms, 256, 0, s>>>(r, P, cols, d_Zh, d_X[0]);
-        int cur = 0;
+        tangent_init_kernel<<<c.num_sms, 256, 0, s>>>(r, P, cols, d_Zh, d_Xl[0]);
         size_t woff = 0;
         for (int l = 0; l < c.nhid; ++l) {
             const int R = c.hrows[l], K = c.hcols[l];
             if (!tc.enabled ||
-                !tc.gemm_general(s, hA[l].A, hA[l].tiles, hA[l].S, R, d_X[cur], P * cols, K, P * cols, d_Q, P * cols)) {
+                !tc.gemm_general(s, hA[l].A, hA[l].tiles, hA[l].S, R, d_Xl[l], P * cols, K, P * cols, d_Ql[l], P * cols)) {
                 dim3 g((P * cols + 127) / 128, (R + 127) / 128);
-                sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_X[cur], P * cols, d_Q, P * cols);
+                sgemm_nn_kernel<<<g, 256, 0, s>>>(R, P * cols, K, d_Whf + woff, K, d_Xl[l], P * cols, d_Ql[l], P * cols);
             }
-            tangent_act_kernel<<<c.num_sms * 8, 256, 0, s>>>(R, P, r, cols, d_Q, c.d_bh + c.boff[l], c.hact[l], d_X[cur ^ 1]);
+            tangent_act_kernel<<<c.num_sms * 8, 256, 0, s>>>(R, P, r, cols, d_Ql[l], c.d_bh + c.boff[l], c.hact[l],
+                                                             d_Xl[l + 1]);
             woff += (size_t)R * K;
-            cur ^= 1;
         }
-        const float* XL = d_X[cur];
+        const float* XL = d_Xl[c.nhid];
         tangent_pack_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, XL, d_Bt);
         if (!tc.enabled ||
             !tc.gemm_general(s, tc.A1, tc.tiles1, tc.S1, n, d_Bt, P * (1 + r), h, P * (1 + r), d_Ct, P * (1 + r))) {
@@ -1518,6 +1697,39 @@ double lipschitz_loss(Context& c, int P, const double* Z1, const double* Z2) {
         for (int k = 0; k < r * r; ++k) d2 += (H1[k] - H2[k]) * (H1[k] - H2[k]);
         for (int k = 0; k < r; ++k) dz2 += (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]) * (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]);
         total += d2 / dz2;
+    }
+    return total / P;
+}
+
+// Order-2 Lipschitz loss and dL/dtheta: grad holds, per decoder
+// layer in order (hidden layers, then the output layer), W row-major then b.
+double lipschitz_loss_grad(Context& c, int P, const double* Z1, const double* Z2, double* grad) {
+    BatchedEngine& eng = engine(c);
+    if (!eng.theta_ready) eng.init_theta(c);
+    cuda_check(cudaMemsetAsync(eng.d_gW, 0, 8 * eng.gw_total, c.stream), "gW");
+    cuda_check(cudaMemsetAsync(eng.d_gb, 0, 8 * eng.gb_total, c.stream), "gb");
+    const int r = c.r;
+    std::vector<double> Z(2 * (size_t)P * r);
+    for (int p = 0; p < P; ++p) {
+        std::memcpy(&Z[(2 * (size_t)p) * r], Z1 + (size_t)p * r, 8 * r);
+        std::memcpy(&Z[(2 * (size_t)p + 1) * r], Z2 + (size_t)p * r, 8 * r);
+    }
+    double total = 0.0;
+    for (int b0 = 0; b0 < 2 * P; b0 += BatchedEngine::PH) {
+        const int N = std::min(BatchedEngine::PH, 2 * P - b0);
+        eng.run_theta_chunk(c, N, Z.data() + (size_t)b0 * r, 1.0 / P, total);
+    }
+    std::vector<double> gW(eng.gw_total), gb(eng.gb_total);
+    c.copy(gW.data(), eng.d_gW, 8 * gW.size(), cudaMemcpyDeviceToHost, "gW");
+    c.copy(gb.data(), eng.d_gb, 8 * gb.size(), cudaMemcpyDeviceToHost, "gb");
+    size_t o = 0;
+    for (int l = 0; l <= c.nhid; ++l) {
+        const size_t nw = (l < c.nhid ? eng.gb_off[l + 1] : eng.gb_total) - eng.gb_off[l];
+        const size_t ww = (l < c.nhid ? eng.gw_off[l + 1] : eng.gw_total) - eng.gw_off[l];
+        std::memcpy(grad + o, gW.data() + eng.gw_off[l], 8 * ww);
+        o += ww;
+        std::memcpy(grad + o, gb.data() + eng.gb_off[l], 8 * nw);
+        o += nw;
     }
     return total / P;
 }

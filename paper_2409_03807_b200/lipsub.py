@@ -434,6 +434,26 @@ class ReducedSystem:
         check(lib().lsb_lipschitz_loss(self._h, Z1.shape[0], dptr(Z1), dptr(Z2), C.byref(out)))
         return out.value
 
+    def lipschitz_loss_grad(self, Z1: np.ndarray, Z2: np.ndarray):
+        """(loss, [(dL/dW, dL/db) per decoder layer]): the order-2 Lipschitz loss and its
+        parameter gradient, i.e. build_lipschitz_loss + Tape::backward + param_gradient
+        (losses.cpp:196-213, tape.cpp:46-79)."""
+        Z1 = np.ascontiguousarray(Z1, np.float64).reshape(-1, self.r)
+        Z2 = np.ascontiguousarray(Z2, np.float64).reshape(-1, self.r)
+        if Z1.shape != Z2.shape:
+            raise ValueError("lipschitz loss: pair arrays differ in shape")
+        shapes = [l.W.shape for l in self.model.decoder]
+        flat = np.zeros(sum(r * (c + 1) for r, c in shapes))
+        out = C.c_double()
+        check(lib().lsb_lipschitz_loss_grad(self._h, Z1.shape[0], dptr(Z1), dptr(Z2), C.byref(out), dptr(flat)))
+        grads, o = [], 0
+        for r, c in shapes:
+            gW = flat[o:o + r * c].reshape(r, c)
+            o += r * c
+            grads.append((gW, flat[o:o + r].copy()))
+            o += r
+        return out.value, grads
+
     # --- execution path
     def solve_kernel_info(self):
         g, u = C.c_int(), C.c_int()
