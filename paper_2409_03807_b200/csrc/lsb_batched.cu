@@ -988,11 +988,14 @@ struct BatchedEngine : BatchedBase {
     // Blocks of tb consecutive tets with their touched free vertices (slots), local slot of
     // every tet corner, and per free vertex its slots in ascending block order.
     struct FreeBlocks {
-        int nblk = 0, nslots = 0, max_nv = 0;
+        int nblk = 0, nslots = 0, max_nv = 0, max_nva = 0;
         int *tet0 = nullptr, *vptr = nullptr, *vslot_ptr = nullptr, *vslot = nullptr;
         short* loc = nullptr;
+        // with_all: every touched vertex (free and pinned) per block, for shared-memory staging
+        int *aptr = nullptr, *avert = nullptr;
+        short* aloc = nullptr;
     };
-    FreeBlocks build_free_blocks(Context& c, int tb) {
+    FreeBlocks build_free_blocks(Context& c, int tb, bool with_all = false) {
         const HostMesh& m = c.mesh;
         FreeBlocks fb;
         fb.nblk = (m.E + tb - 1) / tb;
@@ -1039,6 +1042,31 @@ struct BatchedEngine : BatchedBase {
         c.copy(fb.loc, loc.data(), 2 * loc.size(), cudaMemcpyHostToDevice, "blk");
         c.copy(fb.vslot_ptr, sptr.data(), 4 * sptr.size(), cudaMemcpyHostToDevice, "blk");
         c.copy(fb.vslot, slots.data(), 4 * slots.size(), cudaMemcpyHostToDevice, "blk");
+        if (with_all) {
+            std::vector<int> aptr(fb.nblk + 1, 0), avert;
+            std::vector<short> aloc(4 * (size_t)m.E, -1);
+            for (int bk = 0; bk < fb.nblk; ++bk) {
+                const int e1 = std::min(m.E, (bk + 1) * tb);
+                std::vector<int> verts;
+                for (int e = bk * tb; e < e1; ++e)
+                    for (int k = 0; k < 4; ++k) verts.push_back(m.T[4 * (size_t)e + k]);
+                std::sort(verts.begin(), verts.end());
+                verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+                for (int e = bk * tb; e < e1; ++e)
+                    for (int k = 0; k < 4; ++k)
+                        aloc[4 * (size_t)e + k] = (short)(std::lower_bound(verts.begin(), verts.end(),
+                                                                           m.T[4 * (size_t)e + k]) - verts.begin());
+                aptr[bk + 1] = aptr[bk] + (int)verts.size();
+                fb.max_nva = std::max(fb.max_nva, (int)verts.size());
+                avert.insert(avert.end(), verts.begin(), verts.end());
+            }
+            fb.aptr = alloc<int>(fb.nblk + 1);
+            fb.avert = alloc<int>(avert.size());
+            fb.aloc = alloc<short>(aloc.size());
+            c.copy(fb.aptr, aptr.data(), 4 * aptr.size(), cudaMemcpyHostToDevice, "blk");
+            c.copy(fb.avert, avert.data(), 4 * avert.size(), cudaMemcpyHostToDevice, "blk");
+            c.copy(fb.aloc, aloc.data(), 2 * aloc.size(), cudaMemcpyHostToDevice, "blk");
+        }
         return fb;
     }
     FreeBlocks eb;  // the batched evaluation's (smaller) element blocks
@@ -1362,6 +1390,7 @@ struct BatchedEngine : BatchedBase {
     size_t gw_total = 0, gb_total = 0, spart_floats = 0, tsmem = 0;
     std::vector<size_t> gw_off, gb_off, hw_off;  // per layer (hidden..., output); fp32 hidden weight offsets
 
+    FreeBlocks tbk;  // the theta pass's element blocks (LSB_THETA_TB tets, default 24)
     static constexpr int kSplitOut = 64;  // split-K of W_out^T Abar (K = n)
     static constexpr int kSplitHid = 32;  // split-K of Abar_l X_l^T (K = PH * cols)
 
@@ -1379,8 +1408,13 @@ struct BatchedEngine : BatchedBase {
         d_gbar = alloc<float>((size_t)V * 3 * P);
         cuda_check(cudaMemsetAsync(d_Wv, 0, 4 * (size_t)V * 3 * P * r, c.stream), "Wv");
         cuda_check(cudaMemsetAsync(d_gbar, 0, 4 * (size_t)V * 3 * P, c.stream), "Gb");
-        d_partJ = alloc<float>((size_t)nslots * 3 * P * r);
-        d_partq = alloc<float>((size_t)nslots * 3 * P);
+        {
+            const char* e = getenv("LSB_THETA_TB");
+            const int tb = e ? std::max(1, std::min(48, atoi(e))) : 24;
+            tbk = build_free_blocks(c, tb, true);
+        }
+        d_partJ = alloc<float>((size_t)tbk.nslots * 3 * P * r);
+        d_partq = alloc<float>((size_t)tbk.nslots * 3 * P);
         d_Abar = alloc<float>((size_t)n * P * (r + 2));
         d_XbL = alloc<float>((size_t)h * P * (r + 2));
         d_Xbar[0] = alloc<float>((size_t)hmax * P * hcols);
@@ -1408,7 +1442,8 @@ struct BatchedEngine : BatchedBase {
         d_gW = alloc<double>(gw_total);
         d_gb = alloc<double>(gb_total);
         const int gp = 128 / r;
-        tsmem = ((size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp * r + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;
+        tsmem = ((size_t)tbk.max_nva * 3 * gp + (size_t)tbk.max_nv * 3 * gp * r + (size_t)tbk.max_nv * 3 * gp) *
+                    sizeof(float) + 64;
         if (tsmem > 227 * 1024 - 4096)
             throw LsbError(LSB_EINVAL, "lipschitz grad: element blocks too large for shared memory");
         if (r == 8) cuda_check(cudaFuncSetAttribute(theta::elem_theta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem), "smem");
@@ -1432,11 +1467,11 @@ struct BatchedEngine : BatchedBase {
     template <int R>
     void launch_theta_elem(Context& c, int P) {
         constexpr int GP = 128 / R;
-        dim3 g(nblk, (P + GP - 1) / GP);
+        dim3 g(tbk.nblk, (P + GP - 1) / GP);
         const float* recf = static_cast<const float*>(rec_f32(c));
         const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
-        theta::elem_theta_kernel<R><<<g, 128, tsmem, c.stream>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
-                                                                 d_blk_avert, d_tet_aloc, d_Uh, d_Jv, d_Wv, d_gbar, P,
+        theta::elem_theta_kernel<R><<<g, 128, tsmem, c.stream>>>(tt, recf, tbk.tet0, tbk.vptr, tbk.loc, tbk.aptr,
+                                                                 tbk.avert, tbk.aloc, d_Uh, d_Jv, d_Wv, d_gbar, P,
                                                                  d_partJ, d_partq);
     }
     template <int R>
@@ -1506,7 +1541,7 @@ struct BatchedEngine : BatchedBase {
         if (r == 8) launch_theta_elem<8>(c, P);
         else if (r == 16) launch_theta_elem<16>(c, P);
         else launch_theta_elem<32>(c, P);
-        theta::theta_combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_vslot_ptr, d_vslot, d_partJ, d_partq,
+        theta::theta_combine_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, tbk.vslot_ptr, tbk.vslot, d_partJ, d_partq,
                                                                    c.d_eprow, d_Th, d_Abar);
         const int w2 = P * (r + 2);
         // output layer: dW_out += Abar Bfwd, db_out += sum_p s qbar

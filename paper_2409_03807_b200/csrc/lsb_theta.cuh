@@ -193,14 +193,16 @@ __device__ __forceinline__ float ddot9(const float* a, const float* b) {
 }
 
 // Element pass of the backward.  CTA = (block of tets, GP = 128 / R points); thread
-// (point pl, direction c).  Per tet and point, lane c forms dF of J_c and W_c and
+// (point pl, direction c).  Tets go in batches of R: first thread (pl, t) forms, once per
+// (tet, point), F, cof(F), the SNH derivatives and the gbar HVP's local forces
+// (potential_gradient backward) into shared memory; then, per tet of the batch, lane c
+// forms dF of J_c and W_c and
 //   * the HVP of W_c -> local forces, accumulated as Jbar (x 2) in the block's slot
 //     accumulators (column c owned by this thread: race-free, tet order);
 //   * its share V_c of the third-contraction vector (snh_third_contraction,
-//     energy.cpp:303-320, is linear in M = sym(A B^T) / 2, so it splits over columns),
-//     plus component c (< 9) of the gbar HVP; V = sum_c V_c by an xor butterfly over
-//     the point's lanes (all lanes get the identical sum), and lane c (< 12) adds local
-//     dof c of vol B^T V to qbar.
+//     energy.cpp:303-320, is linear in M = sym(A B^T) / 2, so it splits over columns);
+//     V = sum_c V_c by an xor butterfly over the point's lanes (identical on every lane),
+//     and lanes own local dofs d = c, c + R, ... (< 12) of vol B^T V + the gbar forces.
 template <int R>
 __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const float* rec, const int* blk_tet0,
                                                         const int* blk_vptr, const short* tet_loc,
@@ -210,8 +212,10 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
                                                         float* partq) {
     constexpr int GP = 128 / R;
     constexpr int TBMAX = 48;
+    constexpr int NB = 34;  // per (tet, point) batch record: F 9, cof 9, psiI, psiII, psiIII, psiJ, gbar forces 12
     __shared__ __align__(16) float sh_rec[TBMAX][12];
     __shared__ short sh_loc[TBMAX][8];
+    __shared__ float sh_b[R][GP][NB];
     extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
     const int pl = tid / R, c = tid % R;
@@ -240,9 +244,8 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
     const bool live = p0 + pl < P;
     const float* Jp = Jv + (size_t)(p0 + pl) * R + c;
     const float* Wp = Wv + (size_t)(p0 + pl) * R + c;
-    const float* Gp = Gb + (p0 + pl);
     const size_t jstride = (size_t)P * R;
-    float jn[12], wn[12], gn[12];
+    float jn[12], wn[12];
     if (live && e0 < e1) {
         const int4 t = __ldg(tets + e0);
         const int vv[4] = {t.x, t.y, t.z, t.w};
@@ -253,153 +256,194 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
                 const size_t row = (size_t)vv[k] * 3 + a;
                 jn[k * 3 + a] = __ldg(Jp + row * jstride);
                 wn[k * 3 + a] = __ldg(Wp + row * jstride);
-                gn[k * 3 + a] = __ldg(Gp + row * P);
             }
     }
-    for (int e = e0; e < e1; ++e) {
-        float V[9];
+    for (int eb = e0; eb < e1; eb += R) {
+        // ---- batch phase: thread (pl, t = c) handles tet eb + c for point pl
+        {
+            const int e = eb + c;
+            if (live && e < e1) {
+                float rc[12], uu[12], gu[12];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) V[k] = 0.f;
-        float rc[12];
+                for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
+                const int4 tt = __ldg(tets + e);
+                const int vv[4] = {tt.x, tt.y, tt.z, tt.w};
 #pragma unroll
-        for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
-        if (live) {
-            float ju[12], wu[12], gu[12], uu[12];
-#pragma unroll
-            for (int q = 0; q < 12; ++q) {
-                ju[q] = jn[q];
-                wu[q] = wn[q];
-                gu[q] = gn[q];
-            }
-            if (e + 1 < e1) {
-                const int4 t = __ldg(tets + e + 1);
-                const int vv[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < 4; ++k) {
+                    const int la = sh_loc[e - e0][4 + k];
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
-                        const size_t row = (size_t)vv[k] * 3 + a;
-                        jn[k * 3 + a] = __ldg(Jp + row * jstride);
-                        wn[k * 3 + a] = __ldg(Wp + row * jstride);
-                        gn[k * 3 + a] = __ldg(Gp + row * P);
+                        uu[k * 3 + a] = Us[(la * 3 + a) * GP + pl];
+                        gu[k * 3 + a] = __ldg(Gb + ((size_t)vv[k] * 3 + a) * P + p0 + pl);
                     }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int la = sh_loc[e - e0][4 + k];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) uu[k * 3 + a] = Us[(la * 3 + a) * GP + pl];
-            }
-            // ---- per point: F, cof, SNH derivatives (snh_core, energy.cpp:199-221)
-            float A[9], F[9], cof[9];
-            grad_of(uu, rc, A);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
-            bilin_cof(F, F, cof);  // = 2 cof(F)
-#pragma unroll
-            for (int k = 0; k < 9; ++k) cof[k] *= 0.5f;
-            const float vol = rc[9], mu = rc[10], lam = rc[11];
-            const float trA = A[0] + A[4] + A[8];
-            float qA = 0.f;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) qA = fmaf(A[k], A[k], qA);
-            const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
-            const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
-                               A[6] * (A[1] * A[5] - A[4] * A[2]);
-            const float jm1 = trA + m2 + detA;
-            const float uI = 4.f + 2.f * trA + qA;
-            const float iu = 1.f / uI;
-            const float psiI = 0.5f * mu * (1.f - iu);
-            const float psiII = 0.5f * mu * iu * iu;
-            const float psiIII = -mu * iu * iu * iu;
-            const float psiJ = lam * jm1 - 0.75f * mu;
-            // ---- HVP of W_c:  M = 2 psiI dW + psiII (gI.dW) gI + lam (gJ.dW) gJ + psiJ KJ dW
-            float dW[9], dcW[9];
-            grad_of(wu, rc, dW);
-            bilin_cof(F, dW, dcW);
-            const float s1 = 2.f * ddot9(F, dW), s2 = ddot9(cof, dW);
-            {
-                float M[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k)
-                    M[k] = vol * (2.f * psiI * dW[k] + psiII * s1 * 2.f * F[k] + lam * s2 * cof[k] + psiJ * dcW[k]);
-                // local forces B^T M, x 2 (Jbar = hj Hbar^T + K hj-bar = 2 K W)
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    float h0 = 0.f;
-#pragma unroll
-                    for (int k = 1; k < 4; ++k) {
-                        const float hk = 2.f * (M[a * 3] * rc[(k - 1) * 3] + M[a * 3 + 1] * rc[(k - 1) * 3 + 1] +
-                                                M[a * 3 + 2] * rc[(k - 1) * 3 + 2]);
-                        h0 -= hk;
-                        const int lv = sh_loc[e - e0][k];
-                        if (lv >= 0) accJ[((size_t)(lv * 3 + a) * GP + pl) * R + c] += hk;
-                    }
-                    const int lv0 = sh_loc[e - e0][0];
-                    if (lv0 >= 0) accJ[((size_t)(lv0 * 3 + a) * GP + pl) * R + c] += h0;
                 }
-            }
-            // ---- third contraction share of column c (A = J_c, B = W_c)
-            float dA[9], tmp[9];
-            grad_of(ju, rc, dA);
-            const float aI = 2.f * ddot9(F, dA), aJ = ddot9(cof, dA);
-            const float trM = ddot9(dA, dW), kJM = ddot9(dA, dcW), qII = aI * s1;
-            const float cI = 2.f * (psiIII * qII + 2.f * psiII * trM);  // coefficient of F (gI = 2F)
+                // F, cof(F), SNH derivatives (snh_core, energy.cpp:199-221)
+                float A[9], F[9], cof[9];
+                grad_of(uu, rc, A);
 #pragma unroll
-            for (int k = 0; k < 9; ++k)
-                V[k] = cI * F[k] + 2.f * psiII * (dA[k] * s1 + dW[k] * aI) + lam * (dcW[k] * aJ + kJM * cof[k]);
-            bilin_cof(F, dA, tmp);  // KJ dA
+                for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
+                bilin_cof(F, F, cof);
 #pragma unroll
-            for (int k = 0; k < 9; ++k) V[k] = fmaf(lam * s2, tmp[k], V[k]);
-            bilin_cof(dA, dW, tmp);  // j_third share
+                for (int k = 0; k < 9; ++k) cof[k] *= 0.5f;
+                const float vol = rc[9], mu = rc[10], lam = rc[11];
+                const float trA = A[0] + A[4] + A[8];
+                float qA = 0.f;
 #pragma unroll
-            for (int k = 0; k < 9; ++k) V[k] = fmaf(psiJ, tmp[k], V[k]);
-            // ---- component c of the gbar HVP (potential_gradient backward)
-            {
-                float dG[9], dcG[9];
+                for (int k = 0; k < 9; ++k) qA = fmaf(A[k], A[k], qA);
+                const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+                const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
+                                   A[6] * (A[1] * A[5] - A[4] * A[2]);
+                const float jm1 = trA + m2 + detA;
+                const float uI = 4.f + 2.f * trA + qA;
+                const float iu = 1.f / uI;
+                const float psiI = 0.5f * mu * (1.f - iu);
+                const float psiII = 0.5f * mu * iu * iu;
+                const float psiIII = -mu * iu * iu * iu;
+                const float psiJ = lam * jm1 - 0.75f * mu;
+                // gbar HVP -> local forces vol B^T (H gbar)
+                float dG[9], dcG[9], Mg[9];
                 grad_of(gu, rc, dG);
                 bilin_cof(F, dG, dcG);
                 const float t1 = 2.f * ddot9(F, dG), t2 = ddot9(cof, dG);
 #pragma unroll
                 for (int k = 0; k < 9; ++k)
-                    if (k % R == c)  // lanes c, c + R, ... own component k (R = 8 has fewer lanes than 9)
-                        V[k] += 2.f * psiI * dG[k] + psiII * t1 * 2.f * F[k] + lam * t2 * cof[k] + psiJ * dcG[k];
+                    Mg[k] = vol * (2.f * psiI * dG[k] + psiII * t1 * 2.f * F[k] + lam * t2 * cof[k] + psiJ * dcG[k]);
+                float* o = sh_b[c][pl];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    o[k] = F[k];
+                    o[9 + k] = cof[k];
+                }
+                o[18] = psiI;
+                o[19] = psiII;
+                o[20] = psiIII;
+                o[21] = psiJ;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    float h0 = 0.f;
+#pragma unroll
+                    for (int k = 1; k < 4; ++k) {
+                        const float hk = Mg[a * 3] * rc[(k - 1) * 3] + Mg[a * 3 + 1] * rc[(k - 1) * 3 + 1] +
+                                         Mg[a * 3 + 2] * rc[(k - 1) * 3 + 2];
+                        h0 -= hk;
+                        o[22 + k * 3 + a] = hk;
+                    }
+                    o[22 + a] = h0;
+                }
             }
-#pragma unroll
-            for (int k = 0; k < 9; ++k) V[k] *= vol;
         }
-        // V = sum over the point's R lanes (xor butterfly: identical on every lane)
+        __syncthreads();
+        const int nb = min(R, e1 - eb);
+        for (int tb = 0; tb < nb; ++tb) {
+            const int e = eb + tb;
+            float V[9];
 #pragma unroll
-        for (int off = R / 2; off >= 1; off >>= 1)
+            for (int k = 0; k < 9; ++k) V[k] = 0.f;
+            float rc[12];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) V[k] += __shfl_xor_sync(0xffffffffu, V[k], off);
-        if (live) {
-            // local dofs d = c, c + R, ... (< 12) = (corner d / 3, component d % 3) of vol B^T V
+            for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
+            const float* bq = sh_b[tb][pl];
+            if (live) {
+                float ju[12], wu[12];
 #pragma unroll
-            for (int d0 = 0; d0 < 12; d0 += R) {
-                const int d = d0 + c;
-                if (d < 12) {
-                    float hv = 0.f;
+                for (int q = 0; q < 12; ++q) {
+                    ju[q] = jn[q];
+                    wu[q] = wn[q];
+                }
+                if (e + 1 < e1) {
+                    const int4 t = __ldg(tets + e + 1);
+                    const int vv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const size_t row = (size_t)vv[k] * 3 + a;
+                            jn[k * 3 + a] = __ldg(Jp + row * jstride);
+                            wn[k * 3 + a] = __ldg(Wp + row * jstride);
+                        }
+                }
+                float F[9], cof[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    F[k] = bq[k];
+                    cof[k] = bq[9 + k];
+                }
+                const float psiI = bq[18], psiII = bq[19], psiIII = bq[20], psiJ = bq[21];
+                const float vol = rc[9], lam = rc[11];
+                // ---- HVP of W_c:  M = 2 psiI dW + psiII (gI.dW) gI + lam (gJ.dW) gJ + psiJ KJ dW
+                float dW[9], dcW[9];
+                grad_of(wu, rc, dW);
+                bilin_cof(F, dW, dcW);
+                const float s1 = 2.f * ddot9(F, dW), s2 = ddot9(cof, dW);
+                {
+                    float M[9];
+#pragma unroll
+                    for (int k = 0; k < 9; ++k)
+                        M[k] = vol * (2.f * psiI * dW[k] + psiII * s1 * 2.f * F[k] + lam * s2 * cof[k] + psiJ * dcW[k]);
+                    // local forces B^T M, x 2 (Jbar = hj Hbar^T + K hj-bar = 2 K W)
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
                         float h0 = 0.f;
 #pragma unroll
                         for (int k = 1; k < 4; ++k) {
-                            const float hk = V[a * 3] * rc[(k - 1) * 3] + V[a * 3 + 1] * rc[(k - 1) * 3 + 1] +
-                                             V[a * 3 + 2] * rc[(k - 1) * 3 + 2];
+                            const float hk = 2.f * (M[a * 3] * rc[(k - 1) * 3] + M[a * 3 + 1] * rc[(k - 1) * 3 + 1] +
+                                                    M[a * 3 + 2] * rc[(k - 1) * 3 + 2]);
                             h0 -= hk;
-                            if (d == k * 3 + a) hv = hk;
+                            const int lv = sh_loc[e - e0][k];
+                            if (lv >= 0) accJ[((size_t)(lv * 3 + a) * GP + pl) * R + c] += hk;
                         }
-                        if (d == a) hv = h0;
+                        const int lv0 = sh_loc[e - e0][0];
+                        if (lv0 >= 0) accJ[((size_t)(lv0 * 3 + a) * GP + pl) * R + c] += h0;
                     }
-                    const int lv = sh_loc[e - e0][d / 3];
-                    if (lv >= 0) accq[(lv * 3 + d % 3) * GP + pl] += hv;
+                }
+                // ---- third contraction share of column c (A = J_c, B = W_c)
+                float dA[9], tmp[9], x[9];
+                grad_of(ju, rc, dA);
+                const float aI = 2.f * ddot9(F, dA), aJ = ddot9(cof, dA);
+                const float trM = ddot9(dA, dW), kJM = ddot9(dA, dcW), qII = aI * s1;
+                const float cI = 2.f * (psiIII * qII + 2.f * psiII * trM);  // coefficient of F (gI = 2F)
+                // lam s2 KJ dA + psiJ j_third(dA, dW) = bilin_cof(dA, lam s2 F + psiJ dW)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) x[k] = lam * s2 * F[k] + psiJ * dW[k];
+                bilin_cof(dA, x, tmp);
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    V[k] = cI * F[k] + 2.f * psiII * (dA[k] * s1 + dW[k] * aI) + lam * (dcW[k] * aJ + kJM * cof[k]) +
+                           tmp[k];
+            }
+            // V = sum over the point's R lanes (xor butterfly: identical on every lane)
+#pragma unroll
+            for (int off = R / 2; off >= 1; off >>= 1)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) V[k] += __shfl_xor_sync(0xffffffffu, V[k], off);
+            if (live) {
+                // local dofs d = c, c + R, ... (< 12) = (corner d / 3, component d % 3) of vol B^T V
+#pragma unroll
+                for (int d0 = 0; d0 < 12; d0 += R) {
+                    const int d = d0 + c;
+                    if (d < 12) {
+                        float hv = 0.f;
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            float h0 = 0.f;
+#pragma unroll
+                            for (int k = 1; k < 4; ++k) {
+                                const float hk = V[a * 3] * rc[(k - 1) * 3] + V[a * 3 + 1] * rc[(k - 1) * 3 + 1] +
+                                                 V[a * 3 + 2] * rc[(k - 1) * 3 + 2];
+                                h0 -= hk;
+                                if (d == k * 3 + a) hv = hk;
+                            }
+                            if (d == a) hv = h0;
+                        }
+                        const int lv = sh_loc[e - e0][d / 3];
+                        if (lv >= 0) accq[(lv * 3 + d % 3) * GP + pl] += rc[9] * hv + bq[22 + d];
+                    }
                 }
             }
+            __syncwarp();  // accq slots are revisited by other lanes of this point at the next tet
         }
-        __syncwarp();  // accq slots are revisited by other lanes of this point at the next tet
+        __syncthreads();  // sh_b is rewritten by the next batch
     }
-    __syncthreads();
     for (int i = tid; i < nv * 3 * GP * R; i += 128) {
         const int cc = i % R, pp = (i / R) % GP, row = i / (R * GP);
         if (p0 + pp < P) partJ[(((size_t)(v0 * 3) + row) * P + p0 + pp) * R + cc] = accJ[i];
