@@ -616,15 +616,35 @@ __global__ void __launch_bounds__(256) inertia_hess_kernel(int n, int P, int r, 
     if (tid < npair) C[(size_t)p * npair + tid] += inv_dt2 * acc;
 }
 
-// Element Hessian contraction, v2.  CTA = (block of kTB tets, GP = 128/R points);
-// per tet: thread (point pl, direction b) forms dF_b, alpha_b, beta_b and
-// M_b = 2 psi_I dF_b + psi_J dcof[dF_b] into smem (double-buffered, one barrier per
-// tet); threads b < 12 add one force component each to the point's vertex
-// accumulators (same summation order as v1).  The contraction
-//   C_ab += vol (dF_a : M_b) + vol psi_II alpha_a alpha_b + vol lambda beta_a beta_b
-// is register-blocked: each thread owns 4 x 4 (a, b) entries of one point's full
-// R x R matrix and reads 4 dF_a and 4 M_b rows as float4 (24 vector loads for 16
-// entries); the a <= b entries are written out (pair order of v1).
+// Element Hessian contraction.  CTA = (block of kTB tets, GP = 128/R points).  Tets go
+// in batches of R: first thread (point pl, t) forms, once per (tet, point), F, cof(F),
+// the SNH derivatives and the element's elastic forces vol B^T P(F) into shared memory;
+// then per tet thread (pl, direction b) forms the K = 11 rows of its column of
+//   D  = [dF_b (9), alpha_b = gI.dF_b, beta_b = gJ.dF_b]
+//   M' = vol [2 psi_I dF_b + psi_J dcof[dF_b], psi_II alpha_b, lambda beta_b]
+// (double-buffered, one barrier per tet) and lanes own local dofs b, b + R, ... (< 12)
+// of the force accumulation (tet order, as the reference's assemble).  The contraction
+//   C_ab += sum_k D[k][a] M'[k][b]
+//         = vol (dF_a : M_b) + vol psi_II alpha_a alpha_b + vol lambda beta_a beta_b
+// runs on the tensor cores as mma.sync m16n8k8 TF32 with 3xTF32 splitting (fp32-level
+// accuracy), fragments read straight from the [dir][12] rows (conflict-free); each warp
+// owns GP / 4 points; the a <= b entries are written out.
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    return u;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    hi = tf32_bits(x);
+    lo = tf32_bits(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32_16x8x8(float* c, const uint32_t* a, const uint32_t* b) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 template <int R>
 __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const float* rec, const int* blk_tet0,
                                                         const int* blk_vptr, const short* tet_loc,
@@ -632,16 +652,16 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
                                                         const short* tet_aloc, const float* U, const float* Jv,
                                                         int P, float* Cpart, float* gpart) {
     constexpr int GP = 128 / R;               // points per CTA
-    constexpr int NB = R / 4;                 // 4-wide blocks per side
-    constexpr int NBLK = GP * NB * NB;        // 4x4 blocks per CTA
-    constexpr int BPT = (NBLK + 127) / 128;   // blocks per thread
     constexpr int NPAIR = R * (R + 1) / 2;
-    __shared__ __align__(16) float sh_dF[2][GP][R][12];
-    __shared__ __align__(16) float sh_M[2][GP][R][12];
-    __shared__ __align__(16) float sh_ab[2][GP][R][2];
-    __shared__ __align__(16) float sh_sc[2][GP][4];
+    constexpr int NH = 33;                    // batch record: F 9, cof 9, psiI, psiII, psiJ, forces 12
+    constexpr int PPW = GP / 4;               // points per warp (tensor-core contraction)
+    constexpr int MT = R >= 16 ? R / 16 : 1;  // 16-row m tiles (R = 8: rows 8..15 are zero)
+    constexpr int NT = R / 8;                 // 8-column n tiles
+    __shared__ __align__(16) float sh_dF[2][GP][R][12];  // D rows per direction (k 0..11)
+    __shared__ __align__(16) float sh_M[2][GP][R][12];   // M' rows per direction
     __shared__ __align__(16) float sh_rec[kTB][12];   // the block's records
     __shared__ short sh_loc[kTB][8];                  // free slots (4), touched slots (4)
+    __shared__ float sh_b[R][GP][NH];
     extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
     const int pl = tid / R, b = tid % R;
@@ -664,17 +684,16 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
         sh_loc[i >> 2][i & 3] = tet_loc[(size_t)e0 * 4 + i];
         sh_loc[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i];
     }
-    int cpl[BPT], cbi[BPT], cbj[BPT];
-    float cacc[BPT][16];
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+    float cacc[PPW][MT][NT][4];
 #pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-        const int id = tid + 128 * k;
-        cpl[k] = id < NBLK ? id / (NB * NB) : -1;
-        cbi[k] = (id % (NB * NB)) / NB;
-        cbj[k] = id % NB;
+    for (int pp = 0; pp < PPW; ++pp)
 #pragma unroll
-        for (int q = 0; q < 16; ++q) cacc[k][q] = 0.f;
-    }
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cacc[pp][mt][nt][q] = 0.f;
     cp_async_wait_all();
     __syncthreads();
     const bool live = p0 + pl < P;
@@ -691,102 +710,60 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
 #pragma unroll
             for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
     }
-    for (int e = e0; e < e1; ++e) {
-        const int buf = (e - e0) & 1;
-        float rc[12];
+    for (int eb = e0; eb < e1; eb += R) {
+        // ---- batch phase: thread (pl, t = b) forms the per-(tet, point) quantities of tet eb + b
+        {
+            const int e = eb + b;
+            if (live && e < e1) {
+                float rc[12], uu[12];
 #pragma unroll
-        for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
-        if (live) {
-            int la[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) la[k] = sh_loc[e - e0][4 + k];
-            float duc[12];
-#pragma unroll
-            for (int q = 0; q < 12; ++q) duc[q] = dun[q];
-            if (e + 1 < e1) {
-                const int4 t = __ldg(tets + e + 1);
-                const int vv[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-                    for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
-            }
-            float A[9], dA[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                float du[4], uu[4];
+                for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    uu[k] = Us[(la[k] * 3 + a) * GP + pl];
-                    du[k] = duc[k * 3 + a];
+                    const int la = sh_loc[e - e0][4 + k];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) uu[k * 3 + a] = Us[(la * 3 + a) * GP + pl];
                 }
+                float A[9];
 #pragma unroll
-                for (int c2 = 0; c2 < 3; ++c2) {
-                    A[a * 3 + c2] = (uu[1] - uu[0]) * rc[c2] + (uu[2] - uu[0]) * rc[3 + c2] + (uu[3] - uu[0]) * rc[6 + c2];
-                    dA[a * 3 + c2] = (du[1] - du[0]) * rc[c2] + (du[2] - du[0]) * rc[3 + c2] + (du[3] - du[0]) * rc[6 + c2];
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int c2 = 0; c2 < 3; ++c2)
+                        A[a * 3 + c2] = (uu[3 + a] - uu[a]) * rc[c2] + (uu[6 + a] - uu[a]) * rc[3 + c2] +
+                                        (uu[9 + a] - uu[a]) * rc[6 + c2];
+                float F[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
+                float cof[9];
+                cof[0] = F[4] * F[8] - F[7] * F[5];
+                cof[3] = F[7] * F[2] - F[1] * F[8];
+                cof[6] = F[1] * F[5] - F[4] * F[2];
+                cof[1] = F[5] * F[6] - F[8] * F[3];
+                cof[4] = F[8] * F[0] - F[2] * F[6];
+                cof[7] = F[2] * F[3] - F[5] * F[0];
+                cof[2] = F[3] * F[7] - F[6] * F[4];
+                cof[5] = F[6] * F[1] - F[0] * F[7];
+                cof[8] = F[0] * F[4] - F[3] * F[1];
+                const float vol = rc[9], mu = rc[10], lam = rc[11];
+                const float trA = A[0] + A[4] + A[8];
+                float q = 0.f;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) q += A[k] * A[k];
+                const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+                const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
+                                   A[6] * (A[1] * A[5] - A[4] * A[2]);
+                const float jm1 = trA + m2 + detA;
+                const float uI = 4.f + 2.f * trA + q;  // I + 1
+                float* o = sh_b[b][pl];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    o[k] = F[k];
+                    o[9 + k] = cof[k];
                 }
-            }
-            float F[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
-            float cof[9];
-            cof[0] = F[4] * F[8] - F[7] * F[5];
-            cof[3] = F[7] * F[2] - F[1] * F[8];
-            cof[6] = F[1] * F[5] - F[4] * F[2];
-            cof[1] = F[5] * F[6] - F[8] * F[3];
-            cof[4] = F[8] * F[0] - F[2] * F[6];
-            cof[7] = F[2] * F[3] - F[5] * F[0];
-            cof[2] = F[3] * F[7] - F[6] * F[4];
-            cof[5] = F[6] * F[1] - F[0] * F[7];
-            cof[8] = F[0] * F[4] - F[3] * F[1];
-            const float vol = rc[9], mu = rc[10], lam = rc[11];
-            const float trA = A[0] + A[4] + A[8];
-            float q = 0.f;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) q += A[k] * A[k];
-            const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
-            const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
-                               A[6] * (A[1] * A[5] - A[4] * A[2]);
-            const float jm1 = trA + m2 + detA;
-            const float uI = 4.f + 2.f * trA + q;  // I + 1
-            const float psiI = 0.5f * mu * (1.f - 1.f / uI);
-            const float psiII = 0.5f * mu / (uI * uI);
-            const float psiJ = lam * jm1 - 0.75f * mu;
-            float alpha = 0.f, beta = 0.f;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                alpha += 2.f * F[k] * dA[k];
-                beta += cof[k] * dA[k];
-            }
-            float dc[9];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int ci = (c + 1) % 3, cj = (c + 2) % 3;
-                const float a1[3] = {F[ci], F[3 + ci], F[6 + ci]}, a2[3] = {F[cj], F[3 + cj], F[6 + cj]};
-                const float d1[3] = {dA[ci], dA[3 + ci], dA[6 + ci]}, d2[3] = {dA[cj], dA[3 + cj], dA[6 + cj]};
-                dc[0 * 3 + c] = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
-                dc[1 * 3 + c] = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
-                dc[2 * 3 + c] = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
-            }
-            float* dFo = sh_dF[buf][pl][b];
-            float* Mo = sh_M[buf][pl][b];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                dFo[k] = dA[k];
-                Mo[k] = 2.f * psiI * dA[k] + psiJ * dc[k];
-            }
-            dFo[9] = dFo[10] = dFo[11] = 0.f;
-            Mo[9] = Mo[10] = Mo[11] = 0.f;
-            sh_ab[buf][pl][b][0] = alpha;
-            sh_ab[buf][pl][b][1] = beta;
-            if (b == 12 % R) {
-                sh_sc[buf][pl][0] = vol * psiII;
-                sh_sc[buf][pl][1] = vol * lam;
-                sh_sc[buf][pl][2] = vol;
-            }
-            // elastic forces: threads b < 12 own one (vertex, component) each (row of P
-            // selected with compile-time indices only: no local-memory arrays)
-            if (b < 12 || R < 12) {
+                o[18] = 0.5f * mu * (1.f - 1.f / uI);
+                o[19] = 0.5f * mu / (uI * uI);
+                o[20] = lam * jm1 - 0.75f * mu;
+                // elastic forces vol B^T P (cancellation-free first Piola stress)
                 float cA[9];
                 cA[0] = A[4] * A[8] - A[7] * A[5];
                 cA[3] = A[7] * A[2] - A[1] * A[8];
@@ -798,90 +775,160 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
                 cA[5] = A[6] * A[1] - A[0] * A[7];
                 cA[8] = A[0] * A[4] - A[3] * A[1];
                 const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) / (4.f * uI), c3 = lam * jm1;
-                for (int fk = b; fk < 12; fk += R) {
-                    const int kk = fk / 3, a = fk % 3;
-                    float Pa[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int aa = 0; aa < 3; ++aa)
-                        if (aa == a) {
+                for (int aa = 0; aa < 3; ++aa) {
+                    float Pa[3];
 #pragma unroll
-                            for (int bb = 0; bb < 3; ++bb) {
-                                const float id = aa == bb ? 1.f : 0.f;
-                                Pa[bb] = c1 * (A[aa * 3 + bb] + A[bb * 3 + aa] - trA * id - cA[aa * 3 + bb]) +
-                                         c2 * F[aa * 3 + bb] + c3 * cof[aa * 3 + bb];
-                            }
-                        }
+                    for (int bb = 0; bb < 3; ++bb) {
+                        const float id = aa == bb ? 1.f : 0.f;
+                        Pa[bb] = c1 * (A[aa * 3 + bb] + A[bb * 3 + aa] - trA * id - cA[aa * 3 + bb]) +
+                                 c2 * F[aa * 3 + bb] + c3 * cof[aa * 3 + bb];
+                    }
                     float hc[3];
 #pragma unroll
                     for (int c = 0; c < 3; ++c)
                         hc[c] = vol * (Pa[0] * rc[c * 3 + 0] + Pa[1] * rc[c * 3 + 1] + Pa[2] * rc[c * 3 + 2]);
-                    float hv;
-                    if (kk == 0) {
-                        float s0 = 0.f;
-                        s0 += hc[0];
-                        s0 += hc[1];
-                        s0 += hc[2];
-                        hv = -s0;
-                    } else {
-                        hv = kk == 1 ? hc[0] : (kk == 2 ? hc[1] : hc[2]);
-                    }
-                    const int lv = sh_loc[e - e0][kk];
-                    if (lv >= 0) accg[(lv * 3 + a) * GP + pl] += hv;
+                    float s0 = 0.f;
+                    s0 += hc[0];
+                    s0 += hc[1];
+                    s0 += hc[2];
+                    o[21 + aa] = -s0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) o[21 + (c + 1) * 3 + aa] = hc[c];
                 }
             }
         }
         __syncthreads();
+        const int nbt = min(R, e1 - eb);
+        for (int tb = 0; tb < nbt; ++tb) {
+            const int e = eb + tb;
+            const int buf = (e - e0) & 1;
+            if (live) {
+                const float* bq = sh_b[tb][pl];
+                float rc[9];
 #pragma unroll
-        for (int k = 0; k < BPT; ++k) {
-            const int pc = cpl[k];
-            if (pc >= 0 && p0 + pc < P) {
-                float dFr[4][12], Mr[4][12];
+                for (int qq = 0; qq < 9; ++qq) rc[qq] = sh_rec[e - e0][qq];
+                float duc[12];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float4* s1 = reinterpret_cast<const float4*>(sh_dF[buf][pc][4 * cbi[k] + i]);
-                    const float4* s2 = reinterpret_cast<const float4*>(sh_M[buf][pc][4 * cbj[k] + i]);
+                for (int q = 0; q < 12; ++q) duc[q] = dun[q];
+                if (e + 1 < e1) {
+                    const int4 t = __ldg(tets + e + 1);
+                    const int vv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
-                    for (int v = 0; v < 3; ++v) {
-                        const float4 x = s1[v], y = s2[v];
-                        dFr[i][4 * v] = x.x; dFr[i][4 * v + 1] = x.y; dFr[i][4 * v + 2] = x.z; dFr[i][4 * v + 3] = x.w;
-                        Mr[i][4 * v] = y.x; Mr[i][4 * v + 1] = y.y; Mr[i][4 * v + 2] = y.z; Mr[i][4 * v + 3] = y.w;
+                    for (int k = 0; k < 4; ++k)
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
+                }
+                float dA[9];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int c2 = 0; c2 < 3; ++c2)
+                        dA[a * 3 + c2] = (duc[3 + a] - duc[a]) * rc[c2] + (duc[6 + a] - duc[a]) * rc[3 + c2] +
+                                         (duc[9 + a] - duc[a]) * rc[6 + c2];
+                float F[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) F[k] = bq[k];
+                float alpha = 0.f, beta = 0.f;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    alpha += 2.f * F[k] * dA[k];
+                    beta += bq[9 + k] * dA[k];
+                }
+                const float psiI = bq[18], psiJ = bq[20];
+                float dc[9];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int ci = (c + 1) % 3, cj = (c + 2) % 3;
+                    const float a1[3] = {F[ci], F[3 + ci], F[6 + ci]}, a2[3] = {F[cj], F[3 + cj], F[6 + cj]};
+                    const float d1[3] = {dA[ci], dA[3 + ci], dA[6 + ci]}, d2[3] = {dA[cj], dA[3 + cj], dA[6 + cj]};
+                    dc[0 * 3 + c] = d1[1] * a2[2] - d1[2] * a2[1] + a1[1] * d2[2] - a1[2] * d2[1];
+                    dc[1 * 3 + c] = d1[2] * a2[0] - d1[0] * a2[2] + a1[2] * d2[0] - a1[0] * d2[2];
+                    dc[2 * 3 + c] = d1[0] * a2[1] - d1[1] * a2[0] + a1[0] * d2[1] - a1[1] * d2[0];
+                }
+                const float vol = sh_rec[e - e0][9], lam = sh_rec[e - e0][11];
+                float4* dFo = reinterpret_cast<float4*>(sh_dF[buf][pl][b]);
+                float4* Mo = reinterpret_cast<float4*>(sh_M[buf][pl][b]);
+                float Mv[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) Mv[k] = vol * (2.f * psiI * dA[k] + psiJ * dc[k]);
+                dFo[0] = make_float4(dA[0], dA[1], dA[2], dA[3]);
+                dFo[1] = make_float4(dA[4], dA[5], dA[6], dA[7]);
+                dFo[2] = make_float4(dA[8], alpha, beta, 0.f);
+                Mo[0] = make_float4(Mv[0], Mv[1], Mv[2], Mv[3]);
+                Mo[1] = make_float4(Mv[4], Mv[5], Mv[6], Mv[7]);
+                Mo[2] = make_float4(Mv[8], vol * bq[19] * alpha, vol * lam * beta, 0.f);
+                // elastic forces: lanes own local dofs b, b + R, ... (< 12), tet order
+#pragma unroll
+                for (int d0 = 0; d0 < 12; d0 += R) {
+                    const int d = d0 + b;
+                    if (d < 12) {
+                        const int lv = sh_loc[e - e0][d / 3];
+                        if (lv >= 0) accg[(lv * 3 + d % 3) * GP + pl] += bq[21 + d];
                     }
                 }
-                const float4 abA0 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbi[k]])[0];
-                const float4 abA1 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbi[k]])[1];
-                const float4 abB0 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbj[k]])[0];
-                const float4 abB1 = reinterpret_cast<const float4*>(sh_ab[buf][pc][4 * cbj[k]])[1];
-                const float al_a[4] = {abA0.x, abA0.z, abA1.x, abA1.z}, be_a[4] = {abA0.y, abA0.w, abA1.y, abA1.w};
-                const float al_b[4] = {abB0.x, abB0.z, abB1.x, abB1.z}, be_b[4] = {abB0.y, abB0.w, abB1.y, abB1.w};
-                const float4 sc = reinterpret_cast<const float4*>(sh_sc[buf][pc])[0];
+            }
+            __syncthreads();
+            // tensor-core contraction: warp owns points warp * PPW + pp; A = D^T (dir x k),
+            // B = M' (k x dir); k-step 1 = rows 0..7, k-step 2 = rows 8..11 (12..15 zero)
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+            for (int pp = 0; pp < PPW; ++pp) {
+                const int pc = warp * PPW + pp;
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float s = 0.f;
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int k0 = ks * 8;
+                    uint32_t ah[MT][4], al[MT][4], bh[NT][2], bl[NT][2];
 #pragma unroll
-                        for (int k9 = 0; k9 < 9; ++k9) s += dFr[i][k9] * Mr[j][k9];
-                        cacc[k][i * 4 + j] += sc.z * s + sc.x * al_a[i] * al_b[j] + sc.y * be_a[i] * be_b[j];
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const float* r0 = sh_dF[buf][pc][mt * 16 + g];
+                        const float x0 = r0[k0 + t4];
+                        const float x2 = ks == 0 ? r0[k0 + 4 + t4] : 0.f;
+                        float x1 = 0.f, x3 = 0.f;
+                        if (R >= 16) {
+                            const float* r1 = sh_dF[buf][pc][mt * 16 + 8 + g];
+                            x1 = r1[k0 + t4];
+                            x3 = ks == 0 ? r1[k0 + 4 + t4] : 0.f;
+                        }
+                        split_tf32(x0, ah[mt][0], al[mt][0]);
+                        split_tf32(x1, ah[mt][1], al[mt][1]);
+                        split_tf32(x2, ah[mt][2], al[mt][2]);
+                        split_tf32(x3, ah[mt][3], al[mt][3]);
                     }
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const float* rb = sh_M[buf][pc][nt * 8 + g];
+                        const float y0 = rb[k0 + t4];
+                        const float y1 = ks == 0 ? rb[k0 + 4 + t4] : 0.f;
+                        split_tf32(y0, bh[nt][0], bl[nt][0]);
+                        split_tf32(y1, bh[nt][1], bl[nt][1]);
+                    }
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            mma_tf32_16x8x8(cacc[pp][mt][nt], al[mt], bh[nt]);
+                            mma_tf32_16x8x8(cacc[pp][mt][nt], ah[mt], bl[nt]);
+                            mma_tf32_16x8x8(cacc[pp][mt][nt], ah[mt], bh[nt]);
+                        }
+                }
             }
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-        const int pc = cpl[k];
-        if (pc >= 0 && p0 + pc < P) {
+    for (int pp = 0; pp < PPW; ++pp) {
+        const int pc = warp * PPW + pp;
+        if (p0 + pc >= P) continue;
+        float* Co = Cpart + ((size_t)blk * P + p0 + pc) * NPAIR;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int a = 4 * cbi[k] + i, bb = 4 * cbj[k] + j;
-                    if (a <= bb) {
-                        const int pr = a * R - a * (a - 1) / 2 + (bb - a);
-                        Cpart[((size_t)blk * P + p0 + pc) * NPAIR + pr] = cacc[k][i * 4 + j];
-                    }
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int a = mt * 16 + g + (q >= 2 ? 8 : 0), bb = nt * 8 + 2 * t4 + (q & 1);
+                    if (a < R && a <= bb) Co[a * R - a * (a - 1) / 2 + (bb - a)] = cacc[pp][mt][nt][q];
                 }
-        }
     }
     for (int i = tid; i < nv * 3 * GP; i += 128) {
         const int pp = i % GP;
