@@ -507,6 +507,37 @@ int orc_simulate(void* p, const double* gravity, double epsilon, int max_iters, 
     }
 }
 
+// One reduced_step (reduced_solver.cpp:235-277) with an explicit frame: pin positions (V x 3)
+// and the external force on the free DOFs (frame_at, scenario.cpp:187-205).
+int orc_reduced_step(void* p, const double* pin_positions, const double* force, double epsilon, int max_iters,
+                     int max_ls, int history, double dt, int quasi_static, double* positions, double* velocities,
+                     double* z, int* code, int* iters) {
+    try {
+        auto* c = static_cast<Ctx*>(p);
+        SolverConfig cfg;
+        cfg.epsilon = epsilon;
+        cfg.max_iters = max_iters;
+        cfg.max_linesearch = max_ls;
+        cfg.lbfgs_history = history;
+        cfg.dt = dt;
+        const int V = c->mesh.V, r = c->model.r, n = c->mesh.num_dofs();
+        SimState st;
+        st.positions.assign(positions, positions + 3 * V);
+        st.velocities.assign(velocities, velocities + 3 * V);
+        st.z.assign(z, z + r);
+        const std::vector<double> pins(pin_positions, pin_positions + 3 * V), f(force, force + n);
+        const ExitReport rep = reduced_step(st, pins, f, c->model, c->mesh, c->mat, c->mass, cfg, quasi_static != 0);
+        *code = rep.code;
+        *iters = rep.iterations;
+        std::memcpy(positions, st.positions.data(), 3 * V * 8);
+        std::memcpy(velocities, st.velocities.data(), 3 * V * 8);
+        std::memcpy(z, st.z.data(), r * 8);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
 // ---- losses -------------------------------------------------------------------------------------
 int orc_reduced_potential_hessian(void* p, const double* z, double* H) {
     try {

@@ -77,6 +77,8 @@ def lib():
             "orc_lipschitz_loss2": (C.c_int, [C.c_void_p, C.c_int, _D, _D, C.c_int, _D]),
             "orc_elastic_third_contraction": (C.c_int, [C.c_void_p, _D, C.c_int, _D, _D, _D]),
             "orc_lipschitz_loss2_grad": (C.c_int, [C.c_void_p, C.c_int, _D, _D, C.c_int, _D, _D]),
+            "orc_reduced_step": (C.c_int, [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double,
+                                           C.c_int, _D, _D, _D, _I, _I]),
             "orc_hardware_threads": (C.c_int, []),
         }
         for name, (res, args) in sigs.items():
@@ -310,6 +312,19 @@ class Oracle:
                                 _d(gn), _d(ms), _i(ev), _i(vev), _d(zt)))
         return dict(positions=pos, velocities=vel, z=zz, codes=codes, iterations=iters, gnorm=gn, wall_ms=ms,
                     grad_evals=ev, value_evals=vev, z_traj=zt)
+
+    def reduced_step(self, positions, velocities, z, pin_positions, force, cfg, quasi_static=False):
+        """One reduced_step with an explicit frame; returns (positions, velocities, z, code, iters)."""
+        pos = np.ascontiguousarray(positions, np.float64).copy()
+        vel = np.ascontiguousarray(velocities, np.float64).copy()
+        zz = np.ascontiguousarray(z, np.float64).copy()
+        pins = np.ascontiguousarray(pin_positions, np.float64)
+        f = np.ascontiguousarray(force, np.float64)
+        code, iters = C.c_int(), C.c_int()
+        _chk(lib().orc_reduced_step(self.h, _d(pins), _d(f), cfg.epsilon, cfg.max_iters, cfg.max_linesearch,
+                                    cfg.lbfgs_history, cfg.dt, int(quasi_static), _d(pos), _d(vel), _d(zz),
+                                    C.byref(code), C.byref(iters)))
+        return pos, vel, zz, code.value, iters.value
 
     def reduced_potential_hessian(self, z):
         H = np.zeros((self.r, self.r))
