@@ -694,3 +694,15 @@ def lipschitz_loss(system: ReducedSystem, pairs: Sequence[Tuple[np.ndarray, np.n
     Z1 = np.stack([p[0] for p in pairs])
     Z2 = np.stack([p[1] for p in pairs])
     return system.lipschitz_loss(Z1, Z2)
+
+
+def lipschitz_loss_grad(system: ReducedSystem, pairs: Sequence[Tuple[np.ndarray, np.ndarray]], order: int = 2):
+    """build_lipschitz_loss(..., order, pot) + Tape::backward + param_gradient
+    (losses.cpp:196-213, tape.cpp:46-79) for order 2: (loss, [(dW, db) per decoder layer])."""
+    if order != 2:
+        raise ValueError("lipschitz loss: the device path implements order 2")
+    if len(pairs) == 0:
+        raise ValueError("lipschitz loss: no pairs")
+    Z1 = np.stack([p[0] for p in pairs])
+    Z2 = np.stack([p[1] for p in pairs])
+    return system.lipschitz_loss_grad(Z1, Z2)
