@@ -3,6 +3,7 @@
 // before every timed step so W_out is re-read from HBM each step.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -10,6 +11,14 @@
 #include "lsb_context.hpp"
 
 namespace lsb {
+
+// L2 flush as a kernel with the solve kernel's shared-memory carveout (LSB_FLUSH_MODE=kernel,
+// experiment): a memset runs with the default L1/shared split, and switching the split back
+// costs the next kernel its startup.
+__global__ void flush_kernel(uint4* p, size_t n, unsigned v) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(v, v, v, v);
+}
 
 void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms,
                  double* E) {
@@ -21,16 +30,25 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
     if (flush_bytes) cuda_check(cudaMalloc(&flush, flush_bytes), "bench flush");
     cudaEvent_t ev[4];
     for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
+    const char* fm = getenv("LSB_FLUSH_MODE");
+    const bool fkern = fm && !strcmp(fm, "kernel");
+    if (fkern) {
+        cudaFuncSetAttribute(flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    }
     for (int k = 0; k < K; ++k) {
-        if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
+        if (flush && fkern)
+            flush_kernel<<<148 * 2, 512, 200 << 10, c.stream>>>((uint4*)flush, flush_bytes / 16, (unsigned)k);
+        else if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
         cuda_check(cudaMemcpyAsync(c.d_state->zt, dZ + (size_t)k * r, sizeof(double) * r, cudaMemcpyDeviceToDevice,
                                    c.stream),
                    "z");
-        c.impl->eval_timed(c, ev);
+        const int nev = c.impl->eval_timed(c, ev);
         cuda_check(cudaEventSynchronize(ev[3]), "bench sync");
         float t0, t1;
         cudaEventElapsedTime(&t0, ev[0], ev[3]);
-        cudaEventElapsedTime(&t1, ev[1], ev[2]);
+        if (nev == 4) cudaEventElapsedTime(&t1, ev[1], ev[2]);
+        else t1 = t0;
         eval_ms[k] = t0;
         out_ms[k] = t1;
         if (E) c.copy(&E[k], &c.d_state->f_eval, sizeof(double), cudaMemcpyDeviceToHost, "E");

@@ -38,7 +38,10 @@ struct ImplBase {
     virtual void rebind_elements(Context& c) = 0;
     // One evaluation at st->zt as a graph with event-record nodes:
     // ev[0] | ctrl(start) | ev[1] | out_fwd | ev[2] | elem, vjp, ctrl | ev[3]
-    virtual void eval_timed(Context& c, cudaEvent_t* ev) = 0;
+    // Records ev[0] .. ev[3] around one evaluation (ev[1] .. ev[2]: the output-layer kernel)
+    // and returns 4, or records only ev[0] and ev[3] around a single-launch evaluation and
+    // returns 2 (every event record costs ~2.7 us of GPU time inside the bracket).
+    virtual int eval_timed(Context& c, cudaEvent_t* ev) = 0;
     // persistent solve kernel (one cooperative cluster launch per eval / solve / step)
     virtual bool has_solve() const = 0;
     virtual void solve_eval(Context& c) = 0;

@@ -48,6 +48,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* word, int cta, int G) {
     __syncthreads();
 }
 
+// Split-phase form: arrive (returns the pre-add word, thread 0) ... wait.
+__device__ __forceinline__ unsigned grid_arrive(unsigned* word, int cta, int G) {
+    __syncthreads();
+    unsigned old = 0;
+    if (threadIdx.x == 0) {
+        const unsigned inc = cta == 0 ? (0x80000000u - (unsigned)(G - 1)) : 1u;
+        __threadfence();
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(word), "r"(inc) : "memory");
+    }
+    return old;
+}
+__device__ __forceinline__ void grid_wait(unsigned* word, unsigned old) {
+    if (threadIdx.x == 0) {
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(word) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 struct SolveParams {
     int task;         // 0 = eval (ctrl start + one evaluation), 1 = minimize, 2 = step
     int quasi;        // step: quasi-static
@@ -114,27 +136,46 @@ __device__ __forceinline__ int part_owner(int j, int R) {
 // Stage this CTA's weight/bias row slices (+ the solver state on CTA 0): 16-byte
 // aligned pieces as 1-D bulk copies completing on one mbarrier per layer (wbar[l])
 // and one for the state (wbar[kMaxLayers]), so layer 0 can start while the rest
-// is in flight; misaligned pieces fall back to cp.async (waited here).  Users wait
-// with ctrl_wait_layer / ctrl_wait_state (parity 0: free once complete).
+// is in flight; misaligned pieces fall back to cp.async (waited here).  The copies are
+// issued in parallel by lane 0 of different warps (warp 0: the state, warp 1 + l: layer
+// l), since one thread's issue loop costs ~1 us per layer.  Users wait with
+// ctrl_wait_layer / ctrl_wait_state (parity 0: free once complete).
 __device__ __forceinline__ bool bulk_ok(const void* dst, const void* src, size_t bytes) {
     return ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) & 15u) == 0;
 }
 template <typename TS, int CS>
 __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs, int c, bool with_state, uint64_t* wbar) {
-    const int tid = threadIdx.x;
-    int off = 0;
-    bool async_used = false;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     if (tid == 0) {
         for (int l = 0; l <= kMaxLayers; ++l) mbar_init(&wbar[l], 1);
         mbar_fence_init();
     }
     __syncthreads();
     const uint64_t keep = l2_policy(1);
+    bool async_used = false;
+    if (warp == 0 && with_state && c == 0) {
+        double* sd = reinterpret_cast<double*>(cs.sst);
+        const double* ss = reinterpret_cast<const double*>(p.st);
+        const bool s_bulk = bulk_ok(sd, ss, sizeof(DevState));
+        if (!s_bulk) {
+            for (int k = lane; k < (int)(sizeof(DevState) / sizeof(double)); k += 32) cp_async8(sd + k, ss + k);
+            async_used = true;
+        }
+        if (lane == 0) {
+            if (s_bulk) tma_load_1d(sd, ss, (unsigned)sizeof(DevState), &wbar[kMaxLayers], keep);
+            mbar_expect_tx(&wbar[kMaxLayers], s_bulk ? (unsigned)sizeof(DevState) : 0u);
+        }
+    }
     TS* wsl = reinterpret_cast<TS*>(cs.wsl);
-    for (int l = 0; l < p.nhid; ++l) {
+    for (int l = warp - 1; l >= 0 && l < p.nhid; l += nw - 1) {
+        int off = 0;
+        for (int k = 0; k < l; ++k) {
+            const int Rk = p.hrows[k];
+            off += ((part_lo(Rk, CS, c + 1) - part_lo(Rk, CS, c)) * p.hcols[k] + 3) & ~3;
+        }
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), i1 = part_lo(R, CS, c + 1);
-        cs.woff[l] = off;
+        if (lane == 0) cs.woff[l] = off;
         TS* wd = wsl + off;
         const TS* ws = p.Wh_s + p.hoff[l] + (size_t)i0 * C;
         const size_t wb = (size_t)(i1 - i0) * C * sizeof(TS);
@@ -142,11 +183,15 @@ __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs
         const double* bs = p.bh + p.boff[l] + i0;
         const size_t bb = (size_t)(i1 - i0) * 8;
         const bool w_bulk = bulk_ok(wd, ws, wb), b_bulk = bulk_ok(bd, bs, bb);
-        if (!w_bulk)
-            for (int k = tid; k < (i1 - i0) * C; k += blockDim.x) wd[k] = ws[k];
-        if (!b_bulk) stage_doubles(bd, bs, i1 - i0);
-        async_used |= !w_bulk || !b_bulk;
-        if (tid == 0) {
+        if (!w_bulk) {
+            for (int k = lane; k < (i1 - i0) * C; k += 32) wd[k] = ws[k];
+            async_used = true;  // plain copies: published by the barrier below
+        }
+        if (!b_bulk) {
+            for (int k = lane; k < i1 - i0; k += 32) cp_async8(bd + k, bs + k);
+            async_used = true;
+        }
+        if (lane == 0) {
             unsigned tx = 0;
             if (w_bulk && wb) {
                 tma_load_1d(wd, ws, (unsigned)wb, &wbar[l], keep);
@@ -158,23 +203,12 @@ __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs
             }
             mbar_expect_tx(&wbar[l], tx);  // arrive + expect: completes when the bytes land
         }
-        off += ((i1 - i0) * C + 3) & ~3;
     }
-    if (with_state && c == 0) {
-        double* sd = reinterpret_cast<double*>(cs.sst);
-        const double* ss = reinterpret_cast<const double*>(p.st);
-        const bool s_bulk = bulk_ok(sd, ss, sizeof(DevState));
-        if (!s_bulk) stage_doubles(sd, ss, (int)(sizeof(DevState) / sizeof(double)));
-        async_used |= !s_bulk;
-        if (tid == 0) {
-            if (s_bulk) tma_load_1d(sd, ss, (unsigned)sizeof(DevState), &wbar[kMaxLayers], keep);
-            mbar_expect_tx(&wbar[kMaxLayers], s_bulk ? (unsigned)sizeof(DevState) : 0u);
-        }
-    }
-    if (async_used) {  // uniform across the CTA
+    if (__syncthreads_or(async_used)) {
         cp_async_wait_all();
         __syncthreads();
     }
+    __syncthreads();  // woff
 }
 __device__ __forceinline__ void ctrl_wait_layer(uint64_t* wbar, int l) { mbar_wait(&wbar[l], 0); }
 __device__ __forceinline__ void ctrl_wait_state(uint64_t* wbar) { mbar_wait(&wbar[kMaxLayers], 0); }
@@ -228,15 +262,18 @@ __device__ __forceinline__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem&
         }
         __syncthreads();  // tmp is reused below
     }
+    stamp(-400);
     for (int l = p.nhid - 1; l >= 0; --l) {
         const int R = p.hrows[l], C = p.hcols[l];
         const int i0 = part_lo(R, CS, c), nrow = part_lo(R, CS, c + 1) - i0;
+        stamp(-(410 + l * 10 + 0));
         double* gys = cs.tmp;  // own-row gradient times act' (nrow <= 64)
         for (int k = 0; k < 2; ++k) {
             const int i = tid + k * nt;
             if (i < nrow) gys[i] = gy[k] * act_eval(p.hact[l], cs.asl[l * 64 + i], 1);
         }
         __syncthreads();
+        stamp(-(410 + l * 10 + 1));
         const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
         double* rb = cs.rbuf(l & 1);
@@ -256,7 +293,9 @@ __device__ __forceinline__ void ctrl_backward(const EvalParams<TS>& p, CtrlSmem&
             const int jl = l > 0 ? j - part_lo(Rp, CS, o) : j;
             dsmem_st_f64(dsmem_addr(rb + c * 64 + jl, o), s);
         }
+        stamp(-(410 + l * 10 + 2));
         cluster.sync();
+        stamp(-(410 + l * 10 + 3));
         // own rows of layer l-1 (or z for l = 0 on CTA 0): fixed CTA-order sum
         const int nown = l > 0 ? part_lo(Rp, CS, c + 1) - part_lo(Rp, CS, c) : (c == 0 ? C : 0);
         for (int k = 0; k < 2; ++k) {
@@ -333,6 +372,156 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
     }
 }
 
+// ---- uniform-width fast path of the control cluster -------------------------------------------------
+// When every hidden layer is HP wide (HP = the padded output-layer input width, a template
+// parameter) and HP splits evenly over the CS CTAs, the row partition is static: CTA c owns
+// rows [c RPC, (c+1) RPC) of every layer, so loop bounds, lane roles and owners are
+// compile-time constants.  Same data flow as ctrl_forward / ctrl_backward (push over DSMEM,
+// one cluster barrier per layer); shorter dependent chains per layer: fully unrolled dot
+// products with 4 accumulators, unrolled shuffle trees, no integer division.
+template <int HP, int CS>
+struct CtrlFast {
+    static constexpr int RPC = HP / CS;                  // rows per CTA
+    static constexpr int RPW = RPC >= 8 ? RPC / 8 : 1;   // rows per warp (warps 0..7, or 0..RPC-1)
+    static constexpr int LPR = 32 / RPW;                 // lanes per row
+    static constexpr int NCL = HP / LPR;                 // products per lane (layers >= 1)
+    static constexpr int NG = (2 * HP <= kSolveThreads) ? (HP <= 64 ? 4 : 2) : 1;  // backward row groups
+    static constexpr bool kValid = HP % CS == 0 && RPC <= 64 && (RPC >= 8 ? RPC % 8 == 0 : true) &&
+                                   LPR >= CS && NCL >= 1 && HP % LPR == 0 && RPC % NG == 0 &&
+                                   HP * NG <= kSolveThreads && HP <= 128;
+};
+
+template <typename TS, int HP, int CS>
+__device__ __forceinline__ bool ctrl_fast_ok(const EvalParams<TS>& p) {
+    if constexpr (!CtrlFast<HP, CS>::kValid) {
+        return false;
+    } else {
+        if (p.nhid < 1 || p.r > 64 || p.r < 1) return false;
+        for (int l = 0; l < p.nhid; ++l)
+            if (p.hrows[l] != HP || p.hcols[l] != (l == 0 ? p.r : HP)) return false;
+        return true;
+    }
+}
+
+template <typename TS, int HP, int CS>
+__device__ __forceinline__ void ctrl_forward_fast(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c) {
+    using F = CtrlFast<HP, CS>;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        const double* zsrc = cluster.map_shared_rank(cs.sst->zt, 0);
+        for (int j = tid; j < p.r; j += blockDim.x) cs.xin(0)[j] = zsrc[j];
+    }
+    __syncthreads();
+    const int sub = lane / F::LPR, sl = lane % F::LPR;  // compile-time divisors
+    const int il = warp * F::RPW + sub;                 // local row (live iff < RPC)
+    const bool live = warp < 8 && il < F::RPC;
+    const int i0 = c * F::RPC;
+    // remote addresses of this lane's push target (CTA sl) for both input buffers
+    const uint32_t dst0 = sl < CS ? dsmem_addr(cs.xin(0) + i0 + il, sl) : 0u;
+    const uint32_t dst1 = sl < CS ? dsmem_addr(cs.xin(1) + i0 + il, sl) : 0u;
+    for (int l = 0; l < p.nhid; ++l) {
+        const double* x = cs.xin(l & 1);
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
+        if (live) {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            if (l == 0) {
+                const TS* wr = Ws + il * p.r;
+#pragma unroll
+                for (int k = 0; k < (64 + F::LPR - 1) / F::LPR; ++k) {
+                    const int j = sl + k * F::LPR;
+                    if (j < p.r) a[k & 3] = fma((double)wr[j], x[j], a[k & 3]);
+                }
+            } else {
+                const TS* wr = Ws + il * HP + sl;
+                const double* xr = x + sl;
+#pragma unroll
+                for (int k = 0; k < F::NCL; ++k) a[k & 3] = fma((double)wr[k * F::LPR], xr[k * F::LPR], a[k & 3]);
+            }
+            double s = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+            for (int o = F::LPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            const double pre = s + cs.bsl[l * 64 + il];
+            if (sl < CS) dsmem_st_f64((l & 1) ? dst0 : dst1, act_eval(p.hact[l], pre, 0));
+            // the fast backward reads act'(pre) (computed here, off its critical path)
+            if (sl == 0) cs.asl[l * 64 + il] = act_eval(p.hact[l], pre, 1);
+        }
+        cluster.sync();
+    }
+    if (c == 0) {
+        const double* x = cs.xin(p.nhid & 1);
+        for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < HP ? x[j] : 0.0;
+    }
+}
+
+// Backward counterpart (see ctrl_backward): ybar of the last hidden layer is the fixed-order
+// sum of the G cluster partials; per layer, partial_c[j] = sum_{own i} W[i][j] gys[i] goes to
+// the owner of j, which sums the CS partials in CTA order.  Result -> sst->gz (CTA 0).
+template <typename TS, int HP, int CS>
+__device__ __forceinline__ void ctrl_backward_fast(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
+                                                   const double* ypart) {
+    using F = CtrlFast<HP, CS>;
+    const int tid = threadIdx.x;
+    const int i0 = c * F::RPC;
+    double gy = 0.0;  // own-row gradient (threads tid < RPC)
+    {
+        // ybar: RPC columns x G partials; spread over the block, then a fixed-order fold
+        constexpr int PER = kSolveThreads / F::RPC;  // threads per column
+        const int col = tid % F::RPC, q = tid / F::RPC;
+        double v = 0.0;
+        if (q < PER)
+            for (int b = q; b < G; b += PER) v += __ldcg(ypart + (size_t)b * p.hp + i0 + col);
+        if (q < PER) cs.tmp[q * F::RPC + col] = v;
+        __syncthreads();
+        if (tid < F::RPC) {
+            double s = 0.0;
+#pragma unroll 8
+            for (int qq = 0; qq < PER; ++qq) s += cs.tmp[qq * F::RPC + tid];
+            gy = s;
+        }
+        __syncthreads();
+    }
+    const int g = tid % F::NG, j = tid / F::NG;  // thread -> (column, row group)
+    constexpr int RG = F::RPC / F::NG;           // rows per group
+    for (int l = p.nhid - 1; l >= 0; --l) {
+        double* gys = cs.tmp;
+        if (tid < F::RPC) gys[tid] = gy * cs.asl[l * 64 + tid];  // act'(pre), stored by ctrl_forward_fast
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
+        __syncthreads();
+        double* rb = cs.rbuf(l & 1);
+        const int C = l == 0 ? p.r : HP;
+        double s = 0.0;
+        if (j < C) {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < RG; ++k) {
+                const int i = g * RG + k;
+                a[k & 3] = fma((double)Ws[i * C + j], gys[i], a[k & 3]);
+            }
+            s = (a[0] + a[1]) + (a[2] + a[3]);
+        }
+        // partner lanes (same column) are adjacent and share the branch outcome
+#pragma unroll
+        for (int o = 1; o < F::NG; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (j < C && g == 0) {
+            const int o = l > 0 ? j / F::RPC : 0;
+            const int jl = l > 0 ? j - o * F::RPC : j;
+            dsmem_st_f64(dsmem_addr(rb + c * 64 + jl, o), s);
+        }
+        cluster.sync();
+        const int nown = l > 0 ? F::RPC : (c == 0 ? p.r : 0);
+        if (tid < nown) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < CS; ++q) s += rb[q * 64 + tid];
+            gy = s;
+            if (l == 0) cs.sst->gz[tid] = s;
+        }
+    }
+    __syncthreads();
+}
+
 // ---- the persistent kernel ---------------------------------------------------------------------------
 template <typename TS, int HP, int CS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParams<TS> p, const SolveParams sp) {
@@ -382,6 +571,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     };
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
+    const bool fast_ctrl = !(sp.exp & 64) && ctrl_fast_ok<TS, HP, CS>(p);
     int tr = 0;
     auto stamp = [&](int tag) {
         // tag < 0: fine-grained cycle stamp (clock64), recorded only with LSB_SOLVE_EXP & 32
@@ -392,6 +582,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         }
     };
     stamp(0);
+    if (sp.trace && tid == 0 && cta < 256) sp.trace[512 + cta] = globaltimer();
 
     // ---- control cluster: stage weights (+ state) once.  Issued before any other bulk
     // traffic: an SM's TMA engine serves requests in order.
@@ -400,34 +591,17 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     cs.wbar = s_wbar;
     cs.woff = s_woff;
     if (is_ctrl) ctrl_stage<TS, CS>(p, cs, crank, true, s_wbar);
+    stamp(6);
     // the first forward tiles do not depend on z: prefetch now (a step rewrites the
     // qbar column of the row records first, so it prefetches after that)
-    if (sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
-    // cold start (e.g. after an L2 flush): while the control cluster stages weights and runs
-    // the hidden forward, pull this CTA's share of W_out, the row records and the element
-    // arrays into L2 (only when W_out is L2-resident by policy)
-    if (p.w_resident && !is_ctrl && !(sp.exp & 8)) {
-        // the non-control CTAs cover every row / tet; they start once the control
-        // cluster's (latency-critical) staging has landed, so the bulk traffic overlaps
-        // the hidden forward instead of delaying it
-        if (lane == 0) {
-            unsigned s;
-            do {
-                asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(s) : "l"(&sp.sh->staged_seq) : "memory");
-            } while (s != sp.seq);
-        }
-        __syncwarp();
-        const int q = cta - CS, Q = G - CS;
-        const size_t r0 = (size_t)p.n * q / Q, r1 = (size_t)p.n * (q + 1) / Q;
-        prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
-        prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
-        const size_t e0 = (size_t)p.E * q / Q, e1 = (size_t)p.E * (q + 1) / Q;
-        prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
-        prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
-        prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
-    }
+    // (non-control CTAs issue theirs once the control staging has landed: their bulk reads
+    // would otherwise queue ahead of it in HBM)
+    const bool defer_pf = p.w_resident && !is_ctrl && !(sp.exp & 8) && !(sp.exp & 128);
+    if (sp.task != 2 && !defer_pf) ring_prefetch(ring, t0, t1, issue_f);
     if (is_ctrl && crank == 0) {
+        stamp(4);
         ctrl_wait_state(s_wbar);  // the state is written below
+        stamp(5);
         if (p.nhid > 0) ctrl_wait_layer(s_wbar, 0);
         if (tid == 0) asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&sp.sh->staged_seq), "r"(sp.seq) : "memory");
     }
@@ -483,11 +657,41 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             st->inv_dt2 = s->inv_dt2;
         }
         cluster.sync();
-        ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
+        if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
+        else ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
     }
     stamp(2);
     fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
-    grid_barrier(&sp.sh->grid_bar, cta, G);
+    {
+        const unsigned gold = grid_arrive(&sp.sh->grid_bar, cta, G);
+        if (sp.trace && tid == 0 && cta < 256) sp.trace[768 + cta] = globaltimer();
+        // cold start (e.g. after an L2 flush): while the control cluster runs the hidden forward,
+        // pull this CTA's share of W_out, the row records and the element arrays into L2 (only
+        // when W_out is L2-resident by policy).  Issued after this CTA's grid-barrier arrival:
+        // bulk-copy issue stalls while the SM's TMA queue is full, and must not delay the barrier.
+        if (p.w_resident && !is_ctrl && !(sp.exp & 8)) {
+            // the non-control CTAs cover every row / tet; they start once the control
+            // cluster's (latency-critical) staging has landed, so the bulk traffic overlaps
+            // the hidden forward instead of delaying it
+            if (lane == 0) {
+                unsigned s;
+                do {
+                    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(s) : "l"(&sp.sh->staged_seq) : "memory");
+                } while (s != sp.seq);
+            }
+            __syncwarp();
+            if (sp.task != 2 && defer_pf) ring_prefetch(ring, t0, t1, issue_f);
+            const int q = cta - CS, Q = G - CS;
+            const size_t r0 = (size_t)p.n * q / Q, r1 = (size_t)p.n * (q + 1) / Q;
+            prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
+            prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
+            const size_t e0 = (size_t)p.E * q / Q, e1 = (size_t)p.E * (q + 1) / Q;
+            prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
+            prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
+            prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
+        }
+        grid_wait(&sp.sh->grid_bar, gold);
+    }
     stamp(3);
     if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
 
@@ -694,8 +898,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 if (need) s->grad_evals++;
             }
             // pre-activations of the point just evaluated are in asl (own rows)
+            stamp(-390);
             cluster.sync();
-            if (need) ctrl_backward<TS, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
+            stamp(-391);
+            if (need) {
+                if (fast_ctrl) ctrl_backward_fast<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
+                else ctrl_backward<TS, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
+            }
             if (crank == 0) {
                 if (warp == 0) {
                     int m = 0;
@@ -717,9 +926,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 }
                 __syncthreads();
             }
+            stamp(-392);
             cluster.sync();
+            stamp(-393);
             const int more = *cluster.map_shared_rank(&s_flag, 0);
-            if (more) ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
+            if (more) {
+                if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
+                else ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
+            }
         }
         stamp(50);
         grid_barrier(&sp.sh->grid_bar, cta, G);
@@ -727,6 +941,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         if (__ldcg(&sh->done)) break;
     }
     ring_drain(ring, t0, t1);
+    stamp(60);
     // ---- epilogue: publish state; step finalize (reference reduced_step :266-276)
     if (is_ctrl && crank == 0) {
         __syncthreads();
@@ -772,7 +987,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         }
     }
     if (cta == 0 && tid == 0 && sp.launch_acc) sp.launch_acc[0] += 0;  // single launch
+    stamp(61);
     cluster.sync();  // keep DSMEM alive until every remote read is done
+    stamp(62);
 }
 
 }  // namespace lsb

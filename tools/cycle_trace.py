@@ -23,6 +23,6 @@ P.check(P.lib().lsb_get_trace(sysm.handle, buf, 512, C.byref(cnt)))
 prev = None
 for i in range(cnt.value):
     tag, t = buf[2 * i], buf[2 * i + 1]
-    if tag >= 300:
+    if tag >= 300 and tag < 1000 and (len(sys.argv) < 3 or str(tag)[0] in sys.argv[2]):
         print(f"{tag}: +{t - prev if prev else 0} cyc")
         prev = t

@@ -10,8 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2409_03807_b200 as P  # noqa: E402
 from paper_2409_03807_b200 import configs  # noqa: E402
 
-names = {0: "enter", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
-         30: "tv gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid"}
+names = {0: "enter", 6: "ctrl_stage", 7: "mbar init", 8: "bulk issued", 9: "ASYNC USED", 4: "ring pf", 5: "state", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
+         30: "tv gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid", 60: "drain", 61: "epilogue", 62: "exit"}
 flush = "--flush" in sys.argv
 if flush:
     import torch
@@ -37,3 +37,12 @@ for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["c2"]:
         out.append(f"{names.get(tag, tag)}:{(t - prev) / 1000:.1f}")
         prev = t
     print(name, sysm.solve_kernel_info(), f"total {(prev - t0) / 1000:.1f} us |", " ".join(out))
+    if "--ctas" in sys.argv:
+        raw = (C.c_ulonglong * 1024)()
+        P.check(P.lib().lsb_get_trace_raw(sysm.handle, raw))
+        G = sysm.solve_kernel_info()["grid"]
+        ent = np.array([raw[512 + b] for b in range(G)], dtype=np.int64) - int(t0)
+        arr = np.array([raw[768 + b] for b in range(G)], dtype=np.int64) - int(t0)
+        print(f"  CTA entry (us after CTA 0): min {ent.min()/1e3:.2f} median {np.median(ent)/1e3:.2f} max {ent.max()/1e3:.2f}"
+              f" (slowest CTA {int(ent.argmax())}); first grid arrival: median {np.median(arr)/1e3:.2f}"
+              f" max {arr.max()/1e3:.2f} (CTA {int(arr.argmax())})")
