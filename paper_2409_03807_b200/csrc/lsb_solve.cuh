@@ -15,7 +15,10 @@
 
 namespace lsb {
 
-constexpr int kSolveThreads = 288;  // 9 warps: all stream (self-issued rings) and all compute
+#ifndef LSB_SOLVE_THREADS
+#define LSB_SOLVE_THREADS 288
+#endif
+constexpr int kSolveThreads = LSB_SOLVE_THREADS;  // 9 warps: all stream (self-issued rings) and all compute
 constexpr int kSolveMaxStages = 36;
 constexpr int kSolveBarBytes = 512;  // full barriers (kSolveMaxStages x 8 B, padded)
 
@@ -572,6 +575,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     const bool fast_ctrl = !(sp.exp & 64) && ctrl_fast_ok<TS, HP, CS>(p);
+    auto gbar = [&]() { grid_barrier(&sp.sh->grid_bar, cta, G); };
     int tr = 0;
     auto stamp = [&](int tag) {
         // tag < 0: fine-grained cycle stamp (clock64), recorded only with LSB_SOLVE_EXP & 32
@@ -695,6 +699,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     stamp(3);
     if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
 
+    bool ring_pending = true;  // a prefetch of the ring is outstanding (drained before exit)
     double inv_dt2 = __ldcg(&st->inv_dt2);
     int has_inertia = __ldcg(&st->has_inertia);
     for (;;) {
@@ -728,7 +733,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
         stamp(10);
-        grid_barrier(&sp.sh->grid_bar, cta, G);
+        gbar();
         stamp(11);
         // ================= element pass
         {
@@ -764,7 +769,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_elem[cta] = tot;
         }
         stamp(20);
-        grid_barrier(&sp.sh->grid_bar, cta, G);
+        gbar();
         stamp(21);
         // ================= gradient, speculatively: whether the line search accepts this
         // point (Armijo) needs E, but the VJP is wanted in all other cases and nearly always
@@ -839,7 +844,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     }
                 }
                 __syncthreads();
-                ring_prefetch(ring, t0, t1, issue_f);
+                if (sp.task != 0) ring_prefetch(ring, t0, t1, issue_f);  // the next pass's first tiles
+                else ring_pending = false;
                 cluster.sync();
                 {
                     const int j0 = part_lo(HP, CS, crank), j1 = part_lo(HP, CS, crank + 1);
@@ -855,7 +861,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 }
             }
             stamp(40);
-            grid_barrier(&sp.sh->grid_bar, cta, G);
+            gbar();
             stamp(41);
         }
         // ================= control cluster: gradient, L-BFGS, next hidden forward
@@ -936,11 +942,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             }
         }
         stamp(50);
-        grid_barrier(&sp.sh->grid_bar, cta, G);
+        // a single evaluation ends here: its control cluster decides alone, and no CTA needs
+        // the state of another before exiting
+        if (sp.task == 0) break;
+        gbar();
         stamp(51);
         if (__ldcg(&sh->done)) break;
     }
-    ring_drain(ring, t0, t1);
+    if (ring_pending) ring_drain(ring, t0, t1);
     stamp(60);
     // ---- epilogue: publish state; step finalize (reference reduced_step :266-276)
     if (is_ctrl && crank == 0) {
@@ -951,7 +960,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         for (int k = tid; k < nwords; k += blockDim.x) dst[k] = src[k];
     }
     if (sp.task == 2) {
-        grid_barrier(&sp.sh->grid_bar, cta, G);
+        gbar();
         const double dt = __ldcg(&st->dt);
         for (int v = cta * blockDim.x + tid; v < p.V; v += G * blockDim.x)
             for (int c = 0; c < 3; ++c) {

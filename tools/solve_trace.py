@@ -12,7 +12,8 @@ from paper_2409_03807_b200 import configs  # noqa: E402
 
 names = {0: "enter", 6: "ctrl_stage", 7: "mbar init", 8: "bulk issued", 9: "ASYNC USED", 4: "ring pf", 5: "state", 1: "staged", 2: "fwd done", 3: "grid", 10: "out_fwd", 11: "grid", 20: "elem", 21: "grid",
          30: "tv gather", 31: "grid", 40: "vjp", 41: "grid", 50: "ctrl", 51: "grid", 60: "drain", 61: "epilogue", 62: "exit"}
-flush = "--flush" in sys.argv
+flush = "--flush" in sys.argv or "--rflush" in sys.argv
+rflush = "--rflush" in sys.argv  # diagnosis: evict by reading (leaves clean lines)
 if flush:
     import torch
     fbuf = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -22,7 +23,9 @@ for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["c2"]:
     sysm.set_inertia(configs.timestep0_qbar(pr, sysm.mass), configs.DT)
     z = 0.5 * np.random.default_rng(0).standard_normal(pr.model.r)
     for rep in range(3):
-        if flush:
+        if rflush:
+            fbuf.view(torch.int64).sum()
+        elif flush:
             fbuf.zero_()
             torch.cuda.synchronize()
         sysm.eval(z)
