@@ -375,6 +375,48 @@ __device__ __forceinline__ void ctrl_forward(const EvalParams<TS>& p, CtrlSmem& 
     }
 }
 
+// ---- DSMEM data-carried signalling for the fast path ----------------------------------------------
+// Layer exchanges without cluster barriers: a producer stores each value into the consumer
+// CTA with st.async, which also credits its byte count to an mbarrier in that CTA
+// (complete_tx); the consumer waits for the layer's full byte count.  Barriers: fx[l] =
+// input of forward layer l (l = 1..nhid, nhid = the last layer's output), bx[l] = partials
+// of backward layer l; each completes once per pass, parities in fph / bph.  Every barrier
+// is armed (arrive.expect_tx) before the cluster barrier that precedes its pass, so no byte
+// can land in an unarmed phase.
+struct CtrlSig {
+    uint64_t fx[kMaxLayers + 1];
+    uint64_t bx[kMaxLayers];
+    unsigned fph, bph;
+};
+__device__ __forceinline__ CtrlSig& ctrl_sig() {
+    __shared__ __align__(8) CtrlSig sig;
+    return sig;
+}
+__device__ __forceinline__ void ctrl_sig_init() {
+    CtrlSig& g = ctrl_sig();
+    if (threadIdx.x == 0) {
+        for (int l = 0; l <= kMaxLayers; ++l) mbar_init(&g.fx[l], 1);
+        for (int l = 0; l < kMaxLayers; ++l) mbar_init(&g.bx[l], 1);
+        g.fph = 0;
+        g.bph = 0;
+        mbar_fence_init();
+    }
+}
+__device__ __forceinline__ void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote_addr),
+                 "l"(__double_as_longlong(v)), "r"(remote_bar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // ---- uniform-width fast path of the control cluster -------------------------------------------------
 // When every hidden layer is HP wide (HP = the padded output-layer input width, a template
 // parameter) and HP splits evenly over the CS CTAs, the row partition is static: CTA c owns
@@ -525,6 +567,146 @@ __device__ __forceinline__ void ctrl_backward_fast(const EvalParams<TS>& p, Ctrl
     __syncthreads();
 }
 
+// Arm the fast forward's / backward's exchange barriers (thread 0; call before the cluster
+// barrier that precedes the pass).
+template <int HP, int CS>
+__device__ __forceinline__ void ctrl_arm_forward(int nhid) {
+    CtrlSig& g = ctrl_sig();
+    if (threadIdx.x == 0)
+        for (int l = 1; l <= nhid; ++l) mbar_expect_tx(&g.fx[l], HP * 8u);
+}
+template <int HP, int CS>
+__device__ __forceinline__ void ctrl_arm_backward(int nhid, int r, int c) {
+    using F = CtrlFast<HP, CS>;
+    CtrlSig& g = ctrl_sig();
+    if (threadIdx.x == 0)
+        for (int l = 0; l < nhid; ++l)
+            mbar_expect_tx(&g.bx[l], l > 0 ? (unsigned)(CS * F::RPC * 8) : (c == 0 ? (unsigned)(CS * r * 8) : 0u));
+}
+
+// ctrl_forward_fast with the exchange carried by st.async (no cluster barrier per layer).
+template <typename TS, int HP, int CS>
+__device__ __forceinline__ void ctrl_forward_async(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c) {
+    using F = CtrlFast<HP, CS>;
+    CtrlSig& g = ctrl_sig();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        const double* zsrc = cluster.map_shared_rank(cs.sst->zt, 0);
+        for (int j = tid; j < p.r; j += blockDim.x) cs.xin(0)[j] = zsrc[j];
+    }
+    const unsigned ph = g.fph;
+    __syncthreads();
+    const int sub = lane / F::LPR, sl = lane % F::LPR;
+    const int il = warp * F::RPW + sub;
+    const bool live = warp < 8 && il < F::RPC;
+    const int i0 = c * F::RPC;
+    const uint32_t dst0 = sl < CS ? dsmem_addr(cs.xin(0) + i0 + il, sl) : 0u;
+    const uint32_t dst1 = sl < CS ? dsmem_addr(cs.xin(1) + i0 + il, sl) : 0u;
+    for (int l = 0; l < p.nhid; ++l) {
+        const double* x = cs.xin(l & 1);
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
+        if (l > 0) mbar_wait_cluster(&g.fx[l], ph);
+        if (live) {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+            if (l == 0) {
+                const TS* wr = Ws + il * p.r;
+#pragma unroll
+                for (int k = 0; k < (64 + F::LPR - 1) / F::LPR; ++k) {
+                    const int j = sl + k * F::LPR;
+                    if (j < p.r) a[k & 3] = fma((double)wr[j], x[j], a[k & 3]);
+                }
+            } else {
+                const TS* wr = Ws + il * HP + sl;
+                const double* xr = x + sl;
+#pragma unroll
+                for (int k = 0; k < F::NCL; ++k) a[k & 3] = fma((double)wr[k * F::LPR], xr[k * F::LPR], a[k & 3]);
+            }
+            double s = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+            for (int o = F::LPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            const double pre = s + cs.bsl[l * 64 + il];
+            if (sl < CS)
+                st_async_f64((l & 1) ? dst0 : dst1, act_eval(p.hact[l], pre, 0), dsmem_addr(&g.fx[l + 1], sl));
+            if (sl == 0) cs.asl[l * 64 + il] = act_eval(p.hact[l], pre, 1);
+        }
+    }
+    mbar_wait_cluster(&g.fx[p.nhid], ph);
+    if (c == 0) {
+        const double* x = cs.xin(p.nhid & 1);
+        for (int j = tid; j < p.hp; j += blockDim.x) p.y_last[j] = j < HP ? x[j] : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) g.fph = ph ^ 1u;
+}
+
+// ctrl_backward_fast with the exchange carried by st.async.
+template <typename TS, int HP, int CS>
+__device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
+                                                    const double* ypart) {
+    using F = CtrlFast<HP, CS>;
+    CtrlSig& g = ctrl_sig();
+    const int tid = threadIdx.x;
+    const int i0 = c * F::RPC;
+    const unsigned ph = g.bph;
+    double gy = 0.0;
+    {
+        constexpr int PER = kSolveThreads / F::RPC;
+        const int col = tid % F::RPC, q = tid / F::RPC;
+        double v = 0.0;
+        if (q < PER)
+            for (int b = q; b < G; b += PER) v += __ldcg(ypart + (size_t)b * p.hp + i0 + col);
+        if (q < PER) cs.tmp[q * F::RPC + col] = v;
+        __syncthreads();
+        if (tid < F::RPC) {
+            double s = 0.0;
+#pragma unroll 8
+            for (int qq = 0; qq < PER; ++qq) s += cs.tmp[qq * F::RPC + tid];
+            gy = s;
+        }
+        __syncthreads();
+    }
+    const int g4 = tid % F::NG, j = tid / F::NG;
+    constexpr int RG = F::RPC / F::NG;
+    for (int l = p.nhid - 1; l >= 0; --l) {
+        double* gys = cs.tmp + (l & 1) * 64;  // alternate: the next layer's writes race no reader
+        if (tid < F::RPC) gys[tid] = gy * cs.asl[l * 64 + tid];
+        const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
+        ctrl_wait_layer(cs.wbar, l);
+        __syncthreads();
+        double* rb = cs.rbuf(l & 1);
+        const int C = l == 0 ? p.r : HP;
+        double s = 0.0;
+        if (j < C) {
+            double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int k = 0; k < RG; ++k) {
+                const int i = g4 * RG + k;
+                a[k & 3] = fma((double)Ws[i * C + j], gys[i], a[k & 3]);
+            }
+            s = (a[0] + a[1]) + (a[2] + a[3]);
+        }
+#pragma unroll
+        for (int o = 1; o < F::NG; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (j < C && g4 == 0) {
+            const int o = l > 0 ? j / F::RPC : 0;
+            const int jl = l > 0 ? j - o * F::RPC : j;
+            st_async_f64(dsmem_addr(rb + c * 64 + jl, o), s, dsmem_addr(&g.bx[l], o));
+        }
+        mbar_wait_cluster(&g.bx[l], ph);
+        const int nown = l > 0 ? F::RPC : (c == 0 ? p.r : 0);
+        if (tid < nown) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < CS; ++q) t += rb[q * 64 + tid];
+            gy = t;
+            if (l == 0) cs.sst->gz[tid] = t;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) g.bph = ph ^ 1u;
+}
+
 // ---- the persistent kernel ---------------------------------------------------------------------------
 template <typename TS, int HP, int CS>
 __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParams<TS> p, const SolveParams sp) {
@@ -575,6 +757,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     DevState* st = p.st;
     SolveShared* sh = sp.sh;
     const bool fast_ctrl = !(sp.exp & 64) && ctrl_fast_ok<TS, HP, CS>(p);
+    const bool async_ctrl = fast_ctrl && !(sp.exp & 2048);  // st.async layer exchange
     auto gbar = [&]() { grid_barrier(&sp.sh->grid_bar, cta, G); };
     int tr = 0;
     auto stamp = [&](int tag) {
@@ -660,8 +843,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             st->has_inertia = s->has_inertia;
             st->inv_dt2 = s->inv_dt2;
         }
+        if (async_ctrl) {
+            ctrl_sig_init();
+            __syncthreads();
+            ctrl_arm_forward<HP, CS>(p.nhid);
+        }
         cluster.sync();
-        if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
+        if (async_ctrl) ctrl_forward_async<TS, HP, CS>(p, cs, cluster, crank);
+        else if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
         else ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
     }
     stamp(2);
@@ -677,7 +866,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             // the non-control CTAs cover every row / tet; they start once the control
             // cluster's (latency-critical) staging has landed, so the bulk traffic overlaps
             // the hidden forward instead of delaying it
-            if (lane == 0) {
+            if (lane == 0 && !(sp.exp & 4096)) {
                 unsigned s;
                 do {
                     asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(s) : "l"(&sp.sh->staged_seq) : "memory");
@@ -905,10 +1094,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             }
             // pre-activations of the point just evaluated are in asl (own rows)
             stamp(-390);
+            if (need && async_ctrl) ctrl_arm_backward<HP, CS>(p.nhid, p.r, crank);
             cluster.sync();
             stamp(-391);
             if (need) {
-                if (fast_ctrl) ctrl_backward_fast<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
+                if (async_ctrl) ctrl_backward_async<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
+                else if (fast_ctrl) ctrl_backward_fast<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
                 else ctrl_backward<TS, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
             }
             if (crank == 0) {
@@ -933,11 +1124,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 __syncthreads();
             }
             stamp(-392);
+            if (async_ctrl) ctrl_arm_forward<HP, CS>(p.nhid);
             cluster.sync();
             stamp(-393);
             const int more = *cluster.map_shared_rank(&s_flag, 0);
             if (more) {
-                if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
+                if (async_ctrl) ctrl_forward_async<TS, HP, CS>(p, cs, cluster, crank);
+                else if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
                 else ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
             }
         }
