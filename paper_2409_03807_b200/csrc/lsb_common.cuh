@@ -174,13 +174,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned
 }
 // Bulk L2 prefetch of [p, p + bytes) (16-byte granules, evict_last), in 32 KB
 // pieces spread over the lanes-0 of the CTA's warps.
-__device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes) {
+__device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes, uintptr_t kPiece = 32768) {
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) != 0 || p == nullptr) return;
     const uintptr_t a0 = (reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15;
     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes) & ~(uintptr_t)15;
     const uint64_t pol = l2_policy(1);
-    constexpr uintptr_t kPiece = 32768;
     for (uintptr_t a = a0 + (uintptr_t)warp * kPiece; a < a1; a += (uintptr_t)nw * kPiece) {
         const unsigned n = (unsigned)((a1 - a) < kPiece ? (a1 - a) : kPiece);
         asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a), "r"(n), "l"(pol)

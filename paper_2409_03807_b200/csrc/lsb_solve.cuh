@@ -876,12 +876,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (sp.task != 2 && defer_pf) ring_prefetch(ring, t0, t1, issue_f);
             const int q = cta - CS, Q = G - CS;
             const size_t r0 = (size_t)p.n * q / Q, r1 = (size_t)p.n * (q + 1) / Q;
-            prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB);
-            prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48);
+            const uintptr_t piece = (sp.exp & 8192) ? (uintptr_t)1 << 20 : 32768;
+            prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB, piece);
+            prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48, piece);
             const size_t e0 = (size_t)p.E * q / Q, e1 = (size_t)p.E * (q + 1) / Q;
-            prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4));
-            prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4));
-            prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS));
+            prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4), piece);
+            prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4), piece);
+            prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS), piece);
         }
         grid_wait(&sp.sh->grid_bar, gold);
     }
