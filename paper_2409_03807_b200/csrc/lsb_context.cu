@@ -199,6 +199,7 @@ struct Impl final : ImplBase {
     KernelSet<TS> ks{};
     void (*ctrl)(const EvalParams<TS>, int, int, int) = nullptr;
     size_t vjp_smem = 0, ctrl_smem = 0, out_smem = 0;
+    int ctrl_threads = 256;
     int grid_gather = 1;
     // persistent solve kernel (cooperative launch of thread-block clusters)
     typename SolveFn<TS>::type solve = nullptr;
@@ -237,7 +238,7 @@ struct Impl final : ImplBase {
             int cm = kCtrlStart, mode = kModeEval, want = 1;
             EvalParams<TS> pg = p;
             void* sargs[] = {&pg, &cm, &mode, &want};
-            cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs);
+            cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs, ctrl_threads);
             cuda_check(cudaGraphAddEventRecordNode(&e1, g, &n0, 1, ev[1]), "event node");
             void* a1[] = {&pg};
             cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
@@ -247,7 +248,7 @@ struct Impl final : ImplBase {
             cudaGraphNode_t n3 = add_kernel(g, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
             int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
             void* a4[] = {&pg, &cm2, &z0, &z1};
-            cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4);
+            cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
             cuda_check(cudaGraphAddEventRecordNode(&e3, g, &n4, 1, ev[3]), "event node");
             cuda_check(cudaGraphInstantiate(&g_timed, g, 0), "graph instantiate (timed eval)");
             cudaGraphDestroy(g);
@@ -350,6 +351,24 @@ struct Impl final : ImplBase {
         p.ctrl_smem_w = (int)slice_words(cs);
         ctrl_smem = p.ctrl_smem_w * sizeof(double) + fixed;
         ctrl = cs == 8 ? ctrl_kernel<TS, 8> : ctrl_kernel<TS, 16>;
+        ctrl_threads = 256;
+        // uniform-width decoders: the fast-path control kernel (static row partition, st.async
+        // layer exchange); LSB_CTRL_FAST=0 keeps the generic kernel
+        {
+            bool uniform = c.nhid >= 1 && c.r >= 1 && c.r <= 64 && (c.hp == 128 || c.hp == 256);
+            for (int l = 0; l < c.nhid && uniform; ++l)
+                uniform = c.hrows[l] == c.hp && c.hcols[l] == (l == 0 ? c.r : c.hp);
+            const char* fe = getenv("LSB_CTRL_FAST");
+            if (uniform && !(fe && fe[0] == '0')) {
+                const size_t fsm = ctrl_fast_smem<TS>(c.nhid, c.hcols, c.hp / cs);
+                if (fsm + 1024 <= 227 * 1024) {
+                    if (c.hp == 128) ctrl = cs == 8 ? ctrl_fast_kernel<TS, 128, 8> : ctrl_fast_kernel<TS, 128, 16>;
+                    else ctrl = cs == 8 ? ctrl_fast_kernel<TS, 256, 8> : ctrl_fast_kernel<TS, 256, 16>;
+                    ctrl_smem = fsm;
+                    ctrl_threads = kSolveThreads;
+                }
+            }
+        }
         if (cs == 16)
             cuda_check(cudaFuncSetAttribute(ctrl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
         cuda_check(cudaFuncSetAttribute(ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem),
@@ -523,7 +542,7 @@ struct Impl final : ImplBase {
     void solve_step(Context& c, int quasi) override { launch_solve(c, 2, quasi); }
 
     void launch_ctrl(cudaStream_t s, int cmode, int smode, int want) {
-        ctrl<<<cs, 256, ctrl_smem, s>>>(p, cmode, smode, want);
+        ctrl<<<cs, ctrl_threads, ctrl_smem, s>>>(p, cmode, smode, want);
     }
 
     // One evaluation body, stream-launched (non-graph path).
@@ -618,7 +637,7 @@ struct Impl final : ImplBase {
         cudaGraphNode_t n2 = add_kernel(body, n1, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
         cudaGraphNode_t n2b = add_kernel(body, n2, (void*)gather_kernel<TS>, grid_gather, 0, a1);
         cudaGraphNode_t n3 = add_kernel(body, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
-        add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4);
+        add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
         return wnode;
     }
 
@@ -626,7 +645,7 @@ struct Impl final : ImplBase {
         int cm = kCtrlStart, mode = kModeLbfgs, want = 1;
         EvalParams<TS> pg = p;
         void* args[] = {&pg, &cm, &mode, &want};
-        return add_kernel(graph, dep, (void*)ctrl, cs, ctrl_smem, args);
+        return add_kernel(graph, dep, (void*)ctrl, cs, ctrl_smem, args, ctrl_threads);
     }
 
     void build_min_graph(Context& c) {

@@ -433,7 +433,7 @@ struct CtrlFast {
     static constexpr int NG = (2 * HP <= kSolveThreads) ? (HP <= 64 ? 4 : 2) : 1;  // backward row groups
     static constexpr bool kValid = HP % CS == 0 && RPC <= 64 && (RPC >= 8 ? RPC % 8 == 0 : true) &&
                                    LPR >= CS && NCL >= 1 && HP % LPR == 0 && RPC % NG == 0 &&
-                                   HP * NG <= kSolveThreads && HP <= 128;
+                                   HP * NG <= kSolveThreads && HP <= 256;
 };
 
 template <typename TS, int HP, int CS>
@@ -1193,6 +1193,123 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     stamp(61);
     cluster.sync();  // keep DSMEM alive until every remote read is done
     stamp(62);
+}
+
+// ---- multi-kernel path: the control cluster as its own launch, fast path ----------------------------
+// Same role as ctrl_kernel (lsb_kernels.cuh) -- kCtrlStart: reset the solver state and run the
+// hidden forward at zt; kCtrlAfterEval: hidden backward (if the gradient is needed), L-BFGS
+// step, and the next hidden forward if the solve continues -- for decoders whose hidden layers
+// are all HP wide, using the uniform-width fast path (ctrl_forward_async / ctrl_backward_async).
+// act'(a) of the last forward is kept in p.a_hid between launches (ctrl_kernel keeps a there;
+// a context uses one of the two kernels).
+template <typename TS, int HP, int CS>
+__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kSolveThreads, 1)
+    ctrl_fast_kernel(const EvalParams<TS> p, int cmode, int start_mode, int start_want_grad) {
+    using F = CtrlFast<HP, CS>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int c = (int)cluster.block_rank();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int wsl_elems = 0;
+    for (int l = 0; l < p.nhid; ++l) wsl_elems += (F::RPC * p.hcols[l] + 3) & ~3;
+    const int wsl_words = (int)((wsl_elems * sizeof(TS) + 7) / 8);
+    double* cbase = reinterpret_cast<double*>(smem);
+    CtrlSmem cs;
+    cs.wsl = cbase;
+    cs.xin0 = cbase + wsl_words;
+    cs.xin1 = cs.xin0 + kMaxHidden;
+    cs.rbuf0 = cs.xin1 + kMaxHidden;
+    cs.rbuf1 = cs.rbuf0 + kCtrlRecv;
+    cs.tmp = cs.rbuf1 + kCtrlRecv;
+    cs.bsl = cs.tmp + kSolveThreads;
+    cs.asl = cs.bsl + kMaxLayers * 64;
+    cs.sst = reinterpret_cast<DevState*>(cs.asl + kMaxLayers * 64);
+    __shared__ __align__(8) uint64_t s_wbar[kMaxLayers + 1];
+    __shared__ int s_woff[kMaxLayers];
+    __shared__ int more_s;
+    cs.wbar = s_wbar;
+    cs.woff = s_woff;
+    ctrl_sig_init();
+    ctrl_stage<TS, CS>(p, cs, c, true, s_wbar);
+    if (c == 0) ctrl_wait_state(s_wbar);
+    DevState* sst = cs.sst;
+    const int need = cmode == kCtrlAfterEval ? __ldcg(&p.st->need_grad) : 0;
+    int more = 1;
+    if (cmode == kCtrlAfterEval) {
+        if (need) {
+            for (int k = tid; k < p.nhid * F::RPC; k += blockDim.x) {
+                const int l = k / F::RPC, i = k - l * F::RPC;
+                cs.asl[l * 64 + i] = __ldcg(p.a_hid + l * kMaxHidden + c * F::RPC + i);
+            }
+            ctrl_arm_backward<HP, CS>(p.nhid, p.r, c);
+            cluster.sync();
+            ctrl_backward_async<TS, HP, CS>(p, cs, cluster, c, p.n_groups, p.ybar_grp);
+        }
+        __syncthreads();
+        if (c == 0) {
+            if (warp == 0) {
+                int m = 0;
+                if (sst->mode == kModeLbfgs) m = lbfgs_control(sst, p.r);
+                else if (lane == 0) sst->done = 1;
+                if (lane == 0) {
+                    sst->loop_iters++;
+                    if (!m) {
+                        sst->phase = kPhaseDone;
+                        sst->t_end = globaltimer();
+                    }
+                    more_s = m;
+                }
+            }
+            __syncthreads();
+            more = more_s;
+        }
+    } else if (c == 0 && tid == 0) {  // kCtrlStart: fresh evaluation / solve at st->zt
+        sst->mode = start_mode;
+        sst->want_grad = start_want_grad;
+        sst->status = kStOk;
+        sst->phase = kPhaseInit;
+        sst->done = 0;
+        sst->code = 4;
+        sst->iter = 0;
+        sst->ls = 0;
+        sst->hist_n = 0;
+        sst->hist_head = 0;
+        sst->value_evals = 0;
+        sst->grad_evals = 0;
+        sst->need_grad = 0;
+        sst->accept = 0;
+        sst->gnorm = 0.0;
+        sst->loop_iters = 0;
+        sst->t_start = globaltimer();
+    }
+    if (c == 0 && tid == 0) more_s = more;
+    ctrl_arm_forward<HP, CS>(p.nhid);
+    cluster.sync();
+    more = *cluster.map_shared_rank(&more_s, 0);
+    if (more) {
+        ctrl_forward_async<TS, HP, CS>(p, cs, cluster, c);
+        for (int k = tid; k < p.nhid * F::RPC; k += blockDim.x) {
+            const int l = k / F::RPC, i = k - l * F::RPC;
+            p.a_hid[l * kMaxHidden + c * F::RPC + i] = cs.asl[l * 64 + i];
+        }
+    }
+    if (c == 0) {
+        __syncthreads();
+        const int nwords = sizeof(DevState) / 4;
+        int* dst = reinterpret_cast<int*>(p.st);
+        const int* src = reinterpret_cast<const int*>(sst);
+        for (int k = tid; k < nwords; k += blockDim.x) dst[k] = src[k];
+        if (tid == 0 && p.in_graph) cudaGraphSetConditional(p.cond, more ? 1u : 0u);
+    }
+    cluster.sync();  // keep shared memory alive until all remote reads are done
+}
+
+// smem bytes of ctrl_fast_kernel for a decoder with hidden input widths hcols[0..nhid)
+template <typename TS>
+inline size_t ctrl_fast_smem(int nhid, const int* hcols, int rpc) {
+    size_t e = 0;
+    for (int l = 0; l < nhid; ++l) e += ((size_t)rpc * hcols[l] + 3) & ~(size_t)3;
+    return ((e * sizeof(TS) + 7) / 8 + ctrl_fixed_words()) * sizeof(double);
 }
 
 }  // namespace lsb

@@ -69,7 +69,29 @@ def test_simulate_c1_free_running(path, oracle, product):
     assert rel_err(fin.velocities, res["velocities"]) < 1e-6
 
 
-def test_reduced_step_api_teacher_forced_c2(oracle, product):
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_lbfgs_device_matches_oracle_c2(path, oracle, product):
+    """Config 2 (uniform 128-wide decoder: the fast-path control cluster on both device paths)."""
+    from paper_2409_03807_b200 import configs
+    P = product
+    pr = configs.build("c2")
+    sysm = pr.system("fp64")
+    sysm.use_solve_kernel(path == "solve")
+    ob = oracle.problem("c2")
+    qbar = configs.timestep0_qbar(pr, ob.mass)
+    cfg = configs.solver_config()
+    obj = P.ReducedObjective(sysm, qbar, configs.DT)
+    z = np.zeros(pr.model.r)
+    rep = P.lbfgs_minimize(obj, z, cfg)
+    zo, code, iters, gn = oracle.lbfgs_minimize(lambda x, g: _ofun(ob, qbar, x, g), np.zeros(pr.model.r),
+                                                cfg.epsilon, cfg.max_iters, cfg.max_linesearch, cfg.lbfgs_history)
+    assert rep.code == code
+    assert rep.iterations == iters
+    assert np.max(np.abs(z - zo)) < 1e-8
+
+
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_reduced_step_api_teacher_forced_c2(path, oracle, product):
     """One reduced_step from an oracle-produced state (teacher forcing)."""
     from paper_2409_03807_b200 import configs
     P = product
@@ -80,6 +102,7 @@ def test_reduced_step_api_teacher_forced_c2(oracle, product):
     res3 = ob.simulate(1, cfg, gravity=configs.GRAVITY, positions=res["positions"], velocities=res["velocities"],
                        z=res["z"])
     sysm = pr.system("fp64")
+    sysm.use_solve_kernel(path == "solve")
     state = P.SimState(res["positions"].copy(), res["velocities"].copy(), res["z"].copy(), 0.0)
     frame = P.FrameInput(pr.mesh.vertices.copy(), P.gravity_force(pr.mesh, sysm.mass, configs.GRAVITY))
     rep = P.reduced_step(state, frame, sysm, cfg)
