@@ -201,3 +201,64 @@ def test_runtime_cubature_matches_oracle(precision, path, oracle, product):
     assert np.abs(z - zo).max() < 1e-5
     sysm.set_cubature(None)
     assert rel_err(obj.eval(z0), E_full) < 1e-15
+
+
+@pytest.mark.parametrize("path", ["solve", "graph"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("width,r", [(128, 16), (256, 32)])
+def test_uniform_width_decoder_fast_control(width, r, precision, path, oracle, product):
+    """Decoders whose hidden layers are all `width` wide run the control cluster's fast path
+    (static row partition, st.async layer exchange): inside the persistent kernel (path
+    "solve") and as the multi-kernel path's ctrl_fast_kernel (path "graph", config 3's
+    shape at width 256).  E / grad E and a device L-BFGS solve against the oracle."""
+    P = product
+    mesh = P.make_bar_mesh(4, 3, 3, 1.0, 0.4, 0.5, jitter_frac=0.05, seed=9, pin_left=True)
+    rng = np.random.default_rng(21)
+    n = mesh.num_dofs()
+    dims = [r] + [width] * 5 + [n]
+    layers = []
+    for i in range(len(dims) - 1):
+        last = i == len(dims) - 2
+        W = rng.standard_normal((dims[i + 1], dims[i])) / np.sqrt(dims[i]) * (0.05 if last else 1.0)
+        b = 0.05 * rng.standard_normal(dims[i + 1])
+        layers.append(P.Layer(W, b, P.Activation.Identity if last else P.Activation.Elu))
+    shift = P.dof_pack(mesh, mesh.vertices)
+    scale = 0.5 + 0.1 * rng.random(n)
+    model = P.SubspaceModel(r, n, layers, shift, scale)
+    mu = 2.0 + rng.random(mesh.num_elements())
+    lam = 1.5 + rng.random(mesh.num_elements())
+    o = oracle.Oracle.from_mesh(mesh.vertices, mesh.elements, mesh.pinned)
+    o.set_material(mu, lam, 5.0)
+    o.set_decoder([(l.W, l.b, int(l.act)) for l in layers], shift, scale, r)
+    sysm = P.ReducedSystem(mesh, mu, lam, 5.0, model, precision)
+    sysm.use_solve_kernel(path == "solve")
+    if path == "solve" and not sysm.solve_kernel_info()["in_use"]:
+        pytest.skip("persistent kernel unavailable for this decoder: " + sysm.solve_kernel_info()["reason"])
+    qbar = P.dof_pack(mesh, mesh.vertices) + 0.01 * rng.standard_normal(n)
+    obj = P.ReducedObjective(sysm, qbar, 0.05)
+    for _ in range(3):
+        z = 0.3 * rng.standard_normal(r)
+        g = np.zeros(r)
+        E = obj.eval(z, g)
+        Eo, go = o.eval(z, qbar=qbar, dt=0.05)
+        assert rel_err(E, Eo) < TOL[precision]
+        assert rel_err(g, go) < TOL[precision]
+
+    def fo(zz, gg):
+        if gg is None:
+            return o.eval(zz, qbar=qbar, dt=0.05, want_grad=False)
+        e, gq = o.eval(zz, qbar=qbar, dt=0.05)
+        gg[:] = gq
+        return e
+
+    from paper_2409_03807_b200 import configs
+    cfg = configs.solver_config()
+    z = np.zeros(r)
+    rep = P.lbfgs_minimize(obj, z, cfg)
+    zo, code, iters, _ = oracle.lbfgs_minimize(fo, np.zeros(r), epsilon=cfg.epsilon, history=cfg.lbfgs_history)
+    assert rep.code == code
+    if precision == "fp64":
+        assert rep.iterations == iters
+        assert np.abs(z - zo).max() < 1e-7
+    else:
+        assert np.abs(z - zo).max() < 1e-3
