@@ -196,8 +196,9 @@ lsb_status lsb_set_solve_kernel(lsb_context* ctx, int enable);
 /* Phase timestamps of the last solve-kernel launch (contexts created with LSB_TRACE=1):
  * pairs (tag, globaltimer ns), count pairs. */
 lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int cap, int* count);
-/* The raw 1024-word trace buffer: [0] pair count, [1..510] pairs, [512 + b] entry and
- * [768 + b] first grid-barrier arrival (globaltimer ns) of CTA b < 256. */
+/* The raw 2048-word trace buffer: [0] pair count, [1..510] pairs; [512 + 256 k + b] for CTA
+ * b < 256 (globaltimer ns): k = 0 entry, 1 first grid-barrier arrival, 2 / 3 / 4 end of the first
+ * evaluation's output-layer / element / VJP phase. */
 lsb_status lsb_get_trace_raw(const lsb_context* ctx, unsigned long long* out);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------------------------ */

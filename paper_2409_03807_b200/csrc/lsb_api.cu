@@ -490,7 +490,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         upload_pins(c);
         {
             const char* tr = getenv("LSB_TRACE");
-            if (tr && tr[0] == '1') c.d_trace = static_cast<unsigned long long*>(c.dmalloc(8 * 1024));
+            if (tr && tr[0] == '1') c.d_trace = static_cast<unsigned long long*>(c.dmalloc(8 * 2048));
         }
         c.impl = make_impl(precision);
         c.impl->setup(c);
@@ -748,7 +748,7 @@ lsb_status lsb_get_trace_raw(const lsb_context* ctx, unsigned long long* out) {
     return run([&] {
         check_ctx(ctx);
         require(ctx->c.d_trace != nullptr, "trace: LSB_TRACE=1 not set at create");
-        ctx->c.copy(out, ctx->c.d_trace, 8 * 1024, cudaMemcpyDeviceToHost, "trace");
+        ctx->c.copy(out, ctx->c.d_trace, 8 * 2048, cudaMemcpyDeviceToHost, "trace");
     });
 }
 

@@ -208,6 +208,7 @@ struct Impl final : ImplBase {
     int solve_spw = 1, solve_spw_ctrl = 1, solve_tv_cap = 0, solve_tv_off = 0, solve_tv_off_ctrl = 0;
     int solve_wsl_words = 0, solve_tv_global = 0;
     int solve_grid = 0;
+    float solve_ctrl_tile_w = 0.5f;
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
     SolveShared* d_sh = nullptr;
     int cs = 8;
@@ -464,9 +465,15 @@ struct Impl final : ImplBase {
             return;
         }
         solve_grid = nclusters * cs;
+        if (const char* e = getenv("LSB_CTRL_TILE_W")) solve_ctrl_tile_w = (float)atof(e);  // developer tuning
+        solve_ctrl_tile_w = std::min(1.0f, std::max(0.0f, solve_ctrl_tile_w));
         if (!solve_tv_global) {
             const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
-            if ((ntiles + solve_grid - 1) / solve_grid * ks.tile_rows > solve_tv_cap) {
+            int share = 0;  // largest per-CTA tile share
+            for (int k = 0; k < solve_grid; ++k)
+                share = std::max(share, solve_tile_start(ntiles, k + 1, solve_grid, cs, solve_ctrl_tile_w) -
+                                            solve_tile_start(ntiles, k, solve_grid, cs, solve_ctrl_tile_w));
+            if (share * ks.tile_rows > solve_tv_cap) {
                 c.solve_reason = "tv scratch too small for " + std::to_string(solve_grid) + " CTAs";
                 solve = nullptr;
                 return;
@@ -497,6 +504,7 @@ struct Impl final : ImplBase {
         sp.tv_off = solve_tv_off;
         sp.tv_off_ctrl = solve_tv_off_ctrl;
         sp.tv_cap = solve_tv_cap;
+        sp.ctrl_tile_w = solve_ctrl_tile_w;
         sp.tv_global = solve_tv_global;
         sp.wsl_words = solve_wsl_words;
         if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);

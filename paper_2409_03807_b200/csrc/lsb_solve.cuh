@@ -73,6 +73,13 @@ __device__ __forceinline__ void grid_wait(unsigned* word, unsigned old) {
     __syncthreads();
 }
 
+// First W_out tile of CTA k when the CS control CTAs take weight wc and the others 1.
+__host__ __device__ __forceinline__ int solve_tile_start(int ntiles, int k, int G, int CS, float wc) {
+    const double W = k <= CS ? k * (double)wc : CS * (double)wc + (k - CS);
+    const double Wt = CS * (double)wc + (G - CS);
+    return k >= G ? ntiles : (int)((double)ntiles * W / Wt);
+}
+
 struct SolveParams {
     int task;         // 0 = eval (ctrl start + one evaluation), 1 = minimize, 2 = step
     int quasi;        // step: quasi-static
@@ -86,6 +93,7 @@ struct SolveParams {
     int wsl_words;    // control-area weight slices, in 8-byte words (stored as TS)
     unsigned seq;     // launch sequence number (host-incremented)
     int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
+    float ctrl_tile_w;  // control CTAs' share of the W_out tiles relative to the others
     // dynamics
     const double* u_state;
     const double* v_state;
@@ -740,8 +748,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     ring_init(ring.full, NW * ring.spw);
     __syncthreads();
     const int ntiles = (p.n + C::TR - 1) / C::TR;
-    const int t0 = (int)(((long long)ntiles * cta) / G);
-    const int t1 = (int)(((long long)ntiles * (cta + 1)) / G);
+    // W_out tiles per CTA: the control CTAs run a shallower ring (their control area follows
+    // it) and start streaming after the hidden forward, so they take a reduced share
+    // (sp.ctrl_tile_w of a full one) of the forward / VJP tiles
+    const int t0 = solve_tile_start(ntiles, cta, G, CS, sp.ctrl_tile_w);
+    const int t1 = solve_tile_start(ntiles, cta + 1, G, CS, sp.ctrl_tile_w);
     const uint64_t pol_w = l2_policy(p.w_resident), pol_keep = l2_policy(1);
     auto issue_f = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol_w, pol_keep); };
     double* tv_s = reinterpret_cast<double*>(smem + (is_ctrl ? sp.tv_off_ctrl : sp.tv_off));
@@ -857,7 +868,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
     {
         const unsigned gold = grid_arrive(&sp.sh->grid_bar, cta, G);
-        if (sp.trace && tid == 0 && cta < 256) sp.trace[768 + cta] = globaltimer();
+        if (sp.trace && tid == 0 && cta < 256) sp.trace[512 + 256 + cta] = globaltimer();
         // cold start (e.g. after an L2 flush): while the control cluster runs the hidden forward,
         // pull this CTA's share of W_out, the row records and the element arrays into L2 (only
         // when W_out is L2-resident by policy).  Issued after this CTA's grid-barrier arrival:
@@ -890,6 +901,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
 
     bool ring_pending = true;  // a prefetch of the ring is outstanding (drained before exit)
+    bool first_pass = true;    // trace: per-CTA phase-end times of the first evaluation
     double inv_dt2 = __ldcg(&st->inv_dt2);
     int has_inertia = __ldcg(&st->has_inertia);
     for (;;) {
@@ -923,6 +935,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_out[cta] = 0.5 * inv_dt2 * tot;
         }
         stamp(10);
+        if (sp.trace && tid == 0 && cta < 256 && first_pass) sp.trace[512 + 256 * 2 + cta] = globaltimer();
         gbar();
         stamp(11);
         // ================= element pass
@@ -959,6 +972,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             if (tid == 0) p.e_part_elem[cta] = tot;
         }
         stamp(20);
+        if (sp.trace && tid == 0 && cta < 256 && first_pass) sp.trace[512 + 256 * 3 + cta] = globaltimer();
         gbar();
         stamp(21);
         // ================= gradient, speculatively: whether the line search accepts this
@@ -1051,6 +1065,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 }
             }
             stamp(40);
+            if (sp.trace && tid == 0 && cta < 256 && first_pass) sp.trace[512 + 256 * 4 + cta] = globaltimer();
             gbar();
             stamp(41);
         }
@@ -1139,6 +1154,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         // a single evaluation ends here: its control cluster decides alone, and no CTA needs
         // the state of another before exiting
         if (sp.task == 0) break;
+        first_pass = false;
         gbar();
         stamp(51);
         if (__ldcg(&sh->done)) break;

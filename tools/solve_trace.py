@@ -41,11 +41,12 @@ for name in [a for a in sys.argv[1:] if not a.startswith("--")] or ["c2"]:
         prev = t
     print(name, sysm.solve_kernel_info(), f"total {(prev - t0) / 1000:.1f} us |", " ".join(out))
     if "--ctas" in sys.argv:
-        raw = (C.c_ulonglong * 1024)()
+        raw = (C.c_ulonglong * 2048)()
         P.check(P.lib().lsb_get_trace_raw(sysm.handle, raw))
         G = sysm.solve_kernel_info()["grid"]
-        ent = np.array([raw[512 + b] for b in range(G)], dtype=np.int64) - int(t0)
-        arr = np.array([raw[768 + b] for b in range(G)], dtype=np.int64) - int(t0)
-        print(f"  CTA entry (us after CTA 0): min {ent.min()/1e3:.2f} median {np.median(ent)/1e3:.2f} max {ent.max()/1e3:.2f}"
-              f" (slowest CTA {int(ent.argmax())}); first grid arrival: median {np.median(arr)/1e3:.2f}"
-              f" max {arr.max()/1e3:.2f} (CTA {int(arr.argmax())})")
+        for k, nm in enumerate(["entry", "barrier 1 arrival", "out_fwd end", "elem end", "vjp end"]):
+            t = np.array([raw[512 + 256 * k + b] for b in range(G)], dtype=np.int64) - int(t0)
+            order = np.argsort(t)
+            print(f"  {nm:18s} (us after CTA 0 entry): min {t.min()/1e3:6.2f} median {np.median(t)/1e3:6.2f} "
+                  f"max {t.max()/1e3:6.2f}; last CTAs {list(order[-6:])}; control-cluster median "
+                  f"{np.median(t[:8])/1e3:6.2f}")
