@@ -36,39 +36,39 @@ struct SolveShared {
 // other CTA adds 1, so the top bit flips exactly when all G have arrived; waiters
 // spin until their generation bit changes.  gpu-scope fences on both sides order
 // every thread's prior writes (via bar.sync) before every later read.
-__device__ __forceinline__ void grid_barrier(unsigned* word, int cta, int G) {
+__device__ __forceinline__ void grid_barrier(unsigned* word, int cta, int G, bool fences = true) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned inc = cta == 0 ? (0x80000000u - (unsigned)(G - 1)) : 1u;
-        __threadfence();
+        if (fences) __threadfence();
         unsigned old, cur;
         asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(word), "r"(inc) : "memory");
         do {
             asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(word) : "memory");
         } while (((old ^ cur) & 0x80000000u) == 0);
-        __threadfence();
+        if (fences) __threadfence();
     }
     __syncthreads();
 }
 
 // Split-phase form: arrive (returns the pre-add word, thread 0) ... wait.
-__device__ __forceinline__ unsigned grid_arrive(unsigned* word, int cta, int G) {
+__device__ __forceinline__ unsigned grid_arrive(unsigned* word, int cta, int G, bool fences = true) {
     __syncthreads();
     unsigned old = 0;
     if (threadIdx.x == 0) {
         const unsigned inc = cta == 0 ? (0x80000000u - (unsigned)(G - 1)) : 1u;
-        __threadfence();
+        if (fences) __threadfence();
         asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(word), "r"(inc) : "memory");
     }
     return old;
 }
-__device__ __forceinline__ void grid_wait(unsigned* word, unsigned old) {
+__device__ __forceinline__ void grid_wait(unsigned* word, unsigned old, bool fences = true) {
     if (threadIdx.x == 0) {
         unsigned cur;
         do {
             asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(word) : "memory");
         } while (((old ^ cur) & 0x80000000u) == 0);
-        __threadfence();
+        if (fences) __threadfence();
     }
     __syncthreads();
 }
@@ -769,7 +769,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     SolveShared* sh = sp.sh;
     const bool fast_ctrl = !(sp.exp & 64) && ctrl_fast_ok<TS, HP, CS>(p);
     const bool async_ctrl = fast_ctrl && !(sp.exp & 2048);  // st.async layer exchange
-    auto gbar = [&]() { grid_barrier(&sp.sh->grid_bar, cta, G); };
+    // The barrier word's atom.add.release.gpu (after bar.sync) and the poll's ld.acquire.gpu
+    // (before bar.sync) order every CTA's prior writes before every later read; the extra
+    // fence.sc on both sides cost ~2 us per evaluation under load (exp bit 16384 restores it).
+    const bool gfence = (sp.exp & 16384) != 0;
+    auto gbar = [&]() { grid_barrier(&sp.sh->grid_bar, cta, G, gfence); };
     int tr = 0;
     auto stamp = [&](int tag) {
         // tag < 0: fine-grained cycle stamp (clock64), recorded only with LSB_SOLVE_EXP & 32
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     stamp(2);
     fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
     {
-        const unsigned gold = grid_arrive(&sp.sh->grid_bar, cta, G);
+        const unsigned gold = grid_arrive(&sp.sh->grid_bar, cta, G, gfence);
         if (sp.trace && tid == 0 && cta < 256) sp.trace[512 + 256 + cta] = globaltimer();
         // cold start (e.g. after an L2 flush): while the control cluster runs the hidden forward,
         // pull this CTA's share of W_out, the row records and the element arrays into L2 (only
@@ -895,7 +899,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             prefetch_l2_range(p.fpos + e0, (e1 - e0) * sizeof(int4), piece);
             prefetch_l2_range(p.rec + e0 * 12, (e1 - e0) * 12 * sizeof(TS), piece);
         }
-        grid_wait(&sp.sh->grid_bar, gold);
+        grid_wait(&sp.sh->grid_bar, gold, gfence);
     }
     stamp(3);
     if (sp.task == 2) ring_prefetch(ring, t0, t1, issue_f);
