@@ -631,7 +631,7 @@ lsb_status lsb_lbfgs(lsb_context* ctx, double* z, const lsb_solver_config* cfg, 
         c.impl->minimize(c);
         get_state(c);
         const DevState* s = c.h_state;
-        if (!(c.use_solve && c.impl->has_solve())) c.launches += 5LL * s->loop_iters;
+        if (!(c.use_solve && c.impl->has_solve())) c.launches += (long long)c.body_kernels * s->loop_iters;
         if (s->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
         std::memcpy(z, s->x, sizeof(double) * c.r);
         fill_report(s, report);

@@ -99,9 +99,9 @@ __global__ void finalize_step_kernel(int V, const double* U, const char* vpinned
     }
 }
 
-__global__ void count_loop_kernel(const DevState* st, long long* acc) {
-    // device-side launch accounting for WHILE-loop bodies: 5 kernels per body
-    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += 5LL * st->loop_iters;
+__global__ void count_loop_kernel(const DevState* st, long long* acc, int per_body) {
+    // device-side launch accounting for WHILE-loop bodies: per_body kernels per body
+    if (threadIdx.x == 0 && blockIdx.x == 0) acc[0] += (long long)per_body * st->loop_iters;
 }
 
 // ------------------------------------------------------------------ Impl<TS>
@@ -111,6 +111,7 @@ template <typename TS>
 struct KernelSet {
     void (*out_fwd)(const EvalParams<TS>);
     void (*vjp)(const EvalParams<TS>);
+    void (*vjp_gather)(const EvalParams<TS>);  // gather folded into the VJP (tv in smem)
     size_t smem;      // dynamic smem of both streaming kernels (ring + scratch)
     int tile_rows;
     size_t stage_bytes;  // one ring stage (tile + side records)
@@ -118,7 +119,7 @@ struct KernelSet {
 
 template <typename TS, int HP>
 KernelSet<TS> kernels_for() {
-    return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
+    return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, vjp_gather_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
             StreamCfg<TS, HP>::TR, (size_t)StreamCfg<TS, HP>::STAGEB};
 }
 
@@ -198,7 +199,8 @@ struct Impl final : ImplBase {
     EvalParams<TS> p{};
     KernelSet<TS> ks{};
     void (*ctrl)(const EvalParams<TS>, int, int, int) = nullptr;
-    size_t vjp_smem = 0, ctrl_smem = 0, out_smem = 0;
+    size_t vjp_smem = 0, ctrl_smem = 0, out_smem = 0, vjpg_smem = 0;
+    bool fuse_gather = false;
     int ctrl_threads = 256;
     int grid_gather = 1;
     // persistent solve kernel (cooperative launch of thread-block clusters)
@@ -245,8 +247,7 @@ struct Impl final : ImplBase {
             cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
             cuda_check(cudaGraphAddEventRecordNode(&e2, g, &n1, 1, ev[2]), "event node");
             cudaGraphNode_t n2 = add_kernel(g, e2, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-            cudaGraphNode_t n2b = add_kernel(g, n2, (void*)gather_kernel<TS>, grid_gather, 0, a1);
-            cudaGraphNode_t n3 = add_kernel(g, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
+            cudaGraphNode_t n3 = add_gather_vjp(g, n2, a1);
             int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
             void* a4[] = {&pg, &cm2, &z0, &z1};
             cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
@@ -255,7 +256,7 @@ struct Impl final : ImplBase {
             cudaGraphDestroy(g);
         }
         cuda_check(cudaGraphLaunch(g_timed, c.stream), "graph launch (timed eval)");
-        c.launches += 6;  // ctrl, out_fwd, elem, gather, vjp, ctrl
+        c.launches += fuse_gather ? 5 : 6;  // ctrl, out_fwd, elem, [gather,] vjp, ctrl
         return 4;
     }
 
@@ -325,6 +326,25 @@ struct Impl final : ImplBase {
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, kStreamThreads, vjp_smem),
                    "occupancy vjp");
         p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
+        // fused gather + VJP: tv for a CTA's rows in shared memory (same grid as the VJP)
+        {
+            const char* fe = getenv("LSB_FUSE_GATHER");
+            fuse_gather = !(fe && fe[0] == '0');
+            const size_t tvb = ((size_t)((ntiles + p.grid_vjp - 1) / p.grid_vjp) * ks.tile_rows * sizeof(double) + 127) &
+                               ~(size_t)127;
+            vjpg_smem = vjp_smem + tvb;
+            int occ2 = 0;
+            if (fuse_gather &&
+                (cudaFuncSetAttribute(ks.vjp_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjpg_smem) !=
+                     cudaSuccess ||
+                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ks.vjp_gather, kStreamThreads, vjpg_smem) !=
+                     cudaSuccess ||
+                 occ2 * c.num_sms < p.grid_vjp)) {
+                cudaGetLastError();
+                fuse_gather = false;  // keep the VJP grid; fall back to the separate gather kernel
+            }
+            c.body_kernels = fuse_gather ? 4 : 5;
+        }
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<TS>, 256, 0), "occupancy gather");
         grid_gather = std::max(1, std::min((m.n_free + 255) / 256, c.num_sms * std::max(1, occ)));
         p.group = 16;
@@ -549,6 +569,21 @@ struct Impl final : ImplBase {
     void solve_minimize(Context& c) override { launch_solve(c, 1, 0); }
     void solve_step(Context& c, int quasi) override { launch_solve(c, 2, quasi); }
 
+    void launch_gather_vjp(cudaStream_t s) {
+        if (fuse_gather) {
+            ks.vjp_gather<<<p.grid_vjp, kStreamThreads, vjpg_smem, s>>>(p);
+        } else {
+            gather_kernel<TS><<<grid_gather, 256, 0, s>>>(p);
+            ks.vjp<<<p.grid_vjp, kStreamThreads, vjp_smem, s>>>(p);
+        }
+    }
+    // graph form: returns the last node
+    cudaGraphNode_t add_gather_vjp(cudaGraph_t g, cudaGraphNode_t dep, void** args) {
+        if (fuse_gather) return add_kernel(g, dep, (void*)ks.vjp_gather, p.grid_vjp, vjpg_smem, args, kStreamThreads);
+        cudaGraphNode_t n = add_kernel(g, dep, (void*)gather_kernel<TS>, grid_gather, 0, args);
+        return add_kernel(g, n, (void*)ks.vjp, p.grid_vjp, vjp_smem, args, kStreamThreads);
+    }
+
     void launch_ctrl(cudaStream_t s, int cmode, int smode, int want) {
         ctrl<<<cs, ctrl_threads, ctrl_smem, s>>>(p, cmode, smode, want);
     }
@@ -557,10 +592,9 @@ struct Impl final : ImplBase {
     void launch_eval_body(cudaStream_t s, Context& c) {
         ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
         elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
-        gather_kernel<TS><<<grid_gather, 256, 0, s>>>(p);
-        ks.vjp<<<p.grid_vjp, kStreamThreads, vjp_smem, s>>>(p);
+        launch_gather_vjp(s);
         launch_ctrl(s, kCtrlAfterEval, 0, 0);
-        c.launches += 5;
+        c.launches += fuse_gather ? 4 : 5;
     }
 
     void eval(Context& c, bool want_grad) override {
@@ -588,12 +622,11 @@ struct Impl final : ImplBase {
             cudaEventRecord(ev[2], s);
             elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
             cudaEventRecord(ev[3], s);
-            gather_kernel<TS><<<grid_gather, 256, 0, s>>>(p);
-            ks.vjp<<<p.grid_vjp, kStreamThreads, vjp_smem, s>>>(p);
+            launch_gather_vjp(s);
             cudaEventRecord(ev[4], s);
             launch_ctrl(s, kCtrlAfterEval, 0, 0);
             cudaEventRecord(ev[5], s);
-            c.launches += 5;
+            c.launches += fuse_gather ? 4 : 5;
             cuda_check(cudaEventSynchronize(ev[5]), "profile sync");
             float t;
             cudaEventElapsedTime(&t, ev[1], ev[2]);
@@ -643,8 +676,7 @@ struct Impl final : ImplBase {
         void* a4[] = {&pg, &cm, &z0, &z1};
         cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
         cudaGraphNode_t n2 = add_kernel(body, n1, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-        cudaGraphNode_t n2b = add_kernel(body, n2, (void*)gather_kernel<TS>, grid_gather, 0, a1);
-        cudaGraphNode_t n3 = add_kernel(body, n2b, (void*)ks.vjp, p.grid_vjp, vjp_smem, a1, kStreamThreads);
+        cudaGraphNode_t n3 = add_gather_vjp(body, n2, a1);
         add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
         return wnode;
     }
@@ -694,7 +726,8 @@ struct Impl final : ImplBase {
         cudaGraphNode_t n_fin = add_kernel(g, n_while, (void*)finalize_step_kernel, grid_v, 0, a_fin);
         long long* acc = c.d_launch_acc;
         const DevState* cst = c.d_state;
-        void* a_cnt[] = {&cst, &acc};
+        int per_body = c.body_kernels;
+        void* a_cnt[] = {&cst, &acc, &per_body};
         cudaKernelNodeParams kp = {};
         kp.func = (void*)count_loop_kernel;
         kp.gridDim = dim3(1);

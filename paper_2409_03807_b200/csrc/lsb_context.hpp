@@ -59,6 +59,7 @@ struct Context {
     int precision = LSB_FP64, device = 0, num_sms = 148;
     size_t wsize = 8;
     cudaStream_t stream = nullptr;
+    int body_kernels = 5;  // kernels per multi-kernel evaluation body (out_fwd, elem, [gather,] vjp, ctrl)
     HostMesh mesh;
     std::vector<double> mass;        // n
     double total_mass = 0.0;

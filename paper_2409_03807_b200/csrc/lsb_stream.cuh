@@ -82,6 +82,15 @@ __device__ __forceinline__ void issue_vjp_w(const EvalParams<TS>& p, int t, unsi
     mbar_expect_tx(bar, (unsigned)rows * C::ROWB + tv_bytes<TS, HP>(p, t));
     tma_load_1d(stg, p.Wout + (size_t)r0 * HP, rows * C::ROWB, bar, pol);
 }
+// VJP tile t, W rows only (tv comes from shared memory)
+template <typename TS, int HP>
+__device__ __forceinline__ void issue_w_only(const EvalParams<TS>& p, int t, unsigned char* stg, uint64_t* bar,
+                                             uint64_t pol) {
+    using C = StreamCfg<TS, HP>;
+    const int r0 = t * C::TR, rows = min(C::TR, p.n - r0);
+    mbar_expect_tx(bar, (unsigned)rows * C::ROWB);
+    tma_load_1d(stg, p.Wout + (size_t)r0 * HP, rows * C::ROWB, bar, pol);
+}
 template <typename TS, int HP>
 __device__ __forceinline__ void issue_vjp_tv(const EvalParams<TS>& p, int t, unsigned char* stg, uint64_t* bar,
                                              uint64_t keep) {
@@ -372,6 +381,73 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_tma_kernel(const EvalParam
         for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
     ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) {
         vjp_tile<TS, HP>(p, b, reinterpret_cast<const double*>(b + C::TILEB), t, acc);
+    });
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q) wred[warp * HP + (c * 32 + lane) * C::V4 + q] = acc[c][q];
+    __syncthreads();
+    for (int j = tid; j < HP; j += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += wred[w * HP + j];
+        p.ybar_part[(size_t)blockIdx.x * HP + j] = s;
+    }
+    // group-last block sums its group's partials in block order
+    __threadfence();
+    __syncthreads();
+    const int grp = blockIdx.x / p.group;
+    const int g0 = grp * p.group, g1 = min(g0 + p.group, (int)gridDim.x);
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(p.grp_cnt + grp, 1u);
+        am_grp_last = (prev == (unsigned)(g1 - g0 - 1));
+    }
+    __syncthreads();
+    if (!am_grp_last) return;
+    __threadfence();
+    for (int j = tid; j < HP; j += blockDim.x) {
+        double s = 0.0;
+        for (int b = g0; b < g1; ++b) s += __ldcg(p.ybar_part + (size_t)b * HP + j);
+        p.ybar_grp[(size_t)grp * HP + j] = s;
+    }
+    if (tid == 0) p.grp_cnt[grp] = 0;
+}
+
+// ---------------------------------------------------------------- K3b + K4 fused: gather + VJP
+// vjp_tma_kernel with the vertex gather folded in: each CTA gathers tv for its own rows
+// into shared memory (gather_rows_smem, as the persistent kernel does) while its first W
+// tiles are already in flight, then streams W only.  Saves the gather kernel's launch and
+// its tv round trip through global memory.
+template <typename TS, int HP>
+__global__ void __launch_bounds__(kStreamThreads) vjp_gather_tma_kernel(const EvalParams<TS> p) {
+    using C = StreamCfg<TS, HP>;
+    extern __shared__ __align__(128) unsigned char ssm[];
+    constexpr int NW = kStreamThreads / 32;
+    __shared__ int am_grp_last;
+    DevState* st = p.st;
+    if (!st->need_grad) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WarpRing r{ssm + 512, reinterpret_cast<uint64_t*>(ssm), NW, kStreamSpw, C::STAGEB, 0u};
+    double* wred = reinterpret_cast<double*>(ssm + 512 + (size_t)NW * kStreamSpw * C::STAGEB);  // NW x HP
+    double* tv_s = wred + (size_t)NW * HP;                                                        // own rows
+    ring_init(r.full, NW * kStreamSpw);
+    __syncthreads();
+    const int ntiles = (p.n + C::TR - 1) / C::TR;
+    const int t0 = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
+    const uint64_t pol = l2_policy(p.w_resident);
+    auto issue = [&](int t, unsigned char* b, uint64_t* bar) { issue_w_only<TS, HP>(p, t, b, bar, pol); };
+    ring_prefetch(r, t0, t1, issue);
+    const int R0 = t0 * C::TR, R1 = min(t1 * C::TR, p.n);
+    gather_rows_smem(p, R0, R1, tv_s, st->has_inertia, p.out_act == kIdentity);
+    __syncthreads();
+    double acc[C::NCH][C::V4];
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
+    ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) {
+        vjp_tile<TS, HP>(p, b, tv_s + (t * C::TR - R0), t, acc);
     });
 #pragma unroll
     for (int c = 0; c < C::NCH; ++c)
