@@ -525,6 +525,8 @@ struct Impl final : ImplBase {
         sp.tv_off_ctrl = solve_tv_off_ctrl;
         sp.tv_cap = solve_tv_cap;
         sp.ctrl_tile_w = solve_ctrl_tile_w;
+        sp.pf_frac = 1.0f;
+        if (const char* e = getenv("LSB_PREFETCH_FRAC")) sp.pf_frac = std::min(1.0f, std::max(0.0f, (float)atof(e)));
         sp.tv_global = solve_tv_global;
         sp.wsl_words = solve_wsl_words;
         if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);

@@ -94,6 +94,7 @@ struct SolveParams {
     unsigned seq;     // launch sequence number (host-incremented)
     int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
     float ctrl_tile_w;  // control CTAs' share of the W_out tiles relative to the others
+    float pf_frac;      // fraction of W_out prefetched into L2 at a cold start
     // dynamics
     const double* u_state;
     const double* v_state;
@@ -892,7 +893,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             const int q = cta - CS, Q = G - CS;
             const size_t r0 = (size_t)p.n * q / Q, r1 = (size_t)p.n * (q + 1) / Q;
             const uintptr_t piece = (sp.exp & 8192) ? (uintptr_t)1 << 20 : 32768;
-            prefetch_l2_range(p.Wout + r0 * HP, (r1 - r0) * C::ROWB, piece);
+            // the first pf_frac of this CTA's W_out share (the rest streams on demand)
+            const size_t wrows = (size_t)((double)(r1 - r0) * sp.pf_frac);
+            prefetch_l2_range(p.Wout + r0 * HP, wrows * C::ROWB, piece);
             prefetch_l2_range(p.eprow + r0 * 6, (r1 - r0) * 48, piece);
             const size_t e0 = (size_t)p.E * q / Q, e1 = (size_t)p.E * (q + 1) / Q;
             prefetch_l2_range(p.tets + e0, (e1 - e0) * sizeof(int4), piece);
