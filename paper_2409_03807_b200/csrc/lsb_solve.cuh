@@ -650,14 +650,15 @@ __device__ __forceinline__ void ctrl_forward_async(const EvalParams<TS>& p, Ctrl
 }
 
 // ctrl_backward_fast with the exchange carried by st.async.
-template <typename TS, int HP, int CS>
+template <typename TS, int HP, int CS, typename Stamp>
 __device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, CtrlSmem& cs, cg::cluster_group& cluster, int c, int G,
-                                                    const double* ypart) {
+                                                    const double* ypart, Stamp& stamp) {
     using F = CtrlFast<HP, CS>;
     CtrlSig& g = ctrl_sig();
     const int tid = threadIdx.x;
     const int i0 = c * F::RPC;
     const unsigned ph = g.bph;
+    stamp(-600);
     double gy = 0.0;
     {
         constexpr int PER = kSolveThreads / F::RPC;
@@ -675,6 +676,7 @@ __device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, Ctr
         }
         __syncthreads();
     }
+    stamp(-601);
     const int g4 = tid % F::NG, j = tid / F::NG;
     constexpr int RG = F::RPC / F::NG;
     for (int l = p.nhid - 1; l >= 0; --l) {
@@ -683,6 +685,7 @@ __device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, Ctr
         const TS* Ws = reinterpret_cast<const TS*>(cs.wsl) + cs.woff[l];
         ctrl_wait_layer(cs.wbar, l);
         __syncthreads();
+        stamp(-(610 + 10 * l));
         double* rb = cs.rbuf(l & 1);
         const int C = l == 0 ? p.r : HP;
         double s = 0.0;
@@ -702,7 +705,9 @@ __device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, Ctr
             const int jl = l > 0 ? j - o * F::RPC : j;
             st_async_f64(dsmem_addr(rb + c * 64 + jl, o), s, dsmem_addr(&g.bx[l], o));
         }
+        stamp(-(611 + 10 * l));
         mbar_wait_cluster(&g.bx[l], ph);
+        stamp(-(612 + 10 * l));
         const int nown = l > 0 ? F::RPC : (c == 0 ? p.r : 0);
         if (tid < nown) {
             double t = 0.0;
@@ -714,6 +719,7 @@ __device__ __forceinline__ void ctrl_backward_async(const EvalParams<TS>& p, Ctr
     }
     __syncthreads();
     if (tid == 0) g.bph = ph ^ 1u;
+    ctrl_arm_backward<HP, CS>(p.nhid, p.r, c);  // the next pass's phase (every byte of this one landed)
 }
 
 // ---- the persistent kernel ---------------------------------------------------------------------------
@@ -863,6 +869,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             ctrl_sig_init();
             __syncthreads();
             ctrl_arm_forward<HP, CS>(p.nhid);
+            ctrl_arm_backward<HP, CS>(p.nhid, p.r, crank);
         }
         cluster.sync();
         if (async_ctrl) ctrl_forward_async<TS, HP, CS>(p, cs, cluster, crank);
@@ -1117,11 +1124,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
             }
             // pre-activations of the point just evaluated are in asl (own rows)
             stamp(-390);
-            if (need && async_ctrl) ctrl_arm_backward<HP, CS>(p.nhid, p.r, crank);
-            cluster.sync();
+            // (async: the backward's barriers were armed at the start / by the previous pass, so
+            // no cluster barrier is needed before the first st.async)
+            if (async_ctrl) __syncthreads();
+            else cluster.sync();
             stamp(-391);
             if (need) {
-                if (async_ctrl) ctrl_backward_async<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
+                if (async_ctrl) ctrl_backward_async<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
                 else if (fast_ctrl) ctrl_backward_fast<TS, HP, CS>(p, cs, cluster, crank, G / CS, p.ybar_part);
                 else ctrl_backward<TS, CS>(p, cs, cluster, crank, G / CS, p.ybar_part, stamp);
             }
@@ -1147,10 +1156,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 __syncthreads();
             }
             stamp(-392);
-            if (async_ctrl) ctrl_arm_forward<HP, CS>(p.nhid);
-            cluster.sync();
-            stamp(-393);
-            const int more = *cluster.map_shared_rank(&s_flag, 0);
+            // a single evaluation (task 0) has no next forward
+            int more = 0;
+            if (sp.task != 0) {
+                if (async_ctrl) ctrl_arm_forward<HP, CS>(p.nhid);
+                cluster.sync();
+                stamp(-393);
+                more = *cluster.map_shared_rank(&s_flag, 0);
+            }
             if (more) {
                 if (async_ctrl) ctrl_forward_async<TS, HP, CS>(p, cs, cluster, crank);
                 else if (fast_ctrl) ctrl_forward_fast<TS, HP, CS>(p, cs, cluster, crank);
@@ -1266,7 +1279,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kSolveThreads, 1)
             }
             ctrl_arm_backward<HP, CS>(p.nhid, p.r, c);
             cluster.sync();
-            ctrl_backward_async<TS, HP, CS>(p, cs, cluster, c, p.n_groups, p.ybar_grp);
+            auto nostamp = [](int) {};
+            ctrl_backward_async<TS, HP, CS>(p, cs, cluster, c, p.n_groups, p.ybar_grp, nostamp);
         }
         __syncthreads();
         if (c == 0) {
