@@ -44,7 +44,7 @@ enum Mode : int { kModeEval = 0, kModeLbfgs = 1 };
 enum DevStatus : int { kStOk = 0, kStNonFinite = 2 };
 enum CtrlMode : int { kCtrlStart = 0, kCtrlAfterEval = 1 };
 
-struct alignas(16) DevState {  // 16-byte size: staged by one bulk copy
+struct alignas(16) DevState {  // 16-byte size: staged by one bulk copy, published with 16-byte stores
     // configuration
     int mode, want_grad;
     double eps;

@@ -806,7 +806,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     // (non-control CTAs issue theirs once the control staging has landed: their bulk reads
     // would otherwise queue ahead of it in HBM)
     const bool defer_pf = p.w_resident && !is_ctrl && !(sp.exp & 8) && !(sp.exp & 128);
-    if (sp.task != 2 && !defer_pf) ring_prefetch(ring, t0, t1, issue_f);
+    // (the control CTAs issue theirs after the hidden forward: their staging and forward are
+    // the critical path of the launch)
+    if (sp.task != 2 && !defer_pf && !is_ctrl) ring_prefetch(ring, t0, t1, issue_f);
     if (is_ctrl && crank == 0) {
         stamp(4);
         ctrl_wait_state(s_wbar);  // the state is written below
@@ -877,6 +879,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         else ctrl_forward<TS, CS>(p, cs, cluster, crank, stamp);
     }
     stamp(2);
+    if (is_ctrl && sp.task != 2) ring_prefetch(ring, t0, t1, issue_f);
     fence_proxy_async();  // generic-proxy row-record writes -> later bulk copies
     {
         const unsigned gold = grid_arrive(&sp.sh->grid_bar, cta, G, gfence);
@@ -1184,10 +1187,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     // ---- epilogue: publish state; step finalize (reference reduced_step :266-276)
     if (is_ctrl && crank == 0) {
         __syncthreads();
-        const int nwords = sizeof(DevState) / 4;
-        int* dst = reinterpret_cast<int*>(st);
-        const int* src = reinterpret_cast<const int*>(cs.sst);
-        for (int k = tid; k < nwords; k += blockDim.x) dst[k] = src[k];
+        const int nvec = sizeof(DevState) / 16;  // 16-byte sized and aligned
+        int4* dst = reinterpret_cast<int4*>(st);
+        const int4* src = reinterpret_cast<const int4*>(cs.sst);
+        for (int k = tid; k < nvec; k += blockDim.x) dst[k] = src[k];
     }
     if (sp.task == 2) {
         gbar();
@@ -1332,10 +1335,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kSolveThreads, 1)
     }
     if (c == 0) {
         __syncthreads();
-        const int nwords = sizeof(DevState) / 4;
-        int* dst = reinterpret_cast<int*>(p.st);
-        const int* src = reinterpret_cast<const int*>(sst);
-        for (int k = tid; k < nwords; k += blockDim.x) dst[k] = src[k];
+        const int nvec = sizeof(DevState) / 16;  // 16-byte sized and aligned
+        int4* dst = reinterpret_cast<int4*>(p.st);
+        const int4* src = reinterpret_cast<const int4*>(sst);
+        for (int k = tid; k < nvec; k += blockDim.x) dst[k] = src[k];
         if (tid == 0 && p.in_graph) cudaGraphSetConditional(p.cond, more ? 1u : 0u);
     }
     cluster.sync();  // keep shared memory alive until all remote reads are done
