@@ -225,17 +225,18 @@ __global__ void __launch_bounds__(kEcols) elem_batched2_kernel(const TR* rec, co
     const int col = blockIdx.y * kEcols + tid;
     const int e0 = blk_tet0[blk], ne = blk_tet0[blk + 1] - e0;
     const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
-    float* acc = sm;                    // [nv * 3][kEcols]
-    float* rs = acc + nv * 3 * kEcols;  // [kTB][12]
+    float* acc = sm;                          // [(nv + 1) * 3][kEcols]; slot nv absorbs pinned corners
+    float* rs = acc + (nv + 1) * 3 * kEcols;  // [kTB][12]
     int* vs = reinterpret_cast<int*>(rs + kTB * 12);  // [kTB][4] row offsets v * 3 * N
-    short* ls = reinterpret_cast<short*>(vs + kTB * 4);  // [kTB][4] free slots
+    int* los = vs + kTB * 4;                          // [kTB][4] accumulator offsets slot * 3 * kEcols
     for (int i = tid; i < nv * 3 * kEcols; i += kEcols) acc[i] = 0.f;
     for (int i = tid; i < ne * 12; i += kEcols) rs[i] = (float)rec[(size_t)e0 * 12 + i];
     for (int i = tid; i < ne * 4; i += kEcols) {
         const int4 t = __ldg(tets + e0 + (i >> 2));
         const int k = i & 3;
         vs[i] = (k == 0 ? t.x : k == 1 ? t.y : k == 2 ? t.z : t.w) * 3 * N;
-        ls[i] = tet_loc[(size_t)e0 * 4 + i];
+        const int lv = tet_loc[(size_t)e0 * 4 + i];
+        los[i] = (lv >= 0 ? lv : nv) * 3 * kEcols;
     }
     __syncthreads();
     double esum = 0.0;
@@ -264,15 +265,14 @@ __global__ void __launch_bounds__(kEcols) elem_batched2_kernel(const TR* rec, co
             for (int q = 0; q < 12; ++q) rc[q] = rs[e * 12 + q];
             float f[12];
             esum += (double)tet_energy_forces_t<float>(u[0], u[1], u[2], u[3], rc, f);
-            const short* L = ls + e * 4;
+            // branch-free scatter: one 16-byte load of the 4 slot offsets (pinned -> slot nv)
+            const int4 o4 = *reinterpret_cast<const int4*>(los + e * 4);
+            const int off[4] = {o4.x, o4.y, o4.z, o4.w};
+            float* at = acc + tid;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int lv = L[k];
-                if (lv >= 0) {
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[(lv * 3 + c) * kEcols + tid] += f[k * 3 + c];
-                }
-            }
+                for (int c = 0; c < 3; ++c) at[off[k] + c * kEcols] += f[k * 3 + c];
         }
         for (int i = 0; i < nv * 3; ++i) partial[((size_t)(v0 * 3) + i) * N + col] = acc[i * kEcols + tid];
         eblk[(size_t)blk * N + col] = esum;
@@ -1241,8 +1241,8 @@ struct BatchedEngine : BatchedBase {
                 for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
             }
         c.copy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "U pins");
-        esmem2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
-                 kTB * 4 * sizeof(short);
+        esmem2 = (size_t)(eb.max_nv + 1) * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) +
+                 kTB * 4 * sizeof(int) + kTB * 4 * sizeof(int);
         esmem_f2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float2) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
                    kTB * 4 * sizeof(short);
         cuda_check(cudaFuncSetAttribute(elem_batched_f2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
