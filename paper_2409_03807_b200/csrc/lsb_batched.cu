@@ -455,33 +455,58 @@ __global__ void combine_kernel(int n, int N, const int* vslot_ptr, const int* vs
 // as a tf32 hi/lo pair in the K-major core-matrix tiles (B row = col, K = row; lsb_tc.cuh).
 __global__ void combine_pack_kernel(int n, int N, const int* vslot_ptr, const int* vslot, const float* partial,
                                     const float* rin, int has_inertia, const double* eprow, float* B2) {
-    // thread = (4 consecutive rows = one 16-byte core-matrix chunk, column): the hi and lo
-    // chunks are float4 stores, contiguous across adjacent columns; partial reads stay
-    // coalesced over columns
-    const int nq = (n + 3) / 4;
-    const size_t total = (size_t)nq * N;
+    // thread = (4 consecutive rows = one 16-byte core-matrix chunk, 4 consecutive columns): every
+    // partial / inertia read is a 16-byte load (4 columns), so a warp moves 512 B per load; the
+    // per-(row, column) sums keep the block order of combine_kernel
+    const int nq = (n + 3) / 4, ncq = N / 4;  // N is a multiple of 4 (column chunks of 64 / 128 / 256)
+    const size_t total = (size_t)nq * ncq;
     for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
-        const int q4 = (int)(idx / N), col = (int)(idx % N);
-        float hi[4], lo[4];
+        const int q4 = (int)(idx / ncq), col0 = 4 * (int)(idx % ncq);
+        float x[4][4];  // [row e][column j]
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int row = 4 * q4 + e;
-            float x = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[e][j] = 0.f;
             if (row < n) {
                 const int f = row / 3, c = row - 3 * f;
-                double g = 0.0;
-                for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) g += partial[((size_t)vslot[k] * 3 + c) * N + col];
-                if (has_inertia) g += rin[(size_t)row * N + col];
-                x = (float)(g * eprow[(size_t)row * 6 + 1]);
+                double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+                const int kb = __ldg(vslot_ptr + f), ke = __ldg(vslot_ptr + f + 1);
+                for (int k = kb; k < ke; ++k) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(partial + ((size_t)__ldg(vslot + k) * 3 + c) * N + col0));
+                    g0 += v.x;
+                    g1 += v.y;
+                    g2 += v.z;
+                    g3 += v.w;
+                }
+                if (has_inertia) {
+                    const float4 ri = __ldg(reinterpret_cast<const float4*>(rin + (size_t)row * N + col0));
+                    g0 += ri.x;
+                    g1 += ri.y;
+                    g2 += ri.z;
+                    g3 += ri.w;
+                }
+                const double sc = __ldg(eprow + (size_t)row * 6 + 1);
+                x[e][0] = (float)(g0 * sc);
+                x[e][1] = (float)(g1 * sc);
+                x[e][2] = (float)(g2 * sc);
+                x[e][3] = (float)(g3 * sc);
             }
-            hi[e] = tc::tf32_rna(x);
-            lo[e] = x - hi[e];
         }
         const int row0 = 4 * q4;
         float* blk = B2 + (size_t)(row0 / tc::kSliceK) * tc::slice_floats(N);
-        const size_t o = tc::core_off(col, row0 % tc::kSliceK, N);  // 16-byte aligned chunk of 4 rows
-        *reinterpret_cast<float4*>(blk + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<float4*>(blk + (size_t)N * tc::kSliceK + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                hi[e] = tc::tf32_rna(x[e][j]);
+                lo[e] = x[e][j] - hi[e];
+            }
+            const size_t o = tc::core_off(col0 + j, row0 % tc::kSliceK, N);  // 16-byte aligned chunk of 4 rows
+            *reinterpret_cast<float4*>(blk + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<float4*>(blk + (size_t)N * tc::kSliceK + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
     }
 }
 
