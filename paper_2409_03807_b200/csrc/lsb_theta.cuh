@@ -466,14 +466,35 @@ __global__ void theta_combine_kernel(int n, int P, int r, const int* vslot_ptr, 
         const int f = row / 3, cc = row - 3 * f;
         const float s = (float)eprow[(size_t)row * 6 + 1];
         float* o = Abar + (size_t)row * P * w + (size_t)p * w;
+        const int kb = __ldg(vslot_ptr + f), ke = __ldg(vslot_ptr + f + 1);
         double q = 0.0;
-        for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k) q += partq[((size_t)vslot[k] * 3 + cc) * P + p];
+        for (int k = kb; k < ke; ++k) q += partq[((size_t)__ldg(vslot + k) * 3 + cc) * P + p];
         o[0] = s * (float)q;
-        for (int a = 0; a < r; ++a) {
-            double jb = 0.0;
-            for (int k = vslot_ptr[f]; k < vslot_ptr[f + 1]; ++k)
-                jb += partJ[(((size_t)vslot[k] * 3 + cc) * P + p) * r + a];
-            o[1 + a] = s * (float)jb;
+        if (r == 16) {
+            // the 16 direction entries of one (slot, row, point) are 64 contiguous bytes: four
+            // 16-byte loads per slot; per-direction sums keep the slot order
+            double jb[16];
+#pragma unroll
+            for (int a = 0; a < 16; ++a) jb[a] = 0.0;
+            for (int k = kb; k < ke; ++k) {
+                const float4* src = reinterpret_cast<const float4*>(partJ + (((size_t)__ldg(vslot + k) * 3 + cc) * P + p) * 16);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const float4 x = __ldg(src + v);
+                    jb[4 * v] += x.x;
+                    jb[4 * v + 1] += x.y;
+                    jb[4 * v + 2] += x.z;
+                    jb[4 * v + 3] += x.w;
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 16; ++a) o[1 + a] = s * (float)jb[a];
+        } else {
+            for (int a = 0; a < r; ++a) {
+                double jb = 0.0;
+                for (int k = kb; k < ke; ++k) jb += partJ[(((size_t)vslot[k] * 3 + cc) * P + p) * r + a];
+                o[1 + a] = s * (float)jb;
+            }
         }
         o[1 + r] = Th[(size_t)row * P + p];
     }
