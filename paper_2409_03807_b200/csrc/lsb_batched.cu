@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
     __shared__ __align__(16) float sh_dF[2][GP][R][12];  // D rows per direction (k 0..11)
     __shared__ __align__(16) float sh_M[2][GP][R][12];   // M' rows per direction
     __shared__ __align__(16) float sh_rec[kTB][12];   // the block's records
-    __shared__ short sh_loc[kTB][8];                  // free slots (4), touched slots (4)
+    __shared__ int sh_off[kTB][8];  // accg offsets of the free slots (pinned -> scratch slot nv) (4), Us offsets of the touched slots (4)
     __shared__ float sh_b[R][GP][NH];
     extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
@@ -703,11 +703,12 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
         const int va = __ldg(blk_avert + a0 + vcl / 3), c = vcl % 3;
         cp_async16(Us + (size_t)vcl * GP + 4 * k4, U + ((size_t)va * 3 + c) * P + p0 + 4 * k4);
     }
-    for (int i = tid; i < nv * 3 * GP; i += 128) accg[i] = 0.f;
+    for (int i = tid; i < (nv + 1) * 3 * GP; i += 128) accg[i] = 0.f;
     for (int i = tid; i < (e1 - e0) * 12; i += 128) sh_rec[i / 12][i % 12] = rec[(size_t)e0 * 12 + i];
     for (int i = tid; i < (e1 - e0) * 4; i += 128) {
-        sh_loc[i >> 2][i & 3] = tet_loc[(size_t)e0 * 4 + i];
-        sh_loc[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i];
+        const int lv = tet_loc[(size_t)e0 * 4 + i];
+        sh_off[i >> 2][i & 3] = (lv >= 0 ? lv : nv) * 3 * GP;
+        sh_off[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i] * 3 * GP;
     }
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     float cacc[PPW][MT][NT][4];
@@ -745,9 +746,9 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
                 for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[e - e0][qq];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const int la = sh_loc[e - e0][4 + k];
+                    const int uo = sh_off[e - e0][4 + k] + pl;
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) uu[k * 3 + a] = Us[(la * 3 + a) * GP + pl];
+                    for (int a = 0; a < 3; ++a) uu[k * 3 + a] = Us[uo + a * GP];
                 }
                 float A[9];
 #pragma unroll
@@ -887,10 +888,7 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
 #pragma unroll
                 for (int d0 = 0; d0 < 12; d0 += R) {
                     const int d = d0 + b;
-                    if (d < 12) {
-                        const int lv = sh_loc[e - e0][d / 3];
-                        if (lv >= 0) accg[(lv * 3 + d % 3) * GP + pl] += bq[21 + d];
-                    }
+                    if (d < 12) accg[sh_off[e - e0][d / 3] + (d % 3) * GP + pl] += bq[21 + d];
                 }
             }
             __syncthreads();
@@ -1642,7 +1640,7 @@ struct BatchedEngine : BatchedBase {
 
     size_t hess_smem(int r) const {
         const int gp = 128 / r;
-        return ((size_t)max_nva * 3 * gp + (size_t)max_nv * 3 * gp) * sizeof(float) + 64;  // Us + accg (elem_hess2)
+        return ((size_t)max_nva * 3 * gp + (size_t)(max_nv + 1) * 3 * gp) * sizeof(float) + 64;  // Us + accg (elem_hess2)
     }
 
     // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
