@@ -247,17 +247,24 @@ def main():
     vevals = [reps[i].value_evals for i in range(T)]
     codes = sorted(set(reps[i].code for i in range(T)))
 
-    # ---- e2e: the public API call (host z in, host E and grad out), per step
+    # ---- e2e: the reference-facing C-ABI call lsb_eval (host z in, host E and grad out, the
+    # copies inside every call), K calls timed on the host clock; and the same through the
+    # Python binding (ReducedSystem.eval), reported beside it
     sysm.set_inertia(qbar, configs.DT)
-    Ze = configs.gaussian_latents(7, K + W, r)
-    for k in range(W):
-        sysm.eval(Ze[k])
-    e2e_t = 0.0
+    Ze = np.ascontiguousarray(configs.gaussian_latents(7, K + W, r))
+    Ee, Ge = np.zeros(K + W), np.zeros((K + W, r))
+    secs = C.c_double()
+    P.check(L.lsb_bench_e2e(sysm.handle, W, P.dptr(Ze[:W]), P.dptr(Ee[:W]), P.dptr(Ge[:W]), C.byref(secs)))
+    P.check(L.lsb_bench_e2e(sysm.handle, K, P.dptr(np.ascontiguousarray(Ze[W:])), P.dptr(Ee[W:]),
+                            P.dptr(Ge[W:]), C.byref(secs)))
+    e2e_t = secs.value
+    e2e_value = ws * K / e2e_t if e2e_t > 0 else None
+    py_t = 0.0
     for k in range(W, W + K):
         t0 = time.perf_counter()
         sysm.eval(Ze[k])
-        e2e_t += time.perf_counter() - t0
-    e2e_value = ws * K / e2e_t if e2e_t > 0 else None
+        py_t += time.perf_counter() - t0
+    e2e_python = ws * K / py_t if py_t > 0 else None
 
     # ---- roofline of the dominant kernel
     hbm, peak_kind = peaks()
@@ -300,7 +307,8 @@ def main():
             "timestep_iterations": iters, "timestep_value_evals": vevals, "timestep_codes": codes,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": 8 * r,
-                    "d2h_bytes_per_step": 8 * (1 + r)},
+                    "d2h_bytes_per_step": 8 * (1 + r), "api": "lsb_eval (C ABI), host buffers",
+                    "python_binding_value": e2e_python},
             "clocks": clk.summary(), "gpu_launches": int(launches),
             "energy_check": float(Es[0]),
         }

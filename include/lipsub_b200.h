@@ -220,6 +220,10 @@ lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flus
  * flush; per step: device time (CUDA events) and exit report. */
 lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg, int quasi_static,
                            size_t flush_bytes, double* step_ms, lsb_exit_report* reports);
+/* End-to-end through the C ABI: K calls of lsb_eval(ctx, Z + k r, &E[k], G + k r) on host
+ * buffers (host z in, host E and grad out, the copies inside every call), timed on the host
+ * clock around the loop: *seconds. */
+lsb_status lsb_bench_e2e(lsb_context* ctx, int K, const double* Z, double* E, double* G, double* seconds);
 
 #ifdef __cplusplus
 }

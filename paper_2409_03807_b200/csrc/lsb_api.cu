@@ -803,6 +803,21 @@ lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flus
     });
 }
 
+lsb_status lsb_bench_e2e(lsb_context* ctx, int K, const double* Z, double* E, double* G, double* seconds) {
+    return run([&] {
+        check_ctx(ctx);
+        require(K >= 1 && Z && E && G && seconds, "bench e2e: bad arguments");
+        const int r = ctx->c.r;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int k = 0; k < K; ++k) {
+            const lsb_status st = lsb_eval(ctx, Z + (size_t)k * r, E + k, G + (size_t)k * r);
+            if (st != LSB_OK) throw LsbError(st, "bench e2e: lsb_eval failed");
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
 lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg, int quasi_static,
                            size_t flush_bytes, double* step_ms, lsb_exit_report* reports) {
     return run([&] {
