@@ -31,6 +31,7 @@ Context::~Context() {
     batched.reset();
     for (void* p : allocations) cudaFree(p);
     if (h_state) cudaFreeHost(h_state);
+    if (h_out) cudaFreeHost(h_out);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -472,6 +473,16 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.d_y_last = static_cast<double*>(c.dmalloc(c.hp * 8));
         c.d_state = static_cast<DevState*>(c.dmalloc(sizeof(DevState)));
         cuda_check(cudaMallocHost(&c.h_state, sizeof(DevState)), "pinned state");
+        if (cudaHostAlloc(&c.h_out, sizeof(double) * (2 + kMaxLatent), cudaHostAllocMapped) == cudaSuccess) {
+            if (cudaHostGetDevicePointer(&c.d_out, c.h_out, 0) != cudaSuccess) {
+                cudaFreeHost(c.h_out);
+                c.h_out = nullptr;
+                c.d_out = nullptr;
+            }
+        } else {
+            c.h_out = nullptr;
+        }
+        cudaGetLastError();
         std::memset(c.h_state, 0, sizeof(DevState));
         // dynamics
         c.d_u_state = static_cast<double*>(c.dmalloc(sizeof(double) * 3 * (size_t)m.V));
@@ -594,6 +605,20 @@ lsb_status lsb_eval(lsb_context* ctx, const double* z, double* value, double* gr
         check_ctx(ctx);
         require(z && value, "eval: null argument");
         Context& c = ctx->c;
+        // direct path (persistent kernel): z travels with the launch and the kernel writes
+        // {E, status, grad} into host-mapped memory -- no separate copies
+        if (c.h_out && c.impl->eval_direct(c, z, grad != nullptr, c.d_out)) {
+            sync(c);
+            // keep the host mirror's evaluation block current (as get_eval_result does)
+            std::memcpy(c.h_state->zt, z, sizeof(double) * c.r);
+            c.h_state->f_eval = c.h_out[0];
+            c.h_state->status = (int)c.h_out[1];
+            if (grad) std::memcpy(c.h_state->gz, c.h_out + 2, sizeof(double) * c.r);
+            if (c.h_state->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
+            *value = c.h_out[0];
+            if (grad) std::memcpy(grad, c.h_out + 2, sizeof(double) * c.r);
+            return;
+        }
         put_zt(c, z);
         c.impl->eval(c, grad != nullptr);
         get_eval_result(c);

@@ -546,8 +546,19 @@ struct Impl final : ImplBase {
         return sp;
     }
 
-    void launch_solve(Context& c, int task, int quasi, int want_grad = 1) {
+    bool eval_direct(Context& c, const double* z, bool want_grad, double* out_dev) override {
+        if (!(solve && c.use_solve) || c.r > kMaxLatent) return false;
+        launch_solve(c, 0, 0, want_grad ? 1 : 0, z, out_dev);
+        return true;
+    }
+
+    void launch_solve(Context& c, int task, int quasi, int want_grad = 1, const double* z = nullptr,
+                      double* out_dev = nullptr) {
         SolveParams sp = solve_params(c, task, quasi, want_grad);
+        sp.out_map = out_dev;
+        sp.z_in = z ? 1 : 0;
+        if (z)
+            for (int i = 0; i < c.r; ++i) sp.z[i] = z[i];
         cudaLaunchConfig_t cfg = {};
         // cluster launch only: the grid barrier is the kernel's own (grid_barrier), and
         // the grid never exceeds the co-resident cluster count

@@ -42,6 +42,9 @@ struct ImplBase {
     // and returns 4, or records only ev[0] and ev[3] around a single-launch evaluation and
     // returns 2 (every event record costs ~2.7 us of GPU time inside the bracket).
     virtual int eval_timed(Context& c, cudaEvent_t* ev) = 0;
+    // One evaluation at z with z passed by value and {E, status, grad} written by the kernel into
+    // host-mapped memory out (device view out_dev); false when this path is unavailable.
+    virtual bool eval_direct(Context& c, const double* z, bool want_grad, double* out_dev) = 0;
     // persistent solve kernel (one cooperative cluster launch per eval / solve / step)
     virtual bool has_solve() const = 0;
     virtual void solve_eval(Context& c) = 0;
@@ -99,6 +102,8 @@ struct Context {
     unsigned int* d_grp_cnt = nullptr;
     DevState* d_state = nullptr;
     DevState* h_state = nullptr;  // pinned mirror
+    double* h_out = nullptr;      // host-mapped {E, status, grad[kMaxLatent]} (direct evaluation)
+    double* d_out = nullptr;      // its device view
     // dynamics
     double *d_u_state = nullptr, *d_v_state = nullptr, *d_z_state = nullptr, *d_a_ext = nullptr;
     double* d_pin_disp = nullptr;

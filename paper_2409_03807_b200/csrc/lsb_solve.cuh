@@ -107,6 +107,11 @@ struct SolveParams {
     SolveShared* sh;
     long long* launch_acc;
     unsigned long long* trace;  // optional phase timestamps (CTA 0), nullptr = off
+    // direct evaluation (task 0 through lsb_eval): z by value, result {E, status, grad[r]}
+    // written by CTA 0 into host-mapped memory (nullptr = off)
+    double* out_map;
+    int z_in;
+    double z[kMaxLatent];
 };
 
 
@@ -812,6 +817,10 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
     if (is_ctrl && crank == 0) {
         stamp(4);
         ctrl_wait_state(s_wbar);  // the state is written below
+        if (sp.z_in) {  // z passed with the launch (no separate upload)
+            for (int i = tid; i < p.r; i += blockDim.x) cs.sst->zt[i] = sp.z[i];
+            __syncthreads();
+        }
         stamp(5);
         if (p.nhid > 0) ctrl_wait_layer(s_wbar, 0);
         if (tid == 0) asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(&sp.sh->staged_seq), "r"(sp.seq) : "memory");
@@ -1191,6 +1200,13 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
         int4* dst = reinterpret_cast<int4*>(st);
         const int4* src = reinterpret_cast<const int4*>(cs.sst);
         for (int k = tid; k < nvec; k += blockDim.x) dst[k] = src[k];
+        if (sp.out_map) {  // the evaluation's result straight into host memory
+            for (int i = tid; i < p.r; i += blockDim.x) sp.out_map[2 + i] = cs.sst->gz[i];
+            if (tid == 0) {
+                sp.out_map[0] = cs.sst->f_eval;
+                sp.out_map[1] = (double)cs.sst->status;
+            }
+        }
     }
     if (sp.task == 2) {
         gbar();
