@@ -92,7 +92,13 @@ struct SolveParams {
     int tv_global;    // 1: tv lives in global memory and streams with the VJP tiles (large n)
     int wsl_words;    // control-area weight slices, in 8-byte words (stored as TS)
     unsigned seq;     // launch sequence number (host-incremented)
-    int exp;          // developer timing experiments (LSB_SOLVE_EXP; 0 = off; results invalid when set)
+    // developer A/B switches (LSB_SOLVE_EXP; 0 = the production path).  Bits 1 / 4 skip the tile
+    // math / the tv gather (timing only, results invalid); 2: VJP prefetch after the gather;
+    // 8: no cold-start L2 prefetch; 32: cycle stamps; 64: generic control cluster; 128: no
+    // deferral of the non-control CTAs' first ring prefetch; 2048: fast path with cluster
+    // barriers instead of st.async; 4096: L2 prefetch without waiting for the control staging;
+    // 8192: 1 MB prefetch pieces; 16384: fence.sc around the grid barrier's atomic / poll
+    int exp;
     float ctrl_tile_w;  // control CTAs' share of the W_out tiles relative to the others
     float pf_frac;      // fraction of W_out prefetched into L2 at a cold start
     // dynamics
