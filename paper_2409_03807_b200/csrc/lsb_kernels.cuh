@@ -391,7 +391,22 @@ __device__ __forceinline__ double tet_energy_forces(const double* u0, const doub
     return tet_energy_forces_t<double>(u0, u1, u2, u3, rec, f);
 }
 
-// Scatter one tet's 12 local forces to their vertices' CSR slots (32-byte vectors).
+// Scatter one tet's 12 local forces to their vertices' CSR slots: 32-byte {fx, fy, fz, 0}
+// double entries, or in fp32-storage mode (TS = float) 16-byte float entries -- the force
+// array is a bandwidth-bound intermediate like W_out and the element records;
+// the gather sums them in fp64.
+template <typename TS>
+__device__ __forceinline__ void store_forces_csr_t(double* F, int4 pos, const double* f);
+template <>
+__device__ __forceinline__ void store_forces_csr_t<float>(double* F, int4 pos, const double* f) {
+    float* Ff = reinterpret_cast<float*>(F);
+    const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (ps[k] >= 0)
+            __stcg(reinterpret_cast<float4*>(Ff + (size_t)ps[k] * 4),
+                   make_float4((float)f[3 * k], (float)f[3 * k + 1], (float)f[3 * k + 2], 0.f));
+}
 __device__ __forceinline__ void store_forces_csr(double* F, int4 pos, const double* f) {
     const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
 #pragma unroll
@@ -401,6 +416,10 @@ __device__ __forceinline__ void store_forces_csr(double* F, int4 pos, const doub
             __stcg(o, make_double2(f[3 * k], f[3 * k + 1]));
             __stcg(o + 1, make_double2(f[3 * k + 2], 0.0));
         }
+}
+template <>
+__device__ __forceinline__ void store_forces_csr_t<double>(double* F, int4 pos, const double* f) {
+    store_forces_csr(F, pos, f);
 }
 
 template <typename TS>
@@ -433,7 +452,7 @@ __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
             load_rec<TS>(p.rec, (size_t)e, rec);
             double f[12];
             eacc += tet_energy_forces(u[q][0], u[q][1], u[q][2], u[q][3], rec, f);
-            store_forces_csr(p.forces, __ldg(p.fpos + e), f);
+            store_forces_csr_t<TS>(p.forces, __ldg(p.fpos + e), f);
         }
     }
     const double tot = block_sum(eacc, red);

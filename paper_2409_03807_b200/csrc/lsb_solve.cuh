@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     load_rec<TS>(p.rec, (size_t)e, rc);
                     double f[12];
                     eacc += tet_energy_forces(u[k][0], u[k][1], u[k][2], u[k][3], rc, f);
-                    store_forces_csr(p.forces, __ldg(p.fpos + e), f);
+                    store_forces_csr_t<TS>(p.forces, __ldg(p.fpos + e), f);
                 }
             }
             const double tot = block_sum(eacc, red);

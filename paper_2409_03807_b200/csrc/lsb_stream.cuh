@@ -10,6 +10,8 @@
 // per-warp issue reaches 5.8 TB/s cold / 6.5 TB/s L2-warm.
 #pragma once
 
+#include <type_traits>
+
 #include "lsb_kernels.cuh"
 
 namespace lsb {
@@ -312,16 +314,31 @@ __device__ __forceinline__ void gather_vertex1(const EvalParams<TS>& p, int f, i
         sc[c] = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
     }
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    for (int k0 = b; k0 < e; k0 += 24) {
-        double4 v[24];
+    if constexpr (std::is_same<TS, float>::value) {  // fp32-storage mode: 16-byte float entries
+        const float4* F4 = reinterpret_cast<const float4*>(p.forces);
+        for (int k0 = b; k0 < e; k0 += 24) {
+            float4 v[24];
 #pragma unroll
-        for (int u = 0; u < 24; ++u)
-            v[u] = k0 + u < e ? ld_cg_d4(p.forces + 4 * (size_t)(k0 + u)) : make_double4(0.0, 0.0, 0.0, 0.0);
+            for (int u = 0; u < 24; ++u) v[u] = k0 + u < e ? __ldcg(F4 + k0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 24; ++u) {
-            gx += v[u].x;
-            gy += v[u].y;
-            gz += v[u].z;
+            for (int u = 0; u < 24; ++u) {
+                gx += (double)v[u].x;
+                gy += (double)v[u].y;
+                gz += (double)v[u].z;
+            }
+        }
+    } else {
+        for (int k0 = b; k0 < e; k0 += 24) {
+            double4 v[24];
+#pragma unroll
+            for (int u = 0; u < 24; ++u)
+                v[u] = k0 + u < e ? ld_cg_d4(p.forces + 4 * (size_t)(k0 + u)) : make_double4(0.0, 0.0, 0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 24; ++u) {
+                gx += v[u].x;
+                gy += v[u].y;
+                gz += v[u].z;
+            }
         }
     }
     const double g[3] = {gx, gy, gz};
