@@ -262,3 +262,23 @@ def test_uniform_width_decoder_fast_control(width, r, precision, path, oracle, p
         assert np.abs(z - zo).max() < 1e-7
     else:
         assert np.abs(z - zo).max() < 1e-3
+
+
+def test_bench_e2e_hook_matches_eval(product):
+    """lsb_bench_e2e (the bench's C-ABI end-to-end loop over lsb_eval with host buffers) returns
+    exactly what single lsb_eval calls return (deterministic reductions, same launch path)."""
+    import ctypes as C
+    from paper_2409_03807_b200 import configs
+    P = product
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    sysm.set_inertia(configs.timestep0_qbar(pr, sysm.mass), configs.DT)
+    Z = np.ascontiguousarray(0.4 * np.random.default_rng(5).standard_normal((6, pr.model.r)))
+    E = np.zeros(6)
+    G = np.zeros((6, pr.model.r))
+    secs = C.c_double()
+    P.check(P.lib().lsb_bench_e2e(sysm.handle, 6, P.dptr(Z), P.dptr(E), P.dptr(G), C.byref(secs)))
+    assert secs.value > 0
+    for k in range(6):
+        e, g = sysm.eval(Z[k])
+        assert e == E[k] and np.array_equal(g, G[k])
