@@ -412,9 +412,10 @@ __device__ __forceinline__ void store_forces_csr(double* F, int4 pos, const doub
 #pragma unroll
     for (int k = 0; k < 4; ++k)
         if (ps[k] >= 0) {
-            double2* o = reinterpret_cast<double2*>(F + (size_t)ps[k] * 4);
-            __stcg(o, make_double2(f[3 * k], f[3 * k + 1]));
-            __stcg(o + 1, make_double2(f[3 * k + 2], 0.0));
+            // one 256-bit store of the 32-byte entry {fx, fy, fz, 0}
+            asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(F + (size_t)ps[k] * 4), "d"(f[3 * k]),
+                         "d"(f[3 * k + 1]), "d"(f[3 * k + 2]), "d"(0.0)
+                         : "memory");
         }
 }
 template <>
