@@ -335,13 +335,13 @@ __device__ __forceinline__ void load_rec<float>(const float* rec, size_t e, doub
 }
 template <>
 __device__ __forceinline__ void load_rec<double>(const double* rec, size_t e, double* o) {
-    const double2* p = reinterpret_cast<const double2*>(rec + e * 12);
+    // three 256-bit read-only loads of the 96-byte record
+    const double* p = rec + e * 12;
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        const double2 v = __ldg(p + k);
-        o[2 * k] = v.x;
-        o[2 * k + 1] = v.y;
-    }
+    for (int k = 0; k < 3; ++k)
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(o[4 * k]), "=d"(o[4 * k + 1]), "=d"(o[4 * k + 2]), "=d"(o[4 * k + 3])
+            : "l"(p + 4 * k));
 }
 __device__ __forceinline__ void load_u(const double* U, int v, double* o) {
     const double2 a = *reinterpret_cast<const double2*>(U + (size_t)v * 4);
