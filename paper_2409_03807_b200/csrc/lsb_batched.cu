@@ -595,7 +595,15 @@ __global__ void tangent_out_kernel(int n, int P, int r, const float* C, const do
         const double u = e6[1] * ((double)c[0] + e6[0]) + e6[2];
         U[vc * P + p] = (float)u;
         if (inertia) rin[(size_t)row * P + p] = (float)(inv_dt2 * e6[3] * (u - e6[5]));
-        for (int a = 0; a < r; ++a) Jv[(vc * P + p) * r + a] = (float)(e6[1] * c[1 + a]);
+        float* jo = Jv + (vc * P + p) * r;
+        if ((r & 3) == 0) {  // 16-byte stores (rows of r floats are 16-byte aligned)
+            const double sc = e6[1];
+            for (int a = 0; a < r; a += 4)
+                *reinterpret_cast<float4*>(jo + a) = make_float4((float)(sc * c[1 + a]), (float)(sc * c[2 + a]),
+                                                                 (float)(sc * c[3 + a]), (float)(sc * c[4 + a]));
+        } else {
+            for (int a = 0; a < r; ++a) jo[a] = (float)(e6[1] * c[1 + a]);
+        }
     }
 }
 
