@@ -157,7 +157,13 @@ __global__ void theta_out_kernel(int n, int P, int r, const float* C2, const dou
         const int slot = (int)e6[4];
         const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
         const float s = (float)e6[1];
-        for (int a = 0; a < r; ++a) Wv[(vc * P + p) * r + a] = s * c[a];
+        float* wo = Wv + (vc * P + p) * r;
+        if ((r & 3) == 0) {  // 16-byte stores (rows of r floats are 16-byte aligned)
+            for (int a = 0; a < r; a += 4)
+                *reinterpret_cast<float4*>(wo + a) = make_float4(s * c[a], s * c[a + 1], s * c[a + 2], s * c[a + 3]);
+        } else {
+            for (int a = 0; a < r; ++a) wo[a] = s * c[a];
+        }
         Gb[vc * P + p] = s * c[r];
     }
 }
