@@ -975,8 +975,18 @@ __global__ void __launch_bounds__(256) hess_reduce_kernel(int nblk, int P, int n
     const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
     const int w = threadIdx.x >> 5;
     double s = 0.0;
-    if (idx < total)
-        for (int b = w; b < nblk; b += 8) s += Cpart[(size_t)b * total + idx];
+    if (idx < total) {
+        // 8 independent loads in flight per thread, summed in the same (block) order
+        int b = w;
+        for (; b + 56 < nblk; b += 64) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(Cpart + (size_t)(b + 8 * k) * total + idx);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += v[k];
+        }
+        for (; b < nblk; b += 8) s += Cpart[(size_t)b * total + idx];
+    }
     red[w][threadIdx.x & 31] = s;
     __syncthreads();
     if (w == 0 && idx < total) {
