@@ -517,7 +517,15 @@ __global__ void __launch_bounds__(256) energy_reduce_kernel(int N, int nrow_tile
     __shared__ double red[32];
     const int col = blockIdx.x;
     double s = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += eblk[(size_t)b * N + col];
+    int b = threadIdx.x;
+    for (; b + 7 * (int)blockDim.x < nblk; b += 8 * blockDim.x) {  // 8 loads in flight, same order
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = __ldg(eblk + (size_t)(b + k * blockDim.x) * N + col);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    for (; b < nblk; b += blockDim.x) s += eblk[(size_t)b * N + col];
     if (has_inertia)
         for (int b = threadIdx.x; b < nrow_tiles; b += blockDim.x) s += epart[(size_t)b * N + col];
     const double tot = block_sum(s, red);

@@ -371,8 +371,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
 __global__ void reduce_parts_kernel(const float* __restrict__ part, int njobs, int h, int N, float* __restrict__ out,
                                     int ldo) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h * N; i += gridDim.x * blockDim.x) {
+        // 8 independent loads in flight, summed in job order
         float s = 0.f;
-        for (int j = 0; j < njobs; ++j) s += __ldg(part + (size_t)j * kTileM * N + i);
+        int j = 0;
+        for (; j + 8 <= njobs; j += 8) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = __ldg(part + (size_t)(j + k) * kTileM * N + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += v[k];
+        }
+        for (; j < njobs; ++j) s += __ldg(part + (size_t)j * kTileM * N + i);
         out[(size_t)(i / N) * ldo + i % N] = s;
     }
 }
