@@ -174,7 +174,15 @@ __global__ void __launch_bounds__(256) sgemm_tn_splitk_kernel(int H, int N, int 
 __global__ void splitk_reduce_kernel(int HN, int nk, const float* P, float* out, int N = 0, int ldo = 0) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HN; i += gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int k = 0; k < nk; ++k) s += P[(size_t)k * HN + i];
+        int k = 0;
+        for (; k + 8 <= nk; k += 8) {  // 8 loads in flight, summed in k order
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = __ldg(P + (size_t)(k + q) * HN + i);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += v[q];
+        }
+        for (; k < nk; ++k) s += P[(size_t)k * HN + i];
         out[ldo ? (size_t)(i / N) * ldo + i % N : (size_t)i] = (float)s;
     }
 }
@@ -1012,8 +1020,19 @@ __global__ void hess_final_kernel(int h, int P, int r, int cols, const double* C
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
         const int p = idx / npair, pr = idx % npair;
         double s = C[idx];
-        for (int j = 0; j < h; ++j)
-            s += (double)Ybar[(size_t)j * P + p] * (double)X[(size_t)j * P * cols + (size_t)p * cols + 1 + r + pr];
+        const float* xp = X + (size_t)p * cols + 1 + r + pr;
+        int j = 0;
+        for (; j + 8 <= h; j += 8) {  // 8 independent load pairs in flight, summed in j order
+            float yv[8], xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                yv[k] = __ldg(Ybar + (size_t)(j + k) * P + p);
+                xv[k] = __ldg(xp + (size_t)(j + k) * P * cols);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += (double)yv[k] * (double)xv[k];
+        }
+        for (; j < h; ++j) s += (double)Ybar[(size_t)j * P + p] * (double)xp[(size_t)j * P * cols];
         int a = 0, rem = pr;
         while (rem >= r - a) {
             rem -= r - a;
