@@ -904,9 +904,12 @@ std::vector<double> ReducedObjective::hessian(const std::vector<double>& z) cons
 ExitReport reduced_step(SimState& state, const std::vector<double>& pin_positions,
                         const std::vector<double>& external_force, const Model& model,
                         const Mesh& mesh, const Material& mat, const std::vector<double>& mass,
-                        const SolverConfig& cfg, bool quasi_static) {
-    // reduced_solver.cpp:235-277 (L-BFGS method, no runtime cubature)
+                        const SolverConfig& cfg, bool quasi_static, const std::vector<int>* cub_ids,
+                        const std::vector<double>* cub_w) {
+    // reduced_solver.cpp:235-277 (L-BFGS method); cfg.runtime_cubature (:246) as cub_ids / cub_w
     ReducedObjective obj;
+    obj.cub_ids = cub_ids;
+    obj.cub_w = cub_w;
     obj.model = &model;
     obj.mesh = &mesh;
     obj.mat = &mat;

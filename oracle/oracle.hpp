@@ -191,7 +191,8 @@ struct SimState {  // reduced_solver.hpp:43-48
 ExitReport reduced_step(SimState& state, const std::vector<double>& pin_positions,
                         const std::vector<double>& external_force, const Model& model,
                         const Mesh& mesh, const Material& mat, const std::vector<double>& mass,
-                        const SolverConfig& cfg, bool quasi_static);
+                        const SolverConfig& cfg, bool quasi_static,
+                        const std::vector<int>* cub_ids = nullptr, const std::vector<double>* cub_w = nullptr);
 
 // frame_at external force (scenario.cpp:193-199): f = m_i * g_c on free DOFs.
 std::vector<double> gravity_force(const Mesh& mesh, const std::vector<double>& mass, const double g[3]);

@@ -489,7 +489,8 @@ int orc_simulate(void* p, const double* gravity, double epsilon, int max_iters, 
         const std::vector<double> f = gravity_force(c->mesh, c->mass, gravity);
         for (int s = 0; s < steps; ++s) {
             const ExitReport rep = reduced_step(st, c->pins, f, c->model, c->mesh, c->mat, c->mass, cfg,
-                                                quasi_static != 0);
+                                                quasi_static != 0, c->has_cub ? &c->cub_ids : nullptr,
+                                                c->has_cub ? &c->cub_w : nullptr);
             if (codes) codes[s] = rep.code;
             if (iters) iters[s] = rep.iterations;
             if (gnorm) gnorm[s] = rep.final_grad_inf_norm;
@@ -526,7 +527,8 @@ int orc_reduced_step(void* p, const double* pin_positions, const double* force, 
         st.velocities.assign(velocities, velocities + 3 * V);
         st.z.assign(z, z + r);
         const std::vector<double> pins(pin_positions, pin_positions + 3 * V), f(force, force + n);
-        const ExitReport rep = reduced_step(st, pins, f, c->model, c->mesh, c->mat, c->mass, cfg, quasi_static != 0);
+        const ExitReport rep = reduced_step(st, pins, f, c->model, c->mesh, c->mat, c->mass, cfg, quasi_static != 0,
+                                            c->has_cub ? &c->cub_ids : nullptr, c->has_cub ? &c->cub_w : nullptr);
         *code = rep.code;
         *iters = rep.iterations;
         std::memcpy(positions, st.positions.data(), 3 * V * 8);

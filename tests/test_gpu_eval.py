@@ -282,3 +282,33 @@ def test_bench_e2e_hook_matches_eval(product):
     for k in range(6):
         e, g = sysm.eval(Z[k])
         assert e == E[k] and np.array_equal(g, G[k])
+
+
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_wls_step_device(path, product):
+    """test_solvers.cpp:196-225 through the device: with the elastic term removed by runtime
+    cubature (one element of weight 0 = the reference's empty ElementSubset), one reduced_step
+    of a linear-span decoder (here identity hidden layer then the basis) lands on the closed-form
+    weighted least-squares z* = (B^T M B)^-1 B^T M (qbar - q_prev) at 1e-8."""
+    P = product
+    mesh = P.make_bar_mesh(3, 2, 2, 1.0, 0.4, 0.5, jitter_frac=0.05, seed=3)
+    n, r = mesh.num_dofs(), 3
+    rng = np.random.default_rng(407)
+    basis = 0.1 * rng.standard_normal((n, r))
+    shift = P.dof_pack(mesh, mesh.vertices)
+    layers = [P.Layer(np.eye(r), np.zeros(r), P.Activation.Identity),
+              P.Layer(basis, np.zeros(n), P.Activation.Identity)]
+    model = P.SubspaceModel(r, n, layers, shift, np.ones(n))
+    sysm = P.ReducedSystem(mesh, 2.0, 1.5, 3.0, model, "fp64")
+    sysm.use_solve_kernel(path == "solve")
+    sysm.set_cubature(np.array([0]), np.array([0.0]))
+    mass = sysm.mass
+    force = np.zeros(n)
+    force[1::3] = -0.5 * mass[1::3]
+    cfg = P.SolverConfig(epsilon=1e-12, max_iters=1024, max_linesearch=128, lbfgs_history=8, dt=0.05)
+    state = P.rest_state(mesh, r)
+    rep = P.reduced_step(state, P.FrameInput(mesh.vertices.copy(), force), sysm, cfg)
+    qbar = shift + cfg.dt ** 2 * force / mass
+    z_star = np.linalg.solve(basis.T @ (mass[:, None] * basis), basis.T @ (mass * (qbar - shift)))
+    assert rep.code == 1
+    assert np.abs(state.z - z_star).max() < 1e-8, np.abs(state.z - z_star).max()
