@@ -205,6 +205,10 @@ lsb_status lsb_get_trace_raw(const lsb_context* ctx, unsigned long long* out);
 /* Number of kernels this library launched since creation (every launch, graph node
  * executions counted per execution as reported by the device counters). */
 lsb_status lsb_get_launch_count(const lsb_context* ctx, long long* launches);
+/* Developer switches this context was created with ("NAME=value ..."; empty when none): the
+ * LSB_* environment variables are read once, at lsb_create, and never change results except
+ * the timing-only LSB_SOLVE_EXP bits, which a production build rejects. */
+lsb_status lsb_get_dev_flags(const lsb_context* ctx, char* buf, int cap);
 /* Average device duration (ms) of the output-layer forward kernel over the last
  * lsb_profile_eval call, measured with CUDA events on the launching stream. */
 lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double* ms_out_fwd,

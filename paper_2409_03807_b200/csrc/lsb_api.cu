@@ -184,6 +184,37 @@ void upload_pins(Context& c) {
 
 }  // namespace
 
+namespace lsb {
+DevFlags read_dev_flags() {
+    DevFlags f;
+    auto get = [&](const char* name) -> const char* {
+        const char* v = getenv(name);
+        if (v && *v) f.active += std::string(f.active.empty() ? "" : " ") + name + "=" + v;
+        return (v && *v) ? v : nullptr;
+    };
+    if (const char* v = get("LSB_TC")) f.tc = v[0] != '0';
+    if (const char* v = get("LSB_FUSE_GATHER")) f.fuse_gather = v[0] != '0';
+    if (const char* v = get("LSB_CTRL_CLUSTER")) f.ctrl_cluster16 = atoi(v) == 16;
+    if (const char* v = get("LSB_CTRL_FAST")) f.ctrl_fast = v[0] != '0';
+    if (const char* v = get("LSB_DISABLE_SOLVE_KERNEL")) f.disable_solve = v[0] == '1';
+    if (const char* v = get("LSB_SOLVE_TV_GLOBAL")) f.solve_tv_global = v[0] == '1';
+    if (const char* v = get("LSB_CTRL_TILE_W")) f.ctrl_tile_w = (float)atof(v);
+    if (const char* v = get("LSB_PREFETCH_FRAC")) f.pf_frac = std::min(1.0f, std::max(0.0f, (float)atof(v)));
+    if (const char* v = get("LSB_SOLVE_EXP")) f.solve_exp = atoi(v);
+    if (const char* v = get("LSB_TRACE")) f.trace = v[0] == '1';
+    if (const char* v = get("LSB_ELEM_F2")) f.elem_f2 = v[0] == '1';
+    if (const char* v = get("LSB_THETA_TB")) f.theta_tb = std::max(1, std::min(48, atoi(v)));
+    if (const char* v = get("LSB_NONCOOP")) f.noncoop = v[0] == '1';
+    if (const char* v = get("LSB_PIPE")) f.pipe = v[0] != '0';
+#ifndef LSB_TIMING_EXPERIMENTS
+    // bits 1 / 4 skip the tile math / the tv gather: results invalid, timing builds only
+    if (f.solve_exp & (1 | 4))
+        throw LsbError(LSB_EINVAL, "LSB_SOLVE_EXP bits 1/4 (results invalid) need a -DLSB_TIMING_EXPERIMENTS build");
+#endif
+    return f;
+}
+}  // namespace lsb
+
 extern "C" {
 
 const char* lsb_last_error(void) { return g_last_error.c_str(); }
@@ -323,6 +354,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.num_sms = prop.multiProcessorCount;
         c.l2_bytes = (size_t)prop.l2CacheSize;
         c.wsize = precision == LSB_FP64 ? 8 : 4;
+        c.dev = read_dev_flags();
         cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
 
         // ---- mesh (build_mesh semantics) ----
@@ -499,10 +531,7 @@ lsb_status lsb_create(const lsb_mesh_desc* mesh, const lsb_decoder_desc* dec, in
         c.d_launch_acc = static_cast<long long*>(c.dmalloc(sizeof(long long)));
         cuda_check(cudaStreamSynchronize(c.stream), "sync");
         upload_pins(c);
-        {
-            const char* tr = getenv("LSB_TRACE");
-            if (tr && tr[0] == '1') c.d_trace = static_cast<unsigned long long*>(c.dmalloc(8 * 2048));
-        }
+        if (c.dev.trace) c.d_trace = static_cast<unsigned long long*>(c.dmalloc(8 * 2048));
         c.impl = make_impl(precision);
         c.impl->setup(c);
         // defaults: dt 0.05 (SolverConfig), history 8, no inertia
@@ -575,6 +604,8 @@ lsb_status lsb_set_inertia(lsb_context* ctx, const double* qbar, double dt) {
                 for (int k = 0; k < 3; ++k)
                     ut[3 * f + k] = qbar[3 * f + k] - c.mesh.X[3 * (size_t)c.mesh.free_vertex[f] + k];
             c.copy(c.d_ut, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice, "ut");
+            if (!c.d_ut_user) c.d_ut_user = static_cast<double*>(c.dmalloc(sizeof(double) * c.n));
+            c.copy(c.d_ut_user, ut.data(), ut.size() * 8, cudaMemcpyHostToDevice, "ut (user)");
             for (int i = 0; i < c.n; ++i) c.h_eprow[6 * (size_t)i + 5] = ut[i];
             c.copy(c.d_eprow, c.h_eprow.data(), c.h_eprow.size() * 8, cudaMemcpyHostToDevice, "eprow");
         }
@@ -729,6 +760,7 @@ lsb_status lsb_step(lsb_context* ctx, const lsb_solver_config* cfg, int quasi_st
         Context& c = ctx->c;
         prepare_steps(c, 1, cfg, quasi_static);
         c.impl->step(c);
+        restore_user_objective(c);
         get_state(c);
         if (c.h_state->status == kStNonFinite) throw LsbError(LSB_ENONFINITE, "reduced objective: non-finite energy");
         if (report) c.copy(report, c.d_reports, sizeof(lsb_exit_report), cudaMemcpyDeviceToHost, "report");
@@ -742,6 +774,7 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
         Context& c = ctx->c;
         prepare_steps(c, steps, cfg, quasi_static);
         for (int s = 0; s < steps; ++s) c.impl->step(c);
+        restore_user_objective(c);
         sync(c);
         get_state(c);
         if (reports) c.copy(reports, c.d_reports, sizeof(lsb_exit_report) * steps, cudaMemcpyDeviceToHost, "reports");
@@ -790,6 +823,17 @@ lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int ca
             out[2 * i + 1] = t[2 + 2 * i];
         }
         *count = n;
+    });
+}
+
+lsb_status lsb_get_dev_flags(const lsb_context* ctx, char* buf, int cap) {
+    return run([&] {
+        check_ctx(ctx);
+        require(buf && cap > 0, "dev flags: null buffer");
+        const std::string& a = ctx->c.dev.active;
+        const size_t k = std::min(a.size(), (size_t)cap - 1);
+        std::memcpy(buf, a.data(), k);
+        buf[k] = 0;
     });
 }
 
@@ -851,8 +895,8 @@ lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg
         Context& c = ctx->c;
         prepare_steps(c, K, cfg, quasi_static);
         bench_steps(c, K, flush_bytes, step_ms, reports);
+        restore_user_objective(c);
         get_state(c);
-        c.launches += 3LL * 0;
     });
 }
 

@@ -1315,17 +1315,14 @@ struct BatchedEngine : BatchedBase {
                    kTB * 4 * sizeof(short);
         cuda_check(cudaFuncSetAttribute(elem_batched_f2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem_f2), "elem f2 smem");
-        {
-            const char* e = getenv("LSB_ELEM_F2");
-            // measured slower than the scalar kernel (half the threads per column tile lowers
-            // occupancy more than FFMA2 saves issue slots): opt-in
-            use_f2 = (e && e[0] == '1') && BC % (2 * kEcols) == 0;
-        }
+        // measured slower than the scalar kernel (half the threads per column tile lowers
+        // occupancy more than FFMA2 saves issue slots): opt-in
+        use_f2 = c.dev.elem_f2 && BC % (2 * kEcols) == 0;
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem2), "elem2 smem");
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem2), "elem2 smem");
-        tc.init(c.stream, d_W, n, h, BC, c.num_sms);
+        if (c.dev.tc) tc.init(c.stream, d_W, n, h, BC, c.num_sms);
     }
 
     // One group of N <= kGroup columns; Z (N x r, host) -> E (N), G (N x r or null).
@@ -1523,11 +1520,7 @@ struct BatchedEngine : BatchedBase {
         d_gbar = alloc<float>((size_t)V * 3 * P);
         cuda_check(cudaMemsetAsync(d_Wv, 0, 4 * (size_t)V * 3 * P * r, c.stream), "Wv");
         cuda_check(cudaMemsetAsync(d_gbar, 0, 4 * (size_t)V * 3 * P, c.stream), "Gb");
-        {
-            const char* e = getenv("LSB_THETA_TB");
-            const int tb = e ? std::max(1, std::min(48, atoi(e))) : 24;
-            tbk = build_free_blocks(c, tb, true);
-        }
+        tbk = build_free_blocks(c, c.dev.theta_tb, true);
         d_partJ = alloc<float>((size_t)tbk.nslots * 3 * P * r);
         d_partq = alloc<float>((size_t)tbk.nslots * 3 * P);
         d_Abar = alloc<float>((size_t)n * P * (r + 2));

@@ -60,6 +60,31 @@ __global__ void prep_step_kernel(int n, const int* vfree, const double* u_state,
     }
 }
 
+// After a step / simulate: put back the objective lsb_set_inertia installed (the step
+// objective's qbar lives in the same ut / eprow column 5 slots; reference reduced_step builds a
+// fresh ReducedObjective per step and leaves the caller's untouched, reduced_solver.cpp:241-254).
+__global__ void restore_objective_kernel(int n, const double* ut_user, double* ut, double* eprow, DevState* st,
+                                         int has_inertia, double inv_dt2, double dt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double v = ut_user ? ut_user[i] : 0.0;
+        ut[i] = v;
+        eprow[6 * (size_t)i + 5] = v;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->has_inertia = has_inertia;
+        st->quasi_static = has_inertia ? 0 : 1;
+        st->inv_dt2 = inv_dt2;
+        st->dt = dt;
+    }
+}
+
+void restore_user_objective(Context& c) {
+    const bool inert = c.has_qbar && c.d_ut_user;
+    restore_objective_kernel<<<std::max(1, std::min((c.n + 255) / 256, 4 * c.num_sms)), 256, 0, c.stream>>>(
+        c.n, inert ? c.d_ut_user : nullptr, c.d_ut, c.d_eprow, c.d_state, inert ? 1 : 0, 1.0 / (c.dt * c.dt), c.dt);
+    cuda_check(cudaGetLastError(), "restore objective");
+}
+
 // x' = unpack(decode(z*)), v' = (x' - x) / dt over all V rows (:266-276), report.
 __global__ void finalize_step_kernel(int V, const double* U, const char* vpinned, const double* pin_disp,
                                      double* u_state, double* v_state, double* z_state, int r, DevState* st) {
@@ -328,8 +353,7 @@ struct Impl final : ImplBase {
         p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
         // fused gather + VJP: tv for a CTA's rows in shared memory (same grid as the VJP)
         {
-            const char* fe = getenv("LSB_FUSE_GATHER");
-            fuse_gather = !(fe && fe[0] == '0');
+            fuse_gather = c.dev.fuse_gather != 0;
             const size_t tvb = ((size_t)((ntiles + p.grid_vjp - 1) / p.grid_vjp) * ks.tile_rows * sizeof(double) + 127) &
                                ~(size_t)127;
             vjpg_smem = vjp_smem + tvb;
@@ -364,8 +388,7 @@ struct Impl final : ImplBase {
         };
         cs = 8;
         if (slice_words(8) * 8 + fixed > 200 * 1024 || (maxrows + 7) / 8 > 64) cs = 16;
-        if (const char* e = getenv("LSB_CTRL_CLUSTER"))  // developer override (8 or 16)
-            if (atoi(e) == 16) cs = 16;
+        if (c.dev.ctrl_cluster16) cs = 16;  // developer override
         if (slice_words(cs) * 8 + fixed > 220 * 1024 || (maxrows + cs - 1) / cs > 64)
             throw LsbError(LSB_EINVAL, "decoder: hidden layers too large for the control cluster");
         p.cs = cs;
@@ -379,8 +402,7 @@ struct Impl final : ImplBase {
             bool uniform = c.nhid >= 1 && c.r >= 1 && c.r <= 64 && (c.hp == 128 || c.hp == 256);
             for (int l = 0; l < c.nhid && uniform; ++l)
                 uniform = c.hrows[l] == c.hp && c.hcols[l] == (l == 0 ? c.r : c.hp);
-            const char* fe = getenv("LSB_CTRL_FAST");
-            if (uniform && !(fe && fe[0] == '0')) {
+            if (uniform && c.dev.ctrl_fast) {
                 const size_t fsm = ctrl_fast_smem<TS>(c.nhid, c.hcols, c.hp / cs);
                 if (fsm + 1024 <= 227 * 1024) {
                     if (c.hp == 128) ctrl = cs == 8 ? ctrl_fast_kernel<TS, 128, 8> : ctrl_fast_kernel<TS, 128, 16>;
@@ -409,8 +431,7 @@ struct Impl final : ImplBase {
     }
 
     void setup_solve(Context& c) {
-        const char* env = getenv("LSB_DISABLE_SOLVE_KERNEL");
-        if (env && env[0] == '1') {
+        if (c.dev.disable_solve) {
             c.solve_reason = "disabled by LSB_DISABLE_SOLVE_KERNEL";
             return;
         }
@@ -432,8 +453,7 @@ struct Impl final : ImplBase {
         const size_t cap = 227 * 1024 - 2048;  // static smem of the kernel (barriers, flags) + margin
         const size_t ctrl_area = ((size_t)solve_wsl_words + ctrl_fixed_words()) * sizeof(double);
         const int nw = kSolveThreads / 32;
-        const char* tvenv = getenv("LSB_SOLVE_TV_GLOBAL");  // developer / test override
-        for (int tvg = (tvenv && tvenv[0] == '1') ? 1 : 0; tvg < 2; ++tvg) {
+        for (int tvg = c.dev.solve_tv_global; tvg < 2; ++tvg) {
             solve_tv_global = tvg;
             if (tvg == 0) {
                 const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
@@ -485,7 +505,12 @@ struct Impl final : ImplBase {
             return;
         }
         solve_grid = nclusters * cs;
-        if (const char* e = getenv("LSB_CTRL_TILE_W")) solve_ctrl_tile_w = (float)atof(e);  // developer tuning
+        if (solve_grid > kSolveMaxGrid) {  // the control cluster sums the per-CTA partials with 5 x 32 lanes
+            c.solve_reason = "grid of " + std::to_string(solve_grid) + " CTAs exceeds " + std::to_string(kSolveMaxGrid);
+            solve = nullptr;
+            return;
+        }
+        if (c.dev.ctrl_tile_w >= 0.f) solve_ctrl_tile_w = c.dev.ctrl_tile_w;  // developer tuning
         solve_ctrl_tile_w = std::min(1.0f, std::max(0.0f, solve_ctrl_tile_w));
         if (!solve_tv_global) {
             const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
@@ -525,11 +550,10 @@ struct Impl final : ImplBase {
         sp.tv_off_ctrl = solve_tv_off_ctrl;
         sp.tv_cap = solve_tv_cap;
         sp.ctrl_tile_w = solve_ctrl_tile_w;
-        sp.pf_frac = 1.0f;
-        if (const char* e = getenv("LSB_PREFETCH_FRAC")) sp.pf_frac = std::min(1.0f, std::max(0.0f, (float)atof(e)));
+        sp.pf_frac = c.dev.pf_frac;
         sp.tv_global = solve_tv_global;
         sp.wsl_words = solve_wsl_words;
-        if (const char* e = getenv("LSB_SOLVE_EXP")) sp.exp = atoi(e);
+        sp.exp = c.dev.solve_exp;
         sp.seq = ++launch_seq;
         sp.want_grad = want_grad;
         sp.u_state = c.d_u_state;
@@ -560,19 +584,23 @@ struct Impl final : ImplBase {
         if (z)
             for (int i = 0; i < c.r; ++i) sp.z[i] = z[i];
         cudaLaunchConfig_t cfg = {};
-        // cluster launch only: the grid barrier is the kernel's own (grid_barrier), and
-        // the grid never exceeds the co-resident cluster count
-        cudaLaunchAttribute at[1];
+        // cooperative cluster launch: the kernel's own grid barrier (grid_barrier) needs every
+        // CTA co-resident, which the cooperative attribute makes the driver guarantee (or
+        // refuse the launch) even when other contexts or processes share the GPU.
+        // LSB_NONCOOP=1 (profiling only) drops the attribute so ncu can replay the kernel.
+        cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = cs;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
         cfg.gridDim = dim3(solve_grid);
         cfg.blockDim = dim3(kSolveThreads);
         cfg.dynamicSmemBytes = solve_smem;
         cfg.stream = c.stream;
         cfg.attrs = at;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = c.dev.noncoop ? 1 : 2;
         cuda_check(cudaLaunchKernelEx(&cfg, solve, ps, sp), "solve kernel launch");
         c.launches += 1;
     }

@@ -26,6 +26,30 @@ void cuda_check(cudaError_t e, const char* what);
 
 struct Context;
 
+// Developer switches (A/B experiments, tests, profiling).  Read from the environment exactly
+// once, when a context is created (lsb_create) -- never per launch -- and reported by
+// lsb_get_dev_flags so a bench line records any that were set.  None changes results except
+// LSB_SOLVE_EXP bits 1 and 4 (timing-only experiments that skip work), which are rejected
+// unless the library is built with -DLSB_TIMING_EXPERIMENTS.
+struct DevFlags {
+    int tc = 1;               // LSB_TC=0: batched GEMMs on the CUDA-core SGEMM instead of tcgen05
+    int fuse_gather = 1;      // LSB_FUSE_GATHER=0: separate vertex-gather kernel (multi-kernel path)
+    int ctrl_cluster16 = 0;   // LSB_CTRL_CLUSTER=16: 16-CTA control clusters
+    int ctrl_fast = 1;        // LSB_CTRL_FAST=0: generic control-cluster kernel
+    int disable_solve = 0;    // LSB_DISABLE_SOLVE_KERNEL=1: multi-kernel path only
+    int solve_tv_global = 0;  // LSB_SOLVE_TV_GLOBAL=1: persistent kernel's tv in global memory
+    float ctrl_tile_w = -1.f; // LSB_CTRL_TILE_W: control CTAs' W_out tile share (<0: default)
+    float pf_frac = 1.f;      // LSB_PREFETCH_FRAC: cold-start L2 prefetch fraction
+    int solve_exp = 0;        // LSB_SOLVE_EXP: persistent-kernel A/B bits (lsb_solve.cuh SolveParams::exp)
+    int trace = 0;            // LSB_TRACE=1: persistent-kernel phase timestamps
+    int elem_f2 = 0;          // LSB_ELEM_F2=1: FFMA2 batched element kernel
+    int theta_tb = 24;        // LSB_THETA_TB: tets per block of the theta element pass
+    int noncoop = 0;          // LSB_NONCOOP=1: persistent kernel as a plain cluster launch (ncu replay)
+    int pipe = 1;             // LSB_PIPE=0: classic multi-kernel body instead of the pipelined pass
+    std::string active;       // "NAME=value ..." of every switch found set
+};
+DevFlags read_dev_flags();
+
 struct ImplBase {
     virtual ~ImplBase() = default;
     virtual void setup(Context& c) = 0;
@@ -52,6 +76,7 @@ struct ImplBase {
     virtual void solve_step(Context& c, int quasi) = 0;
 };
 std::unique_ptr<ImplBase> make_impl(int precision);
+void restore_user_objective(Context& c);
 
 // Batched / second-order engines (lsb_batched.cu, lsb_hessian.cu).
 struct BatchedBase {
@@ -83,6 +108,7 @@ struct Context {
     void* d_Wout = nullptr;  // n x hp
     double *d_bout = nullptr, *d_sout = nullptr, *d_cout = nullptr, *d_dsout = nullptr;
     double *d_mass = nullptr, *d_ut = nullptr, *d_rin = nullptr;
+    double* d_ut_user = nullptr;  // qbar - X of the lsb_set_inertia objective (restored after steps)
     double* d_eprow = nullptr;  // n x 6 {b, s, shift - X, m, U slot, qbar - X}
     std::vector<double> h_eprow;
     double* d_tv = nullptr;     // n
@@ -118,6 +144,8 @@ struct Context {
     bool use_solve = true;
     std::string solve_reason;
     unsigned long long* d_trace = nullptr;  // solve-kernel phase trace (LSB_TRACE=1)  // route eval/minimize/step through the persistent kernel when available
+
+    DevFlags dev;
 
     std::unique_ptr<ImplBase> impl;
     std::unique_ptr<BatchedBase> batched;

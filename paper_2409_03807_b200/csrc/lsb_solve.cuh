@@ -20,6 +20,7 @@ namespace lsb {
 #endif
 constexpr int kSolveThreads = LSB_SOLVE_THREADS;  // 9 warps: all stream (self-issued rings) and all compute
 constexpr int kSolveMaxStages = 36;
+constexpr int kSolveMaxGrid = 160;  // control-cluster partial sums: 5 x 32 lanes
 constexpr int kSolveBarBytes = 512;  // full barriers (kSolveMaxStages x 8 B, padded)
 
 // Launch-wide scalars the non-control CTAs need (written by the control CTA).

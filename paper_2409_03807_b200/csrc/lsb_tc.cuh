@@ -406,8 +406,6 @@ struct TcGemm {
 
     // W: device fp32 n x h row-major.  N = batch columns per call.
     void init(cudaStream_t s, const float* W, int n_, int h_, int N_, int num_sms) {
-        const char* env = getenv("LSB_TC");
-        if (env && env[0] == '0') return;
         if (h_ > tc::kTileM || N_ % 32 != 0 || N_ > 256 || N_ < 32) return;
         n = n_;
         h = h_;

@@ -463,6 +463,12 @@ class ReducedSystem:
     def use_solve_kernel(self, enable: bool):
         check(lib().lsb_set_solve_kernel(self._h, int(enable)))
 
+    def dev_flags(self) -> str:
+        """Developer switches (LSB_* environment, read once at creation) active on this context."""
+        buf = C.create_string_buffer(1024)
+        check(lib().lsb_get_dev_flags(self._h, buf, 1024))
+        return buf.value.decode()
+
     # --- measurement hooks
     def launch_count(self) -> int:
         v = C.c_longlong()

@@ -122,3 +122,39 @@ def test_cpp_api_binary():
     res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert res.stdout.startswith("ok")
+
+
+@pytest.mark.parametrize("path", ["solve", "graph"])
+def test_step_leaves_user_objective_intact(path, oracle, product):
+    """lsb_set_inertia, then lsb_step / lsb_simulate, then lsb_eval / lsb_eval_batched: the
+    evaluations still see the objective the caller installed (reference reduced_step builds
+    its own ReducedObjective, reduced_solver.cpp:241-254)."""
+    from paper_2409_03807_b200 import configs
+    P = product
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    sysm.use_solve_kernel(path == "solve")
+    ob = oracle.problem("c1")
+    rng = np.random.default_rng(17)
+    qbar = configs.timestep0_qbar(pr, ob.mass) + 1e-3 * rng.standard_normal(pr.model.n)
+    dt = 0.02
+    sysm.set_inertia(qbar, dt)
+    sysm.set_state(pr.initial_state())
+    sysm.set_external_force(P.gravity_force(pr.mesh, sysm.mass, configs.GRAVITY))
+    cfg = configs.solver_config()
+    sysm.step(cfg)
+    sysm.simulate(2, cfg)
+    Z = 0.5 * rng.standard_normal((3, pr.model.r))
+    for z in Z:
+        E, g = sysm.eval(z)
+        Eo, go = ob.eval(z, qbar=qbar, dt=dt)
+        assert rel_err(E, Eo) < 1e-10 and rel_err(g, go) < 1e-10, (rel_err(E, Eo), rel_err(g, go))
+    Eb, Gb = sysm.eval_batched(Z)
+    Eo, Go = ob.eval_batch(Z, qbar=qbar, dt=dt)
+    assert rel_err(Eb, Eo) < 1e-4 and rel_err(Gb, Go) < 1e-4
+    # quasi-static user objective survives a dynamic step too
+    sysm.set_inertia(None, dt)
+    sysm.step(cfg)
+    E, g = sysm.eval(Z[0])
+    Eo, go = ob.eval(Z[0], qbar=None)
+    assert rel_err(E, Eo) < 1e-10 and rel_err(g, go) < 1e-10
