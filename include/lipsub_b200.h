@@ -220,6 +220,14 @@ lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double*
  * stream), and the energy. */
 lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, double* eval_ms,
                            double* out_fwd_ms, double* E);
+/* lsb_bench_evals with want_grad = 0: value-only evaluations (lsb_eval with grad == NULL). */
+lsb_status lsb_bench_evals_ex(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, int want_grad,
+                              double* eval_ms, double* out_fwd_ms, double* E);
+/* reps calls of lsb_eval_batched (kind 0: B latents Z1 -> E, G) or lsb_lipschitz_loss (kind 1: B pairs
+ * Z1, Z2 -> loss), each preceded by an L2 flush and bracketed by CUDA events on the context stream
+ * (the bracket includes the call's own small host<->device copies); ms[k] per call. */
+lsb_status lsb_bench_batched(lsb_context* ctx, int kind, int B, const double* Z1, const double* Z2, int reps,
+                             size_t flush_bytes, double* ms, double* E, double* G, double* loss);
 /* K reduced steps from the current state (lsb_set_state), each preceded by an L2
  * flush; per step: device time (CUDA events) and exit report. */
 lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg, int quasi_static,

@@ -103,6 +103,8 @@ SIGNATURES = [
     ("lsb_lipschitz_loss_grad", C.c_int, [_CTX, C.c_int, _D, _D, _D, _D]),
     ("lsb_bench_evals", C.c_int, [_CTX, C.c_int, _D, C.c_size_t, _D, _D, _D]),
     ("lsb_bench_e2e", C.c_int, [_CTX, C.c_int, _D, _D, _D, _D]),
+    ("lsb_bench_evals_ex", C.c_int, [_CTX, C.c_int, _D, C.c_size_t, C.c_int, _D, _D, _D]),
+    ("lsb_bench_batched", C.c_int, [_CTX, C.c_int, C.c_int, _D, _D, C.c_int, C.c_size_t, _D, _D, _D, _D]),
     ("lsb_bench_steps", C.c_int, [_CTX, C.c_int, C.POINTER(lsb_solver_config), C.c_int, C.c_size_t, _D,
                                   C.POINTER(lsb_exit_report)]),
     ("lsb_get_solve_info", C.c_int, [_CTX, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

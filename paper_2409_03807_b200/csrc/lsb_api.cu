@@ -17,7 +17,9 @@
 #include "lsb_newton.hpp"
 
 namespace lsb {
-void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms, double* E);
+void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms, double* E,
+                 bool want_grad);
+void bench_call(Context& c, int reps, size_t flush_bytes, double* ms, const std::function<void()>& call);
 void bench_steps(Context& c, int K, size_t flush_bytes, double* step_ms, lsb_exit_report* reps);
 }  // namespace lsb
 
@@ -865,10 +867,39 @@ lsb_status lsb_profile_eval(lsb_context* ctx, const double* z, int reps, double*
 
 lsb_status lsb_bench_evals(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, double* eval_ms,
                            double* out_fwd_ms, double* E) {
+    return lsb_bench_evals_ex(ctx, K, Z, flush_bytes, 1, eval_ms, out_fwd_ms, E);
+}
+
+lsb_status lsb_bench_evals_ex(lsb_context* ctx, int K, const double* Z, size_t flush_bytes, int want_grad,
+                              double* eval_ms, double* out_fwd_ms, double* E) {
     return run([&] {
         check_ctx(ctx);
         require(K >= 1 && Z && eval_ms && out_fwd_ms, "bench: bad arguments");
-        bench_evals(ctx->c, K, Z, flush_bytes, eval_ms, out_fwd_ms, E);
+        bench_evals(ctx->c, K, Z, flush_bytes, eval_ms, out_fwd_ms, E, want_grad != 0);
+    });
+}
+
+lsb_status lsb_bench_batched(lsb_context* ctx, int kind, int B, const double* Z1, const double* Z2, int reps,
+                             size_t flush_bytes, double* ms, double* E, double* G, double* loss) {
+    return run([&] {
+        check_ctx(ctx);
+        require(reps >= 1 && B >= 1 && Z1 && ms, "bench batched: bad arguments");
+        Context& c = ctx->c;
+        if (kind == 0) {
+            require(E != nullptr, "bench batched: E required");
+            bench_call(c, reps, flush_bytes, ms, [&] { batched_eval(c, B, Z1, E, G); });
+        } else if (kind == 1) {
+            require(Z2 && loss, "bench batched: Z2 and loss required");
+            for (int p = 0; p < B; ++p) {  // losses.cpp:202-204
+                double dz2 = 0.0;
+                for (int k = 0; k < c.r; ++k)
+                    dz2 += (Z1[p * c.r + k] - Z2[p * c.r + k]) * (Z1[p * c.r + k] - Z2[p * c.r + k]);
+                require(dz2 > 0.0, "lipschitz loss: coincident pair");
+            }
+            bench_call(c, reps, flush_bytes, ms, [&] { *loss = lipschitz_loss(c, B, Z1, Z2); });
+        } else {
+            throw LsbError(LSB_EINVAL, "bench batched: kind must be 0 (eval_batched) or 1 (lipschitz loss)");
+        }
     });
 }
 

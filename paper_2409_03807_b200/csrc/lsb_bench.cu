@@ -5,6 +5,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <vector>
 
 #include "../../include/lipsub_b200.h"
@@ -21,7 +22,7 @@ __global__ void flush_kernel(uint4* p, size_t n, unsigned v) {
 }
 
 void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms,
-                 double* E) {
+                 double* E, bool want_grad) {
     const int r = c.r;
     double* dZ = nullptr;
     cuda_check(cudaMalloc(&dZ, sizeof(double) * (size_t)K * r), "bench Z");
@@ -43,7 +44,7 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
         cuda_check(cudaMemcpyAsync(c.d_state->zt, dZ + (size_t)k * r, sizeof(double) * r, cudaMemcpyDeviceToDevice,
                                    c.stream),
                    "z");
-        const int nev = c.impl->eval_timed(c, ev);
+        const int nev = c.impl->eval_timed(c, ev, want_grad);
         cuda_check(cudaEventSynchronize(ev[3]), "bench sync");
         float t0, t1;
         cudaEventElapsedTime(&t0, ev[0], ev[3]);
@@ -78,6 +79,30 @@ void bench_steps(Context& c, int K, size_t flush_bytes, double* step_ms, lsb_exi
     cudaEventDestroy(e1);
     if (flush) cudaFree(flush);
     if (reps) c.copy(reps, c.d_reports, sizeof(lsb_exit_report) * K, cudaMemcpyDeviceToHost, "reports");
+}
+
+// One library call (batched evaluation or Lipschitz loss, `call`) per rep, each preceded by an L2
+// flush and bracketed by CUDA events on the context stream.  The bracket holds everything the
+// call enqueues on that stream, including its small host<->device copies of Z and results.
+void bench_call(Context& c, int reps, size_t flush_bytes, double* ms, const std::function<void()>& call) {
+    void* flush = nullptr;
+    if (flush_bytes) cuda_check(cudaMalloc(&flush, flush_bytes), "bench flush");
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    for (int k = 0; k < reps; ++k) {
+        if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
+        cuda_check(cudaEventRecord(e0, c.stream), "ev");
+        call();
+        cuda_check(cudaEventRecord(e1, c.stream), "ev");
+        cuda_check(cudaEventSynchronize(e1), "bench sync");
+        float t;
+        cudaEventElapsedTime(&t, e0, e1);
+        ms[k] = t;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (flush) cudaFree(flush);
 }
 
 }  // namespace lsb

@@ -241,6 +241,7 @@ struct Impl final : ImplBase {
     int cs = 8;
     cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_timed = nullptr;
     cudaEvent_t timed_ev[4] = {};
+    int timed_want = 1;
     cudaGraphConditionalHandle h_min{}, h_step{};
 
     ~Impl() override {
@@ -249,21 +250,22 @@ struct Impl final : ImplBase {
         if (g_timed) cudaGraphExecDestroy(g_timed);
     }
 
-    int eval_timed(Context& c, cudaEvent_t* ev) override {
+    int eval_timed(Context& c, cudaEvent_t* ev, bool want_grad) override {
         if (solve && c.use_solve) {
             cuda_check(cudaEventRecord(ev[0], c.stream), "ev");
-            launch_solve(c, 0, 0, 1);
+            launch_solve(c, 0, 0, want_grad ? 1 : 0);
             cuda_check(cudaEventRecord(ev[3], c.stream), "ev");
             return 2;
         }
-        if (!g_timed || ev[0] != timed_ev[0]) {
+        if (!g_timed || ev[0] != timed_ev[0] || timed_want != (int)want_grad) {
             if (g_timed) cudaGraphExecDestroy(g_timed);
             for (int k = 0; k < 4; ++k) timed_ev[k] = ev[k];
+            timed_want = want_grad ? 1 : 0;
             cudaGraph_t g;
             cuda_check(cudaGraphCreate(&g, 0), "graph create");
             cudaGraphNode_t e0, e1, e2, e3;
             cuda_check(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ev[0]), "event node");
-            int cm = kCtrlStart, mode = kModeEval, want = 1;
+            int cm = kCtrlStart, mode = kModeEval, want = timed_want;
             EvalParams<TS> pg = p;
             void* sargs[] = {&pg, &cm, &mode, &want};
             cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs, ctrl_threads);

@@ -65,7 +65,7 @@ struct ImplBase {
     // Records ev[0] .. ev[3] around one evaluation (ev[1] .. ev[2]: the output-layer kernel)
     // and returns 4, or records only ev[0] and ev[3] around a single-launch evaluation and
     // returns 2 (every event record costs ~2.7 us of GPU time inside the bracket).
-    virtual int eval_timed(Context& c, cudaEvent_t* ev) = 0;
+    virtual int eval_timed(Context& c, cudaEvent_t* ev, bool want_grad = true) = 0;
     // One evaluation at z with z passed by value and {E, status, grad} written by the kernel into
     // host-mapped memory out (device view out_dev); false when this path is unavailable.
     virtual bool eval_direct(Context& c, const double* z, bool want_grad, double* out_dev) = 0;
