@@ -161,6 +161,28 @@ lsb_status lsb_simulate(lsb_context* ctx, int steps, const lsb_solver_config* cf
 
 /* ---- batched / second order ----------------------------------------------------------------- */
 /* E and grad for B latent vectors (Z: B*r row-major) of the current objective. */
+/* ---- the reference's secondary hot-path primitives, evaluated on the device over the context's
+ * resident mesh, per-tet material (the active element set under lsb_set_cubature) and decoder.
+ * q is a free-DOF configuration (n, the layout of decode), pinned vertices sit at the context's pin
+ * positions (dof_unpack, proj/src/mesh.cpp:448-461).  fp64 arithmetic; element records in the
+ * context's storage precision. */
+/* assemble(ctx, q) elastic branch (proj/include/lipsub/energy.hpp:99-101; proj/src/energy.cpp:404-437):
+ * value = sum_e E_e over all elements (pinned included), grad (nullable) = free-DOF gradient (n). */
+lsb_status lsb_assemble(lsb_context* ctx, const double* q, double* value, double* grad /* nullable */);
+/* element_snh (proj/include/lipsub/energy.hpp:71-72; proj/src/energy.cpp:280-298) for `count` element ids at
+ * full-space positions (V x 3) with each element's own mu, lambda: energy[k], grad[12 k..] (local order
+ * vertex-major, k*3+a), hess[144 k..] (12 x 12 row-major, nullable). */
+lsb_status lsb_element_snh(lsb_context* ctx, int count, const int* ids, const double* positions, double* energy,
+                           double* grad, double* hess /* nullable */);
+/* elastic_hessian_apply (proj/include/lipsub/energy.hpp:109-112; proj/src/energy.cpp:481-493):
+ * out += H(q) in, in / out n x k row-major. */
+lsb_status lsb_elastic_hessian_apply(lsb_context* ctx, const double* q, int k, const double* in, double* out);
+/* decode_jacobian (proj/include/lipsub/net.hpp:52-53; proj/src/net.cpp:159-190): J = d decode / dz, n x r row-major. */
+lsb_status lsb_decode_jacobian(lsb_context* ctx, const double* z, double* J);
+/* decode_second_directional (proj/include/lipsub/net.hpp:57-59; proj/src/net.cpp:192-240): d2 decode / dz2 (u, v). */
+lsb_status lsb_decode_second_directional(lsb_context* ctx, const double* z, const double* u, const double* v,
+                                         double* out);
+
 lsb_status lsb_eval_batched(lsb_context* ctx, int B, const double* Z, double* E, double* G /* nullable */);
 /* Reduced elastic-potential Hessians d2P/dz2 (B*r*r) — reduced_potential_hessian. */
 lsb_status lsb_hessian_batched(lsb_context* ctx, int B, const double* Z, double* H);

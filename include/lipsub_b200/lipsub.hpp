@@ -203,6 +203,35 @@ class ReducedSystem {
         check(lsb_decode(ctx_, z.data(), q.data()));
         return q;
     }
+    // decode_jacobian (net.hpp:52-53): n x r, row-major.
+    VectorXd decode_jacobian(const VectorXd& z) {
+        if ((int)z.size() != r_) throw std::invalid_argument("decode: z has wrong length");
+        VectorXd J((size_t)n_ * r_);
+        check(lsb_decode_jacobian(ctx_, z.data(), J.data()));
+        return J;
+    }
+    // decode_second_directional (net.hpp:57-59).
+    VectorXd decode_second_directional(const VectorXd& z, const VectorXd& u, const VectorXd& v) {
+        if ((int)z.size() != r_ || (int)u.size() != r_ || (int)v.size() != r_)
+            throw std::invalid_argument("decode: z has wrong length");
+        VectorXd out(n_);
+        check(lsb_decode_second_directional(ctx_, z.data(), u.data(), v.data(), out.data()));
+        return out;
+    }
+    // assemble (energy.hpp:99-101), elastic branch: value and (optionally) the free-DOF gradient.
+    double assemble(const VectorXd& q, VectorXd* grad) {
+        if ((int)q.size() != n_) throw std::invalid_argument("assemble: q has wrong length");
+        double v = 0.0;
+        if (grad) grad->resize(n_);
+        check(lsb_assemble(ctx_, q.data(), &v, grad ? grad->data() : nullptr));
+        return v;
+    }
+    // elastic_hessian_apply (energy.hpp:109-112): out += H(q) in, n x k row-major.
+    void elastic_hessian_apply(const VectorXd& q, int k, const VectorXd& in, VectorXd& out) {
+        if ((int)q.size() != n_ || (long long)in.size() != (long long)n_ * k || in.size() != out.size())
+            throw std::invalid_argument("elastic_hessian_apply: shape mismatch");
+        check(lsb_elastic_hessian_apply(ctx_, q.data(), k, in.data(), out.data()));
+    }
     double eval(const VectorXd& z, VectorXd* grad) {
         if ((int)z.size() != r_) throw std::invalid_argument("decode: z has wrong length");
         double v = 0.0;

@@ -95,6 +95,11 @@ SIGNATURES = [
     ("lsb_step", C.c_int, [_CTX, C.POINTER(lsb_solver_config), C.c_int, C.POINTER(lsb_exit_report)]),
     ("lsb_simulate", C.c_int, [_CTX, C.c_int, C.POINTER(lsb_solver_config), C.c_int, C.POINTER(lsb_exit_report), _D]),
     ("lsb_eval_batched", C.c_int, [_CTX, C.c_int, _D, _D, _D]),
+    ("lsb_assemble", C.c_int, [_CTX, _D, _D, _D]),
+    ("lsb_element_snh", C.c_int, [_CTX, C.c_int, C.POINTER(C.c_int), _D, _D, _D, _D]),
+    ("lsb_elastic_hessian_apply", C.c_int, [_CTX, _D, C.c_int, _D, _D]),
+    ("lsb_decode_jacobian", C.c_int, [_CTX, _D, _D]),
+    ("lsb_decode_second_directional", C.c_int, [_CTX, _D, _D, _D, _D]),
     ("lsb_hessian_batched", C.c_int, [_CTX, C.c_int, _D, _D]),
     ("lsb_objective_hessian", C.c_int, [_CTX, C.c_int, _D, _D]),
     ("lsb_set_cubature", C.c_int, [_CTX, C.c_int, C.POINTER(C.c_int), _D]),

@@ -15,6 +15,7 @@
 #include "lsb_batched.hpp"
 #include "lsb_context.hpp"
 #include "lsb_newton.hpp"
+#include "lsb_refops.hpp"
 
 namespace lsb {
 void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms, double* E,
@@ -928,6 +929,52 @@ lsb_status lsb_bench_steps(lsb_context* ctx, int K, const lsb_solver_config* cfg
         bench_steps(c, K, flush_bytes, step_ms, reports);
         restore_user_objective(c);
         get_state(c);
+    });
+}
+
+lsb_status lsb_assemble(lsb_context* ctx, const double* q, double* value, double* grad) {
+    return run([&] {
+        check_ctx(ctx);
+        require(q && value, "assemble: null argument");
+        refops_assemble(ctx->c, q, value, grad);
+    });
+}
+
+lsb_status lsb_element_snh(lsb_context* ctx, int count, const int* ids, const double* positions, double* energy,
+                           double* grad, double* hess) {
+    return run([&] {
+        check_ctx(ctx);
+        require(count >= 0 && (count == 0 || (ids && positions && energy && grad)), "element_snh: bad arguments");
+        if (count == 0) return;
+        for (int k = 0; k < count; ++k)
+            require(ids[k] >= 0 && ids[k] < ctx->c.mesh.E, "element_snh: element id out of range");
+        refops_element_snh(ctx->c, count, ids, positions, energy, grad, hess);
+    });
+}
+
+lsb_status lsb_elastic_hessian_apply(lsb_context* ctx, const double* q, int k, const double* in, double* out) {
+    return run([&] {
+        check_ctx(ctx);
+        require(k >= 0 && q && (k == 0 || (in && out)), "elastic_hessian_apply: bad arguments");
+        if (k == 0) return;
+        refops_elastic_hessian_apply(ctx->c, q, k, in, out);
+    });
+}
+
+lsb_status lsb_decode_jacobian(lsb_context* ctx, const double* z, double* J) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z && J, "decode_jacobian: null argument");
+        refops_decode_jacobian(ctx->c, z, J);
+    });
+}
+
+lsb_status lsb_decode_second_directional(lsb_context* ctx, const double* z, const double* u, const double* v,
+                                         double* out) {
+    return run([&] {
+        check_ctx(ctx);
+        require(z && u && v && out, "decode_second_directional: null argument");
+        refops_decode_second_directional(ctx->c, z, u, v, out);
     });
 }
 

@@ -149,6 +149,7 @@ struct Context {
 
     std::unique_ptr<ImplBase> impl;
     std::unique_ptr<BatchedBase> batched;
+    std::unique_ptr<BatchedBase> refops;  // scratch of the reference-primitive operations (lsb_refops.cu)
     long long batched_launches = 0;
     std::vector<void*> allocations;
     void dfree(void* p);

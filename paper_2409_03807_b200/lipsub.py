@@ -340,6 +340,57 @@ class ReducedSystem:
         check(lib().lsb_decode(self._h, dptr(z), dptr(q)))
         return q
 
+    # --- the reference's secondary primitives (device; energy.hpp:71-112, net.hpp:52-59)
+    def decode_jacobian(self, z: np.ndarray) -> np.ndarray:
+        """decode_jacobian (net.cpp:159-190): n x r."""
+        z = np.ascontiguousarray(z, np.float64)
+        if z.shape[0] != self.r:
+            raise ValueError("decode: z has wrong length")
+        J = np.zeros((self.n, self.r))
+        check(lib().lsb_decode_jacobian(self._h, dptr(z), dptr(J)))
+        return J
+
+    def decode_second_directional(self, z: np.ndarray, u: np.ndarray, v: np.ndarray) -> np.ndarray:
+        """decode_second_directional (net.cpp:192-240)."""
+        z, u, v = (np.ascontiguousarray(a, np.float64) for a in (z, u, v))
+        if not (z.shape[0] == u.shape[0] == v.shape[0] == self.r):
+            raise ValueError("decode: z has wrong length")
+        out = np.zeros(self.n)
+        check(lib().lsb_decode_second_directional(self._h, dptr(z), dptr(u), dptr(v), dptr(out)))
+        return out
+
+    def assemble(self, q: np.ndarray, want_grad: bool = True):
+        """assemble (energy.cpp:404-437), elastic branch: (value, free-DOF gradient)."""
+        q = np.ascontiguousarray(q, np.float64)
+        if q.shape[0] != self.n:
+            raise ValueError("assemble: q has wrong length")
+        v = C.c_double()
+        g = np.zeros(self.n) if want_grad else None
+        check(lib().lsb_assemble(self._h, dptr(q), C.byref(v), dptr(g)))
+        return (v.value, g) if want_grad else v.value
+
+    def element_snh(self, ids, positions: np.ndarray, want_hessian: bool = True):
+        """element_snh (energy.cpp:280-298) for element ids at full-space positions (V x 3):
+        (energy[k], grad[k, 12], hess[k, 12, 12] or None), each element with its own mu, lambda."""
+        ids = np.ascontiguousarray(np.atleast_1d(ids), np.int32)
+        pos = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        if pos.shape[0] != self.mesh.num_vertices():
+            raise ValueError("element_snh: positions must be V x 3")
+        k = ids.size
+        e, g = np.zeros(k), np.zeros((k, 12))
+        H = np.zeros((k, 12, 12)) if want_hessian else None
+        check(lib().lsb_element_snh(self._h, k, ids.ctypes.data_as(C.POINTER(C.c_int)), dptr(pos), dptr(e), dptr(g),
+                                    dptr(H)))
+        return e, g, H
+
+    def elastic_hessian_apply(self, q: np.ndarray, Y: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """elastic_hessian_apply (energy.cpp:481-493): out += H(q) Y, Y n x k."""
+        q = np.ascontiguousarray(q, np.float64)
+        Y = np.ascontiguousarray(Y, np.float64).reshape(self.n, -1)
+        res = np.zeros_like(Y) if out is None else np.ascontiguousarray(out, np.float64).copy()
+        check(lib().lsb_elastic_hessian_apply(self._h, dptr(q), Y.shape[1], dptr(Y), dptr(res)))
+        return res
+
     def lbfgs(self, z: np.ndarray, cfg: SolverConfig) -> Tuple[np.ndarray, ExitReport]:
         cfg.validate()
         z = np.array(z, dtype=np.float64, copy=True)
