@@ -342,8 +342,7 @@ def single_instance(name, K, W, T, R, want_cpu, cpu_sample, e2e=True):
             "traffic": TRAFFIC.get((name, solve["in_use"])), "kernel": kname, "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": alg,
             "algorithmic_formula": "w(2nh+9n)+E(16+10w)[+2wE] per E+grad eval (SURVEY 8d)",
-            "value_only_frac": alg_vo / (float(vo_ms.mean()) * 1e-3) / 1e9 / hbm,
-            "output_layer_kernel_ms": float(of_ms.mean()) if not solve["in_use"] else None}
+            "value_only_frac": alg_vo / (float(vo_ms.mean()) * 1e-3) / 1e9 / hbm}
     rec = {
         "config": {"workload": f"{name}: {spec.grid[0]}x{spec.grid[1]}x{spec.grid[2]} Kuhn bar, {E} tets, n={n}, "
                                f"d={r}, {spec.hidden_layers}x{h} ELU, {sysm.precision}"

@@ -222,6 +222,9 @@ lsb_status lsb_get_trace(const lsb_context* ctx, unsigned long long* out, int ca
  * b < 256 (globaltimer ns): k = 0 entry, 1 first grid-barrier arrival, 2 / 3 / 4 end of the first
  * evaluation's output-layer / element / VJP phase. */
 lsb_status lsb_get_trace_raw(const lsb_context* ctx, unsigned long long* out);
+/* Developer hook (LSB_TRACE=1 at create): per ticket of the last sweep-pass launch
+ * {cta << 32 | item code, t_start, t_dependencies_met, t_end} (globaltimer ns); *count = tickets. */
+lsb_status lsb_get_sweep_trace(const lsb_context* ctx, unsigned long long* out, int cap, int* count);
 
 /* ---- measurement hooks (bench.py) ------------------------------------------------------------ */
 /* Number of kernels this library launched since creation (every launch, graph node

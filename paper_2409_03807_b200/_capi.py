@@ -116,6 +116,7 @@ SIGNATURES = [
     ("lsb_set_solve_kernel", C.c_int, [_CTX, C.c_int]),
     ("lsb_get_trace", C.c_int, [_CTX, C.POINTER(C.c_ulonglong), C.c_int, C.POINTER(C.c_int)]),
     ("lsb_get_trace_raw", C.c_int, [_CTX, C.POINTER(C.c_ulonglong)]),
+    ("lsb_get_sweep_trace", C.c_int, [_CTX, C.POINTER(C.c_ulonglong), C.c_int, C.POINTER(C.c_int)]),
     ("lsb_get_launch_count", C.c_int, [_CTX, C.POINTER(C.c_longlong)]),
     ("lsb_get_dev_flags", C.c_int, [_CTX, C.c_char_p, C.c_int]),
     ("lsb_profile_eval", C.c_int, [_CTX, _D, C.c_int, _D, _D, _D, _D]),

@@ -208,7 +208,11 @@ DevFlags read_dev_flags() {
     if (const char* v = get("LSB_ELEM_F2")) f.elem_f2 = v[0] == '1';
     if (const char* v = get("LSB_THETA_TB")) f.theta_tb = std::max(1, std::min(48, atoi(v)));
     if (const char* v = get("LSB_NONCOOP")) f.noncoop = v[0] == '1';
-    if (const char* v = get("LSB_PIPE")) f.pipe = v[0] != '0';
+    if (const char* v = get("LSB_SWEEP")) f.sweep = v[0] == '1';
+    if (const char* v = get("LSB_PDL")) f.pdl = atoi(v) & 15;
+    if (const char* v = get("LSB_L2PF")) f.l2_pf = std::max(0, std::min(256, atoi(v)));
+    if (const char* v = get("LSB_ELEM_F32")) f.elem_f32 = v[0] != '0';
+    if (const char* v = get("LSB_SWEEP_LAG")) f.sweep_lag = std::min(8.0f, std::max(0.0f, (float)atof(v)));
 #ifndef LSB_TIMING_EXPERIMENTS
     // bits 1 / 4 skip the tile math / the tv gather: results invalid, timing builds only
     if (f.solve_exp & (1 | 4))
@@ -810,6 +814,17 @@ lsb_status lsb_get_trace_raw(const lsb_context* ctx, unsigned long long* out) {
         check_ctx(ctx);
         require(ctx->c.d_trace != nullptr, "trace: LSB_TRACE=1 not set at create");
         ctx->c.copy(out, ctx->c.d_trace, 8 * 2048, cudaMemcpyDeviceToHost, "trace");
+    });
+}
+
+lsb_status lsb_get_sweep_trace(const lsb_context* ctx, unsigned long long* out, int cap, int* count) {
+    return run([&] {
+        check_ctx(ctx);
+        require(count != nullptr, "sweep trace: null count");
+        *count = ctx->c.d_sweep_trace ? ctx->c.sweep_tickets : 0;
+        if (!ctx->c.d_sweep_trace || !out) return;
+        const size_t words = std::min<size_t>((size_t)cap, 4 * (size_t)ctx->c.sweep_tickets);
+        ctx->c.copy(out, ctx->c.d_sweep_trace, 8 * words, cudaMemcpyDeviceToHost, "sweep trace");
     });
 }
 

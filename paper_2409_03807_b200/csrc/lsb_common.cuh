@@ -205,6 +205,11 @@ __device__ __forceinline__ double dsmem_ld_f64(uint32_t addr) {
 // Order this thread's generic-proxy global writes before later async-proxy
 // (cp.async.bulk) reads of them; used before the barrier that publishes them.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// Programmatic dependent launch (no-ops unless the kernel was launched with a programmatic
+// dependency): let the next kernel's CTAs start, and wait for the previous kernel's completion
+// and memory before touching anything it writes.
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

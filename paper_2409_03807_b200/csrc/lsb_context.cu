@@ -16,6 +16,7 @@
 #include "../../include/lipsub_b200.h"
 #include "lsb_context.hpp"
 #include "lsb_solve.cuh"
+#include "lsb_sweep.cuh"
 
 namespace lsb {
 
@@ -217,6 +218,29 @@ KernelSet<double> select_kernels<double>(int hp) {
     throw LsbError(LSB_EINVAL, "decoder: unsupported padded width");
 }
 
+template <typename TS>
+using SweepFn = void (*)(const EvalParams<TS>, const SweepParams);
+template <typename TS>
+SweepFn<TS> select_sweep(int hp, size_t* smem);
+template <>
+SweepFn<float> select_sweep<float>(int hp, size_t* smem) {
+    switch (hp) {
+        case 128: *smem = sweep_smem_bytes<float, 128>(); return sweep_kernel<float, 128>;
+        case 256: *smem = sweep_smem_bytes<float, 256>(); return sweep_kernel<float, 256>;
+        case 512: *smem = sweep_smem_bytes<float, 512>(); return sweep_kernel<float, 512>;
+    }
+    return nullptr;
+}
+template <>
+SweepFn<double> select_sweep<double>(int hp, size_t* smem) {
+    switch (hp) {
+        case 64: *smem = sweep_smem_bytes<double, 64>(); return sweep_kernel<double, 64>;
+        case 128: *smem = sweep_smem_bytes<double, 128>(); return sweep_kernel<double, 128>;
+        case 256: *smem = sweep_smem_bytes<double, 256>(); return sweep_kernel<double, 256>;
+    }
+    return nullptr;
+}
+
 using CtrlFn = void (*)(int, int, int);  // placeholder type for table entries
 
 template <typename TS>
@@ -239,52 +263,69 @@ struct Impl final : ImplBase {
     EvalParams<TS> ps{};  // params with solve-sized partial buffers
     SolveShared* d_sh = nullptr;
     int cs = 8;
-    cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_timed = nullptr;
-    cudaEvent_t timed_ev[4] = {};
-    int timed_want = 1;
+    cudaGraphExec_t g_min = nullptr, g_step = nullptr, g_eval[2] = {nullptr, nullptr};
+    // sweep pass (lsb_sweep.cuh): out_fwd + elem + gather/VJP as one ticketed kernel
+    SweepFn<TS> sweep = nullptr;
+    SweepParams swp{};
+    size_t sweep_smem = 0;
+    int sweep_grid = 0;
+    bool use_sweep = false;
+    std::vector<void*> sweep_bufs;
+    EvalParams<TS> pc{};  // params of the control kernels (the sweep's group partials when it runs)
+    int pdl_mask = 15;    // programmatic edges inside graph bodies (LSB_PDL bit mask)
+    void (*elem_fn)(const EvalParams<TS>) = elem_kernel<TS, 0>;
     cudaGraphConditionalHandle h_min{}, h_step{};
 
     ~Impl() override {
         if (g_min) cudaGraphExecDestroy(g_min);
         if (g_step) cudaGraphExecDestroy(g_step);
-        if (g_timed) cudaGraphExecDestroy(g_timed);
+        for (auto& ge : g_eval)
+            if (ge) cudaGraphExecDestroy(ge);
+    }
+
+    // One evaluation (ctrl start -> [sweep | out_fwd -> elem -> gather/VJP] -> ctrl) as a cached
+    // graph per want_grad, with programmatic edges where LSB_PDL enables them.
+    cudaGraphExec_t eval_graph(Context& c, bool want_grad) {
+        cudaGraphExec_t& ge = g_eval[want_grad ? 1 : 0];
+        if (ge) return ge;
+        cudaGraph_t g;
+        cuda_check(cudaGraphCreate(&g, 0), "graph create");
+        int cm = kCtrlStart, mode = kModeEval, want = want_grad ? 1 : 0;
+        EvalParams<TS> pg = p;
+        EvalParams<TS> pcg = pc;
+        SweepParams sw = swp;
+        void* sargs[] = {&pcg, &cm, &mode, &want};
+        cudaGraphNode_t n0 = add_kernel(g, nullptr, (void*)ctrl, cs, ctrl_smem, sargs, ctrl_threads);
+        void* a1[] = {&pg};
+        void* asw[] = {&pg, &sw};
+        const int pm = c.dev.pdl;
+        cudaGraphNode_t n3;
+        if (use_sweep) {
+            n3 = add_kernel_pdl(g, n0, (void*)sweep, sweep_grid, sweep_smem, asw, kSwThreads, pm & 1);
+        } else {
+            cudaGraphNode_t n1 = add_kernel_pdl(g, n0, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads, pm & 1);
+            cudaGraphNode_t n2 = add_kernel_pdl(g, n1, (void*)elem_fn, p.grid_elem, 0, a1, 256, pm & 2);
+            n3 = add_gather_vjp(g, n2, a1, pm & 4);
+        }
+        int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
+        void* a4[] = {&pcg, &cm2, &z0, &z1};
+        add_kernel_pdl(g, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads, pm & 8);
+        cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate (eval)");
+        cudaGraphDestroy(g);
+        return ge;
+    }
+
+    void launch_eval_graph(Context& c, bool want_grad) {
+        cuda_check(cudaGraphLaunch(eval_graph(c, want_grad), c.stream), "graph launch (eval)");
+        c.launches += use_sweep ? 3 : (fuse_gather ? 5 : 6);  // ctrl, [sweep | out_fwd, elem, [gather,] vjp], ctrl
     }
 
     int eval_timed(Context& c, cudaEvent_t* ev, bool want_grad) override {
-        if (solve && c.use_solve) {
-            cuda_check(cudaEventRecord(ev[0], c.stream), "ev");
-            launch_solve(c, 0, 0, want_grad ? 1 : 0);
-            cuda_check(cudaEventRecord(ev[3], c.stream), "ev");
-            return 2;
-        }
-        if (!g_timed || ev[0] != timed_ev[0] || timed_want != (int)want_grad) {
-            if (g_timed) cudaGraphExecDestroy(g_timed);
-            for (int k = 0; k < 4; ++k) timed_ev[k] = ev[k];
-            timed_want = want_grad ? 1 : 0;
-            cudaGraph_t g;
-            cuda_check(cudaGraphCreate(&g, 0), "graph create");
-            cudaGraphNode_t e0, e1, e2, e3;
-            cuda_check(cudaGraphAddEventRecordNode(&e0, g, nullptr, 0, ev[0]), "event node");
-            int cm = kCtrlStart, mode = kModeEval, want = timed_want;
-            EvalParams<TS> pg = p;
-            void* sargs[] = {&pg, &cm, &mode, &want};
-            cudaGraphNode_t n0 = add_kernel(g, e0, (void*)ctrl, cs, ctrl_smem, sargs, ctrl_threads);
-            cuda_check(cudaGraphAddEventRecordNode(&e1, g, &n0, 1, ev[1]), "event node");
-            void* a1[] = {&pg};
-            cudaGraphNode_t n1 = add_kernel(g, e1, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
-            cuda_check(cudaGraphAddEventRecordNode(&e2, g, &n1, 1, ev[2]), "event node");
-            cudaGraphNode_t n2 = add_kernel(g, e2, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-            cudaGraphNode_t n3 = add_gather_vjp(g, n2, a1);
-            int cm2 = kCtrlAfterEval, z0 = 0, z1 = 0;
-            void* a4[] = {&pg, &cm2, &z0, &z1};
-            cudaGraphNode_t n4 = add_kernel(g, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
-            cuda_check(cudaGraphAddEventRecordNode(&e3, g, &n4, 1, ev[3]), "event node");
-            cuda_check(cudaGraphInstantiate(&g_timed, g, 0), "graph instantiate (timed eval)");
-            cudaGraphDestroy(g);
-        }
-        cuda_check(cudaGraphLaunch(g_timed, c.stream), "graph launch (timed eval)");
-        c.launches += fuse_gather ? 5 : 6;  // ctrl, out_fwd, elem, [gather,] vjp, ctrl
-        return 4;
+        cuda_check(cudaEventRecord(ev[0], c.stream), "ev");
+        if (solve && c.use_solve) launch_solve(c, 0, 0, want_grad ? 1 : 0);
+        else launch_eval_graph(c, want_grad);
+        cuda_check(cudaEventRecord(ev[3], c.stream), "ev");
+        return 2;
     }
 
     void setup(Context& c) override {
@@ -298,6 +339,9 @@ struct Impl final : ImplBase {
         p.h = c.h;
         p.hp = c.hp;
         p.out_act = c.out_act;
+        p.elem_f32 = std::is_same<TS, float>::value && c.dev.elem_f32 ? 1 : 0;
+        p.l2_pf_tiles = (c.dev.pdl & 1) ? c.dev.l2_pf : 0;
+        elem_fn = p.elem_f32 ? elem_kernel<TS, 1> : elem_kernel<TS, 0>;
         p.Wout = static_cast<const TS*>(c.d_Wout);
         p.bout = c.d_bout;
         p.sout = c.d_sout;
@@ -347,7 +391,7 @@ struct Impl final : ImplBase {
                    "occupancy out_fwd");
         const int ntiles = (c.n + ks.tile_rows - 1) / ks.tile_rows;
         p.grid_out = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_kernel<TS>, 256, 0), "occupancy elem");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, elem_fn, 256, 0), "occupancy elem");
         c.grid_elem_cap = c.num_sms * std::max(1, occ);
         p.grid_elem = std::max(1, std::min((m.E + 255) / 256, c.grid_elem_cap));
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, kStreamThreads, vjp_smem),
@@ -429,8 +473,117 @@ struct Impl final : ImplBase {
         p.ybar_grp = c.d_ybar_grp;
         p.grp_cnt = c.d_grp_cnt;
         p.in_graph = 0;
+        pdl_mask = c.dev.pdl;
+        setup_sweep(c);
         setup_solve(c);
     }
+
+    // Work-item plan of the sweep pass over the current element set (lsb_sweep.cuh).
+    void setup_sweep(Context& c) {
+        for (void* b : sweep_bufs) c.dfree(b);
+        sweep_bufs.clear();
+        use_sweep = false;
+        pc = p;
+        c.body_kernels = fuse_gather ? 4 : 5;
+        if (!c.dev.sweep) return;
+        sweep = select_sweep<TS>(c.hp, &sweep_smem);
+        if (!sweep || sweep_smem > 227 * 1024) return;
+        if (cudaFuncSetAttribute(sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        int occ = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep, kSwThreads, sweep_smem),
+                   "occupancy sweep");
+        if (occ < 1) return;
+        sweep_grid = c.num_sms * occ;
+        const HostMesh& m = c.mesh;
+        const int TR = ks.tile_rows, RI = kSwItemTiles * TR;
+        const int ntiles = (c.n + TR - 1) / TR;
+        const int nf = (ntiles + kSwItemTiles - 1) / kSwItemTiles, nv = nf;
+        const int ne = (m.E + kSwTets - 1) / kSwTets;
+        const int ng = (c.n + kSwGatherRows - 1) / kSwGatherRows;
+        std::vector<int> depF(ne, -1), depG(ng, -1), depV(nv, 0);
+        for (int e = 0; e < m.E; ++e)
+            for (int k = 0; k < 4; ++k) {
+                const int slot = m.free_index[m.T[4 * (size_t)e + k]];
+                if (slot >= 0) depF[e / kSwTets] = std::max(depF[e / kSwTets], (3 * slot + 2) / RI);
+            }
+        for (int g = 0; g < ng; ++g) {
+            const int R0 = g * kSwGatherRows, R1 = std::min(c.n, R0 + kSwGatherRows);
+            for (int f = R0 / 3; f <= (R1 - 1) / 3; ++f)
+                for (int k = m.csr_ptr[f]; k < m.csr_ptr[f + 1]; ++k)
+                    depG[g] = std::max(depG[g], (m.csr_ent[k] / 4) / kSwTets);
+        }
+        for (int v = 0; v < nv; ++v) depV[v] = (std::min(c.n, (v + 1) * RI) - 1) / kSwGatherRows;
+        // element queue: E items in order; a G item follows its last E dependency by `lag`
+        // tickets (about one grid of element groups), or as soon as nothing else can be emitted
+        const int lag = (int)(c.dev.sweep_lag * sweep_grid);
+        const int etotal = ne + ng;
+        std::vector<int> order;
+        order.reserve(etotal);
+        std::vector<int> posE(ne, 0);
+        int ei = 0, gi = 0;
+        auto g_ready = [&](bool use_lag) {
+            const int d = depG[gi];
+            return d < 0 || (d < ei && (!use_lag || posE[d] + lag <= (int)order.size()));
+        };
+        while ((int)order.size() < etotal) {
+            bool prog = false;
+            if (ei < ne) {
+                posE[ei] = (int)order.size();
+                order.push_back((kSwE << 28) | ei);
+                ++ei;
+                prog = true;
+            }
+            while (gi < ng && g_ready(true)) order.push_back((kSwG << 28) | gi++), prog = true;
+            if (!prog) {
+                if (gi < ng && g_ready(false)) order.push_back((kSwG << 28) | gi++);
+                else throw LsbError(LSB_EMESH, "sweep plan: unsatisfiable dependency");
+            }
+        }
+        auto up = [&](const void* src, size_t bytes) {
+            void* d = c.dmalloc(std::max<size_t>(bytes, 16));
+            sweep_bufs.push_back(d);
+            if (src) c.copy(d, src, bytes, cudaMemcpyHostToDevice, "sweep plan");
+            else cuda_check(cudaMemsetAsync(d, 0, std::max<size_t>(bytes, 16), c.stream), "sweep zero");
+            return d;
+        };
+        const int ngroups = (nv + kSwGroup - 1) / kSwGroup;
+        swp = SweepParams{};
+        swp.eorder = static_cast<const int*>(up(order.data(), 4 * order.size()));
+        swp.etotal = etotal;
+        swp.nf = nf;
+        swp.ne = ne;
+        swp.ng = ng;
+        swp.nv = nv;
+        swp.ngroups = ngroups;
+        swp.depF = static_cast<const int*>(up(depF.data(), 4 * depF.size()));
+        swp.depG = static_cast<const int*>(up(depG.data(), 4 * depG.size()));
+        swp.depV = static_cast<const int*>(up(depV.data(), 4 * depV.size()));
+        swp.f_done = static_cast<unsigned*>(up(nullptr, 4 * (size_t)nf));
+        swp.e_done = static_cast<unsigned*>(up(nullptr, 4 * (size_t)ne));
+        swp.g_done = static_cast<unsigned*>(up(nullptr, 4 * (size_t)ng));
+        swp.e_f = static_cast<double*>(up(nullptr, 8 * (size_t)nf));
+        swp.e_e = static_cast<double*>(up(nullptr, 8 * (size_t)ne));
+        swp.ybar_item = static_cast<double*>(up(nullptr, 8 * (size_t)nv * c.hp));
+        swp.ybar_grp = static_cast<double*>(up(nullptr, 8 * (size_t)ngroups * c.hp));
+        swp.grp_cnt = static_cast<unsigned*>(up(nullptr, 4 * (size_t)ngroups));
+        SweepCounters ctr0{};
+        ctr0.seq = 1;
+        swp.ctr = static_cast<SweepCounters*>(up(&ctr0, sizeof(SweepCounters)));
+        swp.trace_cap = nf + nv + etotal;
+        swp.trace = c.dev.trace ? static_cast<unsigned long long*>(up(nullptr, 32 * (size_t)swp.trace_cap)) : nullptr;
+        c.d_sweep_trace = swp.trace;
+        c.sweep_tickets = swp.trace_cap;
+        cuda_check(cudaStreamSynchronize(c.stream), "sweep plan sync");
+        use_sweep = true;
+        pc.n_groups = ngroups;
+        pc.ybar_grp = swp.ybar_grp;
+        c.body_kernels = 2;  // sweep, ctrl
+    }
+
+    void launch_sweep(cudaStream_t s) { sweep<<<sweep_grid, kSwThreads, sweep_smem, s>>>(p, swp); }
 
     void setup_solve(Context& c) {
         if (c.dev.disable_solve) {
@@ -621,20 +774,27 @@ struct Impl final : ImplBase {
         }
     }
     // graph form: returns the last node
-    cudaGraphNode_t add_gather_vjp(cudaGraph_t g, cudaGraphNode_t dep, void** args) {
-        if (fuse_gather) return add_kernel(g, dep, (void*)ks.vjp_gather, p.grid_vjp, vjpg_smem, args, kStreamThreads);
+    cudaGraphNode_t add_gather_vjp(cudaGraph_t g, cudaGraphNode_t dep, void** args, bool pdl = false) {
+        if (fuse_gather)
+            return add_kernel_pdl(g, dep, (void*)ks.vjp_gather, p.grid_vjp, vjpg_smem, args, kStreamThreads, pdl);
         cudaGraphNode_t n = add_kernel(g, dep, (void*)gather_kernel<TS>, grid_gather, 0, args);
         return add_kernel(g, n, (void*)ks.vjp, p.grid_vjp, vjp_smem, args, kStreamThreads);
     }
 
     void launch_ctrl(cudaStream_t s, int cmode, int smode, int want) {
-        ctrl<<<cs, ctrl_threads, ctrl_smem, s>>>(p, cmode, smode, want);
+        ctrl<<<cs, ctrl_threads, ctrl_smem, s>>>(pc, cmode, smode, want);
     }
 
     // One evaluation body, stream-launched (non-graph path).
     void launch_eval_body(cudaStream_t s, Context& c) {
+        if (use_sweep) {
+            launch_sweep(s);
+            launch_ctrl(s, kCtrlAfterEval, 0, 0);
+            c.launches += 2;
+            return;
+        }
         ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
-        elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
+        elem_fn<<<p.grid_elem, 256, 0, s>>>(p);
         launch_gather_vjp(s);
         launch_ctrl(s, kCtrlAfterEval, 0, 0);
         c.launches += fuse_gather ? 4 : 5;
@@ -645,11 +805,7 @@ struct Impl final : ImplBase {
             launch_solve(c, 0, 0, want_grad ? 1 : 0);
             return;
         }
-        cudaStream_t s = c.stream;
-        launch_ctrl(s, kCtrlStart, kModeEval, want_grad ? 1 : 0);
-        c.launches += 1;
-        launch_eval_body(s, c);
-        cuda_check(cudaGetLastError(), "eval launch");
+        launch_eval_graph(c, want_grad);
     }
 
     void profile(Context& c, int reps, float* ms) override {
@@ -661,15 +817,22 @@ struct Impl final : ImplBase {
             cudaEventRecord(ev[0], s);
             launch_ctrl(s, kCtrlStart, kModeEval, 1);
             cudaEventRecord(ev[1], s);
-            ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
-            cudaEventRecord(ev[2], s);
-            elem_kernel<TS><<<p.grid_elem, 256, 0, s>>>(p);
-            cudaEventRecord(ev[3], s);
-            launch_gather_vjp(s);
-            cudaEventRecord(ev[4], s);
+            if (use_sweep) {
+                launch_sweep(s);
+                cudaEventRecord(ev[2], s);
+                cudaEventRecord(ev[3], s);
+                cudaEventRecord(ev[4], s);
+            } else {
+                ks.out_fwd<<<p.grid_out, kStreamThreads, out_smem, s>>>(p);
+                cudaEventRecord(ev[2], s);
+                elem_fn<<<p.grid_elem, 256, 0, s>>>(p);
+                cudaEventRecord(ev[3], s);
+                launch_gather_vjp(s);
+                cudaEventRecord(ev[4], s);
+            }
             launch_ctrl(s, kCtrlAfterEval, 0, 0);
             cudaEventRecord(ev[5], s);
-            c.launches += fuse_gather ? 4 : 5;
+            c.launches += use_sweep ? 3 : (fuse_gather ? 4 : 5);
             cuda_check(cudaEventSynchronize(ev[5]), "profile sync");
             float t;
             cudaEventElapsedTime(&t, ev[1], ev[2]);
@@ -699,6 +862,19 @@ struct Impl final : ImplBase {
         cuda_check(cudaGraphAddKernelNode(&nd, g, dep ? &dep : nullptr, dep ? 1 : 0, &kp), "kernel node");
         return nd;
     }
+    // Kernel node whose edge from the kernel node `dep` is programmatic (PDL): its CTAs may start
+    // once every CTA of `dep` has executed griddepcontrol.launch_dependents, and it orders its
+    // dependent reads behind griddepcontrol.wait (full completion + memory of `dep`).
+    cudaGraphNode_t add_kernel_pdl(cudaGraph_t g, cudaGraphNode_t dep, void* fn, int grid, size_t smem, void** args,
+                                   int threads, bool pdl) {
+        if (!pdl || !dep) return add_kernel(g, dep, fn, grid, smem, args, threads);
+        cudaGraphNode_t nd = add_kernel(g, nullptr, fn, grid, smem, args, threads);
+        cudaGraphEdgeData ed = {};
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+        cuda_check(cudaGraphAddDependencies_v2(g, &dep, &nd, &ed, 1), "programmatic edge");
+        return nd;
+    }
 
     // WHILE(cond){ out_fwd -> elem -> vjp -> ctrl } appended after `dep`.
     cudaGraphNode_t add_while(cudaGraph_t graph, cudaGraphNode_t dep, cudaGraphConditionalHandle* handle) {
@@ -714,19 +890,30 @@ struct Impl final : ImplBase {
         EvalParams<TS> pg = p;
         pg.in_graph = 1;
         pg.cond = *handle;
+        EvalParams<TS> pcg = pc;
+        pcg.in_graph = 1;
+        pcg.cond = *handle;
+        SweepParams sw = swp;
         void* a1[] = {&pg};
+        void* asw[] = {&pg, &sw};
         int cm = kCtrlAfterEval, z0 = 0, z1 = 0;
-        void* a4[] = {&pg, &cm, &z0, &z1};
-        cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
-        cudaGraphNode_t n2 = add_kernel(body, n1, (void*)elem_kernel<TS>, p.grid_elem, 0, a1);
-        cudaGraphNode_t n3 = add_gather_vjp(body, n2, a1);
-        add_kernel(body, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads);
+        void* a4[] = {&pcg, &cm, &z0, &z1};
+        cudaGraphNode_t n3;
+        const int pm = pdl_mask;
+        if (use_sweep) {
+            n3 = add_kernel(body, nullptr, (void*)sweep, sweep_grid, sweep_smem, asw, kSwThreads);
+        } else {
+            cudaGraphNode_t n1 = add_kernel(body, nullptr, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads);
+            cudaGraphNode_t n2 = add_kernel_pdl(body, n1, (void*)elem_fn, p.grid_elem, 0, a1, 256, pm & 2);
+            n3 = add_gather_vjp(body, n2, a1, pm & 4);
+        }
+        add_kernel_pdl(body, n3, (void*)ctrl, cs, ctrl_smem, a4, ctrl_threads, pm & 8);
         return wnode;
     }
 
     cudaGraphNode_t add_start(cudaGraph_t graph, cudaGraphNode_t dep) {
         int cm = kCtrlStart, mode = kModeLbfgs, want = 1;
-        EvalParams<TS> pg = p;
+        EvalParams<TS> pg = pc;
         void* args[] = {&pg, &cm, &mode, &want};
         return add_kernel(graph, dep, (void*)ctrl, cs, ctrl_smem, args, ctrl_threads);
     }
@@ -818,12 +1005,17 @@ struct Impl final : ImplBase {
         p.grid_elem = std::max(1, std::min((c.mesh.E + 255) / 256, c.grid_elem_cap));
         c.grid_elem = p.grid_elem;
         ps.grid_elem = p.grid_elem;
+        setup_sweep(c);
         invalidate_graphs();
     }
 
     void invalidate_graphs() override {
         if (g_min) cudaGraphExecDestroy(g_min);
         if (g_step) cudaGraphExecDestroy(g_step);
+        for (auto& ge : g_eval) {
+            if (ge) cudaGraphExecDestroy(ge);
+            ge = nullptr;
+        }
         g_min = g_step = nullptr;
     }
 };

@@ -45,7 +45,12 @@ struct DevFlags {
     int elem_f2 = 0;          // LSB_ELEM_F2=1: FFMA2 batched element kernel
     int theta_tb = 24;        // LSB_THETA_TB: tets per block of the theta element pass
     int noncoop = 0;          // LSB_NONCOOP=1: persistent kernel as a plain cluster launch (ncu replay)
-    int pipe = 1;             // LSB_PIPE=0: classic multi-kernel body instead of the pipelined pass
+    int elem_f32 = 1;         // LSB_ELEM_F32=0: fp64 element arithmetic in fp32-storage mode (multi-kernel path)
+    int pdl = 1;              // LSB_PDL bit mask of programmatic edges (1 ctrl->out_fwd, 2 out_fwd->elem, 4 elem->vjp,
+                              // 8 vjp->ctrl); 0: plain full-completion edges
+    int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
+    int sweep = 0;            // LSB_SWEEP=1: fused warp-specialised sweep pass instead of out_fwd, elem, vjp (measured slower)
+    float sweep_lag = 1.5f;   // LSB_SWEEP_LAG: ticket lag between an item and its dependencies, in grids
     std::string active;       // "NAME=value ..." of every switch found set
 };
 DevFlags read_dev_flags();
@@ -143,6 +148,8 @@ struct Context {
     int grid_out = 0, grid_elem = 0, grid_vjp = 0, solve_grid = 0;
     bool use_solve = true;
     std::string solve_reason;
+    unsigned long long* d_sweep_trace = nullptr;  // sweep-pass item trace (LSB_TRACE=1), 4 words per ticket
+    int sweep_tickets = 0;
     unsigned long long* d_trace = nullptr;  // solve-kernel phase trace (LSB_TRACE=1)  // route eval/minimize/step through the persistent kernel when available
 
     DevFlags dev;

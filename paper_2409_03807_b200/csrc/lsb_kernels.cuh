@@ -78,6 +78,8 @@ struct EvalParams {
     int n, n_free, V, E, r, nhid, h, hp, out_act;
     int grid_out, grid_elem, grid_vjp, vpb, group, n_groups;
     int w_resident;   // W_out fits in L2: keep it (evict_last) instead of streaming
+    int elem_f32;     // fp32-storage mode: element strain / stress / forces in fp32 arithmetic
+    int l2_pf_tiles;  // out_fwd: W tiles per CTA bulk-prefetched into L2 before its dependency wait (PDL)
     // output layer (device layout: rows padded to hp columns)
     const TS* Wout;
     const double* bout;
@@ -391,6 +393,71 @@ __device__ __forceinline__ double tet_energy_forces(const double* u0, const doub
     return tet_energy_forces_t<double>(u0, u1, u2, u3, rec, f);
 }
 
+// fp32-storage mode (TS = float): the edge differences of the fp64 displacements are formed in
+// fp64 (no cancellation is introduced by rounding u itself), then the strain, the SNH density
+// and stress and the 12 forces run in fp32 -- the forces are stored as fp32 CSR entries anyway,
+// and the element energy is returned in fp64 for the fp64 block sums.  Relative error ~1e-7 per
+// tet, far inside the fp32 mode's 1e-4 bar and uncorrelated between tets.
+__device__ __forceinline__ double tet_energy_forces_f32(const double* u0, const double* u1, const double* u2,
+                                                        const double* u3, const float* rc, float* f) {
+    float D[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        D[a * 3 + 0] = (float)(u1[a] - u0[a]);
+        D[a * 3 + 1] = (float)(u2[a] - u0[a]);
+        D[a * 3 + 2] = (float)(u3[a] - u0[a]);
+    }
+    float A[9];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            A[a * 3 + b] = D[a * 3 + 0] * rc[0 * 3 + b] + D[a * 3 + 1] * rc[1 * 3 + b] + D[a * 3 + 2] * rc[2 * 3 + b];
+    float P[9];
+    const float vol = rc[9];
+    const float psi = snh_psi_P(A, rc[10], rc[11], P);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float s0 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float hv =
+                vol * (P[a * 3 + 0] * rc[c * 3 + 0] + P[a * 3 + 1] * rc[c * 3 + 1] + P[a * 3 + 2] * rc[c * 3 + 2]);
+            f[(c + 1) * 3 + a] = hv;
+            s0 += hv;
+        }
+        f[a] = -s0;
+    }
+    return (double)vol * (double)psi;
+}
+__device__ __forceinline__ void load_rec_f(const float* rec, size_t e, float* o) {
+    const float4* p = reinterpret_cast<const float4*>(rec + e * 12);
+    const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+    o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+    o[8] = c.x; o[9] = c.y; o[10] = c.z; o[11] = c.w;
+}
+// The CSR force entries are re-read by the vertex gather right after the element pass, while
+// the W_out stream (evict_first) passes through L2: store them with an evict_last hint.
+__device__ __forceinline__ void store_forces_csr_f(double* F, int4 pos, const float* f) {
+    float* Ff = reinterpret_cast<float*>(F);
+    const int ps[4] = {pos.x, pos.y, pos.z, pos.w};
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (ps[k] >= 0)
+            asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Ff + (size_t)ps[k] * 4),
+                         "f"(f[3 * k]), "f"(f[3 * k + 1]), "f"(f[3 * k + 2]), "f"(0.f), "l"(pol)
+                         : "memory");
+}
+
+// One tet of the element pass: energy, forces to the CSR slots (fp32 arithmetic for TS = float
+// when f32 is set, else fp64).
+template <typename TS>
+__device__ __forceinline__ double elem_tet(const TS* rec, size_t e, const double (&u)[4][3], int4 fpos, double* F,
+                                           int f32);
+
 // Scatter one tet's 12 local forces to their vertices' CSR slots: 32-byte {fx, fy, fz, 0}
 // double entries, or in fp32-storage mode (TS = float) 16-byte float entries -- the force
 // array is a bandwidth-bound intermediate like W_out and the element records;
@@ -422,12 +489,39 @@ template <>
 __device__ __forceinline__ void store_forces_csr_t<double>(double* F, int4 pos, const double* f) {
     store_forces_csr(F, pos, f);
 }
+template <>
+__device__ __forceinline__ double elem_tet<double>(const double* rec, size_t e, const double (&u)[4][3], int4 fpos,
+                                                   double* F, int) {
+    double rc[12], f[12];
+    load_rec<double>(rec, e, rc);
+    const double en = tet_energy_forces(u[0], u[1], u[2], u[3], rc, f);
+    store_forces_csr(F, fpos, f);
+    return en;
+}
+template <>
+__device__ __forceinline__ double elem_tet<float>(const float* rec, size_t e, const double (&u)[4][3], int4 fpos,
+                                                  double* F, int f32) {
+    if (f32) {
+        float rc[12], f[12];
+        load_rec_f(rec, e, rc);
+        const double en = tet_energy_forces_f32(u[0], u[1], u[2], u[3], rc, f);
+        store_forces_csr_f(F, fpos, f);
+        return en;
+    }
+    double rc[12], f[12];
+    load_rec<float>(rec, e, rc);
+    const double en = tet_energy_forces(u[0], u[1], u[2], u[3], rc, f);
+    store_forces_csr_t<float>(F, fpos, f);
+    return en;
+}
 
-template <typename TS>
+template <typename TS, int F32 = 0>
 __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
     __shared__ double red[32];
     __shared__ int am_last;
     DevState* st = p.st;
+    griddep_wait();
+    griddep_launch();
     double eacc = 0.0;
     const int stride = gridDim.x * blockDim.x;
     for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < p.E; e0 += 2 * stride) {
@@ -449,11 +543,7 @@ __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
         for (int q = 0; q < 2; ++q) {
             if (q == 1 && !has1) break;
             const int e = q ? e1 : e0;
-            double rec[12];
-            load_rec<TS>(p.rec, (size_t)e, rec);
-            double f[12];
-            eacc += tet_energy_forces(u[q][0], u[q][1], u[q][2], u[q][3], rec, f);
-            store_forces_csr_t<TS>(p.forces, __ldg(p.fpos + e), f);
+            eacc += elem_tet<TS>(p.rec, (size_t)e, u[q], __ldg(p.fpos + e), p.forces, F32);
         }
     }
     const double tot = block_sum(eacc, red);
@@ -544,6 +634,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(256) ctrl_kernel(co
     double* asl = bsl + kMaxLayers * 64;                // pre-activation slices (kMaxLayers * 64)
     DevState* sst = reinterpret_cast<DevState*>(asl + kMaxLayers * 64);
     __shared__ int more_s;
+    griddep_wait();
+    griddep_launch();
     const int need = cmode == kCtrlAfterEval ? p.st->need_grad : 0;
 
     // 0. stage own row slices of every hidden layer, biases, pre-activations and

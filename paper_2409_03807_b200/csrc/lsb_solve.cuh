@@ -178,6 +178,7 @@ __device__ __forceinline__ void ctrl_stage(const EvalParams<TS>& p, CtrlSmem& cs
     const uint64_t keep = l2_policy(1);
     bool async_used = false;
     if (warp == 0 && with_state && c == 0) {
+        griddep_wait();  // the solver state is written by the previous kernel
         double* sd = reinterpret_cast<double*>(cs.sst);
         const double* ss = reinterpret_cast<const double*>(p.st);
         const bool s_bulk = bulk_ok(sd, ss, sizeof(DevState));
@@ -1029,7 +1030,8 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                     }
                 }
                 if (!(sp.exp & 4))
-                    gather_rows_smem(p, R0, R1, sp.tv_global ? p.tv + R0 : tv_s, has_inertia, p.out_act == kIdentity);
+                    gather_rows_smem(p, R0, R1, sp.tv_global ? p.tv + R0 : tv_s, has_inertia, p.out_act == kIdentity,
+                                     false);
                 if (sp.tv_global) fence_proxy_async();  // generic tv writes -> this CTA's bulk copies
                 __syncthreads();
                 stamp(30);
@@ -1292,7 +1294,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(kSolveThreads, 1)
     cs.wbar = s_wbar;
     cs.woff = s_woff;
     ctrl_sig_init();
-    ctrl_stage<TS, CS>(p, cs, c, true, s_wbar);
+    ctrl_stage<TS, CS>(p, cs, c, true, s_wbar);  // weights staged while the previous kernel drains
+    griddep_wait();
+    griddep_launch();
     if (c == 0) ctrl_wait_state(s_wbar);
     DevState* sst = cs.sst;
     const int need = cmode == kCtrlAfterEval ? __ldcg(&p.st->need_grad) : 0;

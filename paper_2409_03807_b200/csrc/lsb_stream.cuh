@@ -159,32 +159,16 @@ __device__ __forceinline__ void ring_init(uint64_t* full, int nst) {
     }
 }
 
-// One warp computes every row of a forward tile: TR independent dot products,
-// one multi-row reduction, lane (32 / TR) j runs the epilogue of row j.
+// Multi-row reduction + epilogue of a forward tile from the per-lane row partials acc[TR]:
+// recursive-halving multi-row reduction, lane (32 / TR) j runs the epilogue of row j.
 template <typename TS, int HP>
-__device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
-                                           const double (&y)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4],
-                                           int has_inertia, double inv_dt2, bool ident) {
+__device__ __forceinline__ double fwd_epilogue(const EvalParams<TS>& p, const unsigned char* st, int t,
+                                               double (&acc)[StreamCfg<TS, HP>::TR], int has_inertia, double inv_dt2,
+                                               bool ident) {
     using C = StreamCfg<TS, HP>;
     const int lane = threadIdx.x & 31;
     const int rows = min(C::TR, p.n - t * C::TR);
-    const TS* tile = reinterpret_cast<const TS*>(st);
     const double* ep = reinterpret_cast<const double*>(st + C::TILEB);
-    double acc[C::TR];
-#pragma unroll
-    for (int j = 0; j < C::TR; ++j) {
-        acc[j] = 0.0;
-        if (j < rows) {
-            const TS* rowp = tile + (size_t)j * HP;
-#pragma unroll
-            for (int c = 0; c < C::NCH; ++c) {
-                double w[C::V4];
-                lds_chunk<TS>(rowp, c * 32 + lane, w);
-#pragma unroll
-                for (int q = 0; q < C::V4; ++q) acc[j] = fma(w[q], y[c][q], acc[j]);
-            }
-        }
-    }
     // recursive-halving multi-row reduction: at offset o the lanes with bit o set keep
     // the upper half of their rows and receive the partner's copy of it, so TR rows
     // cost TR - 1 + log2(32 / TR) shuffles (not 5 TR).  Lane l ends up with the full
@@ -227,6 +211,113 @@ __device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsign
     return e;
 }
 
+// One warp computes every row of a forward tile: TR independent dot products,
+// one multi-row reduction, lane (32 / TR) j runs the epilogue of row j.
+template <typename TS, int HP>
+__device__ __forceinline__ double fwd_tile(const EvalParams<TS>& p, const unsigned char* st, int t,
+                                           const double (&y)[StreamCfg<TS, HP>::NCH][StreamCfg<TS, HP>::V4],
+                                           int has_inertia, double inv_dt2, bool ident) {
+    using C = StreamCfg<TS, HP>;
+    const int lane = threadIdx.x & 31;
+    const int rows = min(C::TR, p.n - t * C::TR);
+    const TS* tile = reinterpret_cast<const TS*>(st);
+    double acc[C::TR];
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j) {
+        acc[j] = 0.0;
+        if (j < rows) {
+            const TS* rowp = tile + (size_t)j * HP;
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c) {
+                double w[C::V4];
+                lds_chunk<TS>(rowp, c * 32 + lane, w);
+#pragma unroll
+                for (int q = 0; q < C::V4; ++q) acc[j] = fma(w[q], y[c][q], acc[j]);
+            }
+        }
+    }
+    return fwd_epilogue<TS, HP>(p, st, t, acc, has_inertia, inv_dt2, ident);
+}
+
+// fp32-storage mode, reduced-cost tile math: the fp64 operand is split into fp32 hi + lo parts
+// (y = hi + lo to ~2^-48), each lane sums its NCH x 4 products w hi + w lo of a row in fp32
+// (fp32 weights times the split operand: the per-lane partial is exact to ~1e-7 relative, the
+// level of the fp32 rounding of W itself) and the partials are promoted to fp64 for the
+// cross-lane reduction and the epilogue.  Two FFMA per weight instead of an F2F conversion and
+// an fp64 FMA -- the streaming warps' issue cost, not their bytes, bounds the fused sweep.
+template <int HP>
+__device__ __forceinline__ double fwd_tile_mixed(const EvalParams<float>& p, const unsigned char* st, int t,
+                                                 const float (&yh)[StreamCfg<float, HP>::NCH][4],
+                                                 const float (&yl)[StreamCfg<float, HP>::NCH][4], int has_inertia,
+                                                 double inv_dt2, bool ident) {
+    using C = StreamCfg<float, HP>;
+    const int lane = threadIdx.x & 31;
+    const int rows = min(C::TR, p.n - t * C::TR);
+    const float* tile = reinterpret_cast<const float*>(st);
+    double acc[C::TR];
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j) {
+        float sh = 0.f, sl = 0.f;
+        if (j < rows) {
+            const float* rowp = tile + (size_t)j * HP;
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c) {
+                const float4 w = *reinterpret_cast<const float4*>(rowp + (c * 32 + lane) * 4);
+                sh = fmaf(w.x, yh[c][0], sh);
+                sl = fmaf(w.x, yl[c][0], sl);
+                sh = fmaf(w.y, yh[c][1], sh);
+                sl = fmaf(w.y, yl[c][1], sl);
+                sh = fmaf(w.z, yh[c][2], sh);
+                sl = fmaf(w.z, yl[c][2], sl);
+                sh = fmaf(w.w, yh[c][3], sh);
+                sl = fmaf(w.w, yl[c][3], sl);
+            }
+        }
+        acc[j] = (double)sh + (double)sl;
+    }
+    return fwd_epilogue<float, HP>(p, st, t, acc, has_inertia, inv_dt2, ident);
+}
+
+// VJP counterpart: per tile, each lane's NCH x 4 column sums over the tile's TR rows in fp32
+// (tv split into hi + lo), promoted to fp64 into the item accumulators.
+template <int HP>
+__device__ __forceinline__ void vjp_tile_mixed(const EvalParams<float>& p, const unsigned char* st, const double* tv,
+                                               int t, double (&acc)[StreamCfg<float, HP>::NCH][4]) {
+    using C = StreamCfg<float, HP>;
+    const int lane = threadIdx.x & 31;
+    const int rows = min(C::TR, p.n - t * C::TR);
+    const float* tile = reinterpret_cast<const float*>(st);
+    float sh[C::NCH][4], sl[C::NCH][4];
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sh[c][q] = sl[c][q] = 0.f;
+#pragma unroll
+    for (int j = 0; j < C::TR; ++j) {
+        if (j < rows) {
+            const double tval = tv[j];
+            const float th = (float)tval, tl = (float)(tval - (double)th);
+            const float* rowp = tile + (size_t)j * HP;
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c) {
+                const float4 w = *reinterpret_cast<const float4*>(rowp + (c * 32 + lane) * 4);
+                sh[c][0] = fmaf(w.x, th, sh[c][0]);
+                sl[c][0] = fmaf(w.x, tl, sl[c][0]);
+                sh[c][1] = fmaf(w.y, th, sh[c][1]);
+                sl[c][1] = fmaf(w.y, tl, sl[c][1]);
+                sh[c][2] = fmaf(w.z, th, sh[c][2]);
+                sl[c][2] = fmaf(w.z, tl, sl[c][2]);
+                sh[c][3] = fmaf(w.w, th, sh[c][3]);
+                sl[c][3] = fmaf(w.w, tl, sl[c][3]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[c][q] += (double)sh[c][q] + (double)sl[c][q];
+}
+
 // One warp accumulates a VJP tile into its per-lane column accumulators.
 template <typename TS, int HP>
 __device__ __forceinline__ void vjp_tile(const EvalParams<TS>& p, const unsigned char* st, const double* tv, int t,
@@ -267,7 +358,13 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
     const int t1 = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
     const uint64_t pol = l2_policy(p.w_resident), keep = l2_policy(1);
     auto issue = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol, keep); };
-    ring_prefetch(r, t0, t1, issue);
+    ring_prefetch(r, t0, t1, issue);  // W tiles and row records do not depend on the previous kernel
+    if (p.l2_pf_tiles > 0) {  // while the control kernel runs (programmatic launch): next tiles into L2
+        const int a = min(t1, t0 + NW * kStreamSpw), b = min(t1, a + p.l2_pf_tiles);
+        if (b > a) prefetch_l2_range(p.Wout + (size_t)a * C::TR * HP, (size_t)(b - a) * C::TILEB, 8192);
+    }
+    griddep_wait();
+    griddep_launch();  // after the wait: dependents never start ahead of this kernel's own inputs
     const double inv_dt2 = p.st->inv_dt2;
     const int has_inertia = p.st->has_inertia;
     const bool ident = p.out_act == kIdentity;
@@ -302,16 +399,19 @@ __device__ __forceinline__ double4 ld_cg_d4(const double* p) {
 // One free vertex f: its CSR segment (ascending tet id) summed in order from one batch
 // of up to 24 independent 256-bit loads; rows 3f..3f+2 inside [R0, R1) are written to
 // dst[row - R0] as tv = s (g + inertia residual).
+// The row scale s comes from the compact sout array (streaming kernels: eprow is no longer in
+// L2) or from the row records' column 1 (the persistent kernel, where they are L2-hot).
 template <typename TS>
 __device__ __forceinline__ void gather_vertex1(const EvalParams<TS>& p, int f, int R0, int R1, double* dst,
-                                               int has_inertia, bool ident) {
+                                               int has_inertia, bool ident, bool scale_compact = true) {
     const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
     double rin[3] = {0.0, 0.0, 0.0}, sc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int row = 3 * f + c;
         if (has_inertia) rin[c] = __ldcg(p.rin + row);
-        sc[c] = ident ? __ldg(p.eprow + 6 * (size_t)row + 1) : __ldcg(p.dsout + row);
+        sc[c] = ident ? (scale_compact ? __ldg(p.sout + row) : __ldg(p.eprow + 6 * (size_t)row + 1))
+                      : __ldcg(p.dsout + row);
     }
     double gx = 0.0, gy = 0.0, gz = 0.0;
     if constexpr (std::is_same<TS, float>::value) {  // fp32-storage mode: 16-byte float entries
@@ -353,9 +453,10 @@ __device__ __forceinline__ void gather_vertex1(const EvalParams<TS>& p, int f, i
 // range edge are computed by both neighbours, identically.
 template <typename TS>
 __device__ __forceinline__ void gather_rows_smem(const EvalParams<TS>& p, int R0, int R1, double* tv_s,
-                                                 int has_inertia, bool ident) {
+                                                 int has_inertia, bool ident, bool scale_compact = true) {
     const int f0 = R0 / 3, nf = R1 > R0 ? (R1 - 1) / 3 - f0 + 1 : 0;
-    for (int k = threadIdx.x; k < nf; k += blockDim.x) gather_vertex1(p, f0 + k, R0, R1, tv_s, has_inertia, ident);
+    for (int k = threadIdx.x; k < nf; k += blockDim.x)
+        gather_vertex1(p, f0 + k, R0, R1, tv_s, has_inertia, ident, scale_compact);
 }
 
 template <typename TS>
@@ -442,7 +543,6 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_gather_tma_kernel(const Ev
     constexpr int NW = kStreamThreads / 32;
     __shared__ int am_grp_last;
     DevState* st = p.st;
-    if (!st->need_grad) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     WarpRing r{ssm + 512, reinterpret_cast<uint64_t*>(ssm), NW, kStreamSpw, C::STAGEB, 0u};
     double* wred = reinterpret_cast<double*>(ssm + 512 + (size_t)NW * kStreamSpw * C::STAGEB);  // NW x HP
@@ -454,7 +554,13 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_gather_tma_kernel(const Ev
     const int t1 = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
     const uint64_t pol = l2_policy(p.w_resident);
     auto issue = [&](int t, unsigned char* b, uint64_t* bar) { issue_w_only<TS, HP>(p, t, b, bar, pol); };
-    ring_prefetch(r, t0, t1, issue);
+    ring_prefetch(r, t0, t1, issue);  // W tiles do not depend on the element pass
+    griddep_wait();
+    griddep_launch();
+    if (!st->need_grad) {  // value only: let the prefetched tiles land before the CTA exits
+        ring_drain(r, t0, t1);
+        return;
+    }
     const int R0 = t0 * C::TR, R1 = min(t1 * C::TR, p.n);
     gather_rows_smem(p, R0, R1, tv_s, st->has_inertia, p.out_act == kIdentity);
     __syncthreads();
