@@ -54,6 +54,10 @@ TRAFFIC = {
     # profiles/r01_solve_c2_v5_full.txt: one c2 fp64 E+grad eval (ncu flushes caches before the
     # launch, like the bench's L2 flush): dram read 75.42 MB + write 5.79 MB
     ("c2", True): 81.20e6,
+    # profiles/r02_launches_c3.txt: one c3 evaluation's streaming kernels under ncu (caches flushed
+    # before every kernel, so the CSR forces the gather re-reads come from DRAM here, from L2 in the
+    # bench): out_fwd 438.5 + 4.1, elem 67.4 + 6.7, vjp_gather 475.1 + 0.3 MB
+    ("c3", False): 992.1e6,
 }
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 LATENT = {"c1": 8, "c2": 16, "c2f": 16, "c3": 32}

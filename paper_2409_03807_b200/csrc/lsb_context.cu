@@ -397,22 +397,36 @@ struct Impl final : ImplBase {
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.vjp, kStreamThreads, vjp_smem),
                    "occupancy vjp");
         p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::max(1, occ)));
-        // fused gather + VJP: tv for a CTA's rows in shared memory (same grid as the VJP)
+        // fused gather + VJP: tv for a CTA's rows in shared memory; W-only stages, column sums in
+        // the drained ring.  Grid: two CTAs per SM (measured on config 3: 4.70K evals/s vs 4.27K with
+        // three, whose per-CTA gather prologues cost more than the extra stages gain), fewer if
+        // the tv scratch does not fit.
         {
             fuse_gather = c.dev.fuse_gather != 0;
-            const size_t tvb = ((size_t)((ntiles + p.grid_vjp - 1) / p.grid_vjp) * ks.tile_rows * sizeof(double) + 127) &
-                               ~(size_t)127;
-            vjpg_smem = vjp_smem + tvb;
-            int occ2 = 0;
-            if (fuse_gather &&
-                (cudaFuncSetAttribute(ks.vjp_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vjpg_smem) !=
-                     cudaSuccess ||
-                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ks.vjp_gather, kStreamThreads, vjpg_smem) !=
-                     cudaSuccess ||
-                 occ2 * c.num_sms < p.grid_vjp)) {
-                cudaGetLastError();
-                fuse_gather = false;  // keep the VJP grid; fall back to the separate gather kernel
+            bool ok = false;
+#ifndef LSB_VJP_MAXCTA
+#define LSB_VJP_MAXCTA 2
+#endif
+            for (int want = LSB_VJP_MAXCTA; fuse_gather && want >= 1 && !ok; --want) {
+                const int grid = std::max(1, std::min(ntiles, c.num_sms * want));
+                const size_t tvb = ((size_t)((ntiles + grid - 1) / grid) * ks.tile_rows * sizeof(double) + 127) &
+                                   ~(size_t)127;
+                const size_t sm = 512 + (size_t)(kStreamThreads / 32) * kStreamSpw * ks.tile_rows * c.hp * sizeof(TS) + tvb;
+                int occ2 = 0;
+                if (cudaFuncSetAttribute(ks.vjp_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+                        cudaSuccess ||
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ks.vjp_gather, kStreamThreads, sm) !=
+                        cudaSuccess) {
+                    cudaGetLastError();
+                    continue;
+                }
+                if (occ2 * c.num_sms >= grid) {
+                    vjpg_smem = sm;
+                    p.grid_vjp = grid;
+                    ok = true;
+                }
             }
+            if (!ok) fuse_gather = false;  // keep the VJP grid; fall back to the separate gather kernel
             c.body_kernels = fuse_gather ? 4 : 5;
         }
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gather_kernel<TS>, 256, 0), "occupancy gather");

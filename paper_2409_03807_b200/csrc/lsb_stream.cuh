@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
         for (int q = 0; q < C::V4; ++q) y[c][q] = p.y_last[(c * 32 + lane) * C::V4 + q];
     double eacc = 0.0;
     ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) {
-        eacc += fwd_tile<TS, HP>(p, b, t, y, has_inertia, inv_dt2, ident);
+        eacc += fwd_tile<TS, HP>(p, b, t, y, has_inertia, inv_dt2, ident);  // HBM-bound: fp64 math is free
     });
     const double tot = block_sum(eacc, red);
     if (threadIdx.x == 0) p.e_part_out[blockIdx.x] = 0.5 * inv_dt2 * tot;
@@ -544,9 +544,12 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_gather_tma_kernel(const Ev
     __shared__ int am_grp_last;
     DevState* st = p.st;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    WarpRing r{ssm + 512, reinterpret_cast<uint64_t*>(ssm), NW, kStreamSpw, C::STAGEB, 0u};
-    double* wred = reinterpret_cast<double*>(ssm + 512 + (size_t)NW * kStreamSpw * C::STAGEB);  // NW x HP
-    double* tv_s = wred + (size_t)NW * HP;                                                        // own rows
+    // stages hold W rows only (tv is in shared memory); the per-warp column sums reuse the ring
+    // once it is drained, so three CTAs fit per SM
+    WarpRing r{ssm + 512, reinterpret_cast<uint64_t*>(ssm), NW, kStreamSpw, C::TILEB, 0u};
+    double* wred = reinterpret_cast<double*>(ssm + 512);                                           // NW x HP
+    double* tv_s = reinterpret_cast<double*>(ssm + 512 + (size_t)NW * kStreamSpw * C::TILEB);     // own rows
+    static_assert(NW * HP * 8 <= NW * kStreamSpw * C::TILEB, "column sums fit in the ring");
     ring_init(r.full, NW * kStreamSpw);
     __syncthreads();
     const int ntiles = (p.n + C::TR - 1) / C::TR;
@@ -570,8 +573,9 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_gather_tma_kernel(const Ev
 #pragma unroll
         for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
     ring_run(r, t0, t1, issue, [&](int t, const unsigned char* b) {
-        vjp_tile<TS, HP>(p, b, tv_s + (t * C::TR - R0), t, acc);
+        vjp_tile<TS, HP>(p, b, tv_s + (t * C::TR - R0), t, acc);  // fp64 math: the mixed form measured no faster here
     });
+    __syncthreads();  // every warp is done with its stages: wred may overwrite the ring
 #pragma unroll
     for (int c = 0; c < C::NCH; ++c)
 #pragma unroll
