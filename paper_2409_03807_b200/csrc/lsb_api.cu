@@ -211,6 +211,7 @@ DevFlags read_dev_flags() {
     if (const char* v = get("LSB_SWEEP")) f.sweep = v[0] == '1';
     if (const char* v = get("LSB_PDL")) f.pdl = atoi(v) & 15;
     if (const char* v = get("LSB_L2PF")) f.l2_pf = std::max(0, std::min(256, atoi(v)));
+    if (const char* v = get("LSB_L2PF_ELEM")) f.l2_pf_elem = std::max(0, std::min(256, atoi(v)));
     if (const char* v = get("LSB_ELEM_F32")) f.elem_f32 = v[0] != '0';
     if (const char* v = get("LSB_SWEEP_LAG")) f.sweep_lag = std::min(8.0f, std::max(0.0f, (float)atof(v)));
 #ifndef LSB_TIMING_EXPERIMENTS

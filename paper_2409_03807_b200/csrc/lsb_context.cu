@@ -340,7 +340,8 @@ struct Impl final : ImplBase {
         p.hp = c.hp;
         p.out_act = c.out_act;
         p.elem_f32 = std::is_same<TS, float>::value && c.dev.elem_f32 ? 1 : 0;
-        p.l2_pf_tiles = (c.dev.pdl & 1) ? c.dev.l2_pf : 0;
+        p.l2_pf_tiles = c.dev.l2_pf;
+        p.l2_pf_elem = c.dev.l2_pf_elem;
         elem_fn = p.elem_f32 ? elem_kernel<TS, 1> : elem_kernel<TS, 0>;
         p.Wout = static_cast<const TS*>(c.d_Wout);
         p.bout = c.d_bout;

@@ -48,6 +48,7 @@ struct DevFlags {
     int elem_f32 = 1;         // LSB_ELEM_F32=0: fp64 element arithmetic in fp32-storage mode (multi-kernel path)
     int pdl = 1;              // LSB_PDL bit mask of programmatic edges (1 ctrl->out_fwd, 2 out_fwd->elem, 4 elem->vjp,
                               // 8 vjp->ctrl); 0: plain full-completion edges
+    int l2_pf_elem = 0;       // LSB_L2PF_ELEM: VJP head tiles prefetched into L2 by the element pass (measured: slower)
     int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
     int sweep = 0;            // LSB_SWEEP=1: fused warp-specialised sweep pass instead of out_fwd, elem, vjp (measured slower)
     float sweep_lag = 1.5f;   // LSB_SWEEP_LAG: ticket lag between an item and its dependencies, in grids

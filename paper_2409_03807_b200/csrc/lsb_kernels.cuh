@@ -80,6 +80,7 @@ struct EvalParams {
     int w_resident;   // W_out fits in L2: keep it (evict_last) instead of streaming
     int elem_f32;     // fp32-storage mode: element strain / stress / forces in fp32 arithmetic
     int l2_pf_tiles;  // out_fwd: W tiles per CTA bulk-prefetched into L2 before its dependency wait (PDL)
+    int l2_pf_elem;   // elem: first W tiles of every VJP CTA range prefetched into L2 (0: off)
     // output layer (device layout: rows padded to hp columns)
     const TS* Wout;
     const double* bout;
@@ -324,6 +325,34 @@ static __device__ int lbfgs_control(DevState* st, int r) {
     return 1;
 }
 
+// Bulk L2 prefetch of the first `tiles` W_out tiles of every CTA range of a streaming kernel
+// with `grid` CTAs (ranges [ntiles k / grid, ntiles (k+1) / grid)), spread over the lane-0s of
+// the calling grid's warps.  Issued from a latency-bound phase (element pass, control kernel)
+// so the next streaming kernel starts on L2-resident tiles.
+template <typename TS>
+__device__ __forceinline__ void prefetch_stream_heads(const EvalParams<TS>& p, int grid, int tiles) {
+    if (tiles <= 0 || grid <= 0 || (threadIdx.x & 31) != 0) return;
+    const int rowb = p.hp * (int)sizeof(TS);
+    const int tr = 8192 / rowb < 8 ? 8 : 8192 / rowb;
+    const int ntiles = (p.n + tr - 1) / tr;
+    const int nw = blockDim.x >> 5;
+    const int gw = (int)(blockIdx.x * nw + (threadIdx.x >> 5)), tw = (int)(gridDim.x * nw);
+    const uint64_t pol = l2_policy(1);
+    for (int k = gw; k < grid; k += tw) {
+        const int t0 = (int)(((long long)ntiles * k) / grid), t1 = (int)(((long long)ntiles * (k + 1)) / grid);
+        const int te = min(t1, t0 + tiles);
+        if (te <= t0) continue;
+        const char* a = reinterpret_cast<const char*>(p.Wout + (size_t)t0 * tr * p.hp);
+        const size_t bytes = (size_t)(min(te * tr, p.n) - t0 * tr) * rowb;
+        for (size_t o = 0; o < bytes; o += 65536) {
+            const unsigned nb = (unsigned)((bytes - o) < 65536 ? (bytes - o) : 65536);
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a + o), "r"(nb),
+                         "l"(pol)
+                         : "memory");
+        }
+    }
+}
+
 // ---------------------------------------------------------------- K3: element pass
 template <typename TS>
 __device__ __forceinline__ void load_rec(const TS* rec, size_t e, double* out12);
@@ -520,6 +549,7 @@ __global__ void __launch_bounds__(256) elem_kernel(const EvalParams<TS> p) {
     __shared__ double red[32];
     __shared__ int am_last;
     DevState* st = p.st;
+    prefetch_stream_heads(p, p.grid_vjp, p.l2_pf_elem);  // the VJP's first tiles, while tets are latency-bound
     griddep_wait();
     griddep_launch();
     double eacc = 0.0;
