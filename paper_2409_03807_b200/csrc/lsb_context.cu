@@ -449,6 +449,9 @@ struct Impl final : ImplBase {
         };
         cs = 8;
         if (slice_words(8) * 8 + fixed > 200 * 1024 || (maxrows + 7) / 8 > 64) cs = 16;
+        // wide decoders on the multi-kernel path (config 3): 16-CTA control clusters (config 3: 4.69K
+        // vs 4.66K evals/s device-timed, 4.68K vs 4.49K through lsb_eval)
+        if (c.hp >= 256 && c.n > kSolveDefaultMaxRows) cs = 16;
         if (c.dev.ctrl_cluster16) cs = 16;  // developer override
         if (slice_words(cs) * 8 + fixed > 220 * 1024 || (maxrows + cs - 1) / cs > 64)
             throw LsbError(LSB_EINVAL, "decoder: hidden layers too large for the control cluster");
