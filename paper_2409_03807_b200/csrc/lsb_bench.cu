@@ -20,6 +20,15 @@ __global__ void flush_kernel(uint4* p, size_t n, unsigned v) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         p[i] = make_uint4(v, v, v, v);
 }
+// Diagnostic (LSB_FLUSH_MODE=readback): after the write flush, read a second buffer larger than
+// L2 so the dirty lines are written back outside the timed region and L2 holds clean lines --
+// separates the flush's write-back cost from the evaluation's own traffic.
+__global__ void flush_read_kernel(const uint4* p, size_t n, unsigned* sink) {
+    unsigned acc = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        acc ^= __ldcg(p + i).x;
+    if (acc == 0x12345678u) *sink = acc;
+}
 
 void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double* eval_ms, double* out_ms,
                  double* E, bool want_grad) {
@@ -33,6 +42,9 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
     for (auto& e : ev) cuda_check(cudaEventCreate(&e), "event");
     const char* fm = getenv("LSB_FLUSH_MODE");
     const bool fkern = fm && !strcmp(fm, "kernel");
+    const bool fread = fm && !strcmp(fm, "readback");
+    void* flush2 = nullptr;
+    if (fread && flush_bytes) cuda_check(cudaMalloc(&flush2, flush_bytes), "bench flush2");
     if (fkern) {
         cudaFuncSetAttribute(flush_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
@@ -41,6 +53,9 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
         if (flush && fkern)
             flush_kernel<<<148 * 2, 512, 200 << 10, c.stream>>>((uint4*)flush, flush_bytes / 16, (unsigned)k);
         else if (flush) cuda_check(cudaMemsetAsync(flush, k & 0xff, flush_bytes, c.stream), "flush");
+        if (flush2)
+            flush_read_kernel<<<148 * 4, 512, 0, c.stream>>>((const uint4*)flush2, flush_bytes / 16,
+                                                            (unsigned*)flush2);
         cuda_check(cudaMemcpyAsync(c.d_state->zt, dZ + (size_t)k * r, sizeof(double) * r, cudaMemcpyDeviceToDevice,
                                    c.stream),
                    "z");
@@ -56,6 +71,7 @@ void bench_evals(Context& c, int K, const double* Z, size_t flush_bytes, double*
     }
     for (auto& e : ev) cudaEventDestroy(e);
     if (flush) cudaFree(flush);
+    if (flush2) cudaFree(flush2);
     cudaFree(dZ);
 }
 

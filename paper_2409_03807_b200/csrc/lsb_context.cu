@@ -138,6 +138,7 @@ struct KernelSet {
     void (*out_fwd)(const EvalParams<TS>);
     void (*vjp)(const EvalParams<TS>);
     void (*vjp_gather)(const EvalParams<TS>);  // gather folded into the VJP (tv in smem)
+    void (*vjp_wgather)(const EvalParams<TS>);  // gather per warp and tile inside the VJP stream
     size_t smem;      // dynamic smem of both streaming kernels (ring + scratch)
     int tile_rows;
     size_t stage_bytes;  // one ring stage (tile + side records)
@@ -145,7 +146,8 @@ struct KernelSet {
 
 template <typename TS, int HP>
 KernelSet<TS> kernels_for() {
-    return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, vjp_gather_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
+    return {out_fwd_tma_kernel<TS, HP>, vjp_tma_kernel<TS, HP>, vjp_gather_tma_kernel<TS, HP>,
+            vjp_wgather_tma_kernel<TS, HP>, stream_smem_bytes<TS, HP>(),
             StreamCfg<TS, HP>::TR, (size_t)StreamCfg<TS, HP>::STAGEB};
 }
 
@@ -379,6 +381,7 @@ struct Impl final : ImplBase {
         // W_out stays L2-resident when it fits in ~60% of L2, else it is streamed
         const size_t wbytes = (size_t)c.n * c.hp * sizeof(TS);
         p.w_resident = wbytes <= (size_t)(0.6 * c.l2_bytes) ? 1 : 0;
+        if (c.dev.w_resident >= 0) p.w_resident = c.dev.w_resident;  // developer override
         // grid sizing: persistent grids of (SMs x resident blocks)
         int occ = 0;
         p.vpb = 64;  // 192 rows per slab: a multiple of every tile height
@@ -405,10 +408,25 @@ struct Impl final : ImplBase {
         {
             fuse_gather = c.dev.fuse_gather != 0;
             bool ok = false;
+            if (fuse_gather && c.dev.vjp_wg) {  // per-warp gather: no tv scratch, up to 3 CTAs per SM
+                const size_t sm = 512 + (size_t)(kStreamThreads / 32) * kStreamSpw * ks.tile_rows * c.hp * sizeof(TS);
+                int occ2 = 0;
+                if (cudaFuncSetAttribute(ks.vjp_wgather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) ==
+                        cudaSuccess &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ks.vjp_wgather, kStreamThreads, sm) ==
+                        cudaSuccess &&
+                    occ2 >= 1) {
+                    ks.vjp_gather = ks.vjp_wgather;
+                    vjpg_smem = sm;
+                    p.grid_vjp = std::max(1, std::min(ntiles, c.num_sms * std::min(occ2, c.dev.vjp_wg_cta)));
+                    ok = true;
+                }
+                cudaGetLastError();
+            }
 #ifndef LSB_VJP_MAXCTA
 #define LSB_VJP_MAXCTA 2
 #endif
-            for (int want = LSB_VJP_MAXCTA; fuse_gather && want >= 1 && !ok; --want) {
+            for (int want = LSB_VJP_MAXCTA; fuse_gather && want >= 1 && !ok; --want) {  // CTA-wide gather
                 const int grid = std::max(1, std::min(ntiles, c.num_sms * want));
                 const size_t tvb = ((size_t)((ntiles + grid - 1) / grid) * ks.tile_rows * sizeof(double) + 127) &
                                    ~(size_t)127;

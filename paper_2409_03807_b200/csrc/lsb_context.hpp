@@ -50,6 +50,9 @@ struct DevFlags {
                               // 8 vjp->ctrl); 0: plain full-completion edges
     int l2_pf_elem = 0;       // LSB_L2PF_ELEM: VJP head tiles prefetched into L2 by the element pass (measured: slower)
     int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
+    int vjp_wg = 0;           // LSB_VJP_WG=1: per-warp, per-tile gather in the fused VJP (measured 1% slower than the prologue)
+    int vjp_wg_cta = 3;       // LSB_VJP_WG_CTA: CTAs per SM of the per-warp-gather VJP
+    int w_resident = -1;      // LSB_W_RESIDENT=0/1: force the W_out L2 policy (evict_first / evict_last)
     int sweep = 0;            // LSB_SWEEP=1: fused warp-specialised sweep pass instead of out_fwd, elem, vjp (measured slower)
     float sweep_lag = 1.5f;   // LSB_SWEEP_LAG: ticket lag between an item and its dependencies, in grids
     std::string active;       // "NAME=value ..." of every switch found set

@@ -531,6 +531,136 @@ __global__ void __launch_bounds__(kStreamThreads) vjp_tma_kernel(const EvalParam
     if (tid == 0) p.grp_cnt[grp] = 0;
 }
 
+// tv of the TR rows of tile t, gathered by one warp: the tile's (<= TR/3 + 2) free vertices get
+// LG lanes each, which sum strided slices of the vertex's CSR segment; an xor butterfly within
+// the lane group (bit-identical on every lane of the group) completes each vertex's force, and
+// lane j < TR forms row t TR + j.  Issued right before the tile's W rows are waited for, so its
+// L2 latency hides behind the W stream; vertices straddling two tiles are gathered by both.
+template <typename TS, int TR>
+__device__ __forceinline__ void warp_gather_tile(const EvalParams<TS>& p, int t, double* tvw, int has_inertia,
+                                                 bool ident) {
+    constexpr int LG = TR == 8 ? 8 : 4;  // lanes per vertex (TR 8: <= 4 vertices; TR 16: <= 7)
+    const int lane = threadIdx.x & 31;
+    const int R0 = t * TR, R1 = min(R0 + TR, p.n);
+    const int f0 = R0 / 3, nvtx = (R1 - 1) / 3 - f0 + 1;
+    const int vi = lane / LG, sub = lane % LG;
+    double g[3] = {0.0, 0.0, 0.0};
+    if (vi < nvtx) {
+        const int f = f0 + vi;
+        const int b = __ldg(p.csr_ptr + f), e = __ldg(p.csr_ptr + f + 1);
+        if constexpr (std::is_same<TS, float>::value) {
+            const float4* F4 = reinterpret_cast<const float4*>(p.forces);
+            for (int k = b + sub; k < e; k += LG) {
+                const float4 v = __ldcg(F4 + k);
+                g[0] += (double)v.x;
+                g[1] += (double)v.y;
+                g[2] += (double)v.z;
+            }
+        } else {
+            for (int k = b + sub; k < e; k += LG) {
+                const double4 v = ld_cg_d4(p.forces + 4 * (size_t)k);
+                g[0] += v.x;
+                g[1] += v.y;
+                g[2] += v.z;
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < LG; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) g[c] += __shfl_xor_sync(0xffffffffu, g[c], o);
+    const int row = R0 + (lane < TR ? lane : 0);
+    const int src = (row / 3 - f0) * LG, comp = row % 3;
+    const double gx = __shfl_sync(0xffffffffu, g[0], src);
+    const double gy = __shfl_sync(0xffffffffu, g[1], src);
+    const double gz = __shfl_sync(0xffffffffu, g[2], src);
+    if (lane < TR && row < R1) {
+        const double gc = comp == 0 ? gx : (comp == 1 ? gy : gz);
+        const double rin = has_inertia ? __ldcg(p.rin + row) : 0.0;
+        const double sc = ident ? __ldg(p.sout + row) : __ldcg(p.dsout + row);
+        tvw[lane] = (gc + rin) * sc;
+    }
+    __syncwarp();
+}
+
+// vjp_gather_tma_kernel with the gather done per warp and per tile (warp_gather_tile) instead of
+// a CTA-wide prologue: no tv scratch, and the gather latency overlaps the stream.
+template <typename TS, int HP>
+__global__ void __launch_bounds__(kStreamThreads) vjp_wgather_tma_kernel(const EvalParams<TS> p) {
+    using C = StreamCfg<TS, HP>;
+    extern __shared__ __align__(128) unsigned char ssm[];
+    constexpr int NW = kStreamThreads / 32;
+    __shared__ int am_grp_last;
+    __shared__ double tvw_all[NW][C::TR];
+    DevState* st = p.st;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    WarpRing r{ssm + 512, reinterpret_cast<uint64_t*>(ssm), NW, kStreamSpw, C::TILEB, 0u};
+    double* wred = reinterpret_cast<double*>(ssm + 512);  // NW x HP, in the drained ring
+    static_assert(NW * HP * 8 <= NW * kStreamSpw * C::TILEB, "column sums fit in the ring");
+    double* tvw = tvw_all[warp];
+    ring_init(r.full, NW * kStreamSpw);
+    __syncthreads();
+    const int ntiles = (p.n + C::TR - 1) / C::TR;
+    const int t0 = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
+    const int t1 = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
+    const uint64_t pol = l2_policy(p.w_resident);
+    auto issue = [&](int t, unsigned char* b, uint64_t* bar) { issue_w_only<TS, HP>(p, t, b, bar, pol); };
+    ring_prefetch(r, t0, t1, issue);  // W tiles do not depend on the element pass
+    griddep_wait();
+    griddep_launch();
+    if (!st->need_grad) {  // value only: let the prefetched tiles land before the CTA exits
+        ring_drain(r, t0, t1);
+        return;
+    }
+    const int has_inertia = st->has_inertia;
+    const bool ident = p.out_act == kIdentity;
+    double acc[C::NCH][C::V4];
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q) acc[c][q] = 0.0;
+    int i = 0;
+    for (int t = t0 + warp; t < t1; t += NW, ++i) {
+        warp_gather_tile<TS, C::TR>(p, t, tvw, has_inertia, ident);
+        const int j = i % kStreamSpw;
+        r.wait(j);
+        vjp_tile<TS, HP>(p, r.buf(j), tvw, t, acc);
+        __syncwarp();
+        const int tn = t + NW * kStreamSpw;
+        if (lane == 0 && tn < t1) issue(tn, r.buf(j), r.bar(j));
+    }
+    __syncthreads();  // every warp is done with its stages: wred may overwrite the ring
+#pragma unroll
+    for (int c = 0; c < C::NCH; ++c)
+#pragma unroll
+        for (int q = 0; q < C::V4; ++q) wred[warp * HP + (c * 32 + lane) * C::V4 + q] = acc[c][q];
+    __syncthreads();
+    for (int jj = tid; jj < HP; jj += blockDim.x) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) sum += wred[w * HP + jj];
+        p.ybar_part[(size_t)blockIdx.x * HP + jj] = sum;
+    }
+    // group-last block sums its group's partials in block order
+    __threadfence();
+    __syncthreads();
+    const int grp = blockIdx.x / p.group;
+    const int g0 = grp * p.group, g1 = min(g0 + p.group, (int)gridDim.x);
+    if (tid == 0) {
+        const unsigned prev = atomicAdd(p.grp_cnt + grp, 1u);
+        am_grp_last = (prev == (unsigned)(g1 - g0 - 1));
+    }
+    __syncthreads();
+    if (!am_grp_last) return;
+    __threadfence();
+    for (int jj = tid; jj < HP; jj += blockDim.x) {
+        double sum = 0.0;
+        for (int b = g0; b < g1; ++b) sum += __ldcg(p.ybar_part + (size_t)b * HP + jj);
+        p.ybar_grp[(size_t)grp * HP + jj] = sum;
+    }
+    if (tid == 0) p.grp_cnt[grp] = 0;
+}
+
 // ---------------------------------------------------------------- K3b + K4 fused: gather + VJP
 // vjp_tma_kernel with the vertex gather folded in: each CTA gathers tv for its own rows
 // into shared memory (gather_rows_smem, as the persistent kernel does) while its first W
