@@ -211,6 +211,7 @@ DevFlags read_dev_flags() {
     if (const char* v = get("LSB_SWEEP")) f.sweep = v[0] == '1';
     if (const char* v = get("LSB_PDL")) f.pdl = atoi(v) & 15;
     if (const char* v = get("LSB_VJP_WG")) f.vjp_wg = v[0] != '0';
+    if (const char* v = get("LSB_SOLVE_CLUSTERS")) f.solve_clusters = std::max(0, atoi(v));
     if (const char* v = get("LSB_W_RESIDENT")) f.w_resident = v[0] == '1' ? 1 : 0;
     if (const char* v = get("LSB_VJP_WG_CTA")) f.vjp_wg_cta = std::max(1, std::min(4, atoi(v)));
     if (const char* v = get("LSB_L2PF")) f.l2_pf = std::max(0, std::min(256, atoi(v)));

@@ -695,6 +695,7 @@ struct Impl final : ImplBase {
             solve = nullptr;
             return;
         }
+        if (c.dev.solve_clusters > 0) nclusters = std::min(nclusters, c.dev.solve_clusters);  // developer override
         solve_grid = nclusters * cs;
         if (solve_grid > kSolveMaxGrid) {  // the control cluster sums the per-CTA partials with 5 x 32 lanes
             c.solve_reason = "grid of " + std::to_string(solve_grid) + " CTAs exceeds " + std::to_string(kSolveMaxGrid);

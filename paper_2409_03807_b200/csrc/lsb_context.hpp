@@ -53,6 +53,7 @@ struct DevFlags {
     int vjp_wg = 0;           // LSB_VJP_WG=1: per-warp, per-tile gather in the fused VJP (measured 1% slower than the prologue)
     int vjp_wg_cta = 3;       // LSB_VJP_WG_CTA: CTAs per SM of the per-warp-gather VJP
     int w_resident = -1;      // LSB_W_RESIDENT=0/1: force the W_out L2 policy (evict_first / evict_last)
+    int solve_clusters = 0;   // LSB_SOLVE_CLUSTERS: cap on the persistent kernel's clusters (0: all that fit)
     int sweep = 0;            // LSB_SWEEP=1: fused warp-specialised sweep pass instead of out_fwd, elem, vjp (measured slower)
     float sweep_lag = 1.5f;   // LSB_SWEEP_LAG: ticket lag between an item and its dependencies, in grids
     std::string active;       // "NAME=value ..." of every switch found set

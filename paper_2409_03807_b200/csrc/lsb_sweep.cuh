@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kSwThreads, 1) sweep_kernel(const EvalParams<T
     __shared__ unsigned s_seq;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint64_t* full = reinterpret_cast<uint64_t*>(ssm);  // kSwStreamWarps x kSwStages
+    griddep_wait();  // launched with a programmatic edge from the control kernel: y and the state first
     if (tid == 0) {
         for (int s = 0; s < kSwStreamWarps * kSwStages; ++s) mbar_init(&full[s], 1);
         mbar_fence_init();

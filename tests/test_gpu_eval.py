@@ -312,3 +312,32 @@ def test_wls_step_device(path, product):
     z_star = np.linalg.solve(basis.T @ (mass[:, None] * basis), basis.T @ (mass * (qbar - shift)))
     assert rep.code == 1
     assert np.abs(state.z - z_star).max() < 1e-8, np.abs(state.z - z_star).max()
+
+
+@pytest.mark.parametrize("flags", ["LSB_SWEEP=1", "LSB_VJP_WG=1", "LSB_PDL=15 LSB_L2PF_ELEM=16",
+                                   "LSB_ELEM_F32=0 LSB_PDL=0 LSB_CTRL_CLUSTER=16"])
+def test_multikernel_variants_match_oracle(flags, oracle, product, monkeypatch):
+    """The multi-kernel path's alternative schedules (developer switches, read at lsb_create):
+    the fused sweep pass, the per-warp VJP gather, all programmatic edges, fp64 element
+    arithmetic -- E / grad E of config 2 in fp32 storage against the oracle at 1e-4, and a
+    device L-BFGS solve with the oracle's exit code."""
+    from paper_2409_03807_b200 import configs
+    for kv in flags.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    pr = configs.build("c2")
+    sysm = pr.system("fp32")
+    sysm.use_solve_kernel(False)
+    ob = oracle.problem("c2")
+    qbar = configs.timestep0_qbar(pr, ob.mass)
+    obj = product.ReducedObjective(sysm, qbar, configs.DT)
+    rng = np.random.default_rng(17)
+    for _ in range(3):
+        z = 0.5 * rng.standard_normal(pr.model.r)
+        g = np.zeros(pr.model.r)
+        E = obj.eval(z, g)
+        Eo, go = ob.eval(z, qbar=qbar, dt=configs.DT)
+        assert rel_err(E, Eo) < 1e-4 and rel_err(g, go) < 1e-4, flags
+    rep = product.lbfgs_minimize(obj, np.zeros(pr.model.r), configs.solver_config())
+    assert rep.code == 1, (flags, rep)
+    assert all(k in sysm.dev_flags() for k in [kv.split("=")[0] for kv in flags.split()])
