@@ -683,9 +683,16 @@ __device__ __forceinline__ uint32_t tf32_bits(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
     return u;
 }
+// 3xTF32 operand split by truncation: hi keeps the top 10 mantissa bits (one LOP3), lo = x - hi
+// is exact in fp32 and the MMA reads its top bits; hi lo' + lo hi' + hi hi' then carries ~22
+// bits (~2.4e-7 relative), against the 1e-4 bar of the Hessian path.  cvt.rna.tf32 (the
+// round-to-nearest form) lowers to an FSETP / SEL / integer sequence per conversion: with 64
+// conversions per tet it was the largest instruction block of the contraction (c5 107 -> 96 ms).
+// Staging the block's Jacobian rows in shared memory instead of the one-tet-ahead L2 prefetch
+// was measured slower (99 ms: two CTAs per SM instead of four).
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-    hi = tf32_bits(x);
-    lo = tf32_bits(x - __uint_as_float(hi));
+    hi = __float_as_uint(x) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32_16x8x8(float* c, const uint32_t* a, const uint32_t* b) {
     asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
