@@ -472,6 +472,11 @@ def lipschitz_record(K, W, R, want_cpu):
     t0 = time.perf_counter()
     sysm.lipschitz_loss(Z1l, Z2l)
     e2e_t = R.max(time.perf_counter() - t0)
+    # training side: the same loss and its parameter gradient dL/dtheta
+    sysm.lipschitz_loss_grad(Z1l[:8], Z2l[:8])
+    t0 = time.perf_counter()
+    sysm.lipschitz_loss_grad(Z1l, Z2l)
+    train_t = R.max(time.perf_counter() - t0)
     hbm, bf16, peak_kind = peaks()
     flops = 890e9 + 640e9  # tangent GEMMs + element HVPs per 1024 pairs
     achieved = flops / (t * 1e-3) / 1e12
@@ -491,6 +496,9 @@ def lipschitz_record(K, W, R, want_cpu):
                 "d2h_bytes_per_step": 8, "api": "lsb_lipschitz_loss (C ABI), host buffers"},
         "gpu_launches": int(launches // reps),
         "timed": "CUDA events on the context stream around each lsb_lipschitz_loss call",
+        "train_step_ms": train_t * 1e3,
+        "train_step": "lsb_lipschitz_loss_grad over the same pairs (loss + dL/dtheta of every decoder parameter), "
+                      "host clock",
     }
     if want_cpu and R.rank == 0 and R.ws == 1:
         ob = oracle_problem("c5")

@@ -717,6 +717,7 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
     __shared__ __align__(16) float sh_M[2][GP][R][12];   // M' rows per direction
     __shared__ __align__(16) float sh_rec[kTB][12];   // the block's records
     __shared__ int sh_off[kTB][8];  // accg offsets of the free slots (pinned -> scratch slot nv) (4), Us offsets of the touched slots (4)
+    __shared__ int4 sh_tq[kTB];     // the block's vertex ids: the one-tet-ahead J prefetch reads them from here
     __shared__ float sh_b[R][GP][NH];
     extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
@@ -741,6 +742,8 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
         sh_off[i >> 2][i & 3] = (lv >= 0 ? lv : nv) * 3 * GP;
         sh_off[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i] * 3 * GP;
     }
+    for (int i = tid; i < e1 - e0; i += 128) sh_tq[i] = __ldg(tets + e0 + i);
+    __syncthreads();
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     float cacc[PPW][MT][NT][4];
 #pragma unroll
@@ -758,14 +761,26 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
     // read from L2 one tet ahead (coalesced over the CTA's points x directions)
     const float* Jp = Jv + ((size_t)(p0 + pl)) * R + b;
     const size_t jstride = (size_t)P * R;  // per (vertex, component) row
-    float dun[12];
+    // two-deep register ring: dun for tet e + 1, dun2 for tet e + 2 (L2 / DRAM latency exceeds
+    // one tet's work)
+    float dun[12], dun2[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) dun[q] = dun2[q] = 0.f;
     if (live && e0 < e1) {
-        const int4 t = __ldg(tets + e0);
+        const int4 t = sh_tq[0];
         const int vv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
             for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
+    }
+    if (live && e0 + 1 < e1) {
+        const int4 t = sh_tq[1];
+        const int vv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dun2[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
     }
     for (int eb = e0; eb < e1; eb += R) {
         // ---- batch phase: thread (pl, t = b) forms the per-(tet, point) quantities of tet eb + b
@@ -867,14 +882,17 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
                 for (int qq = 0; qq < 9; ++qq) rc[qq] = sh_rec[e - e0][qq];
                 float duc[12];
 #pragma unroll
-                for (int q = 0; q < 12; ++q) duc[q] = dun[q];
-                if (e + 1 < e1) {
-                    const int4 t = __ldg(tets + e + 1);
+                for (int q = 0; q < 12; ++q) {
+                    duc[q] = dun[q];
+                    dun[q] = dun2[q];
+                }
+                if (e + 2 < e1) {
+                    const int4 t = sh_tq[e + 2 - e0];
                     const int vv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
 #pragma unroll
-                        for (int a = 0; a < 3; ++a) dun[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
+                        for (int a = 0; a < 3; ++a) dun2[k * 3 + a] = __ldg(Jp + ((size_t)vv[k] * 3 + a) * jstride);
                 }
                 float dA[9];
 #pragma unroll

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
     constexpr int NB = 34;  // per (tet, point) batch record: F 9, cof 9, psiI, psiII, psiIII, psiJ, gbar forces 12
     __shared__ __align__(16) float sh_rec[TBMAX][12];
     __shared__ short sh_loc[TBMAX][8];
+    __shared__ int4 sh_tq[TBMAX];  // the block's vertex ids (the one-tet-ahead J / W prefetch)
     __shared__ float sh_b[R][GP][NB];
     extern __shared__ __align__(16) float dyn[];
     const int tid = threadIdx.x;
@@ -245,7 +246,9 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
         sh_loc[i >> 2][i & 3] = tet_loc[(size_t)e0 * 4 + i];
         sh_loc[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i];
     }
+    for (int i = tid; i < e1 - e0; i += 128) sh_tq[i] = __ldg(tets + e0 + i);
     cp_async_wait_all();
+    __syncthreads();
     __syncthreads();
     const bool live = p0 + pl < P;
     const float* Jp = Jv + (size_t)(p0 + pl) * R + c;
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(128) elem_theta_kernel(const int4* tets, const
                     wu[q] = wn[q];
                 }
                 if (e + 1 < e1) {
-                    const int4 t = __ldg(tets + e + 1);
+                    const int4 t = sh_tq[e + 1 - e0];
                     const int vv[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
