@@ -15,7 +15,7 @@ exit-code histogram (diagnostics.cpp:153-172 layout).
 Per-config records ("records") carry the other BASELINE configs, each with its
 own roofline fraction and CPU baseline:
   c1  fp64, 100 timesteps + E+grad evals/s
-  c2  fp64, 200 timesteps + E+grad evals/s (+ value-only evals/s)
+  c2  fp64, 200 timesteps + E+grad evals/s (+ value-only evals/s); c2f the same in fp32 storage
   c4  4096 z on the c2 problem (tcgen05 GEMMs), evals/s + tensor fraction
   c5  1024 latent pairs on the c2 problem, order-2 Lipschitz loss, ms
 
@@ -555,7 +555,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c2f", "c3"])
-    ap.add_argument("--records", default="c1,c2,c4,c5", help="comma list of extra per-config records, or none")
+    ap.add_argument("--records", default="c1,c2,c2f,c4,c5", help="comma list of extra per-config records, or none")
     ap.add_argument("--timesteps", type=int, default=0, help="timesteps for ms/timestep (0: the config's own)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

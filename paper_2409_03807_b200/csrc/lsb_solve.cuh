@@ -21,6 +21,9 @@ namespace lsb {
 constexpr int kSolveThreads = LSB_SOLVE_THREADS;  // 9 warps: all stream (self-issued rings) and all compute
 constexpr int kSolveMaxStages = 36;
 constexpr int kSolveMaxGrid = 160;  // control-cluster partial sums: 5 x 32 lanes
+#ifndef LSB_SOLVE_ELEM_F32
+#define LSB_SOLVE_ELEM_F32 1
+#endif
 constexpr int kSolveBarBytes = 512;  // full barriers (kSolveMaxStages x 8 B, padded)
 
 // Launch-wide scalars the non-control CTAs need (written by the control CTA).
@@ -995,11 +998,17 @@ __global__ void __launch_bounds__(kSolveThreads, 1) solve_kernel(const EvalParam
                 for (int k = 0; k < 2; ++k) {
                     if (k == 1 && !has1) break;
                     const int e = k ? e1 : e0;
+#if LSB_SOLVE_ELEM_F32
+                    // fp32-storage mode: fp32 element arithmetic, as on the multi-kernel path
+                    eacc += elem_tet<TS>(p.rec, (size_t)e, u[k], __ldg(p.fpos + e), p.forces,
+                                         std::is_same<TS, float>::value ? 1 : 0);
+#else
                     double rc[12];
                     load_rec<TS>(p.rec, (size_t)e, rc);
                     double f[12];
                     eacc += tet_energy_forces(u[k][0], u[k][1], u[k][2], u[k][3], rc, f);
                     store_forces_csr_t<TS>(p.forces, __ldg(p.fpos + e), f);
+#endif
                 }
             }
             const double tot = block_sum(eacc, red);
