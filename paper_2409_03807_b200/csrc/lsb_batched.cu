@@ -1707,7 +1707,10 @@ struct BatchedEngine : BatchedBase {
     }
 
     // Hessians of the elastic potential for N <= PH points Z (N x r) -> H (N x r x r).
-    void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout, bool with_inertia = false) {
+    // Hout_dev (device, N x r x r) instead of Hout: no host copy and no stream synchronisation, so
+    // consecutive chunks queue back to back.
+    void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout, bool with_inertia = false,
+                           double* Hout_dev = nullptr) {
         if (!hess_ready) init_hessian(c);
         cudaStream_t s = c.stream;
         int inertia = 0;
@@ -1774,10 +1777,26 @@ struct BatchedEngine : BatchedBase {
         }
         hess_final_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, d_Ch, d_Yh, XL, d_H);
         c.batched_launches += 10 + 2 * c.nhid;
+        if (Hout_dev) {
+            cuda_check(cudaMemcpyAsync(Hout_dev, d_H, 8 * (size_t)N * r * r, cudaMemcpyDeviceToDevice, s), "H d2d");
+            return;
+        }
         std::vector<double> Hh((size_t)P * r * r);
         cuda_check(cudaMemcpyAsync(Hh.data(), d_H, 8 * Hh.size(), cudaMemcpyDeviceToHost, s), "H");
         cuda_check(cudaStreamSynchronize(s), "sync");
         std::memcpy(Hout, Hh.data(), 8 * (size_t)N * r * r);
+    }
+
+    // device buffer of a whole batch's Hessians (grown on demand, owned by the context)
+    double* d_hall = nullptr;
+    size_t hall_cap = 0;
+    double* hess_all(Context& c, size_t count) {
+        if (count > hall_cap) {
+            if (d_hall) c.dfree(d_hall);
+            d_hall = static_cast<double*>(c.dmalloc(8 * count));
+            hall_cap = count;
+        }
+        return d_hall;
     }
 
     // fp32 copy of the element records (the fp64 context stores them in fp64)
@@ -1842,10 +1861,13 @@ void batched_objective_hessian(Context& c, int B, const double* Z, double* H) {
 void batched_hessian(Context& c, int B, const double* Z, double* H) {
     BatchedEngine& eng = engine(c);
     const int r = c.r;
+    // all chunks write into one device buffer; a single copy and synchronisation at the end
+    double* d_all = eng.hess_all(c, (size_t)B * r * r);
     for (int b0 = 0; b0 < B; b0 += BatchedEngine::PH) {
         const int N = std::min(BatchedEngine::PH, B - b0);
-        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, H + (size_t)b0 * r * r);
+        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r);
     }
+    c.copy(H, d_all, 8 * (size_t)B * r * r, cudaMemcpyDeviceToHost, "hessians");
 }
 
 // mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2 (losses.cpp:196-213, order 2), fp64 combine.
