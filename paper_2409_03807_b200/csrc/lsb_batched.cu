@@ -665,6 +665,45 @@ __global__ void __launch_bounds__(256) inertia_hess_kernel(int n, int P, int r, 
     if (tid < npair) C[(size_t)p * npair + tid] += inv_dt2 * acc;
 }
 
+// Order-2 Lipschitz loss backward on the device (losses.cpp:196-213 through scale / dot / sub, then
+// symmetric_from_entries, tape.cpp:212-222): per pair q (points 2q, 2q + 1, factor f = 2 / (P |dz|^2)),
+// Hbar = +-f (H1 - H2) as fp32 rows, ebar_ab = Hbar_ab + Hbar_ba (a < b) / Hbar_aa, and the pair's
+// |H1 - H2|^2 (fixed-order block sum) for the loss.  One CTA per pair.  With hb = eb = null only the
+// |H1 - H2|^2 (the loss-only path uses the same reduction, so loss and loss + gradient agree bitwise).
+__global__ void __launch_bounds__(256) lipschitz_dldh_kernel(int npairs, int r, const double* H, const double* fac,
+                                                             float* hb, float* eb, double* d2out) {
+    __shared__ double red[32];
+    const int q = blockIdx.x;
+    if (q >= npairs) return;
+    const int rr = r * r, npair = r * (r + 1) / 2;
+    const double* H1 = H + (size_t)(2 * q) * rr;
+    const double* H2 = H1 + rr;
+    const double f = fac ? fac[q] : 0.0;
+    double d2 = 0.0;
+    for (int k = threadIdx.x; k < rr; k += blockDim.x) {
+        const double d = H1[k] - H2[k];
+        d2 += d * d;
+        if (hb) {
+            hb[(size_t)(2 * q) * rr + k] = (float)(f * d);
+            hb[(size_t)(2 * q + 1) * rr + k] = (float)(-f * d);
+        }
+    }
+    for (int sidx = threadIdx.x; eb && sidx < npair; sidx += blockDim.x) {
+        int a = 0, rem = sidx;
+        while (rem >= r - a) {
+            rem -= r - a;
+            ++a;
+        }
+        const int b = a + rem;
+        const double hab = f * (H1[a * r + b] - H2[a * r + b]);
+        const double v = a != b ? hab + f * (H1[b * r + a] - H2[b * r + a]) : hab;
+        eb[(size_t)(2 * q) * npair + sidx] = (float)v;
+        eb[(size_t)(2 * q + 1) * npair + sidx] = (float)(-v);
+    }
+    const double t = block_sum(d2, red);
+    if (threadIdx.x == 0) d2out[q] = t;
+}
+
 // Element Hessian contraction.  CTA = (block of kTB tets, GP = 128/R points).  Tets go
 // in batches of R: first thread (point pl, t) forms, once per (tet, point), F, cof(F),
 // the SNH derivatives and the element's elastic forces vol B^T P(F) into shared memory;
@@ -1521,6 +1560,7 @@ struct BatchedEngine : BatchedBase {
     // ---------------------------------------------------------------- theta-gradient (lsb_theta.cuh)
     bool theta_ready = false;
     float *d_Hbf = nullptr, *d_ebf = nullptr, *d_Bt2 = nullptr, *d_Bfwd = nullptr, *d_Ct2 = nullptr;
+    double* d_fac = nullptr;  // per-pair factors 2 / (P |dz|^2) of a chunk
     float *d_Wv = nullptr, *d_gbar = nullptr, *d_partJ = nullptr, *d_partq = nullptr, *d_Abar = nullptr;
     float *d_XbL = nullptr, *d_Xbar[2] = {}, *d_Abl = nullptr, *d_spart = nullptr;
     double *d_gW = nullptr, *d_gb = nullptr;
@@ -1538,6 +1578,7 @@ struct BatchedEngine : BatchedBase {
         for (int l = 0; l < c.nhid; ++l) hmax = std::max(hmax, c.hrows[l]);
         d_Hbf = alloc<float>((size_t)P * r * r);
         d_ebf = alloc<float>((size_t)P * npair);
+        d_fac = alloc<double>((size_t)P / 2 + 1);
         d_Bt2 = alloc<float>((size_t)h * P * (r + 1));
         d_Bfwd = alloc<float>((size_t)P * (r + 2) * h);
         d_Ct2 = alloc<float>((size_t)n * P * (r + 1));
@@ -1629,39 +1670,27 @@ struct BatchedEngine : BatchedBase {
     // One chunk of N <= PH points (pairs interleaved z1, z2): H via run_hessian_chunk, the
     // loss terms and dL/dH on the host (fp64), then the device reverse sweep accumulating
     // dL/dtheta into d_gW / d_gb.  inv_P = 1 / (number of pairs in the whole loss).
-    void run_theta_chunk(Context& c, int N, const double* Z, double inv_P, double& loss_sum) {
+    // One chunk of N (even) points = N / 2 pairs: Hessians into the device buffer, dL/dH on the device
+    // (lipschitz_dldh_kernel) with the pair factors f = 2 inv_P / |dz|^2 from the host, |H1 - H2|^2
+    // into d2_out (device, N / 2); no host round trip inside the chunk.
+    void run_theta_chunk(Context& c, int N, const double* Z, double inv_P, double* d2_out) {
         if (!theta_ready) init_theta(c);
-        const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols, npair = r * (r + 1) / 2;
-        std::vector<double> H((size_t)N * r * r);
-        run_hessian_chunk(c, N, Z, H.data());
+        const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols;
         cudaStream_t s = c.stream;
-        // scale(sum, 1/P) . scale(dot(diff, diff), 1/dz2) . sub(H1, H2) backward; then the
-        // symmetric_from_entries backward (tape.cpp:212-222) for ebar
-        std::vector<float> hb((size_t)P * r * r, 0.f), eb((size_t)P * npair, 0.f);
-        std::vector<double> Hb((size_t)r * r);
-        for (int q = 0; q + 1 < N; q += 2) {
-            const double* H1 = &H[(size_t)q * r * r];
-            const double* H2 = &H[(size_t)(q + 1) * r * r];
-            const double* z1 = Z + (size_t)q * r;
-            const double* z2 = Z + (size_t)(q + 1) * r;
-            double d2 = 0.0, dz2 = 0.0;
-            for (int k = 0; k < r * r; ++k) d2 += (H1[k] - H2[k]) * (H1[k] - H2[k]);
+        double* d_Hc = hess_all(c, (size_t)P * r * r);
+        run_hessian_chunk(c, N, Z, nullptr, false, d_Hc);
+        std::vector<double> fac(N / 2);
+        for (int q = 0; q < N / 2; ++q) {
+            const double* z1 = Z + (size_t)(2 * q) * r;
+            const double* z2 = z1 + r;
+            double dz2 = 0.0;
             for (int k = 0; k < r; ++k) dz2 += (z1[k] - z2[k]) * (z1[k] - z2[k]);
-            loss_sum += d2 / dz2;
-            const double f = 2.0 * inv_P / dz2;
-            for (int k = 0; k < r * r; ++k) Hb[k] = f * (H1[k] - H2[k]);
-            for (int side = 0; side < 2; ++side) {
-                const double sg = side == 0 ? 1.0 : -1.0;
-                const int pt = q + side;
-                for (int k = 0; k < r * r; ++k) hb[(size_t)pt * r * r + k] = (float)(sg * Hb[k]);
-                int sidx = 0;
-                for (int a = 0; a < r; ++a)
-                    for (int b = a; b < r; ++b, ++sidx)
-                        eb[(size_t)pt * npair + sidx] = (float)(sg * (Hb[a * r + b] + (a != b ? Hb[b * r + a] : 0.0)));
-            }
+            fac[q] = 2.0 * inv_P / dz2;
         }
-        c.copy(d_Hbf, hb.data(), 4 * hb.size(), cudaMemcpyHostToDevice, "Hbar");
-        c.copy(d_ebf, eb.data(), 4 * eb.size(), cudaMemcpyHostToDevice, "ebar");
+        cuda_check(cudaMemcpyAsync(d_fac, fac.data(), 8 * fac.size(), cudaMemcpyHostToDevice, s), "pair factors");
+        cuda_check(cudaMemsetAsync(d_Hbf, 0, 4 * (size_t)P * r * r, s), "Hbar");
+        cuda_check(cudaMemsetAsync(d_ebf, 0, 4 * (size_t)P * (r * (r + 1) / 2), s), "ebar");
+        lipschitz_dldh_kernel<<<N / 2, 256, 0, s>>>(N / 2, r, d_Hc, d_fac, d_Hbf, d_ebf, d2_out);
         // h-level operands, output GEMM -> W = J Hbar and gbar in the vertex layout
         theta_small(c, 0);
         if (!tc.enabled ||
@@ -1870,23 +1899,32 @@ void batched_hessian(Context& c, int B, const double* Z, double* H) {
     c.copy(H, d_all, 8 * (size_t)B * r * r, cudaMemcpyDeviceToHost, "hessians");
 }
 
-// mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2 (losses.cpp:196-213, order 2), fp64 combine.
+// mean_p |H(z1_p) - H(z2_p)|_F^2 / |z1_p - z2_p|^2 (losses.cpp:196-213, order 2), fp64 combine:
+// the Hessians stay on the device, |H1 - H2|^2 per pair comes from lipschitz_dldh_kernel (the
+// reduction the gradient path uses), and the host sums d2 / |dz|^2 in pair order.
 double lipschitz_loss(Context& c, int P, const double* Z1, const double* Z2) {
+    BatchedEngine& eng = engine(c);
     const int r = c.r;
-    std::vector<double> Z(2 * (size_t)P * r), H(2 * (size_t)P * r * r);
+    std::vector<double> Z(2 * (size_t)P * r);
     for (int p = 0; p < P; ++p) {  // interleave z1, z2 so both Hessians of a pair share a chunk
         std::memcpy(&Z[(2 * (size_t)p) * r], Z1 + (size_t)p * r, 8 * r);
         std::memcpy(&Z[(2 * (size_t)p + 1) * r], Z2 + (size_t)p * r, 8 * r);
     }
-    batched_hessian(c, 2 * P, Z.data(), H.data());
+    double* d_all = eng.hess_all(c, 2 * (size_t)P * r * r + P);
+    double* d_d2 = d_all + 2 * (size_t)P * r * r;
+    for (int b0 = 0; b0 < 2 * P; b0 += BatchedEngine::PH) {
+        const int N = std::min(BatchedEngine::PH, 2 * P - b0);
+        eng.run_hessian_chunk(c, N, Z.data() + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r);
+    }
+    lipschitz_dldh_kernel<<<P, 256, 0, c.stream>>>(P, r, d_all, nullptr, nullptr, nullptr, d_d2);
+    cuda_check(cudaGetLastError(), "pair losses");
+    std::vector<double> d2(P);
+    c.copy(d2.data(), d_d2, 8 * (size_t)P, cudaMemcpyDeviceToHost, "pair losses");
     double total = 0.0;
     for (int p = 0; p < P; ++p) {
-        double d2 = 0.0, dz2 = 0.0;
-        const double* H1 = &H[(2 * (size_t)p) * r * r];
-        const double* H2 = &H[(2 * (size_t)p + 1) * r * r];
-        for (int k = 0; k < r * r; ++k) d2 += (H1[k] - H2[k]) * (H1[k] - H2[k]);
+        double dz2 = 0.0;
         for (int k = 0; k < r; ++k) dz2 += (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]) * (Z1[(size_t)p * r + k] - Z2[(size_t)p * r + k]);
-        total += d2 / dz2;
+        total += d2[p] / dz2;
     }
     return total / P;
 }
@@ -1904,10 +1942,19 @@ double lipschitz_loss_grad(Context& c, int P, const double* Z1, const double* Z2
         std::memcpy(&Z[(2 * (size_t)p) * r], Z1 + (size_t)p * r, 8 * r);
         std::memcpy(&Z[(2 * (size_t)p + 1) * r], Z2 + (size_t)p * r, 8 * r);
     }
-    double total = 0.0;
+    double* d_d2 = static_cast<double*>(c.dmalloc(8 * (size_t)P));
     for (int b0 = 0; b0 < 2 * P; b0 += BatchedEngine::PH) {
         const int N = std::min(BatchedEngine::PH, 2 * P - b0);
-        eng.run_theta_chunk(c, N, Z.data() + (size_t)b0 * r, 1.0 / P, total);
+        eng.run_theta_chunk(c, N, Z.data() + (size_t)b0 * r, 1.0 / P, d_d2 + b0 / 2);
+    }
+    std::vector<double> d2(P);
+    c.copy(d2.data(), d_d2, 8 * (size_t)P, cudaMemcpyDeviceToHost, "pair losses");
+    c.dfree(d_d2);
+    double total = 0.0;  // losses.cpp:208-211: pair order
+    for (int p = 0; p < P; ++p) {
+        double dz2 = 0.0;
+        for (int k = 0; k < r; ++k) dz2 += (Z1[p * r + k] - Z2[p * r + k]) * (Z1[p * r + k] - Z2[p * r + k]);
+        total += d2[p] / dz2;
     }
     std::vector<double> gW(eng.gw_total), gb(eng.gb_total);
     c.copy(gW.data(), eng.d_gW, 8 * gW.size(), cudaMemcpyDeviceToHost, "gW");
