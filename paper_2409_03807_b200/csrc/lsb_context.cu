@@ -301,6 +301,15 @@ struct Impl final : ImplBase {
         void* a1[] = {&pg};
         void* asw[] = {&pg, &sw};
         const int pm = c.dev.pdl;
+        if (!want_grad && !use_sweep) {
+            // value only (lsb_eval without gradient): E is final after the element pass; neither the
+            // VJP nor the control kernel after it has anything to do
+            cudaGraphNode_t n1 = add_kernel_pdl(g, n0, (void*)ks.out_fwd, p.grid_out, out_smem, a1, kStreamThreads, pm & 1);
+            add_kernel_pdl(g, n1, (void*)elem_fn, p.grid_elem, 0, a1, 256, pm & 2);
+            cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate (eval)");
+            cudaGraphDestroy(g);
+            return ge;
+        }
         cudaGraphNode_t n3;
         if (use_sweep) {
             n3 = add_kernel_pdl(g, n0, (void*)sweep, sweep_grid, sweep_smem, asw, kSwThreads, pm & 1);
@@ -319,7 +328,8 @@ struct Impl final : ImplBase {
 
     void launch_eval_graph(Context& c, bool want_grad) {
         cuda_check(cudaGraphLaunch(eval_graph(c, want_grad), c.stream), "graph launch (eval)");
-        c.launches += use_sweep ? 3 : (fuse_gather ? 5 : 6);  // ctrl, [sweep | out_fwd, elem, [gather,] vjp], ctrl
+        if (!want_grad && !use_sweep) c.launches += 3;  // ctrl, out_fwd, elem
+        else c.launches += use_sweep ? 3 : (fuse_gather ? 5 : 6);  // ctrl, [sweep | out_fwd, elem, [gather,] vjp], ctrl
     }
 
     int eval_timed(Context& c, cudaEvent_t* ev, bool want_grad) override {
