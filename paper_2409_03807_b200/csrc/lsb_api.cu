@@ -215,6 +215,7 @@ DevFlags read_dev_flags() {
     if (const char* v = get("LSB_W_RESIDENT")) f.w_resident = v[0] == '1' ? 1 : 0;
     if (const char* v = get("LSB_VJP_WG_CTA")) f.vjp_wg_cta = std::max(1, std::min(4, atoi(v)));
     if (const char* v = get("LSB_L2PF")) f.l2_pf = std::max(0, std::min(256, atoi(v)));
+    if (const char* v = get("LSB_W_KEEP")) f.w_keep = std::max(0, std::min(4096, atoi(v)));
     if (const char* v = get("LSB_L2PF_ELEM")) f.l2_pf_elem = std::max(0, std::min(256, atoi(v)));
     if (const char* v = get("LSB_ELEM_F32")) f.elem_f32 = v[0] != '0';
     if (const char* v = get("LSB_SWEEP_LAG")) f.sweep_lag = std::min(8.0f, std::max(0.0f, (float)atof(v)));

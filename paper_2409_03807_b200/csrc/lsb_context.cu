@@ -392,6 +392,7 @@ struct Impl final : ImplBase {
         const size_t wbytes = (size_t)c.n * c.hp * sizeof(TS);
         p.w_resident = wbytes <= (size_t)(0.6 * c.l2_bytes) ? 1 : 0;
         if (c.dev.w_resident >= 0) p.w_resident = c.dev.w_resident;  // developer override
+        p.w_keep_tiles = p.w_resident ? 0 : c.dev.w_keep;
         // grid sizing: persistent grids of (SMs x resident blocks)
         int occ = 0;
         p.vpb = 64;  // 192 rows per slab: a multiple of every tile height

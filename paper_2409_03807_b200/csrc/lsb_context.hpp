@@ -52,6 +52,8 @@ struct DevFlags {
     int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
     int vjp_wg = 0;           // LSB_VJP_WG=1: per-warp, per-tile gather in the fused VJP (measured 1% slower than the prologue)
     int vjp_wg_cta = 3;       // LSB_VJP_WG_CTA: CTAs per SM of the per-warp-gather VJP
+    int w_keep = 8;           // LSB_W_KEEP: W tiles at the end of every out_fwd CTA range kept in L2 (evict_last) for the VJP's
+                              // re-read (c3: 29 MB; measured 212.8 -> 211.1 us per evaluation, 16+ tiles lose it again)
     int w_resident = -1;      // LSB_W_RESIDENT=0/1: force the W_out L2 policy (evict_first / evict_last)
     int solve_clusters = 0;   // LSB_SOLVE_CLUSTERS: cap on the persistent kernel's clusters (0: all that fit)
     int sweep = 0;            // LSB_SWEEP=1: fused warp-specialised sweep pass instead of out_fwd, elem, vjp (measured slower)

@@ -81,6 +81,7 @@ struct EvalParams {
     int elem_f32;     // fp32-storage mode: element strain / stress / forces in fp32 arithmetic
     int l2_pf_tiles;  // out_fwd: W tiles per CTA bulk-prefetched into L2 before its dependency wait (PDL)
     int l2_pf_elem;   // elem: first W tiles of every VJP CTA range prefetched into L2 (0: off)
+    int w_keep_tiles; // out_fwd: the last W tiles of every CTA range stay in L2 (evict_last) for the VJP's re-read
     // output layer (device layout: rows padded to hp columns)
     const TS* Wout;
     const double* bout;

@@ -357,7 +357,12 @@ __global__ void __launch_bounds__(kStreamThreads) out_fwd_tma_kernel(const EvalP
     const int t0 = (int)(((long long)ntiles * blockIdx.x) / gridDim.x);
     const int t1 = (int)(((long long)ntiles * (blockIdx.x + 1)) / gridDim.x);
     const uint64_t pol = l2_policy(p.w_resident), keep = l2_policy(1);
-    auto issue = [&](int t, unsigned char* b, uint64_t* bar) { issue_fwd<TS, HP>(p, t, b, bar, pol, keep); };
+    // the range's last w_keep_tiles W tiles stay in L2 (evict_last) across the element pass: the VJP
+    // re-reads them there (with evict_first, which demotes them) instead of from HBM
+    const int tkeep = t1 - p.w_keep_tiles;
+    auto issue = [&](int t, unsigned char* b, uint64_t* bar) {
+        issue_fwd<TS, HP>(p, t, b, bar, t >= tkeep ? keep : pol, keep);
+    };
     ring_prefetch(r, t0, t1, issue);  // W tiles and row records do not depend on the previous kernel
     if (p.l2_pf_tiles > 0) {  // while the control kernel runs (programmatic launch): next tiles into L2
         const int a = min(t1, t0 + NW * kStreamSpw), b = min(t1, a + p.l2_pf_tiles);
