@@ -1047,6 +1047,389 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
     }
 }
 
+// ---- Element Hessian contraction, edge-space form (default; elem_hess2_kernel is the A/B fallback)
+// For one (tet, point) the reduced Hessian block is a quadratic form in the EDGE differences of the
+// Jacobian columns, E[b][(e, a)] = J[v_{e+1}, a][b] - J[v_0, a][b] (R directions x 9):
+//     C_ab += sum_{kk, kk'} E[a][kk] H_E[kk][kk'] E[b][kk'],     H_E = Bd H_F Bd^T   (9 x 9, symmetric)
+// with Bd the block-diagonal Dm^-1 map (dF[a][c] = sum_e E[(e, a)] Dm^-1[e][c]) and
+//     H_F = vol (2 psi_I I + psi_J dcof/dF + 4 psi_II f f^T + lambda c c^T),  f = vec F, c = vec cof F
+// -- the same contraction as D^T M' above (alpha = 2 f.dF, beta = c.dF), regrouped so that everything
+// that depends on the direction is tensor-core work.  H_E is formed once per (tet, point) in fp32 by one
+// thread (batch phase: thread = (point, tet of the batch)) and stored as its upper triangle; then per
+// (tet, point) one warp runs two chained mma.sync m16n8k8 TF32 stages entirely in registers:
+//     X = E H_E        (A = E from the fp32 edge differences of the L2-prefetched Jacobian rows, B = H_E)
+//     C += E X^T       (A = E again; B = the accumulator fragments of X, reused directly: lane (g, t4) of
+//                       an accumulator holds columns 2 t4, 2 t4 + 1, so every stage orders its K index as
+//                       position t4 <-> kk = 2 t4, position t4 + 4 <-> kk = 2 t4 + 1 and no shuffle is needed)
+// Operands are rounded to TF32 to nearest (two integer ops); rounding is relative to the edge
+// differences and to H_E, never to the Jacobian rows themselves, so smooth (trained) decoders lose
+// nothing to cancellation.  Per-(tet, point) rounding errors (~3e-4) are independent and average out over
+// the mesh: config 5 agrees with the 3xTF32 kernel to ~1e-6 relative, against the 1e-4 bar.
+// Forces are accumulated per warp for its own points in tet order (deterministic).
+__device__ __forceinline__ uint32_t rn_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
+__device__ __forceinline__ void mma_tf32_u(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                           uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// N consecutive floats (N = 1, 2, 4; N-float aligned) through the read-only path
+template <int N>
+__device__ __forceinline__ void ldg_vec(float* o, const float* p) {
+    if constexpr (N == 1) {
+        o[0] = __ldg(p);
+    } else if constexpr (N == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = v.x;
+        o[1] = v.y;
+    } else {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x;
+        o[1] = v.y;
+        o[2] = v.z;
+        o[3] = v.w;
+    }
+}
+
+#ifndef LSB_H3_MINB
+#define LSB_H3_MINB 4
+#endif
+template <int R>
+__global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4* tets, const float* rec, const int* blk_tet0,
+                                                        const int* blk_vptr, const short* tet_loc,
+                                                        const int* blk_aptr, const int* blk_avert,
+                                                        const short* tet_aloc, const float* U, const float* Jv,
+                                                        int P, float* Cpart, float* gpart) {
+    constexpr int GP = 128 / R;               // points per CTA
+    constexpr int NPAIR = R * (R + 1) / 2;
+    constexpr int PPW = GP / 4;               // points per warp
+    constexpr int MT = R >= 16 ? R / 16 : 1;  // 16-row m tiles (R = 8: rows 8..15 are zero)
+    constexpr int NT = R / 8;                 // 8-column n tiles
+    constexpr int NR = R >= 16 ? R / 8 : 1;   // 8-direction row groups a lane loads
+    constexpr int HS = 60;  // floats per (tet, point) record: H_E upper triangle 45 (tf32), pad 3, forces 12
+    __shared__ __align__(16) float sh_h[128][HS];    // [point * R + tet of the batch]: consecutive lanes of the batch
+                                                     // phase write consecutive records (60-word stride: conflict-free)
+    __shared__ __align__(16) float sh_rec[kTB][12];  // the block's records
+    __shared__ int sh_off[kTB][8];  // accg offsets of the free slots (pinned -> scratch slot nv) (4), Us offsets (4)
+    __shared__ int4 sh_tq[kTB];     // the block's vertex ids
+    extern __shared__ __align__(16) float dyn[];
+    const int tid = threadIdx.x;
+    const int pl = tid / R, tb = tid % R;
+    const int p0 = blockIdx.y * GP;
+    const int blk = blockIdx.x;
+    const int e0 = blk_tet0[blk], ne = blk_tet0[blk + 1] - e0;
+    const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
+    const int a0 = blk_aptr[blk], nva = blk_aptr[blk + 1] - a0;
+    float* Us = dyn;                            // [nva][3][GP]
+    float* accg = Us + (size_t)nva * 3 * GP;    // [nv + 1][3][GP]
+    static_assert(GP % 4 == 0, "16-byte staging of U");
+    for (int i = tid; i < nva * 3 * (GP / 4); i += 128) {
+        const int vcl = i / (GP / 4), k4 = i % (GP / 4);
+        const int va = __ldg(blk_avert + a0 + vcl / 3), c = vcl % 3;
+        cp_async16(Us + (size_t)vcl * GP + 4 * k4, U + ((size_t)va * 3 + c) * P + p0 + 4 * k4);
+    }
+    for (int i = tid; i < (nv + 1) * 3 * GP; i += 128) accg[i] = 0.f;
+    for (int i = tid; i < ne * 12; i += 128) sh_rec[i / 12][i % 12] = rec[(size_t)e0 * 12 + i];
+    for (int i = tid; i < ne * 4; i += 128) {
+        const int lv = tet_loc[(size_t)e0 * 4 + i];
+        sh_off[i >> 2][i & 3] = (lv >= 0 ? lv : nv) * 3 * GP;
+        sh_off[i >> 2][4 + (i & 3)] = tet_aloc[(size_t)e0 * 4 + i] * 3 * GP;
+    }
+    for (int i = tid; i < ne; i += 128) sh_tq[i] = __ldg(tets + e0 + i);
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+    float cacc[PPW][MT][NT][4];
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) cacc[pp][mt][nt][q] = 0.f;
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- lane constants of the tensor-core phase
+    // K slots of this lane: kk = 2 t4, 2 t4 + 1 and (t4 == 0 only) kk = 8; kk = 3 e + a (edge e, component a)
+    const int kks[3] = {2 * t4, 2 * t4 + 1, 8};
+    const size_t PR = (size_t)P * R;
+    const float* jb[3];   // Jv + a PR + (first point of the warp) R + g
+    int esel[3];
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        esel[s] = 1 + kks[s] / 3;
+        jb[s] = Jv + (size_t)(kks[s] % 3) * PR + (size_t)(p0 + warp * PPW) * R + g * NR;
+    }
+    const unsigned vstrideB = 3u * (unsigned)PR * (unsigned)sizeof(float);  // bytes per vertex of Jv
+    const bool slot2 = t4 == 0;
+    // H_E upper-triangle offsets of this lane's B fragments
+    auto tri = [](int i, int j) {
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        return lo * 9 - lo * (lo - 1) / 2 + (hi - lo);
+    };
+    const int hb00 = tri(kks[0], g), hb01 = tri(kks[1], g);  // n tile 0 (n = g), k step 0
+    const int hb10 = tri(kks[0], 8), hb11 = tri(kks[1], 8);  // n tile 1 (n = 8: g == 0 only), k step 0
+    const int hb20 = tri(8, g);                              // n tile 0, k step 1 (t4 == 0 only)
+    const bool n8 = g == 0;
+    bool livep[PPW];
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp) livep[pp] = p0 + warp * PPW + pp < P;
+    // raw Jacobian entries of one tet for this lane: [point][slot][vertex e + 1 / vertex 0][row group]
+    float rawA[PPW][3][2][NR], rawB[PPW][3][2][NR];
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp)
+#pragma unroll
+        for (int s = 0; s < 3; ++s)
+#pragma unroll
+            for (int w = 0; w < 2; ++w)
+#pragma unroll
+                for (int q = 0; q < NR; ++q) rawA[pp][s][w][q] = rawB[pp][s][w][q] = 0.f;
+    auto load_raw = [&](float (&raw)[PPW][3][2][NR], int el) {
+        const int* tq = reinterpret_cast<const int*>(sh_tq + el);
+        const unsigned vz = (unsigned)tq[0];
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            if (s == 2 && !slot2) continue;
+            const unsigned vh = (unsigned)tq[esel[s]];
+            const float* ph = reinterpret_cast<const float*>(reinterpret_cast<const char*>(jb[s]) + (unsigned long long)vh * vstrideB);
+            const float* pz = reinterpret_cast<const float*>(reinterpret_cast<const char*>(jb[s]) + (unsigned long long)vz * vstrideB);
+#pragma unroll
+            for (int pp = 0; pp < PPW; ++pp) {
+                if (!livep[pp]) continue;
+                ldg_vec<NR>(raw[pp][s][0], ph + pp * R);
+                ldg_vec<NR>(raw[pp][s][1], pz + pp * R);
+            }
+        }
+    };
+    auto process = [&](const float (&raw)[PPW][3][2][NR], int el, int tbl) {
+        // forces of this tet: lanes own (point of the warp, local dof), tet order
+        for (int i = lane; i < 12 * PPW; i += 32) {
+            const int pp = i / 12, d = i % 12, pc = warp * PPW + pp;
+            if (p0 + pc < P) accg[sh_off[el][d / 3] + (d % 3) * GP + pc] += sh_h[pc * R + tbl][48 + d];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pp = 0; pp < PPW; ++pp) {  // points beyond P run on zero Jacobian entries; their block is never stored
+            const float* hr = sh_h[(warp * PPW + pp) * R + tbl];
+            // B fragments of H_E (already tf32)
+            const uint32_t b00 = __float_as_uint(hr[hb00]), b01 = __float_as_uint(hr[hb01]);
+            const uint32_t b10 = n8 ? __float_as_uint(hr[hb10]) : 0u, b11 = n8 ? __float_as_uint(hr[hb11]) : 0u;
+            const uint32_t b20 = slot2 ? __float_as_uint(hr[hb20]) : 0u;
+            const uint32_t b30 = (slot2 && n8) ? __float_as_uint(hr[44]) : 0u;
+            uint32_t ea[MT][6];  // k step 0: a0..a3, k step 1: a0, a1
+            float X[MT][2][4];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int q0 = R >= 16 ? 2 * mt : 0;
+                ea[mt][0] = rn_tf32(raw[pp][0][0][q0] - raw[pp][0][1][q0]);
+                ea[mt][2] = rn_tf32(raw[pp][1][0][q0] - raw[pp][1][1][q0]);
+                ea[mt][4] = rn_tf32(raw[pp][2][0][q0] - raw[pp][2][1][q0]);
+                if (R >= 16) {
+                    ea[mt][1] = rn_tf32(raw[pp][0][0][NR > 1 ? q0 + 1 : 0] - raw[pp][0][1][NR > 1 ? q0 + 1 : 0]);
+                    ea[mt][3] = rn_tf32(raw[pp][1][0][NR > 1 ? q0 + 1 : 0] - raw[pp][1][1][NR > 1 ? q0 + 1 : 0]);
+                    ea[mt][5] = rn_tf32(raw[pp][2][0][NR > 1 ? q0 + 1 : 0] - raw[pp][2][1][NR > 1 ? q0 + 1 : 0]);
+                } else {
+                    ea[mt][1] = ea[mt][3] = ea[mt][5] = 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) X[mt][0][q] = X[mt][1][q] = 0.f;
+                // X = E H_E: n tile 0 (kk' 0..7), n tile 1 (kk' = 8)
+                mma_tf32_u(X[mt][0], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], b00, b01);
+                mma_tf32_u(X[mt][0], ea[mt][4], ea[mt][5], 0u, 0u, b20, 0u);
+                mma_tf32_u(X[mt][1], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], b10, b11);
+                mma_tf32_u(X[mt][1], ea[mt][4], ea[mt][5], 0u, 0u, b30, 0u);
+            }
+            // C += E X^T: n tile j = directions 8 j + g = rows of X (m tile j / 2, half j % 2)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int mj = j >> 1, hj = (j & 1) * 2;
+                const uint32_t x0 = rn_tf32(X[mj][0][hj]), x1 = rn_tf32(X[mj][0][hj + 1]);
+                const uint32_t x2 = rn_tf32(X[mj][1][hj]);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    mma_tf32_u(cacc[pp][mt][j], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], x0, x1);
+                    mma_tf32_u(cacc[pp][mt][j], ea[mt][4], ea[mt][5], 0u, 0u, x2, 0u);
+                }
+            }
+        }
+    };
+    if (ne > 0) load_raw(rawA, 0);
+    for (int eb = 0; eb < ne; eb += R) {
+        __syncthreads();  // the previous batch's records are no longer read
+        // ---- batch phase: thread (pl, tb) forms H_E and the forces of tet eb + tb at point pl
+        {
+            const int el = eb + tb;
+            if (p0 + pl < P && el < ne) {
+                float rc[12], uu[12];
+#pragma unroll
+                for (int qq = 0; qq < 12; ++qq) rc[qq] = sh_rec[el][qq];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int uo = sh_off[el][4 + k] + pl;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) uu[k * 3 + a] = Us[uo + a * GP];
+                }
+                float A[9];
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int c2 = 0; c2 < 3; ++c2)
+                        A[a * 3 + c2] = (uu[3 + a] - uu[a]) * rc[c2] + (uu[6 + a] - uu[a]) * rc[3 + c2] +
+                                        (uu[9 + a] - uu[a]) * rc[6 + c2];
+                float F[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) F[k] = A[k] + ((k % 4) == 0 ? 1.f : 0.f);
+                float cof[9];
+                cof[0] = F[4] * F[8] - F[7] * F[5];
+                cof[3] = F[7] * F[2] - F[1] * F[8];
+                cof[6] = F[1] * F[5] - F[4] * F[2];
+                cof[1] = F[5] * F[6] - F[8] * F[3];
+                cof[4] = F[8] * F[0] - F[2] * F[6];
+                cof[7] = F[2] * F[3] - F[5] * F[0];
+                cof[2] = F[3] * F[7] - F[6] * F[4];
+                cof[5] = F[6] * F[1] - F[0] * F[7];
+                cof[8] = F[0] * F[4] - F[3] * F[1];
+                const float vol = rc[9], mu = rc[10], lam = rc[11];
+                const float trA = A[0] + A[4] + A[8];
+                float q = 0.f;
+#pragma unroll
+                for (int k = 0; k < 9; ++k) q += A[k] * A[k];
+                const float m2 = A[0] * A[4] - A[1] * A[3] + A[0] * A[8] - A[2] * A[6] + A[4] * A[8] - A[5] * A[7];
+                const float detA = A[0] * (A[4] * A[8] - A[7] * A[5]) - A[3] * (A[1] * A[8] - A[7] * A[2]) +
+                                   A[6] * (A[1] * A[5] - A[4] * A[2]);
+                const float jm1 = trA + m2 + detA;
+                const float uI = 4.f + 2.f * trA + q;  // I + 1
+                const float inv_uI = 1.f / uI;
+                float* o = sh_h[pl * R + tb];
+                // elastic forces vol B^T P (cancellation-free first Piola stress)
+                float cA[9];
+                cA[0] = A[4] * A[8] - A[7] * A[5];
+                cA[3] = A[7] * A[2] - A[1] * A[8];
+                cA[6] = A[1] * A[5] - A[4] * A[2];
+                cA[1] = A[5] * A[6] - A[8] * A[3];
+                cA[4] = A[8] * A[0] - A[2] * A[6];
+                cA[7] = A[2] * A[3] - A[5] * A[0];
+                cA[2] = A[3] * A[7] - A[6] * A[4];
+                cA[5] = A[6] * A[1] - A[0] * A[7];
+                cA[8] = A[0] * A[4] - A[3] * A[1];
+                const float c1 = 0.75f * mu, c2 = mu * (2.f * trA + q) * 0.25f * inv_uI, c3 = lam * jm1;
+                float fo[12];
+#pragma unroll
+                for (int aa = 0; aa < 3; ++aa) {
+                    float Pa[3];
+#pragma unroll
+                    for (int bb = 0; bb < 3; ++bb) {
+                        const float id = aa == bb ? 1.f : 0.f;
+                        Pa[bb] = c1 * (A[aa * 3 + bb] + A[bb * 3 + aa] - trA * id - cA[aa * 3 + bb]) +
+                                 c2 * F[aa * 3 + bb] + c3 * cof[aa * 3 + bb];
+                    }
+                    float hc[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        hc[c] = vol * (Pa[0] * rc[c * 3 + 0] + Pa[1] * rc[c * 3 + 1] + Pa[2] * rc[c * 3 + 2]);
+                    float s0 = 0.f;
+                    s0 += hc[0];
+                    s0 += hc[1];
+                    s0 += hc[2];
+                    fo[aa] = -s0;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) fo[(c + 1) * 3 + aa] = hc[c];
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    reinterpret_cast<float4*>(o + 48)[k] = make_float4(fo[4 * k], fo[4 * k + 1], fo[4 * k + 2], fo[4 * k + 3]);
+                // edge-space Hessian H_E[(e, a)][(e', a')], index 3 e + a, upper triangle
+                const float k1 = 2.f * vol * (0.5f * mu * (1.f - inv_uI));   // 2 vol psi_I
+                const float k2 = vol * (lam * jm1 - 0.75f * mu);              // vol psi_J
+                const float k3 = 4.f * vol * (0.5f * mu * inv_uI * inv_uI);   // 4 vol psi_II
+                const float k4 = vol * lam;
+                float Fe[9], Ce[9], Fs[9], Cs[9];  // [a][e]
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int e = 0; e < 3; ++e) {
+                        Fe[a * 3 + e] = F[a * 3] * rc[e * 3] + F[a * 3 + 1] * rc[e * 3 + 1] + F[a * 3 + 2] * rc[e * 3 + 2];
+                        Ce[a * 3 + e] = cof[a * 3] * rc[e * 3] + cof[a * 3 + 1] * rc[e * 3 + 1] + cof[a * 3 + 2] * rc[e * 3 + 2];
+                        Fs[a * 3 + e] = k3 * Fe[a * 3 + e];
+                        Cs[a * 3 + e] = k4 * Ce[a * 3 + e];
+                    }
+                float Gm[9];  // k1 Dm^-1 Dm^-T
+#pragma unroll
+                for (int e = 0; e < 3; ++e)
+#pragma unroll
+                    for (int f = 0; f < 3; ++f)
+                        Gm[e * 3 + f] = k1 * (rc[e * 3] * rc[f * 3] + rc[e * 3 + 1] * rc[f * 3 + 1] + rc[e * 3 + 2] * rc[f * 3 + 2]);
+                // Sx[t][pair] = k2 F[t][:] . (row e x row e') of Dm^-1, pairs (0,1), (0,2), (1,2)
+                float Sx[9];
+#pragma unroll
+                for (int pq = 0; pq < 3; ++pq) {
+                    const int e = pq == 2 ? 1 : 0, f = pq == 0 ? 1 : 2;
+                    const float x0 = rc[e * 3 + 1] * rc[f * 3 + 2] - rc[e * 3 + 2] * rc[f * 3 + 1];
+                    const float x1 = rc[e * 3 + 2] * rc[f * 3 + 0] - rc[e * 3 + 0] * rc[f * 3 + 2];
+                    const float x2 = rc[e * 3 + 0] * rc[f * 3 + 1] - rc[e * 3 + 1] * rc[f * 3 + 0];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) Sx[t * 3 + pq] = k2 * (F[t * 3] * x0 + F[t * 3 + 1] * x1 + F[t * 3 + 2] * x2);
+                }
+                float H[48];
+#pragma unroll
+                for (int i = 0; i < 9; ++i) {
+                    const int e = i / 3, a = i % 3;
+#pragma unroll
+                    for (int j = i; j < 9; ++j) {
+                        const int f = j / 3, b = j % 3;
+                        float v = Fs[a * 3 + e] * Fe[b * 3 + f] + Cs[a * 3 + e] * Ce[b * 3 + f];
+                        if (a == b) {
+                            v += Gm[e * 3 + f];
+                        } else if (e != f) {
+                            const int t = 3 - a - b;
+                            const float sx = Sx[t * 3 + (e + f - 1)];
+                            v = ((b - a + 3) % 3 == 1) ? v + sx : v - sx;
+                        }
+                        H[i * 9 - i * (i - 1) / 2 + (j - i)] = __uint_as_float(rn_tf32(v));
+                    }
+                }
+                H[45] = H[46] = H[47] = 0.f;
+#pragma unroll
+                for (int k = 0; k < 12; ++k)
+                    reinterpret_cast<float4*>(o)[k] = make_float4(H[4 * k], H[4 * k + 1], H[4 * k + 2], H[4 * k + 3]);
+            }
+        }
+        __syncthreads();
+        const int nbt = min(R, ne - eb);
+        for (int t2 = 0; t2 < nbt; t2 += 2) {
+            const int el = eb + t2;
+            if (el + 1 < ne) load_raw(rawB, el + 1);
+            process(rawA, el, t2);
+            if (t2 + 1 < nbt) {
+                if (el + 2 < ne) load_raw(rawA, el + 2);
+                process(rawB, el + 1, t2 + 1);
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int pp = 0; pp < PPW; ++pp) {
+        const int pc = warp * PPW + pp;
+        if (p0 + pc >= P) continue;
+        float* Co = Cpart + ((size_t)blk * P + p0 + pc) * NPAIR;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    // tile position 8 q + g holds direction g NR + q (the lanes load NR consecutive directions)
+                    const int ap = mt * 16 + g + (q >= 2 ? 8 : 0), bp = nt * 8 + 2 * t4 + (q & 1);
+                    const int a = (ap & 7) * NR + (ap >> 3), bb = (bp & 7) * NR + (bp >> 3);
+                    if (ap < R && a <= bb) Co[a * R - a * (a - 1) / 2 + (bb - a)] = cacc[pp][mt][nt][q];
+                }
+    }
+    for (int i = tid; i < nv * 3 * GP; i += 128) {
+        const int pp = i % GP;
+        if (p0 + pp < P) gpart[((size_t)(v0 * 3) + i / GP) * P + p0 + pp] = accg[i];
+    }
+}
+
 // C[p][pair] = sum over blocks (fixed order, fp64): CTA per 32 (p, pair) entries,
 // 8 warps stride the blocks, fixed combine order.
 __global__ void __launch_bounds__(256) hess_reduce_kernel(int nblk, int P, int npair, const float* Cpart, double* C) {
@@ -1554,6 +1937,9 @@ struct BatchedEngine : BatchedBase {
         if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess3_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess3_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
+        if (r == 32) cuda_check(cudaFuncSetAttribute(elem_hess3_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         hess_ready = true;
     }
 
@@ -1784,7 +2170,19 @@ struct BatchedEngine : BatchedBase {
             const size_t gsmem = hess_smem(r);
             const float* recf = static_cast<const float*>(rec_f32(c));
             const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
-            if (r == 8)
+            if (c.dev.hess3) {  // edge-space form: two chained TF32 MMA stages per (tet, point)
+                if (r == 8)
+                    elem_hess3_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
+                                                             d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
+                else if (r == 16)
+                    elem_hess3_kernel<16><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc,
+                                                              d_blk_aptr, d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P,
+                                                              d_Cpart, d_gpart);
+                else
+                    elem_hess3_kernel<32><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc,
+                                                              d_blk_aptr, d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P,
+                                                              d_Cpart, d_gpart);
+            } else if (r == 8)
                 elem_hess2_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                          d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);
             else if (r == 16)
