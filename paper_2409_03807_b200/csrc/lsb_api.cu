@@ -596,6 +596,7 @@ lsb_status lsb_set_pin_positions(lsb_context* ctx, const double* pin_positions) 
         Context& c = ctx->c;
         sync(c);
         c.pin_positions.assign(pin_positions, pin_positions + 3 * (size_t)c.mesh.V);
+        ++c.pins_version;
         upload_pins(c);
     });
 }

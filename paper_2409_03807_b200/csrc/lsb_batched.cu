@@ -595,6 +595,18 @@ __global__ void tangent_pack_kernel(int h, int P, int r, int cols, const float* 
     }
 }
 
+// Pinned rows of the chunk buffers for chunks of P points: U = pin displacement, J = 0.
+__global__ void pinned_rows_kernel(int np, int P, int r, const int* pin_v, const float* pin_d, float* U, float* Jv) {
+    const size_t total = (size_t)np * 3 * P;
+    for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / (3 * (size_t)P)), k = (int)((idx / P) % 3), p = (int)(idx % P);
+        const size_t row = ((size_t)pin_v[i] * 3 + k) * P + p;
+        U[row] = pin_d[3 * i + k];
+        if (Jv)
+            for (int a = 0; a < r; ++a) Jv[row * r + a] = 0.f;
+    }
+}
+
 // u -> U[v][3][P]; J_ia = s_i C_ia -> Jv[v][3][P][r] (pinned rows: pin displacement, zero J).
 // With inertia (objective Hessian): rin[row][p] = m (u - (qbar - X)) / h^2, the inertia part
 // of the full-space residual whose contraction with the decoder curvature enters H.
@@ -1521,7 +1533,12 @@ struct BatchedEngine : BatchedBase {
     std::vector<void*> allocs;
     TcGemm tc;  // tcgen05 GEMM engine (lsb_tc.cuh)
     // second order (config 5)
-    static constexpr int PH = 64;  // points per Hessian chunk
+    static constexpr int PH = 64;  // points per chunk of the theta-gradient path (and the minimum allocation width)
+    int PHmax = PH;                // allocation width of the Hessian buffers: up to 256 points per chunk when they fit
+    int Pcur = 0;                  // chunk width the pinned rows of d_Uh / d_Jv are laid out for
+    int* d_pin_v = nullptr;        // pinned vertex ids and pin displacements (upload_pin_rows)
+    float* d_pin_d = nullptr;
+    int pins_uploaded = -1, pins_hess = -1, pins_eval = 0;  // Context::pins_version last applied
     bool hess_ready = false;
     float *d_Whf = nullptr;  // hidden weights fp32 (concatenated, row-major)
     float *d_Xl[kMaxLayers + 1] = {}, *d_Ql[kMaxLayers] = {}, *d_Bt = nullptr, *d_Ct = nullptr, *d_Uh = nullptr, *d_Jv = nullptr;
@@ -1756,6 +1773,7 @@ struct BatchedEngine : BatchedBase {
                 for (int b = 0; b < BC; ++b) U0[((size_t)v * 3 + k) * BC + b] = d;
             }
         c.copy(d_U, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "U pins");
+        pins_eval = c.pins_version;
         esmem2 = (size_t)(eb.max_nv + 1) * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) +
                  kTB * 4 * sizeof(int) + kTB * 4 * sizeof(int);
         esmem_f2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float2) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
@@ -1779,6 +1797,13 @@ struct BatchedEngine : BatchedBase {
         cudaStream_t s = c.stream;
         const int n = c.n, h = c.h, r = c.r;
         const int Np = (N + BC - 1) / BC * BC;  // padded to whole chunks (zero columns)
+        if (pins_eval != c.pins_version) {  // lsb_set_pin_positions since the last call: pinned rows of U
+            upload_pin_rows(c);
+            const int np = (int)c.mesh.pinned.size();
+            if (np) pinned_rows_kernel<<<c.num_sms * 4, 256, 0, s>>>(np, BC, 0, d_pin_v, d_pin_d, d_U, nullptr);
+            cuda_check(cudaGetLastError(), "pinned rows");
+            pins_eval = c.pins_version;
+        }
         DevState* hs = c.h_state;
         cuda_check(cudaMemcpyAsync(hs, c.d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s), "state");
         cuda_check(cudaStreamSynchronize(s), "sync");
@@ -1909,30 +1934,30 @@ struct BatchedEngine : BatchedBase {
             }
             cuda_check(cudaGetLastError(), "pack hidden");
         }
-        for (int l = 0; l <= c.nhid; ++l) d_Xl[l] = alloc<float>((size_t)hmax * PH * hcols);
-        for (int l = 0; l < c.nhid; ++l) d_Ql[l] = alloc<float>((size_t)hmax * PH * hcols);
-        d_Bt = alloc<float>((size_t)h * PH * (1 + r));
-        d_Ct = alloc<float>((size_t)n * PH * (1 + r));
-        d_Uh = alloc<float>((size_t)c.mesh.V * 3 * PH);
-        d_Jv = alloc<float>((size_t)c.mesh.V * 3 * PH * r);
-        d_Cpart = alloc<float>((size_t)nblk * PH * npair);
-        d_rinh = alloc<float>((size_t)c.n * PH);
-        d_gpart = alloc<float>((size_t)nslots * 3 * PH);
-        d_Th = alloc<float>((size_t)n * PH);
-        d_Yh = alloc<float>((size_t)h * PH);
-        d_Ph = alloc<float>((size_t)nk * h * PH);
-        d_Zh = alloc<float>((size_t)r * PH);
-        d_Ch = alloc<double>((size_t)PH * npair);
-        d_H = alloc<double>((size_t)PH * r * r);
-        // pinned rows: pin displacement in U, zero J
-        std::vector<float> U0((size_t)c.mesh.V * 3 * PH, 0.f);
-        for (int v : c.mesh.pinned)
-            for (int k = 0; k < 3; ++k) {
-                const float d = (float)(c.pin_positions[3 * (size_t)v + k] - c.mesh.X[3 * (size_t)v + k]);
-                for (int p = 0; p < PH; ++p) U0[((size_t)v * 3 + k) * PH + p] = d;
-            }
-        c.copy(d_Uh, U0.data(), 4 * U0.size(), cudaMemcpyHostToDevice, "Uh");
-        cuda_check(cudaMemsetAsync(d_Jv, 0, 4 * (size_t)c.mesh.V * 3 * PH * r, c.stream), "Jv");
+        // chunk width: wide chunks amortise the small hidden-layer GEMMs and launches (config 5: 64 -> 256
+        // points per chunk); bounded by ~4 GB of chunk buffers (a config-3-sized mesh stays at 64)
+        {
+            const double per_point = 4.0 * ((double)n * (3 + r) + (double)c.mesh.V * 3 * (1 + r) + (double)nblk * npair +
+                                            (double)hmax * hcols * (2 * c.nhid + 1));
+            PHmax = PH;
+            while (PHmax < 256 && per_point * (2 * PHmax) <= 4.0e9) PHmax *= 2;
+        }
+        for (int l = 0; l <= c.nhid; ++l) d_Xl[l] = alloc<float>((size_t)hmax * PHmax * hcols);
+        for (int l = 0; l < c.nhid; ++l) d_Ql[l] = alloc<float>((size_t)hmax * PHmax * hcols);
+        d_Bt = alloc<float>((size_t)h * PHmax * (1 + r));
+        d_Ct = alloc<float>((size_t)n * PHmax * (1 + r));
+        d_Uh = alloc<float>((size_t)c.mesh.V * 3 * PHmax);
+        d_Jv = alloc<float>((size_t)c.mesh.V * 3 * PHmax * r);
+        d_Cpart = alloc<float>((size_t)nblk * PHmax * npair);
+        d_rinh = alloc<float>((size_t)c.n * PHmax);
+        d_gpart = alloc<float>((size_t)nslots * 3 * PHmax);
+        d_Th = alloc<float>((size_t)n * PHmax);
+        d_Yh = alloc<float>((size_t)h * PHmax);
+        d_Ph = alloc<float>((size_t)nk * h * PHmax);
+        d_Zh = alloc<float>((size_t)r * PHmax);
+        d_Ch = alloc<double>((size_t)PHmax * npair);
+        d_H = alloc<double>((size_t)PHmax * r * r);
+        Pcur = 0;  // pinned rows of U (pin displacement) and J (zero) are laid out per chunk width: prepare_width
         const size_t gsmem = hess_smem(r);
         if (r == 8) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
         if (r == 16) cuda_check(cudaFuncSetAttribute(elem_hess2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem), "smem");
@@ -2116,6 +2141,44 @@ struct BatchedEngine : BatchedBase {
         c.batched_launches += 12 + 5 * c.nhid;
     }
 
+    // Lay the constant rows of the chunk buffers out for chunks of P points: pinned rows hold the pin
+    // displacement in U and zero in J (tangent_out_kernel writes the free rows only).
+    // device copies of the pinned vertex ids and pin displacements (current pins_version)
+    void upload_pin_rows(Context& c) {
+        if (pins_uploaded == c.pins_version) return;
+        const size_t np = c.mesh.pinned.size();
+        std::vector<int> pv(c.mesh.pinned.begin(), c.mesh.pinned.end());
+        std::vector<float> pd(3 * np);
+        for (size_t i = 0; i < np; ++i)
+            for (int k = 0; k < 3; ++k)
+                pd[3 * i + k] = (float)(c.pin_positions[3 * (size_t)pv[i] + k] - c.mesh.X[3 * (size_t)pv[i] + k]);
+        if (!d_pin_v) {
+            d_pin_v = alloc<int>(std::max<size_t>(1, np));
+            d_pin_d = alloc<float>(std::max<size_t>(1, 3 * np));
+        }
+        if (np) {
+            c.copy(d_pin_v, pv.data(), 4 * np, cudaMemcpyHostToDevice, "pinned ids");
+            c.copy(d_pin_d, pd.data(), 12 * np, cudaMemcpyHostToDevice, "pin displacements");
+        }
+        pins_uploaded = c.pins_version;
+    }
+    void prepare_width(Context& c, int P) {
+        if (P == Pcur && pins_hess == c.pins_version) return;
+        if (P > PHmax || P % 16 != 0) throw LsbError(LSB_EINVAL, "hessian: bad chunk width");
+        // only the pinned rows are constant (tangent_out_kernel rewrites every free row of a chunk)
+        upload_pin_rows(c);
+        const int np = (int)c.mesh.pinned.size();
+        if (np) pinned_rows_kernel<<<c.num_sms * 4, 256, 0, c.stream>>>(np, P, c.r, d_pin_v, d_pin_d, d_Uh, d_Jv);
+        cuda_check(cudaGetLastError(), "pinned rows");
+        Pcur = P;
+        pins_hess = c.pins_version;
+    }
+    // chunk width for a call over `total` points
+    int pick_width(Context& c, int total) {
+        if (!hess_ready) init_hessian(c);
+        return std::min(PHmax, std::max(16, (total + 15) / 16 * 16));
+    }
+
     size_t hess_smem(int r) const {
         const int gp = 128 / r;
         return ((size_t)max_nva * 3 * gp + (size_t)(max_nv + 1) * 3 * gp) * sizeof(float) + 64;  // Us + accg (elem_hess2)
@@ -2125,8 +2188,9 @@ struct BatchedEngine : BatchedBase {
     // Hout_dev (device, N x r x r) instead of Hout: no host copy and no stream synchronisation, so
     // consecutive chunks queue back to back.
     void run_hessian_chunk(Context& c, int N, const double* Z, double* Hout, bool with_inertia = false,
-                           double* Hout_dev = nullptr) {
+                           double* Hout_dev = nullptr, int Pw = PH) {
         if (!hess_ready) init_hessian(c);
+        prepare_width(c, Pw);
         cudaStream_t s = c.stream;
         int inertia = 0;
         double inv_dt2 = 0.0;
@@ -2137,7 +2201,7 @@ struct BatchedEngine : BatchedBase {
             inertia = hs->has_inertia;
             inv_dt2 = hs->inv_dt2;
         }
-        const int r = c.r, h = c.h, n = c.n, P = PH, cols = hcols, npair = r * (r + 1) / 2;
+        const int r = c.r, h = c.h, n = c.n, P = Pw, cols = hcols, npair = r * (r + 1) / 2;
         std::vector<float> zt((size_t)r * P, 0.f);
         for (int p = 0; p < N; ++p)
             for (int k = 0; k < r; ++k) zt[(size_t)k * P + p] = (float)Z[(size_t)p * r + k];
@@ -2279,9 +2343,10 @@ void batched_eval(Context& c, int B, const double* Z, double* E, double* G) {
 void batched_objective_hessian(Context& c, int B, const double* Z, double* H) {
     BatchedEngine& eng = engine(c);
     const int r = c.r;
-    for (int b0 = 0; b0 < B; b0 += BatchedEngine::PH) {
-        const int N = std::min(BatchedEngine::PH, B - b0);
-        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, H + (size_t)b0 * r * r, true);
+    const int W = eng.pick_width(c, B);
+    for (int b0 = 0; b0 < B; b0 += W) {
+        const int N = std::min(W, B - b0);
+        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, H + (size_t)b0 * r * r, true, nullptr, W);
     }
 }
 
@@ -2290,9 +2355,10 @@ void batched_hessian(Context& c, int B, const double* Z, double* H) {
     const int r = c.r;
     // all chunks write into one device buffer; a single copy and synchronisation at the end
     double* d_all = eng.hess_all(c, (size_t)B * r * r);
-    for (int b0 = 0; b0 < B; b0 += BatchedEngine::PH) {
-        const int N = std::min(BatchedEngine::PH, B - b0);
-        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r);
+    const int W = eng.pick_width(c, B);
+    for (int b0 = 0; b0 < B; b0 += W) {
+        const int N = std::min(W, B - b0);
+        eng.run_hessian_chunk(c, N, Z + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r, W);
     }
     c.copy(H, d_all, 8 * (size_t)B * r * r, cudaMemcpyDeviceToHost, "hessians");
 }
@@ -2310,9 +2376,10 @@ double lipschitz_loss(Context& c, int P, const double* Z1, const double* Z2) {
     }
     double* d_all = eng.hess_all(c, 2 * (size_t)P * r * r + P);
     double* d_d2 = d_all + 2 * (size_t)P * r * r;
-    for (int b0 = 0; b0 < 2 * P; b0 += BatchedEngine::PH) {
-        const int N = std::min(BatchedEngine::PH, 2 * P - b0);
-        eng.run_hessian_chunk(c, N, Z.data() + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r);
+    const int W = eng.pick_width(c, 2 * P);  // a multiple of 16: both points of a pair share a chunk
+    for (int b0 = 0; b0 < 2 * P; b0 += W) {
+        const int N = std::min(W, 2 * P - b0);
+        eng.run_hessian_chunk(c, N, Z.data() + (size_t)b0 * r, nullptr, false, d_all + (size_t)b0 * r * r, W);
     }
     lipschitz_dldh_kernel<<<P, 256, 0, c.stream>>>(P, r, d_all, nullptr, nullptr, nullptr, d_d2);
     cuda_check(cudaGetLastError(), "pair losses");

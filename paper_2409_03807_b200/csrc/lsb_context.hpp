@@ -114,6 +114,7 @@ struct Context {
         hact[kMaxLayers] = {};
     // objective host mirror
     std::vector<double> pin_positions;  // V*3
+    int pins_version = 0;               // bumped by lsb_set_pin_positions: the batched engine re-lays its pinned rows
     bool has_qbar = false;
     double dt = 0.05;
 

@@ -60,3 +60,28 @@ def test_batched_tcgen05_matches_cuda_core_sgemm(product, monkeypatch):
     E0, G0 = out["0"]
     assert rel_err(E1, E0) < 1e-6
     assert rel_err(G1, G0) < 1e-5
+
+
+def test_pin_positions_set_after_batched_use(oracle, product):
+    """lsb_set_pin_positions after the batched and Hessian engines were built: their pinned rows of u
+    follow the new pins (the pins enter the energy through u, energy.cpp:155-157)."""
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    ob = oracle.problem("c1")
+    Z = configs.latent_batch_c4(pr.model.r, 12)
+    E0, _ = sysm.eval_batched(Z)          # engines built with the rest-position pins
+    sysm.hessian_batched(Z[:3])
+    pins = pr.mesh.vertices.copy()
+    pins[pr.mesh.pinned] += np.array([0.002, -0.001, 0.0015])
+    sysm.set_pin_positions(pins)
+    ob.set_pins(pins)
+    E, G = sysm.eval_batched(Z)
+    Eo, Go = ob.eval_batch(Z[:4], qbar=None)
+    assert rel_err(E[:4], Eo) < 1e-4 and rel_err(E0[:4], Eo) > 1e-3  # the pins moved the energy
+    assert max(rel_err(G[i], Go[i]) for i in range(4)) < 1e-4
+    H = sysm.hessian_batched(Z[:3])
+    for k in range(3):
+        assert rel_err(H[k], ob.reduced_potential_hessian(Z[k])) < 1e-4
+    e1, g1 = sysm.eval(Z[0])              # single-instance path on the same pins
+    assert rel_err(E[0], e1) < 1e-5
