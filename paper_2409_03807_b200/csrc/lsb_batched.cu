@@ -30,7 +30,10 @@ namespace {
 constexpr int kBC = 256;       // batch columns per chunk (tcgen05 N)
 constexpr int kEcols = 64;     // columns per element CTA
 constexpr int kTB = 48;        // tets per element block (Hessian path; also the staging capacity)
-constexpr int kTBE = 24;       // tets per element block of the batched evaluation (more CTAs resident)
+#ifndef LSB_TBE
+#define LSB_TBE 24
+#endif
+constexpr int kTBE = LSB_TBE;  // tets per element block of the batched evaluation (more CTAs resident)
 
 __device__ __forceinline__ float act_f(int a, float x, int order) {
     return (float)act_eval(a, (double)x, order);
@@ -287,162 +290,177 @@ __global__ void __launch_bounds__(kEcols) elem_batched2_kernel(const TR* rec, co
     }
 }
 
-// ---- packed fp32x2 element math (sm_100 FFMA2/FMUL2/FADD2): two latent columns per thread
-struct f2 {
-    float2 v;
-};
-__device__ __forceinline__ f2 F2(float a) { return {make_float2(a, a)}; }
-__device__ __forceinline__ f2 F2(float a, float b) { return {make_float2(a, b)}; }
-__device__ __forceinline__ f2 add2(f2 a, f2 b) { return {__fadd2_rn(a.v, b.v)}; }
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return {__fadd2_rn(a.v, make_float2(-b.v.x, -b.v.y))}; }
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return {__fmul2_rn(a.v, b.v)}; }
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return {__ffma2_rn(a.v, b.v, c.v)}; }
-// a*b - c*d
-__device__ __forceinline__ f2 dmd2(f2 a, f2 b, f2 c, f2 d) { return fma2(a, b, mul2(F2(-1.f), mul2(c, d))); }
+// ---- packed fp32x2 element pass (sm_100 FFMA2 / FMUL2 / FADD2): two latent columns per thread
+// The scalar kernel above is issue-bound (~390 instructions per tet and column, 246 of them fp32
+// arithmetic).  Here every arithmetic instruction works on the thread's two adjacent columns; operand
+// negation rides on the FFMA2 / FADD2 source modifiers, per-tet constants are staged in shared memory
+// as duplicated pairs (one 64-bit operand, no broadcast moves), the stress is regrouped as
+//   P = (c1 + c2) A + (c1 - c3) (A^T - cof A) + (c2 + c3 - (c1 - c3) tr A) I
+// (algebraically snh_psi_P's form) and the forces use vol Dm^-1 precomputed per tet:
+// ~150 instructions per tet and column.  Forces accumulate per (vertex slot, column pair) in shared
+// memory in tet order -- deterministic, as above.
+__device__ __forceinline__ float2 p2neg(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 p2add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 p2sub(float2 a, float2 b) { return __fadd2_rn(a, p2neg(b)); }
+__device__ __forceinline__ float2 p2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 p2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 p2fms(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, p2neg(c)); }  // a b - c
 
-// SNH energy density and P for two columns (same algebra as snh_psi_P; A row-major)
-__device__ __forceinline__ f2 snh_psi_P2(const f2* A, float mu, float lambda, f2* P) {
-    const f2 trA = add2(add2(A[0], A[4]), A[8]);
-    f2 q = mul2(A[0], A[0]);
-#pragma unroll
-    for (int k = 1; k < 9; ++k) q = fma2(A[k], A[k], q);
-    f2 m2 = dmd2(A[0], A[4], A[1], A[3]);
-    m2 = add2(m2, dmd2(A[0], A[8], A[2], A[6]));
-    m2 = add2(m2, dmd2(A[4], A[8], A[5], A[7]));
-    f2 cA[9];
-    cA[0 * 3 + 0] = dmd2(A[1 * 3 + 1], A[2 * 3 + 2], A[2 * 3 + 1], A[1 * 3 + 2]);
-    cA[1 * 3 + 0] = dmd2(A[2 * 3 + 1], A[0 * 3 + 2], A[0 * 3 + 1], A[2 * 3 + 2]);
-    cA[2 * 3 + 0] = dmd2(A[0 * 3 + 1], A[1 * 3 + 2], A[1 * 3 + 1], A[0 * 3 + 2]);
-    cA[0 * 3 + 1] = dmd2(A[1 * 3 + 2], A[2 * 3 + 0], A[2 * 3 + 2], A[1 * 3 + 0]);
-    cA[1 * 3 + 1] = dmd2(A[2 * 3 + 2], A[0 * 3 + 0], A[0 * 3 + 2], A[2 * 3 + 0]);
-    cA[2 * 3 + 1] = dmd2(A[0 * 3 + 2], A[1 * 3 + 0], A[1 * 3 + 2], A[0 * 3 + 0]);
-    cA[0 * 3 + 2] = dmd2(A[1 * 3 + 0], A[2 * 3 + 1], A[2 * 3 + 0], A[1 * 3 + 1]);
-    cA[1 * 3 + 2] = dmd2(A[2 * 3 + 0], A[0 * 3 + 1], A[0 * 3 + 0], A[2 * 3 + 1]);
-    cA[2 * 3 + 2] = dmd2(A[0 * 3 + 0], A[1 * 3 + 1], A[1 * 3 + 0], A[0 * 3 + 1]);
-    const f2 detA = fma2(A[6], cA[6], fma2(A[3], cA[3], mul2(A[0], cA[0])));
-    const f2 jm1 = add2(add2(trA, m2), detA);
-    const f2 i_minus = fma2(F2(2.f), trA, q);
-    const f2 x = mul2(i_minus, F2(0.25f));
-    const f2 L = F2(log1p_minus_x(x.v.x), log1p_minus_x(x.v.y));
-    // psi = 3/8 mu q - 3/4 mu (m2 + detA) - 1/2 mu L + 1/2 lambda jm1^2
-    f2 psi = mul2(F2(0.375f * mu), q);
-    psi = fma2(F2(-0.75f * mu), add2(m2, detA), psi);
-    psi = fma2(F2(-0.5f * mu), L, psi);
-    psi = fma2(F2(0.5f * lambda), mul2(jm1, jm1), psi);
-    const f2 c1 = F2(0.75f * mu);
-    const f2 c2 = F2(mu * i_minus.v.x / (4.f * (4.f + i_minus.v.x)), mu * i_minus.v.y / (4.f * (4.f + i_minus.v.y)));
-    const f2 c3 = mul2(F2(lambda), jm1);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int bb = 0; bb < 3; ++bb) {
-            const f2 Aab = A[a * 3 + bb], Aba = A[bb * 3 + a];
-            f2 t1 = sub2(add2(Aab, Aba), cA[a * 3 + bb]);
-            f2 cofF = sub2(cA[a * 3 + bb], Aba);
-            f2 F = Aab;
-            if (a == bb) {
-                t1 = sub2(t1, trA);
-                cofF = add2(add2(cofF, F2(1.f)), trA);
-                F = add2(F, F2(1.f));
-            }
-            P[a * 3 + bb] = fma2(c3, cofF, fma2(c2, F, mul2(c1, t1)));
-        }
-    return psi;
-}
+constexpr int kP2Threads = 64;  // threads per CTA = column pairs: 128 columns per CTA
+constexpr int kP2Consts = 26;   // per-tet constant pairs: Dm^-1 (9), vol Dm^-1 (9), energy / stress coefficients (8)
 
-// Two-column element kernel: thread = columns (2 t, 2 t + 1) of a 2 kEcols-column tile.
-template <typename TR>
-__global__ void __launch_bounds__(kEcols) elem_batched_f2_kernel(const TR* rec, const int* blk_tet0,
-                                                                const int* blk_vptr, const short* tet_loc,
-                                                                const int4* tets, const float* U, int N,
-                                                                float* partial, double* eblk) {
-    extern __shared__ float sm[];
-    constexpr int NC = 2 * kEcols;  // columns per CTA
+__global__ void __launch_bounds__(kP2Threads) elem_batched_p2_kernel(const float* rec, const int* blk_tet0,
+                                                                     const int* blk_vptr, const short* tet_loc,
+                                                                     const int4* tets, const float* U, int N,
+                                                                     float* partial, double* eblk) {
+    extern __shared__ __align__(16) float2 sm2[];
     const int blk = blockIdx.x, tid = threadIdx.x;
-    const int col = blockIdx.y * NC + 2 * tid;  // first of the two columns (N is even)
+    const int col = blockIdx.y * (2 * kP2Threads) + 2 * tid;  // first of the two columns (N is even)
     const int e0 = blk_tet0[blk], ne = blk_tet0[blk + 1] - e0;
     const int v0 = blk_vptr[blk], nv = blk_vptr[blk + 1] - v0;
-    float2* acc = reinterpret_cast<float2*>(sm);          // [nv * 3][kEcols] float2
-    float* rs = reinterpret_cast<float*>(acc + nv * 3 * kEcols);  // [kTB][12]
-    int* vs = reinterpret_cast<int*>(rs + kTB * 12);      // [kTB][4] row offsets v * 3 * N
-    short* ls = reinterpret_cast<short*>(vs + kTB * 4);   // [kTB][4] free slots
-    for (int i = tid; i < nv * 3 * kEcols; i += kEcols) acc[i] = make_float2(0.f, 0.f);
-    for (int i = tid; i < ne * 12; i += kEcols) rs[i] = (float)rec[(size_t)e0 * 12 + i];
-    for (int i = tid; i < ne * 4; i += kEcols) {
+    float2* acc = sm2;                                  // [(nv + 1) * 3][kP2Threads]; slot nv absorbs pinned corners
+    float2* cs = acc + (nv + 1) * 3 * kP2Threads;       // [kTBE][kP2Consts]
+    int* vs = reinterpret_cast<int*>(cs + kTBE * kP2Consts);  // [kTBE][4] row offsets v * 3 * N
+    int* los = vs + kTBE * 4;                           // [kTBE][4] accumulator offsets slot * 3 * kP2Threads
+    for (int i = tid; i < (nv + 1) * 3 * kP2Threads; i += kP2Threads) acc[i] = make_float2(0.f, 0.f);
+    for (int t = tid; t < ne; t += kP2Threads) {
+        float rc[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) rc[q] = rec[(size_t)(e0 + t) * 12 + q];
+        float2* c = cs + t * kP2Consts;
+        const float vol = rc[9], mu = rc[10], lam = rc[11];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) {
+            c[q] = make_float2(rc[q], rc[q]);
+            c[9 + q] = make_float2(vol * rc[q], vol * rc[q]);
+        }
+        const float k[8] = {0.375f * mu, -0.75f * mu, -0.5f * mu, 0.5f * lam, 0.75f * mu, 0.25f * mu, lam, vol};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[18 + q] = make_float2(k[q], k[q]);
+    }
+    for (int i = tid; i < ne * 4; i += kP2Threads) {
         const int4 t = __ldg(tets + e0 + (i >> 2));
-        const int k = i & 3;
-        vs[i] = (k == 0 ? t.x : k == 1 ? t.y : k == 2 ? t.z : t.w) * 3 * N;
-        ls[i] = tet_loc[(size_t)e0 * 4 + i];
+        const int kk = i & 3;
+        vs[i] = (kk == 0 ? t.x : kk == 1 ? t.y : kk == 2 ? t.z : t.w) * 3 * N;
+        const int lv = tet_loc[(size_t)e0 * 4 + i];
+        los[i] = (lv >= 0 ? lv : nv) * 3 * kP2Threads;
     }
     __syncthreads();
-    double esum0 = 0.0, esum1 = 0.0;
-    if (col < N) {
-        const float* Uc = U + col;
-        float2 un[12];
+    if (col >= N) return;
+    const float* Uc[3] = {U + col, U + col + N, U + col + 2 * (size_t)N};  // per component: one 64-bit add per load
+    float2 esum = make_float2(0.f, 0.f);
+    float2 un[12];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) un[kk * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc[c] + vs[kk]));
+    for (int e = 0; e < ne; ++e) {
+        float2 u[12];
+#pragma unroll
+        for (int q = 0; q < 12; ++q) u[q] = un[q];
+        if (e + 1 < ne) {
+            const int4 vn = *reinterpret_cast<const int4*>(vs + (e + 1) * 4);
+            const int vv[4] = {vn.x, vn.y, vn.z, vn.w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) un[kk * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc[c] + vv[kk]));
+        }
+        const int4 o4 = *reinterpret_cast<const int4*>(los + e * 4);
+        const int off[4] = {o4.x, o4.y, o4.z, o4.w};
+        float2* at = acc + tid;
+        float2 old[12];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) un[k * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc + vs[k] + c * N));
-        for (int e = 0; e < ne; ++e) {
-            f2 u[12];
+            for (int a = 0; a < 3; ++a) old[k * 3 + a] = at[off[k] + a * kP2Threads];
+        float2 c[kP2Consts];  // the tet's constant pairs: 13 16-byte broadcast loads
 #pragma unroll
-            for (int q = 0; q < 12; ++q) u[q].v = un[q];
-            if (e + 1 < ne) {
-                const int* vn = vs + (e + 1) * 4;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        un[k * 3 + c] = __ldg(reinterpret_cast<const float2*>(Uc + vn[k] + c * N));
-            }
-            const float* rc = rs + e * 12;
-            // D = [u1 - u0, u2 - u0, u3 - u0] (row a = component), A = D Dm^-1
-            f2 D[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                D[a * 3 + 0] = sub2(u[1 * 3 + a], u[0 * 3 + a]);
-                D[a * 3 + 1] = sub2(u[2 * 3 + a], u[0 * 3 + a]);
-                D[a * 3 + 2] = sub2(u[3 * 3 + a], u[0 * 3 + a]);
-            }
-            f2 A[9];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int bb = 0; bb < 3; ++bb)
-                    A[a * 3 + bb] = fma2(D[a * 3 + 2], F2(rc[2 * 3 + bb]),
-                                         fma2(D[a * 3 + 1], F2(rc[1 * 3 + bb]), mul2(D[a * 3 + 0], F2(rc[0 * 3 + bb]))));
-            f2 P[9];
-            const f2 psi = snh_psi_P2(A, rc[10], rc[11], P);
-            const float vol = rc[9];
-            esum0 += (double)(vol * psi.v.x);
-            esum1 += (double)(vol * psi.v.y);
-            const short* L = ls + e * 4;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                f2 s0 = F2(0.f);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const f2 hv = mul2(F2(vol), fma2(P[a * 3 + 2], F2(rc[c * 3 + 2]),
-                                                     fma2(P[a * 3 + 1], F2(rc[c * 3 + 1]), mul2(P[a * 3 + 0], F2(rc[c * 3 + 0])))));
-                    s0 = add2(s0, hv);
-                    const int lv = L[c + 1];
-                    if (lv >= 0) {
-                        float2& d = acc[(lv * 3 + a) * kEcols + tid];
-                        d = __fadd2_rn(d, hv.v);
-                    }
-                }
-                const int lv0 = L[0];
-                if (lv0 >= 0) {
-                    float2& d = acc[(lv0 * 3 + a) * kEcols + tid];
-                    d = __fadd2_rn(d, make_float2(-s0.v.x, -s0.v.y));
-                }
-            }
+        for (int k = 0; k < kP2Consts / 2; ++k) {
+            const float4 t = *reinterpret_cast<const float4*>(cs + e * kP2Consts + 2 * k);
+            c[2 * k] = make_float2(t.x, t.y);
+            c[2 * k + 1] = make_float2(t.z, t.w);
         }
-        for (int i = 0; i < nv * 3; ++i)
-            *reinterpret_cast<float2*>(partial + ((size_t)(v0 * 3) + i) * N + col) = acc[i * kEcols + tid];
-        eblk[(size_t)blk * N + col] = esum0;
-        eblk[(size_t)blk * N + col + 1] = esum1;
+        // D = [u1 - u0, u2 - u0, u3 - u0] (row a = component), A = D Dm^-1
+        float2 A[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float2 d0 = p2sub(u[3 + a], u[a]), d1 = p2sub(u[6 + a], u[a]), d2 = p2sub(u[9 + a], u[a]);
+#pragma unroll
+            for (int b = 0; b < 3; ++b) A[a * 3 + b] = p2fma(d2, c[6 + b], p2fma(d1, c[3 + b], p2mul(d0, c[b])));
+        }
+        const float2 trA = p2add(p2add(A[0], A[4]), A[8]);
+        float2 q = p2mul(A[0], A[0]);
+#pragma unroll
+        for (int k = 1; k < 9; ++k) q = p2fma(A[k], A[k], q);
+        float2 cA[9];  // cofactors of A
+        cA[0] = p2fms(A[4], A[8], p2mul(A[7], A[5]));
+        cA[3] = p2fms(A[7], A[2], p2mul(A[1], A[8]));
+        cA[6] = p2fms(A[1], A[5], p2mul(A[4], A[2]));
+        cA[1] = p2fms(A[5], A[6], p2mul(A[8], A[3]));
+        cA[4] = p2fms(A[8], A[0], p2mul(A[2], A[6]));
+        cA[7] = p2fms(A[2], A[3], p2mul(A[5], A[0]));
+        cA[2] = p2fms(A[3], A[7], p2mul(A[6], A[4]));
+        cA[5] = p2fms(A[6], A[1], p2mul(A[0], A[7]));
+        cA[8] = p2fms(A[0], A[4], p2mul(A[3], A[1]));
+        const float2 m2 = p2add(p2add(cA[0], cA[4]), cA[8]);  // sum of the principal 2 x 2 minors
+        const float2 detA = p2fma(A[6], cA[6], p2fma(A[3], cA[3], p2mul(A[0], cA[0])));
+        const float2 md = p2add(m2, detA);
+        const float2 jm1 = p2add(trA, md);
+        const float2 imin = p2fma(make_float2(2.f, 2.f), trA, q);  // I - 3
+        // L(x) = log1p(x) - x at x = (I - 3) / 4: log1p_minus_x's series for both columns at once, its
+        // log1pf branch per column beyond |x| = 0.05
+        const float2 x = p2mul(make_float2(0.25f, 0.25f), imin);
+        float2 L = p2fma(x, make_float2(1.0f / 7.0f, 1.0f / 7.0f), make_float2(-1.0f / 6.0f, -1.0f / 6.0f));
+        L = p2fma(x, L, make_float2(0.2f, 0.2f));
+        L = p2fma(x, L, make_float2(-0.25f, -0.25f));
+        L = p2fma(x, L, make_float2(1.0f / 3.0f, 1.0f / 3.0f));
+        L = p2fma(x, L, make_float2(-0.5f, -0.5f));
+        L = p2mul(p2mul(x, x), L);
+        if (fabsf(x.x) >= 5e-2f) L.x = log1pf(x.x) - x.x;
+        if (fabsf(x.y) >= 5e-2f) L.y = log1pf(x.y) - x.y;
+        // psi = 3/8 mu q - 3/4 mu (m2 + det A) - 1/2 mu L + 1/2 lambda (J - 1)^2
+        float2 psi = p2mul(c[18], q);
+        psi = p2fma(c[19], md, psi);
+        psi = p2fma(c[20], L, psi);
+        psi = p2fma(c[21], p2mul(jm1, jm1), psi);
+        esum = p2fma(c[25], psi, esum);
+        const float2 c2 = p2mul(c[23], make_float2(__fdividef(imin.x, 4.f + imin.x), __fdividef(imin.y, 4.f + imin.y)));
+        const float2 c3 = p2mul(c[24], jm1);
+        const float2 alpha = p2add(c[22], c2), beta = p2sub(c[22], c3);
+        const float2 kappa = p2fms(p2neg(beta), trA, p2neg(p2add(c2, c3)));  // c2 + c3 - beta tr A
+        float2 Pm[9];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                Pm[a * 3 + b] = p2fma(alpha, A[a * 3 + b], p2mul(beta, p2sub(A[b * 3 + a], cA[a * 3 + b])));
+                if (a == b) Pm[a * 3 + b] = p2add(Pm[a * 3 + b], kappa);
+            }
+        // forces: vertex k + 1 gets P (vol Dm^-1)[k][:]^T, vertex 0 minus their sum.  The four corners of a
+        // tet are distinct vertices, so the 12 accumulator entries are read up front (independent loads,
+        // issued before the arithmetic above needs them) and written back together.
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float2 s0 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float2 hv = p2fma(Pm[a * 3 + 2], c[9 + k * 3 + 2],
+                                        p2fma(Pm[a * 3 + 1], c[9 + k * 3 + 1], p2mul(Pm[a * 3 + 0], c[9 + k * 3 + 0])));
+                s0 = k == 0 ? hv : p2add(s0, hv);
+                old[(k + 1) * 3 + a] = p2add(old[(k + 1) * 3 + a], hv);
+            }
+            old[a] = p2sub(old[a], s0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) at[off[k] + a * kP2Threads] = old[k * 3 + a];
     }
+    for (int i = 0; i < nv * 3; ++i)
+        *reinterpret_cast<float2*>(partial + ((size_t)(v0 * 3) + i) * N + col) = acc[i * kP2Threads + tid];
+    eblk[(size_t)blk * N + col] = (double)esum.x;
+    eblk[(size_t)blk * N + col + 1] = (double)esum.y;
 }
 
 // T[row][N] = s (sum of the vertex's block partials in block order + inertia).
@@ -1776,13 +1794,12 @@ struct BatchedEngine : BatchedBase {
         pins_eval = c.pins_version;
         esmem2 = (size_t)(eb.max_nv + 1) * 3 * kEcols * sizeof(float) + kTB * 12 * sizeof(float) +
                  kTB * 4 * sizeof(int) + kTB * 4 * sizeof(int);
-        esmem_f2 = (size_t)eb.max_nv * 3 * kEcols * sizeof(float2) + kTB * 12 * sizeof(float) + kTB * 4 * sizeof(int) +
-                   kTB * 4 * sizeof(short);
-        cuda_check(cudaFuncSetAttribute(elem_batched_f2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)esmem_f2), "elem f2 smem");
-        // measured slower than the scalar kernel (half the threads per column tile lowers
-        // occupancy more than FFMA2 saves issue slots): opt-in
-        use_f2 = c.dev.elem_f2 && BC % (2 * kEcols) == 0;
+        esmem_f2 = (size_t)(eb.max_nv + 1) * 3 * kP2Threads * sizeof(float2) + (size_t)kTBE * kP2Consts * sizeof(float2) +
+                   kTBE * 4 * sizeof(int) + kTBE * 4 * sizeof(int);
+        cuda_check(cudaFuncSetAttribute(elem_batched_p2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)esmem_f2), "elem p2 smem");
+        // packed fp32x2 element kernel (fp32 contexts; LSB_ELEM_F2=0 selects the scalar kernel)
+        use_f2 = c.dev.elem_f2 && BC % (2 * kP2Threads) == 0;
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)esmem2), "elem2 smem");
         cuda_check(cudaFuncSetAttribute(elem_batched2_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1839,8 +1856,8 @@ struct BatchedEngine : BatchedBase {
             }
             if (use_f2 && c.precision != LSB_FP64) {
                 // packed fp32x2: thread = two adjacent columns, 2 kEcols columns per CTA
-                dim3 g(eb.nblk, (BC + 2 * kEcols - 1) / (2 * kEcols));
-                elem_batched_f2_kernel<float><<<g, kEcols, esmem_f2, s>>>(
+                dim3 g(eb.nblk, (BC + 2 * kP2Threads - 1) / (2 * kP2Threads));
+                elem_batched_p2_kernel<<<g, kP2Threads, esmem_f2, s>>>(
                     static_cast<const float*>(c.d_rec), eb.tet0, eb.vptr, eb.loc,
                     reinterpret_cast<const int4*>(c.d_tets), d_U, BC, d_part, d_eblk);
             } else {

@@ -43,11 +43,11 @@ struct DevFlags {
     int solve_exp = 0;        // LSB_SOLVE_EXP: persistent-kernel A/B bits (lsb_solve.cuh SolveParams::exp)
     int trace = 0;            // LSB_TRACE=1: persistent-kernel phase timestamps
     int hess3 = 1;            // LSB_HESS3=0: the D^T M' 3xTF32 element Hessian kernel instead of the edge-space chained-MMA form
-    int elem_f2 = 0;          // LSB_ELEM_F2=1: FFMA2 batched element kernel
+    int elem_f2 = 1;          // LSB_ELEM_F2=0: scalar batched element kernel instead of the packed fp32x2 one
     int theta_tb = 24;        // LSB_THETA_TB: tets per block of the theta element pass
     int noncoop = 0;          // LSB_NONCOOP=1: persistent kernel as a plain cluster launch (ncu replay)
     int elem_f32 = 1;         // LSB_ELEM_F32=0: fp64 element arithmetic in fp32-storage mode (multi-kernel path)
-    int pdl = 1;              // LSB_PDL bit mask of programmatic edges (1 ctrl->out_fwd, 2 out_fwd->elem, 4 elem->vjp,
+    int pdl = 5;              // LSB_PDL bit mask of programmatic edges (1 ctrl->out_fwd, 2 out_fwd->elem, 4 elem->vjp,
                               // 8 vjp->ctrl); 0: plain full-completion edges
     int l2_pf_elem = 0;       // LSB_L2PF_ELEM: VJP head tiles prefetched into L2 by the element pass (measured: slower)
     int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
