@@ -1180,58 +1180,63 @@ __global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4
     cp_async_wait_all();
     __syncthreads();
     // ---- lane constants of the tensor-core phase
-    // K slots of this lane: kk = 2 t4, 2 t4 + 1 and (t4 == 0 only) kk = 8; kk = 3 e + a (edge e, component a)
-    const int kks[3] = {2 * t4, 2 * t4 + 1, 8};
+    // K slots (kk = 3 e + a: edge e, component a) are dealt to the four t4 lanes so that a lane's slots
+    // share Jacobian rows -- lanes 0..2 take component a = t4 of edges 0 and 1 (lane 0 also edge 2, its k-step-1
+    // slot), lane 3 takes edge 2 of components 1 and 2: 14 row loads per quad instead of 18.  Any assignment
+    // works as long as the H_E operand is permuted the same way (its offsets are per-lane constants) and the
+    // accumulator column order matches: column 2 t4 <-> slot 0 of lane t4, 2 t4 + 1 <-> slot 1, column 8 <->
+    // lane 0's slot 2.
+    //   rows loaded per lane (vertex of the tet, component):        slots
+    //   t4 = 0: R0 (1, 0)  R1 (2, 0)  R2 (3, 0)  R3 (0, 0)          R0 - R3, R1 - R3, R2 - R3
+    //   t4 = 1: R0 (1, 1)  R1 (2, 1)             R3 (0, 1)          R0 - R3, R1 - R3
+    //   t4 = 2: R0 (1, 2)  R1 (2, 2)             R3 (0, 2)          R0 - R3, R1 - R3
+    //   t4 = 3: R0 (3, 1)  R1 (3, 2)  R2 (0, 2)  R3 (0, 1)          R0 - R3, R1 - R2
+    const bool is3 = t4 == 3, slot2 = t4 == 0, has_r2 = slot2 || is3;
+    const int kks[3] = {is3 ? 7 : t4, is3 ? 8 : 3 + t4, 6};   // kk of slots 0, 1 and (lane 0) 2
+    const int rv[4] = {is3 ? 3 : 1, is3 ? 3 : 2, is3 ? 0 : 3, 0};           // vertex of the tet per row
+    const int ra[4] = {is3 ? 1 : t4, is3 ? 2 : t4, is3 ? 2 : 0, is3 ? 1 : t4};  // component per row
     const size_t PR = (size_t)P * R;
-    const float* jb[3];   // Jv + a PR + (first point of the warp) R + g
-    int esel[3];
+    const float* jb[4];   // Jv + a PR + (first point of the warp) R + first direction of the lane
 #pragma unroll
-    for (int s = 0; s < 3; ++s) {
-        esel[s] = 1 + kks[s] / 3;
-        jb[s] = Jv + (size_t)(kks[s] % 3) * PR + (size_t)(p0 + warp * PPW) * R + g * NR;
-    }
+    for (int s = 0; s < 4; ++s) jb[s] = Jv + (size_t)ra[s] * PR + (size_t)(p0 + warp * PPW) * R + g * NR;
     const unsigned vstrideB = 3u * (unsigned)PR * (unsigned)sizeof(float);  // bytes per vertex of Jv
-    const bool slot2 = t4 == 0;
-    // H_E upper-triangle offsets of this lane's B fragments
+    // H_E upper-triangle offsets of this lane's B fragments; accumulator column c holds kk = colk(c)
     auto tri = [](int i, int j) {
         const int lo = i < j ? i : j, hi = i < j ? j : i;
         return lo * 9 - lo * (lo - 1) / 2 + (hi - lo);
     };
-    const int hb00 = tri(kks[0], g), hb01 = tri(kks[1], g);  // n tile 0 (n = g), k step 0
-    const int hb10 = tri(kks[0], 8), hb11 = tri(kks[1], 8);  // n tile 1 (n = 8: g == 0 only), k step 0
-    const int hb20 = tri(8, g);                              // n tile 0, k step 1 (t4 == 0 only)
+    auto colk = [](int c) { return c == 8 ? 6 : c == 6 ? 7 : c == 7 ? 8 : (c & 1) * 3 + (c >> 1); };
+    const int hb00 = tri(kks[0], colk(g)), hb01 = tri(kks[1], colk(g));  // n tile 0 (column g), k step 0
+    const int hb10 = tri(kks[0], colk(8)), hb11 = tri(kks[1], colk(8));  // n tile 1 (column 8: g == 0 only), k step 0
+    const int hb20 = tri(kks[2], colk(g));                               // n tile 0, k step 1 (t4 == 0 only)
+    const int hb30 = tri(kks[2], colk(8));
     const bool n8 = g == 0;
     bool livep[PPW];
 #pragma unroll
     for (int pp = 0; pp < PPW; ++pp) livep[pp] = p0 + warp * PPW + pp < P;
-    // raw Jacobian entries of one tet for this lane: [point][slot][vertex e + 1 / vertex 0][row group]
-    float rawA[PPW][3][2][NR], rawB[PPW][3][2][NR];
+    // raw Jacobian entries of one tet for this lane: [point][row R0..R3][direction of the lane]
+    float rawA[PPW][4][NR], rawB[PPW][4][NR];
 #pragma unroll
     for (int pp = 0; pp < PPW; ++pp)
 #pragma unroll
-        for (int s = 0; s < 3; ++s)
+        for (int s = 0; s < 4; ++s)
 #pragma unroll
-            for (int w = 0; w < 2; ++w)
+            for (int q = 0; q < NR; ++q) rawA[pp][s][q] = rawB[pp][s][q] = 0.f;
+    auto load_raw = [&](float (&raw)[PPW][4][NR], int el) {
+        const int4 tq = sh_tq[el];
 #pragma unroll
-                for (int q = 0; q < NR; ++q) rawA[pp][s][w][q] = rawB[pp][s][w][q] = 0.f;
-    auto load_raw = [&](float (&raw)[PPW][3][2][NR], int el) {
-        const int* tq = reinterpret_cast<const int*>(sh_tq + el);
-        const unsigned vz = (unsigned)tq[0];
-#pragma unroll
-        for (int s = 0; s < 3; ++s) {
-            if (s == 2 && !slot2) continue;
-            const unsigned vh = (unsigned)tq[esel[s]];
-            const float* ph = reinterpret_cast<const float*>(reinterpret_cast<const char*>(jb[s]) + (unsigned long long)vh * vstrideB);
-            const float* pz = reinterpret_cast<const float*>(reinterpret_cast<const char*>(jb[s]) + (unsigned long long)vz * vstrideB);
+        for (int s = 0; s < 4; ++s) {
+            if (s == 2 && !has_r2) continue;
+            const unsigned v = (unsigned)(rv[s] == 0 ? tq.x : rv[s] == 1 ? tq.y : rv[s] == 2 ? tq.z : tq.w);
+            const float* pr = reinterpret_cast<const float*>(reinterpret_cast<const char*>(jb[s]) + (unsigned long long)v * vstrideB);
 #pragma unroll
             for (int pp = 0; pp < PPW; ++pp) {
                 if (!livep[pp]) continue;
-                ldg_vec<NR>(raw[pp][s][0], ph + pp * R);
-                ldg_vec<NR>(raw[pp][s][1], pz + pp * R);
+                ldg_vec<NR>(raw[pp][s], pr + pp * R);
             }
         }
     };
-    auto process = [&](const float (&raw)[PPW][3][2][NR], int el, int tbl) {
+    auto process = [&](const float (&raw)[PPW][4][NR], int el, int tbl) {
         // forces of this tet: lanes own (point of the warp, local dof), tet order
         for (int i = lane; i < 12 * PPW; i += 32) {
             const int pp = i / 12, d = i % 12, pc = warp * PPW + pp;
@@ -1245,19 +1250,20 @@ __global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4
             const uint32_t b00 = __float_as_uint(hr[hb00]), b01 = __float_as_uint(hr[hb01]);
             const uint32_t b10 = n8 ? __float_as_uint(hr[hb10]) : 0u, b11 = n8 ? __float_as_uint(hr[hb11]) : 0u;
             const uint32_t b20 = slot2 ? __float_as_uint(hr[hb20]) : 0u;
-            const uint32_t b30 = (slot2 && n8) ? __float_as_uint(hr[44]) : 0u;
+            const uint32_t b30 = (slot2 && n8) ? __float_as_uint(hr[hb30]) : 0u;
             uint32_t ea[MT][6];  // k step 0: a0..a3, k step 1: a0, a1
             float X[MT][2][4];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
-                const int q0 = R >= 16 ? 2 * mt : 0;
-                ea[mt][0] = rn_tf32(raw[pp][0][0][q0] - raw[pp][0][1][q0]);
-                ea[mt][2] = rn_tf32(raw[pp][1][0][q0] - raw[pp][1][1][q0]);
-                ea[mt][4] = rn_tf32(raw[pp][2][0][q0] - raw[pp][2][1][q0]);
+                const int q0 = R >= 16 ? 2 * mt : 0, q1 = NR > 1 ? q0 + 1 : 0;
+                // slot 0 = R0 - R3, slot 1 = R1 - (lane 3: R2, else R3), slot 2 (lane 0) = R2 - R3
+                ea[mt][0] = rn_tf32(raw[pp][0][q0] - raw[pp][3][q0]);
+                ea[mt][2] = rn_tf32(raw[pp][1][q0] - (is3 ? raw[pp][2][q0] : raw[pp][3][q0]));
+                ea[mt][4] = slot2 ? rn_tf32(raw[pp][2][q0] - raw[pp][3][q0]) : 0u;
                 if (R >= 16) {
-                    ea[mt][1] = rn_tf32(raw[pp][0][0][NR > 1 ? q0 + 1 : 0] - raw[pp][0][1][NR > 1 ? q0 + 1 : 0]);
-                    ea[mt][3] = rn_tf32(raw[pp][1][0][NR > 1 ? q0 + 1 : 0] - raw[pp][1][1][NR > 1 ? q0 + 1 : 0]);
-                    ea[mt][5] = rn_tf32(raw[pp][2][0][NR > 1 ? q0 + 1 : 0] - raw[pp][2][1][NR > 1 ? q0 + 1 : 0]);
+                    ea[mt][1] = rn_tf32(raw[pp][0][q1] - raw[pp][3][q1]);
+                    ea[mt][3] = rn_tf32(raw[pp][1][q1] - (is3 ? raw[pp][2][q1] : raw[pp][3][q1]));
+                    ea[mt][5] = slot2 ? rn_tf32(raw[pp][2][q1] - raw[pp][3][q1]) : 0u;
                 } else {
                     ea[mt][1] = ea[mt][3] = ea[mt][5] = 0u;
                 }
