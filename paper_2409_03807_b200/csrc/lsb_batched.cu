@@ -608,7 +608,9 @@ __global__ void tangent_pack_kernel(int h, int P, int r, int cols, const float* 
     const int w = 1 + r;
     const int total = h * P * w;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const int i = idx / (P * w), rem = idx % (P * w), p = rem / w, j = rem % w;
+        // column order [y (P) | tangents (P x r)]: the J part of an output row is one contiguous run of Jv
+        const int i = idx / (P * w), rem = idx % (P * w);
+        const int p = rem < P ? rem : (rem - P) / r, j = rem < P ? 0 : 1 + (rem - P) % r;
         B[idx] = X[(size_t)i * P * cols + (size_t)p * cols + j];
     }
 }
@@ -635,10 +637,11 @@ __global__ void tangent_out_kernel(int n, int P, int r, const float* C, const do
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
         const int row = idx / P, p = idx % P;
         const double* e6 = eprow + (size_t)row * 6;
-        const float* c = C + (size_t)row * P * w + (size_t)p * w;
+        const float* crow = C + (size_t)row * P * w;   // [u (P) | J (P x r)] (tangent_pack_kernel)
+        const float* c = crow + P + (size_t)p * r - 1;  // c[1 + a] = J column a of point p
         const int slot = (int)e6[4];
         const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
-        const double u = e6[1] * ((double)c[0] + e6[0]) + e6[2];
+        const double u = e6[1] * ((double)crow[p] + e6[0]) + e6[2];
         U[vc * P + p] = (float)u;
         if (inertia) rin[(size_t)row * P + p] = (float)(inv_dt2 * e6[3] * (u - e6[5]));
         float* jo = Jv + (vc * P + p) * r;
@@ -2244,13 +2247,18 @@ struct BatchedEngine : BatchedBase {
         }
         const float* XL = d_Xl[c.nhid];
         tangent_pack_kernel<<<c.num_sms, 256, 0, s>>>(h, P, r, cols, XL, d_Bt);
-        if (!tc.enabled ||
-            !tc.gemm_general(s, tc.A1, tc.tiles1, tc.S1, n, d_Bt, P * (1 + r), h, P * (1 + r), d_Ct, P * (1 + r))) {
-            dim3 g((P * (1 + r) + 127) / 128, (n + 127) / 128);
-            sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (1 + r), h, d_W, h, d_Bt, P * (1 + r), d_Ct, P * (1 + r));
+        // output layer with the tangent-output epilogue fused into the tcgen05 GEMM (U, Jv, inertia residual
+        // straight from TMEM: no n x P (1 + r) product written and re-read); else SGEMM + tangent_out_kernel
+        if (!c.dev.fuse_tangent_out ||
+            !tc.gemm_tangent_out(s, d_Bt, h, P, r, c.d_eprow, d_Uh, d_Jv, d_rinh, inertia, inv_dt2)) {
+            if (!tc.enabled ||
+                !tc.gemm_general(s, tc.A1, tc.tiles1, tc.S1, n, d_Bt, P * (1 + r), h, P * (1 + r), d_Ct, P * (1 + r))) {
+                dim3 g((P * (1 + r) + 127) / 128, (n + 127) / 128);
+                sgemm_nn_kernel<<<g, 256, 0, s>>>(n, P * (1 + r), h, d_W, h, d_Bt, P * (1 + r), d_Ct, P * (1 + r));
+            }
+            tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv, inertia, inv_dt2,
+                                                             d_rinh);
         }
-        tangent_out_kernel<<<c.num_sms * 4, 256, 0, s>>>(n, P, r, d_Ct, c.d_eprow, d_Uh, d_Jv, inertia, inv_dt2,
-                                                         d_rinh);
         {
             const int gp = 128 / r;
             dim3 g(nblk, (P + gp - 1) / gp);

@@ -154,6 +154,11 @@ struct GemmArgs {
     double* epart;        // [tiles][N]
     int has_inertia;
     double inv_dt2;
+    // mode 4 (general tile grid with the tangent-output epilogue fused): output columns are
+    // [u (P) | J (P x r)] per row; u = s (C + b) + shift - X -> U[slot][p], J = s C -> Jv[slot][p][a]
+    // (one contiguous run per row), inertia residual rin[row][p]
+    float* Jv = nullptr;
+    int P = 0, r = 0;
 };
 
 __device__ __forceinline__ void job_slices(const GemmArgs& g, int j, int& s0, int& s1) {
@@ -211,9 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                     const int st = it % g.stages, u = it / g.stages;
                     if (u > 0) mbar_wait(&empty[st], (u - 1) & 1);
                     unsigned char* sa = smem + (size_t)st * stage_bytes;
-                    const size_t a_slice = g.mode == 3 ? (size_t)(j / g.ntn) * g.S + s
-                                           : (g.mode != 1 ? (size_t)j * g.S + s : (size_t)s);
-                    const size_t b_slice = g.mode == 3 ? (size_t)(j % g.ntn) * g.S + s : (size_t)s;
+                    const bool grid2d = g.mode == 3 || g.mode == 4;  // job = (M tile, N tile)
+                    const size_t a_slice = grid2d ? (size_t)(j / g.ntn) * g.S + s
+                                                  : (g.mode != 1 ? (size_t)j * g.S + s : (size_t)s);
+                    const size_t b_slice = grid2d ? (size_t)(j % g.ntn) * g.S + s : (size_t)s;
                     mbar_expect_tx(&full[st], stage_bytes);
                     tma_load_1d(sa, g.A + a_slice * slice_floats(kTileM), a_bytes, &full[st], pol_a);
                     tma_load_1d(sa + a_bytes, g.B + b_slice * slice_floats(N), b_bytes, &full[st], pol_b);
@@ -321,6 +327,41 @@ __global__ void __launch_bounds__(kThreads, 1) gemm3_kernel(const GemmArgs g) {
                     // lane l holds column c0 + bitrev-free index: lanes with bit o set kept the upper
                     // half at each step -> column = lane
                     esum_s[warp][c0 + lane] = e[0];
+                    continue;
+                }
+                if (g.mode == 4) {  // tangent output: columns [u (P) | J (P r)], 4-column groups never straddle P
+                    const int grow = (j / g.ntn) * kTileM + row;
+                    const int col0 = (j % g.ntn) * N + c0;
+                    if (grow < g.m_valid) {
+                        const double* e6 = g.eprow + (size_t)grow * 6;
+                        const double b = e6[0], sc = e6[1], sh = e6[2], m = e6[3], qb = e6[5];
+                        const int slot = (int)e6[4];
+                        const size_t vc = (size_t)(slot >> 2) * 3 + (slot & 3);
+                        float* Ur = g.U + vc * g.P;
+                        float* Jr = g.Jv + vc * g.P * g.r;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            const int col = col0 + i;
+                            if (col >= g.ncols) break;
+                            if (col < g.P) {
+                                float4 uo, ro;
+                                float* up = &uo.x;
+                                float* rp = &ro.x;
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const double u = sc * ((double)v[i + q] + b) + sh;
+                                    up[q] = (float)u;
+                                    rp[q] = (float)(g.inv_dt2 * m * (u - qb));
+                                }
+                                *reinterpret_cast<float4*>(Ur + col) = uo;
+                                if (g.has_inertia) *reinterpret_cast<float4*>(g.rin + (size_t)grow * g.P + col) = ro;
+                            } else {
+                                *reinterpret_cast<float4*>(Jr + (col - g.P)) =
+                                    make_float4((float)(sc * v[i]), (float)(sc * v[i + 1]), (float)(sc * v[i + 2]),
+                                                (float)(sc * v[i + 3]));
+                            }
+                        }
+                    }
                     continue;
                 }
                 if (g.mode == 3) {  // general tile grid, masked columns
@@ -490,6 +531,29 @@ struct TcGemm {
         tc::GemmArgs a{Apacked, Bg, C, 3, tiles_m * ntn, S, N, ldc, m_valid, tmem_cols, stages, ntn, ncols,
                        nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
         tc::gemm3_kernel<<<std::min(tiles_m * ntn, sms), tc::kThreads, smem, s>>>(a);
+        launches += 2;
+        return true;
+    }
+    // gemm_general on the output layer with the tangent-output epilogue fused (mode 4): B holds the columns
+    // [y (P) | tangents (P x r)] feature-major; writes U, Jv (and rin with inertia) instead of C.
+    bool gemm_tangent_out(cudaStream_t s, const float* B, int K, int P, int r, const double* eprow, float* U, float* Jv,
+                          float* rin, int has_inertia, double inv_dt2) {
+        if (!enabled || N != 256 || (P & 3)) return false;
+        const int ncols = P * (1 + r);
+        const int ntn = (ncols + N - 1) / N;
+        const size_t need = (size_t)ntn * S1 * tc::slice_floats(N);
+        if (need > Bg_floats) {
+            if (Bg) cudaFree(Bg);
+            Bg = static_cast<float*>(dalloc(sizeof(float) * need));
+            Bg_floats = need;
+        }
+        tc::pack_kernel<<<sms * 8, 256, 0, s>>>(B, 1, ncols, ncols, K, N, ntn, S1, Bg);
+        tc::GemmArgs a{A1, Bg, nullptr, 4, tiles1 * ntn, S1, N, 0, n, tmem_cols, stages, ntn, ncols,
+                       eprow, nullptr, U, rin, nullptr, has_inertia, inv_dt2};
+        a.Jv = Jv;
+        a.P = P;
+        a.r = r;
+        tc::gemm3_kernel<<<std::min(tiles1 * ntn, sms), tc::kThreads, smem, s>>>(a);
         launches += 2;
         return true;
     }

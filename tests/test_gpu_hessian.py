@@ -107,3 +107,23 @@ def test_projective_newton_matches_oracle(inertia, oracle, product):
     g = np.zeros(pr.model.r)
     obj.eval(z, g)
     assert np.abs(g).max() < 1e-8
+
+
+def test_hessian_chunk_width_changes_are_transparent(oracle, product):
+    """The Hessian path sizes its chunks by the call (16-point multiples up to 256): the same z gives the
+    same Hessian whether it is computed alone, inside a 300-point call, or alone again afterwards (the
+    pinned rows of the chunk buffers are re-laid when the width changes), and matches the oracle."""
+    from paper_2409_03807_b200 import configs
+    pr = configs.build("c1")
+    sysm = pr.system("fp64")
+    ob = oracle.problem("c1")
+    Z1, Z2 = configs.latent_pairs_c5(pr.model.r, 150)
+    Z = np.concatenate([Z1, Z2])
+    H_small = sysm.hessian_batched(Z[:3])
+    H_big = sysm.hessian_batched(Z)
+    H_again = sysm.hessian_batched(Z[:3])
+    assert np.array_equal(H_small, H_again)
+    for k in range(3):
+        assert rel_err(H_big[k], H_small[k]) < 1e-6
+    for k in (0, 150, 299):
+        assert rel_err(H_big[k], ob.reduced_potential_hessian(Z[k])) < 1e-4
