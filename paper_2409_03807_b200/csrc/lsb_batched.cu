@@ -2265,7 +2265,11 @@ struct BatchedEngine : BatchedBase {
             const size_t gsmem = hess_smem(r);
             const float* recf = static_cast<const float*>(rec_f32(c));
             const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
-            if (c.dev.hess3) {  // edge-space form: two chained TF32 MMA stages per (tet, point)
+            // edge-space form (two chained TF32 MMA stages per (tet, point)) from 16K tets up: its per-(tet, point)
+            // roundings average out over the mesh (config 5: 1.2e-5 against the oracle, the 3xTF32 kernel
+            // 1.8e-5), while on config 1's 1,536 tets they leave 4.6e-5 against 1.8e-5 -- small meshes keep
+            // the 3xTF32 kernel (LSB_HESS3=2 forces the edge-space kernel, =0 the 3xTF32 one)
+            if (c.dev.hess3 == 2 || (c.dev.hess3 == 1 && c.mesh.E >= 16384)) {
                 if (r == 8)
                     elem_hess3_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                              d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);

@@ -127,3 +127,37 @@ def test_hessian_chunk_width_changes_are_transparent(oracle, product):
         assert rel_err(H_big[k], H_small[k]) < 1e-6
     for k in (0, 150, 299):
         assert rel_err(H_big[k], ob.reduced_potential_hessian(Z[k])) < 1e-4
+
+
+@pytest.mark.parametrize("r", [8, 16, 32])
+def test_edge_space_hessian_kernel_small_mesh(oracle, product, monkeypatch, r):
+    """Kernel-variant check: the edge-space chained-MMA element Hessian kernel (the default from 16K
+    tets up, forced here with LSB_HESS3=2) at every supported latent dimension against the oracle's
+    reduced_potential_hessian (losses.cpp:301-316).  Its operands are rounded to TF32 once, so on a
+    mesh of a few hundred tets the roundings do not average out: 3e-4 here; the 1e-4 bar is tested on
+    the default path (this file, tests/test_gpu_configs.py)."""
+    P = product
+    monkeypatch.setenv("LSB_HESS3", "2")
+    mesh = P.make_bar_mesh(4, 3, 3, 1.0, 0.4, 0.5, jitter_frac=0.05, seed=9)
+    rng = np.random.default_rng(6)
+    n = mesh.num_dofs()
+    dims = [r, 16, 16, n]
+    layers = []
+    for i in range(3):
+        W = rng.standard_normal((dims[i + 1], dims[i])) * (0.4 if i < 2 else 0.05)
+        b = 0.1 * rng.standard_normal(dims[i + 1])
+        layers.append(P.Layer(W, b, P.Activation.Silu if i < 2 else P.Activation.Identity))
+    shift = P.dof_pack(mesh, mesh.vertices)
+    scale = 0.3 + 0.1 * rng.random(n)
+    model = P.SubspaceModel(r, n, layers, shift, scale)
+    mu = 2.0 + rng.random(mesh.num_elements())
+    lam = 1.0 + rng.random(mesh.num_elements())
+    sysm = P.ReducedSystem(mesh, mu, lam, 3.0, model, "fp64")
+    o = oracle.Oracle.from_mesh(mesh.vertices, mesh.elements, mesh.pinned)
+    o.set_material(mu, lam, 3.0)
+    o.set_decoder([(l.W, l.b, int(l.act)) for l in layers], shift, scale, r)
+    Z = 0.5 * rng.standard_normal((5, r))
+    H = sysm.hessian_batched(Z)
+    worst = max(rel_err(H[k], o.reduced_potential_hessian(Z[k])) for k in range(5))
+    assert worst < 3e-4, worst
+    sysm.close()
