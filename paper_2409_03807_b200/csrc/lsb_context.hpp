@@ -52,7 +52,8 @@ struct DevFlags {
     int pdl = 5;              // LSB_PDL bit mask of programmatic edges (1 ctrl->out_fwd, 2 out_fwd->elem, 4 elem->vjp,
                               // 8 vjp->ctrl); 0: plain full-completion edges
     int l2_pf_elem = 0;       // LSB_L2PF_ELEM: VJP head tiles prefetched into L2 by the element pass (measured: slower)
-    int l2_pf = 16;           // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL)
+    int l2_pf = 8;            // LSB_L2PF: W tiles per out_fwd CTA prefetched into L2 during the control kernel (PDL); 8 and 16
+                              // measured 208.7 and 209.4 us per c3 evaluation, 0: 214.0, 32: 213.6 (tools/l2pf_ab.sh)
     int vjp_wg = 0;           // LSB_VJP_WG=1: per-warp, per-tile gather in the fused VJP (measured 1% slower than the prologue)
     int vjp_wg_cta = 3;       // LSB_VJP_WG_CTA: CTAs per SM of the per-warp-gather VJP
     int w_keep = 8;           // LSB_W_KEEP: W tiles at the end of every out_fwd CTA range kept in L2 (evict_last) for the VJP's
