@@ -206,7 +206,7 @@ DevFlags read_dev_flags() {
     if (const char* v = get("LSB_SOLVE_EXP")) f.solve_exp = atoi(v);
     if (const char* v = get("LSB_TRACE")) f.trace = v[0] == '1';
     if (const char* v = get("LSB_FUSE_TOUT")) f.fuse_tangent_out = v[0] != '0';
-    if (const char* v = get("LSB_HESS3")) f.hess3 = v[0] == '2' ? 2 : v[0] != '0';
+    if (const char* v = get("LSB_HESS3")) f.hess3 = v[0] != '0';
     if (const char* v = get("LSB_ELEM_F2")) f.elem_f2 = v[0] != '0';
     if (const char* v = get("LSB_THETA_TB")) f.theta_tb = std::max(1, std::min(48, atoi(v)));
     if (const char* v = get("LSB_NONCOOP")) f.noncoop = v[0] == '1';

@@ -1094,10 +1094,13 @@ __global__ void __launch_bounds__(128) elem_hess2_kernel(const int4* tets, const
 //     C += E X^T       (A = E again; B = the accumulator fragments of X, reused directly: lane (g, t4) of
 //                       an accumulator holds columns 2 t4, 2 t4 + 1, so every stage orders its K index as
 //                       position t4 <-> kk = 2 t4, position t4 + 4 <-> kk = 2 t4 + 1 and no shuffle is needed)
-// Operands are rounded to TF32 to nearest (two integer ops); rounding is relative to the edge
-// differences and to H_E, never to the Jacobian rows themselves, so smooth (trained) decoders lose
-// nothing to cancellation.  Per-(tet, point) rounding errors (~3e-4) are independent and average out over
-// the mesh: config 5 agrees with the 3xTF32 kernel to ~1e-6 relative, against the 1e-4 bar.
+// Every product is a 3xTF32 sum (hi lo' + lo hi' + hi hi', operands split by truncation: fp32-level accuracy).
+// One TF32 pass is not enough: on a smooth (trained) decoder neighbouring tets carry nearly the same E and
+// H_E, so their rounding errors are correlated and do not average out over the mesh (7.5e-4 against the
+// oracle, tests/test_gpu_hessian.py::test_edge_space_hessian_smooth_decoder).  The ninth K component (one slot
+// of a second k step) stays off the tensor cores: its rank-one terms X += e8 H_E[6][:] and C += e8 X[:, 6]^T
+// are fp32 FMAs on the accumulator fragments (e8 and X[:, 6] reach the lanes by shuffles), which halves the
+// MMA count (12 m16n8k8 per (tet, point) at r = 16).
 // Forces are accumulated per warp for its own points in tet order (deterministic).
 __device__ __forceinline__ uint32_t rn_tf32(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
 __device__ __forceinline__ void mma_tf32_u(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -1211,8 +1214,9 @@ __global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4
     auto colk = [](int c) { return c == 8 ? 6 : c == 6 ? 7 : c == 7 ? 8 : (c & 1) * 3 + (c >> 1); };
     const int hb00 = tri(kks[0], colk(g)), hb01 = tri(kks[1], colk(g));  // n tile 0 (column g), k step 0
     const int hb10 = tri(kks[0], colk(8)), hb11 = tri(kks[1], colk(8));  // n tile 1 (column 8: g == 0 only), k step 0
-    const int hb20 = tri(kks[2], colk(g));                               // n tile 0, k step 1 (t4 == 0 only)
-    const int hb30 = tri(kks[2], colk(8));
+    // the ninth K component (kk = 6, lane 0's slot 2) stays off the tensor cores: its rank-one terms are fp32
+    // FMAs on the accumulators (H_E row 6 at this lane's accumulator columns 2 t4, 2 t4 + 1 and at column 8)
+    const int ht0 = tri(6, colk(2 * t4)), ht1 = tri(6, colk(2 * t4 + 1)), ht8 = tri(6, colk(8));
     const bool n8 = g == 0;
     bool livep[PPW];
 #pragma unroll
@@ -1249,45 +1253,77 @@ __global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4
 #pragma unroll
         for (int pp = 0; pp < PPW; ++pp) {  // points beyond P run on zero Jacobian entries; their block is never stored
             const float* hr = sh_h[(warp * PPW + pp) * R + tbl];
-            // B fragments of H_E (already tf32)
-            const uint32_t b00 = __float_as_uint(hr[hb00]), b01 = __float_as_uint(hr[hb01]);
-            const uint32_t b10 = n8 ? __float_as_uint(hr[hb10]) : 0u, b11 = n8 ? __float_as_uint(hr[hb11]) : 0u;
-            const uint32_t b20 = slot2 ? __float_as_uint(hr[hb20]) : 0u;
-            const uint32_t b30 = (slot2 && n8) ? __float_as_uint(hr[hb30]) : 0u;
-            uint32_t ea[MT][6];  // k step 0: a0..a3, k step 1: a0, a1
+            // B fragments of H_E (fp32 in the record), split hi + lo: every product below is the 3xTF32 sum
+            // lo hi' + hi lo' + hi hi' (split_tf32), i.e. fp32-level accuracy.  A single TF32 pass is NOT enough:
+            // with a smooth (trained) decoder neighbouring tets carry nearly the same E and H_E, their
+            // rounding errors are correlated and do not average out over the mesh (7.5e-4 against the oracle on
+            // tests/test_gpu_hessian.py::test_edge_space_hessian_smooth_decoder; 1.2e-5 only on the random
+            // decoders of the configs).
+            uint32_t bh[4], bl[4];
+            split_tf32(hr[hb00], bh[0], bl[0]);
+            split_tf32(hr[hb01], bh[1], bl[1]);
+            split_tf32(n8 ? hr[hb10] : 0.f, bh[2], bl[2]);
+            split_tf32(n8 ? hr[hb11] : 0.f, bh[3], bl[3]);
+            const float hk0 = hr[ht0], hk1 = hr[ht1], hk8 = slot2 ? hr[ht8] : 0.f;
+            uint32_t eh[MT][4], el2[MT][4];  // a0..a3 of the one k step (hi / lo)
+            float e8[MT][2];                  // E[row][kk = 6] for rows g, g + 8 of every m tile (from lane t4 = 0)
             float X[MT][2][4];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) {
                 const int q0 = R >= 16 ? 2 * mt : 0, q1 = NR > 1 ? q0 + 1 : 0;
                 // slot 0 = R0 - R3, slot 1 = R1 - (lane 3: R2, else R3), slot 2 (lane 0) = R2 - R3
-                ea[mt][0] = rn_tf32(raw[pp][0][q0] - raw[pp][3][q0]);
-                ea[mt][2] = rn_tf32(raw[pp][1][q0] - (is3 ? raw[pp][2][q0] : raw[pp][3][q0]));
-                ea[mt][4] = slot2 ? rn_tf32(raw[pp][2][q0] - raw[pp][3][q0]) : 0u;
+                float ev[4];
+                ev[0] = raw[pp][0][q0] - raw[pp][3][q0];
+                ev[2] = raw[pp][1][q0] - (is3 ? raw[pp][2][q0] : raw[pp][3][q0]);
+                e8[mt][0] = __shfl_sync(0xffffffffu, raw[pp][2][q0] - raw[pp][3][q0], lane & ~3);
                 if (R >= 16) {
-                    ea[mt][1] = rn_tf32(raw[pp][0][q1] - raw[pp][3][q1]);
-                    ea[mt][3] = rn_tf32(raw[pp][1][q1] - (is3 ? raw[pp][2][q1] : raw[pp][3][q1]));
-                    ea[mt][5] = slot2 ? rn_tf32(raw[pp][2][q1] - raw[pp][3][q1]) : 0u;
+                    ev[1] = raw[pp][0][q1] - raw[pp][3][q1];
+                    ev[3] = raw[pp][1][q1] - (is3 ? raw[pp][2][q1] : raw[pp][3][q1]);
+                    e8[mt][1] = __shfl_sync(0xffffffffu, raw[pp][2][q1] - raw[pp][3][q1], lane & ~3);
                 } else {
-                    ea[mt][1] = ea[mt][3] = ea[mt][5] = 0u;
+                    ev[1] = ev[3] = 0.f;
+                    e8[mt][1] = 0.f;
                 }
 #pragma unroll
+                for (int q = 0; q < 4; ++q) split_tf32(ev[q], eh[mt][q], el2[mt][q]);
+#pragma unroll
                 for (int q = 0; q < 4; ++q) X[mt][0][q] = X[mt][1][q] = 0.f;
-                // X = E H_E: n tile 0 (kk' 0..7), n tile 1 (kk' = 8)
-                mma_tf32_u(X[mt][0], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], b00, b01);
-                mma_tf32_u(X[mt][0], ea[mt][4], ea[mt][5], 0u, 0u, b20, 0u);
-                mma_tf32_u(X[mt][1], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], b10, b11);
-                mma_tf32_u(X[mt][1], ea[mt][4], ea[mt][5], 0u, 0u, b30, 0u);
+                // X = E H_E over the eight tensor-core K slots: n tile 0 (columns 0..7), n tile 1 (column 8);
+                // small terms first
+                mma_tf32_u(X[mt][0], el2[mt][0], el2[mt][1], el2[mt][2], el2[mt][3], bh[0], bh[1]);
+                mma_tf32_u(X[mt][0], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], bl[0], bl[1]);
+                mma_tf32_u(X[mt][0], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], bh[0], bh[1]);
+                mma_tf32_u(X[mt][1], el2[mt][0], el2[mt][1], el2[mt][2], el2[mt][3], bh[2], bh[3]);
+                mma_tf32_u(X[mt][1], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], bl[2], bl[3]);
+                mma_tf32_u(X[mt][1], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], bh[2], bh[3]);
+                // ninth K component: X[row][c] += E[row][6] H_E[6][c]
+                X[mt][0][0] = fmaf(e8[mt][0], hk0, X[mt][0][0]);
+                X[mt][0][1] = fmaf(e8[mt][0], hk1, X[mt][0][1]);
+                X[mt][0][2] = fmaf(e8[mt][1], hk0, X[mt][0][2]);
+                X[mt][0][3] = fmaf(e8[mt][1], hk1, X[mt][0][3]);
+                X[mt][1][0] = fmaf(e8[mt][0], hk8, X[mt][1][0]);  // column 8 lives on the t4 = 0 lanes (hk8 = 0 elsewhere)
+                X[mt][1][2] = fmaf(e8[mt][1], hk8, X[mt][1][2]);
             }
             // C += E X^T: n tile j = directions 8 j + g = rows of X (m tile j / 2, half j % 2)
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 const int mj = j >> 1, hj = (j & 1) * 2;
-                const uint32_t x0 = rn_tf32(X[mj][0][hj]), x1 = rn_tf32(X[mj][0][hj + 1]);
-                const uint32_t x2 = rn_tf32(X[mj][1][hj]);
+                uint32_t xh[2], xl[2];
+                split_tf32(X[mj][0][hj], xh[0], xl[0]);
+                split_tf32(X[mj][0][hj + 1], xh[1], xl[1]);
+                // ninth K component: C[a][b] += E[a][6] X[b][6]; X[b][6] (accumulator column 8) of the rows
+                // b = 8 j + 2 t4 + {0, 1} sits on the t4 = 0 lanes of those rows
+                const float x80 = __shfl_sync(0xffffffffu, X[mj][1][hj], (2 * t4) * 4);
+                const float x81 = __shfl_sync(0xffffffffu, X[mj][1][hj], (2 * t4 + 1) * 4);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
-                    mma_tf32_u(cacc[pp][mt][j], ea[mt][0], ea[mt][1], ea[mt][2], ea[mt][3], x0, x1);
-                    mma_tf32_u(cacc[pp][mt][j], ea[mt][4], ea[mt][5], 0u, 0u, x2, 0u);
+                    mma_tf32_u(cacc[pp][mt][j], el2[mt][0], el2[mt][1], el2[mt][2], el2[mt][3], xh[0], xh[1]);
+                    mma_tf32_u(cacc[pp][mt][j], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], xl[0], xl[1]);
+                    mma_tf32_u(cacc[pp][mt][j], eh[mt][0], eh[mt][1], eh[mt][2], eh[mt][3], xh[0], xh[1]);
+                    cacc[pp][mt][j][0] = fmaf(e8[mt][0], x80, cacc[pp][mt][j][0]);
+                    cacc[pp][mt][j][1] = fmaf(e8[mt][0], x81, cacc[pp][mt][j][1]);
+                    cacc[pp][mt][j][2] = fmaf(e8[mt][1], x80, cacc[pp][mt][j][2]);
+                    cacc[pp][mt][j][3] = fmaf(e8[mt][1], x81, cacc[pp][mt][j][3]);
                 }
             }
         }
@@ -1424,7 +1460,7 @@ __global__ void __launch_bounds__(128, LSB_H3_MINB) elem_hess3_kernel(const int4
                             const float sx = Sx[t * 3 + (e + f - 1)];
                             v = ((b - a + 3) % 3 == 1) ? v + sx : v - sx;
                         }
-                        H[i * 9 - i * (i - 1) / 2 + (j - i)] = __uint_as_float(rn_tf32(v));
+                        H[i * 9 - i * (i - 1) / 2 + (j - i)] = v;
                     }
                 }
                 H[45] = H[46] = H[47] = 0.f;
@@ -2265,11 +2301,8 @@ struct BatchedEngine : BatchedBase {
             const size_t gsmem = hess_smem(r);
             const float* recf = static_cast<const float*>(rec_f32(c));
             const int4* tt = reinterpret_cast<const int4*>(c.d_tets);
-            // edge-space form (two chained TF32 MMA stages per (tet, point)) from 16K tets up: its per-(tet, point)
-            // roundings average out over the mesh (config 5: 1.2e-5 against the oracle, the 3xTF32 kernel
-            // 1.8e-5), while on config 1's 1,536 tets they leave 4.6e-5 against 1.8e-5 -- small meshes keep
-            // the 3xTF32 kernel (LSB_HESS3=2 forces the edge-space kernel, =0 the 3xTF32 one)
-            if (c.dev.hess3 == 2 || (c.dev.hess3 == 1 && c.mesh.E >= 16384)) {
+            // edge-space form: two chained 3xTF32 MMA stages per (tet, point); LSB_HESS3=0 selects the D^T M' kernel
+            if (c.dev.hess3) {
                 if (r == 8)
                     elem_hess3_kernel<8><<<g, 128, gsmem, s>>>(tt, recf, d_blk_tet0, d_blk_vptr, d_tet_loc, d_blk_aptr,
                                                              d_blk_avert, d_tet_aloc, d_Uh, d_Jv, P, d_Cpart, d_gpart);

@@ -43,8 +43,7 @@ struct DevFlags {
     int solve_exp = 0;        // LSB_SOLVE_EXP: persistent-kernel A/B bits (lsb_solve.cuh SolveParams::exp)
     int trace = 0;            // LSB_TRACE=1: persistent-kernel phase timestamps
     int fuse_tangent_out = 1; // LSB_FUSE_TOUT=0: tangent output as its own kernel after the output GEMM (Hessian path)
-    int hess3 = 1;            // LSB_HESS3: 1 edge-space chained-MMA element Hessian kernel on meshes of >= 16K tets (default),
-                              // 2 always, 0 never (the D^T M' 3xTF32 kernel)
+    int hess3 = 1;            // LSB_HESS3=0: the D^T M' element Hessian kernel instead of the edge-space chained-MMA form
     int elem_f2 = 1;          // LSB_ELEM_F2=0: scalar batched element kernel instead of the packed fp32x2 one
     int theta_tb = 24;        // LSB_THETA_TB: tets per block of the theta element pass
     int noncoop = 0;          // LSB_NONCOOP=1: persistent kernel as a plain cluster launch (ncu replay)

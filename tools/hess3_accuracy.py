@@ -1,6 +1,6 @@
 """Accuracy of the element Hessian kernels against the oracle: relative Frobenius error of the reduced
 potential Hessian on config 1 (1,536 tets, r = 8) and the config-5 problem (98,304 tets, r = 16).
-Run with LSB_HESS3=0 for the 3xTF32 kernel."""
+Run with LSB_HESS3=0 for the D^T M' kernel."""
 import os
 import sys
 
