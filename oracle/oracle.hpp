@@ -15,9 +15,11 @@
 // snh_core(element_frame(mesh, e, positions), ...) (energy.cpp:158-175).
 // Extensions demanded by BASELINE.json are marked [EXT].
 //
-// Parity pin: the reference ships no golden files; this oracle is pinned by
-// the reference's own known-answer / property tests restated in
-// tests/test_oracle_*.py (SURVEY.md §8c table).
+// Parity pin: PARITY UNPINNED against reference outputs -- the reference ships
+// no golden files and cannot be built here, so no reference binary or fixture
+// checks this restatement.  It is pinned as far as that allows by the
+// reference's own known-answer / property tests restated in
+// tests/test_oracle_*.py (SURVEY.md §8c table; DESIGN.md §2).
 // ============================================================================
 #pragma once
 
