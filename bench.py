@@ -353,6 +353,7 @@ def single_instance(name, K, W, T, R, want_cpu, cpu_sample, e2e=True):
         kname = ("multi-kernel evaluation (ctrl_fast -> out_fwd_tma -> elem -> vjp_gather_tma -> ctrl_fast, "
                  "one CUDA graph per evaluation)")
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "frac_of_nominal_8TBs": achieved / 8000.0,
             "traffic": TRAFFIC.get((name, solve["in_use"])), "kernel": kname, "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": alg,
             "algorithmic_formula": "w(2nh+9n)+E(16+10w)[+2wE] per E+grad eval (SURVEY 8d)",
@@ -505,7 +506,9 @@ def lipschitz_record(K, W, R, want_cpu):
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                      "frac": achieved / bf16, "traffic": None, "algorithmic_flops": flops,
                      "peak_kind": peak_kind + ", dense bf16",
-                     "note": "SURVEY 8(d): tangent GEMMs 890 GFLOP + element HVPs 640 GFLOP per 1024 pairs"},
+                     "note": "SURVEY 8(d): tangent GEMMs 890 GFLOP + element HVPs 640 GFLOP per 1024 pairs",
+                     # the element HVPs alone against the fp32 CUDA-core peak (148 SMs x 128 lanes x 2 x 1.965 GHz)
+                     "element_hvp_fp32_frac": 0.64e12 * Pt / 1024 / (t * 1e-3) / (74.4e12 * R.ws)},
         "e2e": {"value": e2e_t * 1e3, "unit": "ms", "h2d_bytes_per_step": 16 * (hi - lo) * r,
                 "d2h_bytes_per_step": 8, "api": "lsb_lipschitz_loss (C ABI), host buffers"},
         "gpu_launches": int(launches // reps),
